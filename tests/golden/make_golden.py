@@ -1,0 +1,196 @@
+"""Generate golden vectors from the REAL reference implementation.
+
+Run in the build container only (the reference is not on GPU boxes):
+
+    PYTHONPATH=/root/reference/pkg/src:/root/repo OPENBLAS_NUM_THREADS=1 \
+        python tests/golden/make_golden.py
+
+It imports ``sfwave`` from /root/reference/pkg/src (read-only), feeds it the
+seeded inputs of ``paper_1406_6923_b200.configs`` and stores the outputs as
+small ``.npz`` fixtures next to this script.  ``tests/test_oracle_golden.py``
+pins ``oracle/sfw_oracle.py`` against them; the GPU parity tests then compare
+the CUDA path against the pinned oracle and against these fixtures.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "..", ".."))
+
+from sfwave.grid import (  # noqa: E402  (reference package)
+    DomainSpec, MediumModel, assemble_subdomain_operator, build_partition, sample_medium)
+from sfwave.rom import (  # noqa: E402
+    block_lanczos, build_krylov_basis, build_subdomain_model, project_reduced, subdomain_inputs)
+from sfwave.sim import make_pulse  # noqa: E402
+from sfwave.stepper import (  # noqa: E402
+    CoupledStepper, Probe, SourceTerm, cfl_estimate_coupled, make_probe, project_source)
+
+from paper_1406_6923_b200.configs import locate, make_workload  # noqa: E402
+
+
+def chain_blocks(op, m, n, shift, layers):
+    f = subdomain_inputs(op, m)
+    basis, sizes = build_krylov_basis(op.matrix, f, n, shift)
+    w = 6 * m
+    basis = basis[:, :layers * w]
+    at, ft = project_reduced(basis, op.matrix, f)
+    ch = block_lanczos(at, ft)
+    return np.stack(ch.diag_blocks), np.stack(ch.off_blocks), ch.entry_block
+
+
+def workload_models(wl, alphas=None):
+    spec = DomainSpec(tuple((g - 1) * h for g, h in zip(wl.global_shape, wl.spacing)),
+                      wl.counts, wl.p)
+    part = build_partition(spec)
+    ops, models = {}, {}
+    for sub in part.subdomains:
+        if alphas is not None and sub.alpha not in alphas:
+            continue
+        op = assemble_subdomain_operator(part, sub.alpha, wl.c_field)
+        ops[sub.alpha] = op
+        models[sub.alpha] = build_subdomain_model(op, wl.modes_per_face, wl.n, wl.shift)
+    return part, ops, models
+
+
+def pack_models(out, prefix, ops, models, m, n, shift):
+    order = sorted(models)
+    out[prefix + "alphas"] = np.array(order)
+    out[prefix + "gammas"] = np.stack([models[a].gammas for a in order])
+    out[prefix + "hats"] = np.stack([models[a].gamma_hats for a in order])
+    out[prefix + "scales"] = np.stack([models[a].scales for a in order])
+    tds, tos, ents = [], [], []
+    for a in order:
+        td, to, en = chain_blocks(ops[a], m, n, shift, models[a].layers)
+        tds.append(td)
+        tos.append(to)
+        ents.append(en)
+    out[prefix + "tdiag"] = np.stack(tds)
+    out[prefix + "toff"] = np.stack(tos)
+    out[prefix + "entry"] = np.stack(ents)
+
+
+def golden_config(cfg, counts, n_steps, name, record_models=True, basis_rows=True):
+    wl = make_workload(cfg, counts=counts, n_steps=n_steps)
+    part, ops, models = workload_models(wl)
+    out = {"c_field": wl.c_field, "counts": np.array(wl.counts), "m": wl.modes_per_face,
+           "n": wl.n, "shift": wl.shift, "n_steps": wl.n_steps, "f0": wl.f0}
+    if record_models:
+        pack_models(out, "", ops, models, wl.modes_per_face, wl.n, wl.shift)
+    lam, conv = cfl_estimate_coupled(models)
+    dt = 0.9 * 2.0 / math.sqrt(lam)
+    out["lam"] = lam
+    out["dt"] = dt
+    src_alpha, src_row = locate(wl.sources[0], wl.counts, wl.p)
+    pulse = make_pulse("ricker", wl.f0, 1.2 / wl.f0)
+    vec = project_source(models[src_alpha], src_row, 1.0)
+    out["src_alpha"] = np.array(src_alpha)
+    out["src_row"] = src_row
+    out["src_vec"] = vec
+    if basis_rows:
+        out["src_basis_row"] = models[src_alpha].basis[src_row].copy()
+    probes = []
+    for alpha, face in wl.face_receivers:
+        md = models[alpha]
+        for q in range(wl.modes_per_face):
+            wts = np.zeros(md.state_size)
+            wts[face * wl.modes_per_face + q] = 1.0
+            probes.append(Probe(alpha, wts))
+    node_w, node_basis = [], []
+    for ijk in wl.node_receivers:
+        alpha, row = locate(ijk, wl.counts, wl.p)
+        pr = make_probe(models[alpha], row)
+        probes.append(pr)
+        node_w.append(pr.weights)
+        node_basis.append(models[alpha].basis[row].copy())
+    if node_w:
+        out["node_probe_w"] = np.stack(node_w)
+        out["node_basis_rows"] = np.stack(node_basis)
+    with CoupledStepper(models, dt, sources=(SourceTerm(src_alpha, vec, pulse),)) as st:
+        times, rows = st.run(wl.n_steps, probes=probes)
+        out["times"] = times
+        out["rows"] = rows
+        out["message_count"] = st.message_count
+        out["energy"] = st.energy()
+    np.savez_compressed(os.path.join(HERE, name), **out)
+    print(name, {k: np.shape(v) for k, v in out.items()})
+
+
+def golden_toy():
+    """Reference-test-sized cases (p=5, unit cube, dimensionless shift 4)."""
+    out = {}
+    rng = np.random.default_rng(77)
+    for tag, counts, m, n, med in [
+        ("pair", (2, 1, 1), 1, 2, None),
+        ("quad", (2, 2, 1), 4, 2, "layer"),
+    ]:
+        spec = DomainSpec(tuple(float(c) for c in counts), counts, (5, 5, 5))
+        part = build_partition(spec)
+        if med == "layer":
+            from sfwave.grid import Box
+            medium = MediumModel(1.0, ((Box((0.0, 0.0, 0.5), (2.0, 2.0, 1.0)), 1.7),))
+        else:
+            medium = MediumModel(1.0)
+        c = sample_medium(medium, part)
+        ops, models = {}, {}
+        for sub in part.subdomains:
+            ops[sub.alpha] = assemble_subdomain_operator(part, sub.alpha, c)
+            models[sub.alpha] = build_subdomain_model(ops[sub.alpha], m, n, 4.0)
+        pre = tag + "_"
+        out[pre + "c_field"] = c
+        out[pre + "counts"] = np.array(counts)
+        out[pre + "m"] = m
+        out[pre + "n"] = n
+        pack_models(out, pre, ops, models, m, n, 4.0)
+        order = sorted(models)
+        out[pre + "basis"] = np.stack([models[a].basis for a in order])
+        out[pre + "matrix0"] = ops[order[0]].matrix.toarray()
+        lam, conv = cfl_estimate_coupled(models)
+        out[pre + "lam"] = lam
+        dt = 0.5 * 2.0 / math.sqrt(lam)
+        out[pre + "dt"] = dt
+        u0 = {a: rng.standard_normal(models[a].state_size) for a in order}
+        # shared-face replicas must agree
+        for a in order:
+            for f, b in sorted(models[a].neighbors.items()):
+                if b > a:
+                    u0[b][models[b].face_slice(f ^ 1)] = u0[a][models[a].face_slice(f)]
+        v0 = {a: np.zeros(models[a].state_size) for a in order}
+        out[pre + "u0"] = np.stack([u0[a] for a in order])
+        row = 31  # strictly interior node of a p=5 subdomain
+        vec = project_source(models[order[0]], row, 1.0)
+        out[pre + "src_vec"] = vec
+        pr = make_probe(models[order[-1]], row)
+        out[pre + "probe_w"] = pr.weights
+        pulse = make_pulse("ricker", 1.0, 1.2)
+        with CoupledStepper(models, dt, sources=(SourceTerm(order[0], vec, pulse),)) as st:
+            times, rows = st.run(40, probes=[pr], u0=u0, v0=v0)
+            out[pre + "times"] = times
+            out[pre + "rows"] = rows
+            out[pre + "u_curr"] = np.stack([st.u_curr[a] for a in order])
+            out[pre + "u_prev"] = np.stack([st.u_prev[a] for a in order])
+            out[pre + "energy"] = st.energy()
+            out[pre + "messages"] = st.message_count
+    np.savez_compressed(os.path.join(HERE, "golden_toy.npz"), **out)
+    print("golden_toy.npz", len(out))
+
+
+def golden_m9k8():
+    """One interior m=9, k=8 subdomain of the config-3 medium recipe (3x3x3 tiling)."""
+    wl = make_workload(3, counts=(3, 3, 3))
+    part, ops, models = workload_models(wl, alphas={(1, 1, 1), (0, 0, 0)})
+    out = {"c_field": wl.c_field, "counts": np.array(wl.counts), "m": 9, "n": 8, "shift": wl.shift}
+    pack_models(out, "", ops, models, 9, 8, wl.shift)
+    np.savez_compressed(os.path.join(HERE, "golden_m9k8.npz"), **out)
+    print("golden_m9k8.npz")
+
+
+if __name__ == "__main__":
+    golden_toy()
+    golden_config(1, None, 200, "golden_c1.npz")
+    golden_m9k8()

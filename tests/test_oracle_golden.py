@@ -1,0 +1,104 @@
+"""Pin the CPU oracle (oracle/sfw_oracle.py) against reference-generated golden vectors.
+
+The fixtures were produced by tests/golden/make_golden.py from the real
+reference package; the oracle must reproduce them (same numpy/scipy calls,
+same order) to within 1e-12 relative -- in practice bitwise.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import sfw_oracle as so
+from paper_1406_6923_b200.configs import locate, make_workload
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def _spacing(counts, p, extents):
+    gs = so.global_shape(counts, p)
+    return tuple(e / (g - 1) for e, g in zip(extents, gs))
+
+
+@pytest.mark.parametrize("tag", ["pair", "quad"])
+def test_toy_models_and_run(tag):
+    g = np.load(os.path.join(GOLD, "golden_toy.npz"))
+    pre = tag + "_"
+    counts = tuple(int(x) for x in g[pre + "counts"])
+    m, n = int(g[pre + "m"]), int(g[pre + "n"])
+    ops = so.make_subops(counts, (5, 5, 5), _spacing(counts, (5, 5, 5), tuple(map(float, counts))),
+                         g[pre + "c_field"])
+    order = sorted(ops)
+    assert np.allclose(ops[order[0]].matrix.toarray(), g[pre + "matrix0"], rtol=0, atol=1e-13)
+    models = {a: so.build_model(ops[a], m, n, 4.0) for a in order}
+    for i, a in enumerate(order):
+        assert rel(models[a].gammas, g[pre + "gammas"][i]) < 1e-12
+        assert rel(models[a].gamma_hats, g[pre + "hats"][i]) < 1e-12
+        assert rel(models[a].scales, g[pre + "scales"][i]) < 1e-12
+        assert rel(models[a].tdiag, g[pre + "tdiag"][i]) < 1e-12
+        assert rel(models[a].toff, g[pre + "toff"][i]) < 1e-12
+        assert rel(models[a].basis, g[pre + "basis"][i]) < 1e-12
+    lam, conv = so.cfl_power(models)
+    assert conv and abs(lam - float(g[pre + "lam"])) <= 1e-12 * lam
+    vec = so.source_vector(models[order[0]], 31)
+    assert rel(vec, g[pre + "src_vec"]) < 1e-12
+    pw = so.probe_weights(models[order[-1]], 31)
+    assert rel(pw, g[pre + "probe_w"]) < 1e-12
+    dt = float(g[pre + "dt"])
+    u0 = {a: g[pre + "u0"][i] for i, a in enumerate(order)}
+    st = so.Coupled(models, dt, sources=[(order[0], vec, so.ricker(1.0, 1.2))])
+    times, rows = st.run(40, probes=[(order[-1], pw)], u0=u0, v0=None)
+    assert np.array_equal(times, g[pre + "times"])
+    assert rel(rows, g[pre + "rows"]) < 1e-11
+    assert st.message_count == int(g[pre + "messages"])
+    assert abs(st.energy() - float(g[pre + "energy"])) <= 1e-10 * abs(float(g[pre + "energy"]))
+
+
+def test_config1_models_traces():
+    g = np.load(os.path.join(GOLD, "golden_c1.npz"))
+    wl = make_workload(1, n_steps=int(g["n_steps"]))
+    assert np.array_equal(wl.c_field, g["c_field"])
+    ops = so.make_subops(wl.counts, wl.p, wl.spacing, wl.c_field)
+    order = sorted(ops)
+    models = {a: so.build_model(ops[a], wl.modes_per_face, wl.n, wl.shift) for a in order}
+    for i, a in enumerate(order):
+        assert rel(models[a].gammas, g["gammas"][i]) < 1e-12
+        assert rel(models[a].tdiag, g["tdiag"][i]) < 1e-12
+        assert rel(models[a].toff, g["toff"][i]) < 1e-12
+    lam, conv = so.cfl_power(models)
+    assert abs(lam - float(g["lam"])) <= 1e-12 * lam
+    dt = 0.9 * 2.0 / math.sqrt(lam)
+    src_alpha, src_row = locate(wl.sources[0], wl.counts, wl.p)
+    vec = so.source_vector(models[src_alpha], src_row)
+    assert rel(vec, g["src_vec"]) < 1e-12
+    probes = []
+    for alpha, face in wl.face_receivers:
+        for q in range(wl.modes_per_face):
+            wts = np.zeros(models[alpha].state_size)
+            wts[face * wl.modes_per_face + q] = 1.0
+            probes.append((alpha, wts))
+    st = so.Coupled(models, dt, sources=[(src_alpha, vec, so.ricker(wl.f0, wl.delay))])
+    times, rows = st.run(wl.n_steps, probes=probes)
+    assert rel(rows, g["rows"]) < 1e-11
+    assert st.message_count == int(g["message_count"])
+
+
+def test_m9k8_subdomain_build():
+    g = np.load(os.path.join(GOLD, "golden_m9k8.npz"))
+    wl = make_workload(3, counts=(3, 3, 3))
+    assert np.array_equal(wl.c_field, g["c_field"])
+    alphas = [tuple(int(x) for x in a) for a in g["alphas"]]
+    ops = so.make_subops(wl.counts, wl.p, wl.spacing, wl.c_field, alphas=alphas)
+    for i, a in enumerate(alphas):
+        md = so.build_model(ops[a], 9, 8, wl.shift)
+        assert rel(md.tdiag, g["tdiag"][i]) < 1e-12
+        assert rel(md.toff, g["toff"][i]) < 1e-12
+        assert rel(md.gammas, g["gammas"][i]) < 1e-12
+        assert rel(md.gamma_hats, g["hats"][i]) < 1e-12
+        assert rel(md.scales, g["scales"][i]) < 1e-12
