@@ -1,0 +1,160 @@
+/*
+ * sfw_b200.h -- C ABI of the B200-native S-fraction ROM path (libsfw_b200.so).
+ *
+ * The reference (`sfwave`, pure Python) has no FFI; its drop-in boundary is
+ * the Python API re-exported in pkg/src/sfwave/__init__.py:33-43.  Each entry
+ * point below replaces one reference call; the Python mirror in
+ * paper_1406_6923_b200/ binds them with ctypes.
+ *
+ * Conventions
+ *   - plain C types only; pointers documented as HOST or DEVICE.
+ *   - every call returns 0 on success or a negative SFW_E* code; a message is
+ *     written to the caller's errbuf (if non-NULL) and is also retrievable with
+ *     sfw_last_error().  Codes map onto the reference exception taxonomy
+ *     (errors.py:11-41): SFW_ECONFIG -> ConfigError, SFW_ENUMERICAL ->
+ *     NumericalError, SFW_EINSTABLE -> InstabilityError, SFW_EPROTOCOL ->
+ *     ProtocolError, SFW_ECUDA -> a CUDA runtime failure (no fallback exists).
+ *   - all arithmetic is IEEE fp64; results are bitwise deterministic run to run
+ *     (fixed-order reductions, no floating-point atomics) as the reference
+ *     requires (test_stepper.py:308-322, test_acceptance.py:451-484).
+ */
+#ifndef SFW_B200_H
+#define SFW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFW_OK 0
+#define SFW_ECONFIG -1
+#define SFW_ENUMERICAL -2
+#define SFW_EINSTABLE -3
+#define SFW_EPROTOCOL -4
+#define SFW_ECUDA -5
+
+/* Last error message of the calling thread ("" if none). */
+const char* sfw_last_error(void);
+
+/* Number of SMs / device name of the current CUDA device; <0 if no device. */
+int sfw_device_info(int* n_sm, char* name, int name_len);
+
+/* ------------------------------------------------------------------------- */
+/* Stage 2: coupled leapfrog stepping.                                         */
+/* Replaces sfwave.stepper.CoupledStepper (stepper.py:144-449):               */
+/*   __init__ + _pair_interfaces (stepper.py:147-220)  -> sfw_step_create      */
+/*   initialize (stepper.py:325-360)                   -> sfw_step_init        */
+/*   advance / run / _probe_row (stepper.py:362-415)   -> sfw_step_run         */
+/*   u_curr / u_prev attributes                        -> sfw_step_get_state   */
+/*   close / __exit__ (stepper.py:229-239)             -> sfw_step_destroy     */
+/* ------------------------------------------------------------------------- */
+
+typedef struct sfw_stepper sfw_stepper;
+
+typedef struct sfw_step_desc {
+    int n_sub;               /* number of subdomains, in the reference's sorted(alpha) order */
+    int m;                   /* modes per face (uniform); width w = 6m                        */
+    const int* layers;       /* HOST [n_sub] chain layers L_s                                 */
+    const int* neighbors;    /* HOST [n_sub*6] neighbour subdomain index per face, -1 = none  */
+    /* Chain coefficients, dense row-major w x w blocks, subdomain s at block offset
+     * sum_{t<s} L_t: gammas = Gamma_j, gamma_hats = Gamma-hat_j (rom.py:319-356).
+     * Pointer kind given by coef_on_device (0 = HOST, 1 = DEVICE).                 */
+    const double* gammas;
+    const double* gamma_hats;
+    const double* scales;    /* G_j, same layout; may be NULL (then energy is unavailable) */
+    int coef_on_device;
+    double dt;               /* leapfrog step (> 0)                                            */
+    /* Sources (stepper.py:47-53 SourceTerm): vector of length L_s*w of subdomain
+     * src_sub[i]; superposed in list order as stepper.py:313-321 does.           */
+    int n_src;
+    const int* src_sub;      /* HOST [n_src] */
+    const double* src_vec;   /* HOST concat of the n_src vectors */
+    /* Probes (stepper.py:56-61): dense weights of length L_s*w on probe_sub[i]. */
+    int n_probe;
+    const int* probe_sub;    /* HOST [n_probe] */
+    const double* probe_w;   /* HOST concat of the n_probe weight vectors */
+} sfw_step_desc;
+
+/* Validate, upload and pack the chain coefficients (symmetric Gamma / Gamma-hat
+ * are stored packed: w(w+1)/2 doubles per block), build the interface masses
+ * (stepper.py:204-219, computed on the device) and check Gamma-hat_1 = I
+ * (stepper.py:182-186).  Returns a handle in *out. */
+int sfw_step_create(const sfw_step_desc* desc, sfw_stepper** out, char* errbuf, int errlen);
+
+/* Two-level start (stepper.py:325-360).  u0/v0: HOST concat of L_s*w per
+ * subdomain, either may be NULL (zeros).  profile0[i] = source i's profile at
+ * t = 0.  row0_out: HOST [n_probe] probe row of U0 (stepper.py:405-406) or NULL. */
+int sfw_step_init(sfw_stepper* h, const double* u0, const double* v0,
+                  const double* profile0, double* row0_out, char* errbuf, int errlen);
+
+/* Advance n_steps leapfrog steps in ONE persistent kernel launch (one grid-wide
+ * split arrive/wait barrier per step; face exchange, source injection and
+ * probe extraction fused).  profile: HOST [n_src][n_steps] profile values
+ * f_i(t_k), t_k = (steps_done + k) * dt for k = 0..n_steps-1 (stepper.py:367).
+ * limits: HOST [n_steps] growth thresholds GROWTH_LIMIT*max(baseline_k,1e-300)
+ * (stepper.py:379-389) or NULL to skip the check.
+ * rows_out: HOST [n_steps/record_every][n_probe] (probe rows after every
+ * record_every-th step, stepper.py:407-411) or NULL.
+ * norms_out: HOST [n_steps] |U_k|_2 or NULL.  On instability returns
+ * SFW_EINSTABLE and *bad_step = first failing step (1-based, relative). */
+int sfw_step_run(sfw_stepper* h, int n_steps, int record_every,
+                 const double* profile, const double* limits,
+                 double* rows_out, double* norms_out, int* bad_step,
+                 char* errbuf, int errlen);
+
+/* Same as sfw_step_run but leaves rows/norms in device memory (for timing with
+ * inputs resident in HBM); *kernel_ms = CUDA-event duration of the stepping
+ * kernel on the library stream. */
+int sfw_step_run_resident(sfw_stepper* h, int n_steps, int record_every,
+                          const double* profile, float* kernel_ms, char* errbuf, int errlen);
+
+/* Replace the probe set (stepper.py:391-415 passes probes per run). */
+int sfw_step_set_probes(sfw_stepper* h, int n_probe, const int* probe_sub, const double* probe_w,
+                        char* errbuf, int errlen);
+
+/* Acceleration of a state (HOST u, HOST acc_out), including the forcing
+ * sum_i vec_i * profile0[i] (profile0 may be NULL = no forcing);
+ * replaces CoupledStepper._acceleration (stepper.py:251-311). */
+int sfw_step_accel(sfw_stepper* h, const double* u, const double* profile0, double* acc_out,
+                   char* errbuf, int errlen);
+
+/* Largest eigenvalue of minus the coupled acceleration by power iteration
+ * (replaces cfl_estimate_coupled, stepper.py:452-487): x0 = HOST start vector
+ * (the reference draws it from numpy default_rng(seed)); the iterate stays in
+ * HBM, each iteration is one stepping-kernel pass in acceleration mode plus a
+ * fixed-order reduction.  Overwrites the stepper state. */
+int sfw_step_power(sfw_stepper* h, const double* x0, double tol, int max_iter,
+                   double* lam_out, int* converged, int* iters, char* errbuf, int errlen);
+
+/* Copy the current/previous state (HOST concat of L_s*w per subdomain). */
+int sfw_step_get_state(sfw_stepper* h, double* u_curr, double* u_prev);
+
+/* Discrete energy (stepper.py:419-449), computed on the device. */
+int sfw_step_energy(sfw_stepper* h, double* energy, char* errbuf, int errlen);
+
+/* Byte and flop counts of one stepping launch per step (algorithmic, as in
+ * SURVEY.md 8d), and the bytes actually streamed per step by this build. */
+int sfw_step_traffic(sfw_stepper* h, double* alg_bytes, double* alg_flops, double* streamed_bytes);
+
+int sfw_step_destroy(sfw_stepper* h);
+
+/* ------------------------------------------------------------------------- */
+/* Once-per-run state-space maps (stepper.py:91-141), on the device.           */
+/* ------------------------------------------------------------------------- */
+
+/* project_source (stepper.py:91-128): coeff = basis_row * scale (scale =
+ * amplitude / c_s), norms[0] = |coeff|, norms[1] = |coeff[:w]| (the caller
+ * applies the leak / silence checks), first block zeroed, out_j = G_j coeff_j.
+ * scales: HOST L x w x w; basis_row, out: HOST L*w. */
+int sfw_source_vector(int L, int w, const double* scales, const double* basis_row, double scale,
+                      double* out, double* norms, char* errbuf, int errlen);
+
+/* make_probe (stepper.py:131-141): out_j = solve(G_j^T, basis_row_j) * scale. */
+int sfw_probe_weights(int L, int w, const double* scales, const double* basis_row, double scale,
+                      double* out, char* errbuf, int errlen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFW_B200_H */

@@ -1,0 +1,26 @@
+"""B200-native S-fraction multiscale ROM wave solver (arXiv 1406.6923 path).
+
+Drop-in for the reference ``sfwave`` hot path (pkg/src/sfwave/__init__.py:33-43):
+the off-line per-subdomain ROM build and the on-line coupled leapfrog, both
+executed by hand-written sm_100a CUDA in ``libsfw_b200.so`` (C ABI:
+include/sfw_b200.h).  There is no CPU fallback: without the library or a CUDA
+device every compute entry point raises ``DeviceError``.
+"""
+
+__version__ = "0.1.0"
+
+from .errors import (ConfigError, DataError, DeviceError, InstabilityError, NumericalError,  # noqa: F401
+                     ProtocolError, SfwaveError)
+from .grid import (DomainPartition, DomainSpec, SubdomainOperator, assemble_subdomain_operator,  # noqa: F401
+                   build_partition, opposite_face)
+from .rom import SubdomainModel  # noqa: F401
+from .stepper import (CoupledStepper, Probe, SourceTerm, cfl_estimate_coupled, make_probe,  # noqa: F401
+                      project_source, stable_step_coupled)
+
+__all__ = [
+    "ConfigError", "CoupledStepper", "DataError", "DeviceError", "DomainPartition", "DomainSpec",
+    "InstabilityError", "NumericalError", "Probe", "ProtocolError", "SfwaveError", "SourceTerm",
+    "SubdomainModel", "SubdomainOperator", "assemble_subdomain_operator", "build_partition",
+    "cfl_estimate_coupled", "make_probe", "opposite_face", "project_source", "stable_step_coupled",
+    "__version__",
+]

@@ -1,0 +1,166 @@
+// Once-per-run state-space maps of the online stage, on the device:
+//   project_source (reference stepper.py:91-128): coeff = (V Q)^T e_s * amp / c_s,
+//       first layer block checked and zeroed, out_j = G_j coeff_j
+//   make_probe     (reference stepper.py:131-141): w_j = G_j^-T (V Q)[row, blk_j] * c/sqrt(mu)
+// One CTA per chain layer; the w x w solve is Gaussian elimination with partial
+// pivoting (LAPACK gesv semantics) in shared memory.
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "sfw_common.cuh"
+
+namespace sfw {
+
+// out_j = G_j v_j   (kind 0)   or   out_j = G_j^-T v_j   (kind 1); v already scaled
+__global__ void k_layer_map(const double* __restrict__ G, const double* __restrict__ v, int w, int kind,
+                            double* __restrict__ out, int* __restrict__ status) {
+    extern __shared__ double sh[];
+    const int j = blockIdx.x;
+    const double* Gj = G + (size_t)j * w * w;
+    const double* vj = v + (size_t)j * w;
+    double* oj = out + (size_t)j * w;
+    if (kind == 0) {
+        for (int i = threadIdx.x; i < w; i += blockDim.x) {
+            double s = 0.0;
+            for (int k = 0; k < w; ++k) s = fma(Gj[i * w + k], vj[k], s);
+            oj[i] = s;
+        }
+        return;
+    }
+    double* A = sh;          // w x w : A = G^T
+    double* b = sh + w * w;  // w
+    __shared__ int piv;
+    for (int i = threadIdx.x; i < w * w; i += blockDim.x) {
+        const int r = i / w, c = i % w;
+        A[i] = Gj[c * w + r];
+    }
+    for (int i = threadIdx.x; i < w; i += blockDim.x) b[i] = vj[i];
+    __syncthreads();
+    for (int c = 0; c < w; ++c) {
+        if (threadIdx.x == 0) {
+            int pr = c;
+            double best = fabs(A[c * w + c]);
+            for (int r = c + 1; r < w; ++r)
+                if (fabs(A[r * w + c]) > best) {
+                    best = fabs(A[r * w + c]);
+                    pr = r;
+                }
+            piv = pr;
+            if (best == 0.0) status[j] = 1;
+        }
+        __syncthreads();
+        const int pr = piv;
+        if (pr != c) {
+            for (int k = threadIdx.x; k < w; k += blockDim.x) {
+                const double t = A[c * w + k];
+                A[c * w + k] = A[pr * w + k];
+                A[pr * w + k] = t;
+            }
+            if (threadIdx.x == 0) {
+                const double t = b[c];
+                b[c] = b[pr];
+                b[pr] = t;
+            }
+        }
+        __syncthreads();
+        for (int r = c + 1 + threadIdx.x; r < w; r += blockDim.x) {
+            const double l = A[r * w + c] / A[c * w + c];
+            for (int k = c + 1; k < w; ++k) A[r * w + k] -= l * A[c * w + k];
+            b[r] -= l * b[c];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int c = w - 1; c >= 0; --c) {
+            double s = b[c];
+            for (int k = c + 1; k < w; ++k) s -= A[c * w + k] * b[k];
+            b[c] = s / A[c * w + c];
+        }
+        for (int i = 0; i < w; ++i) oj[i] = b[i];
+    }
+}
+
+__global__ void k_scale_vec(const double* __restrict__ x, long long n, double s, double* __restrict__ y) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = x[i] * s;
+}
+
+__global__ void k_norm_pair(const double* __restrict__ x, long long n, int w, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (long long i = 0; i < n; ++i) {
+            a += x[i] * x[i];
+            if (i < w) b += x[i] * x[i];
+        }
+        out[0] = sqrt(a);
+        out[1] = sqrt(b);
+    }
+}
+
+__global__ void k_zero_head(double* __restrict__ x, int w) {
+    for (int i = threadIdx.x; i < w; i += blockDim.x) x[i] = 0.0;
+}
+
+}  // namespace sfw
+
+using namespace sfw;
+
+static int maps_common(int L, int w, const double* G, const double* row, double scale, int kind, double* out,
+                       double* norms, char* errbuf, int errlen) {
+    const size_t K = (size_t)L * w;
+    double *dG = nullptr, *dv = nullptr, *dc = nullptr, *dout = nullptr, *dn = nullptr;
+    int* dst = nullptr;
+    int rc = 0;
+    auto cleanup = [&]() {
+        cudaFree(dG);
+        cudaFree(dv);
+        cudaFree(dc);
+        cudaFree(dout);
+        cudaFree(dn);
+        cudaFree(dst);
+    };
+    if (cudaMalloc(&dG, K * w * 8) != cudaSuccess || cudaMalloc(&dv, K * 8) != cudaSuccess ||
+        cudaMalloc(&dc, K * 8) != cudaSuccess || cudaMalloc(&dout, K * 8) != cudaSuccess ||
+        cudaMalloc(&dn, 16) != cudaSuccess || cudaMalloc(&dst, L * sizeof(int)) != cudaSuccess) {
+        cleanup();
+        return fail(SFW_ECUDA, "cudaMalloc failed in chain maps", errbuf, errlen);
+    }
+    cudaMemcpy(dG, G, K * w * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dv, row, K * 8, cudaMemcpyHostToDevice);
+    cudaMemset(dst, 0, L * sizeof(int));
+    if (kind == 0) {
+        // coeff = row * (amp / c); leak check on the first block; zero it; apply G_j
+        k_scale_vec<<<8, 256>>>(dv, (long long)K, scale, dc);
+        k_norm_pair<<<1, 32>>>(dc, (long long)K, w, dn);
+        cudaMemcpy(norms, dn, 16, cudaMemcpyDeviceToHost);
+        k_zero_head<<<1, 256>>>(dc, w);
+        k_layer_map<<<L, 128>>>(dG, dc, w, 0, dout, dst);
+        cudaMemcpy(out, dout, K * 8, cudaMemcpyDeviceToHost);
+    } else {
+        const size_t sm = (size_t)(w * w + w) * 8;
+        cudaFuncSetAttribute(k_layer_map, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_layer_map<<<L, 128, sm>>>(dG, dv, w, 1, dc, dst);
+        k_scale_vec<<<8, 256>>>(dc, (long long)K, scale, dout);
+        cudaMemcpy(out, dout, K * 8, cudaMemcpyDeviceToHost);
+        std::vector<int> st(L);
+        cudaMemcpy(st.data(), dst, L * sizeof(int), cudaMemcpyDeviceToHost);
+        for (int j = 0; j < L; ++j)
+            if (st[j]) rc = fail(SFW_ENUMERICAL, "singular chain scale matrix in make_probe", errbuf, errlen);
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = fail(SFW_ECUDA, cudaGetErrorString(e), errbuf, errlen);
+    cleanup();
+    return rc;
+}
+
+extern "C" int sfw_source_vector(int L, int w, const double* scales, const double* basis_row, double scale,
+                                 double* out, double* norms, char* errbuf, int errlen) {
+    return maps_common(L, w, scales, basis_row, scale, 0, out, norms, errbuf, errlen);
+}
+
+extern "C" int sfw_probe_weights(int L, int w, const double* scales, const double* basis_row, double scale,
+                                 double* out, char* errbuf, int errlen) {
+    return maps_common(L, w, scales, basis_row, scale, 1, out, nullptr, errbuf, errlen);
+}

@@ -1,0 +1,1417 @@
+// Stage 2: coupled S-fraction leapfrog stepping as ONE persistent sm_100a kernel.
+//
+// Replaces the per-step Python loops of reference stepper.py:243-415
+// (CoupledStepper._flux / _acceleration / _forcing / advance / run) with a
+// cooperative kernel that, per step and per subdomain,
+//   phase A  flux_1 = Gamma_1 (U_2 - U_1), acc_1 = Gamma-hat_1 flux_1      (stepper.py:243-249, 297)
+//            publish flux_1 face slices to a global face buffer        (stepper.py:258-272 mailbox)
+//   -- grid split barrier: arrive here ... --
+//   phase B  layers j >= 2: flux_j = Gamma_j (U_{j+1} - U_j),
+//            acc_j = Gamma-hat_j (flux_j - flux_{j-1}), leapfrog        (stepper.py:301-308, 370-373)
+//   -- ... wait here (phase B hides the barrier latency) --
+//   phase C  shared faces: seg = mass (own + nbr) written identically on both
+//            sides (stepper.py:274-289), exterior faces keep Gamma-hat_1 flux_1,
+//            leapfrog of layer 1, |U|^2 partials (stepper.py:383), probe rows
+//            (stepper.py:414-415), all fused.
+// Chain coefficients (Gamma_j, Gamma-hat_j: symmetric) are stored packed
+// (w(w+1)/2 doubles per block, SURVEY 8d roofline bytes) in a warp-tile layout
+// and streamed HBM -> shared memory by the TMA engine (cp.async.bulk +
+// mbarrier ring per warp).  All reductions have a fixed order, so results are
+// bitwise reproducible run to run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sfw_common.cuh"
+
+namespace sfw {
+
+// ---------------------------------------------------------------------------
+// packed symmetric block layout (w = 6m rows split into 6 face groups of m):
+//   15 off-diagonal m x m tiles (I > K), element e of tile t at  e*15 + t,
+//      element order e -> (r = e % m, c = (e/m + r) % m)   ("diagonal walk")
+//   6 diagonal tiles, lower triangle, element e of tile d at 15 m^2 + e*6 + d,
+//      element order: by sub-diagonal d' = r - c, then r.
+// total = 15 m^2 + 6 m(m+1)/2 = w(w+1)/2; padded to an even count (16-B bulk copies).
+
+__host__ __device__ constexpr int tri_count(int m) { return m * (m + 1) / 2; }
+__host__ __device__ constexpr int packed_len(int m) { return 15 * m * m + 6 * tri_count(m); }
+__host__ __device__ constexpr int packed_stride(int m) { return (packed_len(m) + 1) & ~1; }
+
+__host__ __device__ constexpr int off_I(int t) {
+    return t < 1 ? 1 : t < 3 ? 2 : t < 6 ? 3 : t < 10 ? 4 : 5;
+}
+__host__ __device__ constexpr int off_K(int t) { return t - off_I(t) * (off_I(t) - 1) / 2; }
+__host__ __device__ constexpr int off_tile(int I, int K) { return I * (I - 1) / 2 + K; }
+
+__host__ __device__ constexpr int diag_r(int m, int e) {
+    int d = 0;
+    while (e >= m - d) {
+        e -= m - d;
+        ++d;
+    }
+    return d + e;
+}
+__host__ __device__ constexpr int diag_c(int m, int e) {
+    int d = 0;
+    while (e >= m - d) {
+        e -= m - d;
+        ++d;
+    }
+    return e;
+}
+
+// position of dense element (row, col) of a symmetric w x w block in the packed layout
+__host__ __device__ inline int packed_pos(int m, int row, int col) {
+    if (row < col) {
+        int t = row;
+        row = col;
+        col = t;
+    }
+    int I = row / m, K = col / m, r = row % m, c = col % m;
+    if (I != K) {
+        int t = off_tile(I, K);
+        int q = (c - r + m) % m;  // e/m
+        int e = q * m + r;
+        return e * 15 + t;
+    }
+    // diagonal tile I, lower element (r >= c): sub-diagonal d = r - c
+    int d = r - c;
+    int e = 0;
+    for (int dd = 0; dd < d; ++dd) e += m - dd;
+    e += c;
+    return 15 * m * m + e * 6 + I;
+}
+
+// y = A x for one packed symmetric block, computed by one warp.
+// blk, x, part, y in shared memory; x must be visible to the warp on entry.
+template <int M>
+__device__ __forceinline__ void sym_matvec(const double* __restrict__ blk, const double* x,
+                                           double* part, double* y, int lane) {
+    constexpr int W = 6 * M;
+    if (lane < 15) {
+        const int I = off_I(lane), K = off_K(lane);
+        double xk[M], xi[M], P[M], Q[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            xk[i] = x[K * M + i];
+            xi[i] = x[I * M + i];
+            P[i] = 0.0;
+            Q[i] = 0.0;
+        }
+        const double* b = blk + lane;
+#pragma unroll
+        for (int e = 0; e < M * M; ++e) {
+            const int r = e % M, c = (e / M + r) % M;
+            const double a = b[e * 15];
+            P[r] = fma(a, xk[c], P[r]);
+            Q[c] = fma(a, xi[r], Q[c]);
+        }
+        double* pp = part + lane * 2 * M;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            pp[i] = P[i];
+            pp[M + i] = Q[i];
+        }
+    }
+    if (lane < 6) {
+        const int I = lane;
+        double xi[M], P[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            xi[i] = x[I * M + i];
+            P[i] = 0.0;
+        }
+        const double* b = blk + 15 * M * M + lane;
+#pragma unroll
+        for (int d = 0; d < M; ++d) {
+#pragma unroll
+            for (int r = d; r < M; ++r) {
+                const int c = r - d;
+                const int e = d * M - d * (d - 1) / 2 + c;  // elements before sub-diagonal d, then c
+                const double a = b[e * 6];
+                P[r] = fma(a, xi[c], P[r]);
+                if (d != 0) P[c] = fma(a, xi[r], P[c]);
+            }
+        }
+        double* pp = part + (15 + lane) * 2 * M;
+#pragma unroll
+        for (int i = 0; i < M; ++i) pp[i] = P[i];
+    }
+    __syncwarp();
+    for (int i = lane; i < W; i += 32) {
+        const int R = i / M, r = i % M;
+        double s = 0.0;
+        for (int K = 0; K < R; ++K) s += part[off_tile(R, K) * 2 * M + r];
+        s += part[(15 + R) * 2 * M + r];
+        for (int I = R + 1; I < 6; ++I) s += part[off_tile(I, R) * 2 * M + M + r];
+        y[i] = s;
+    }
+    __syncwarp();
+}
+
+struct StepParams {
+    int n_sub, BS, n_steps, mode, cur, record_every, n_probe, ftab_stride;
+    int evict_first;
+    double dt, dt2, half_dt2;
+    const double* coef;
+    const long long* seq;
+    const int* seq_ptr;
+    const int* wsub;
+    const int* wsub_ptr;
+    const int* cta_sub_ptr;
+    const int* layers;
+    const long long* soff;
+    const int* nbr;
+    const int* mass_idx;
+    const double* mass;
+    double* U0;
+    double* U1;
+    const double* V0;
+    double* acc1;
+    double* fbuf;  // [2][n_sub*W]
+    const int* src_ptr;
+    const int* src_ids;
+    const double* src_vec;
+    const long long* src_voff;
+    const double* ftab;
+    const int* prb_ptr;
+    const int* prb_ids;
+    const int* prb_tap;
+    const double* prb_w;
+    const long long* prb_woff;
+    double* rows;
+    double* sub_norm;
+    double* norm_part;  // [n_steps][gridDim.x]
+    unsigned int* bar;
+};
+
+__device__ __forceinline__ double leap(int mode, double uc, double uo, double v, double tot,
+                                       double dt, double dt2, double half) {
+    // stepper.py:373   2u - u_prev + (dt*dt) * total        (no FMA contraction)
+    // stepper.py:353   u - dt*v + ((0.5*dt)*dt) * total
+    if (mode == 0) return __dadd_rn(__dsub_rn(__dmul_rn(2.0, uc), uo), __dmul_rn(dt2, tot));
+    if (mode == 2) return tot;
+    return __dadd_rn(__dsub_rn(uc, __dmul_rn(dt, v)), __dmul_rn(half, tot));
+}
+
+// total = acc + sum_src vec * f(t)   (stepper.py:313-321 superposes in list order)
+__device__ __forceinline__ double add_force(const StepParams& p, int s, long long idx, int k,
+                                            double acc) {
+    const int a = p.src_ptr[s], b = p.src_ptr[s + 1];
+    if (a == b) return acc;
+    double f = 0.0;
+    for (int q = a; q < b; ++q) {
+        const int src = p.src_ids[q];
+        const double term = __dmul_rn(p.src_vec[p.src_voff[src] + idx], p.ftab[(long long)src * p.ftab_stride + k]);
+        f = (q == a) ? term : __dadd_rn(f, term);
+    }
+    return __dadd_rn(acc, f);
+}
+
+template <int M, int NW, int NS>
+__global__ void __launch_bounds__(NW * 32, 1) k_step(const StepParams p) {
+    constexpr int W = 6 * M;
+    constexpr int WK = 4 * W + 21 * 2 * M;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * NW + warp;
+    double* stages = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)NW * NS * p.BS);
+    double* wk = reinterpret_cast<double*>(bars + NW * NS) + (size_t)warp * WK;
+    double* xs = wk;
+    double* ys = xs + W;
+    double* fs = ys + W;
+    double* fp = fs + W;
+    double* part = fp + W;
+    double* my_stage = stages + (size_t)warp * NS * p.BS;
+    uint64_t* my_bar = bars + warp * NS;
+
+    if (lane == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&my_bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    const uint64_t pol = p.evict_first ? l2_policy_evict_first() : l2_policy_evict_last();
+    const int seq0 = p.seq_ptr[gw];
+    const int seqlen = p.seq_ptr[gw + 1] - seq0;
+    const int n_iter = (p.mode == 0) ? p.n_steps : 1;  // init / accel: one pass
+    const long long total = (long long)seqlen * n_iter;
+    const uint32_t bytes = (uint32_t)p.BS * 8u;
+    long long issued = 0, consumed = 0;
+
+    auto issue = [&]() {
+        if (lane == 0) {
+            while (issued < total && issued < consumed + NS) {
+                const int st = (int)(issued % NS);
+                const long long off = p.seq[seq0 + (int)(issued % seqlen)];
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&my_bar[st], bytes);
+                bulk_g2s(my_stage + (size_t)st * p.BS, p.coef + off, bytes, &my_bar[st], pol);
+                ++issued;
+            }
+        }
+    };
+    auto acquire = [&]() -> const double* {
+        const int st = (int)(consumed % NS);
+        mbar_wait(&my_bar[st], (uint32_t)((consumed / NS) & 1));
+        return my_stage + (size_t)st * p.BS;
+    };
+    auto release = [&]() {
+        __syncwarp();
+        ++consumed;
+        issue();
+    };
+    issue();
+
+    const int ws0 = p.wsub_ptr[gw], ws1 = p.wsub_ptr[gw + 1];
+    const double dt = p.dt, dt2 = p.dt2, half = p.half_dt2;
+
+    for (int k = 1; k <= n_iter; ++k) {
+        const int par = k & 1;
+        const int cb = p.cur ^ ((k - 1) & 1);
+        const double* Uc = cb ? p.U1 : p.U0;
+        double* Un = cb ? p.U0 : p.U1;
+        double* fb = p.fbuf + (size_t)par * p.n_sub * W;
+        const int kk = k - 1;  // profile column
+
+        // ---------------- phase A: layer-1 flux and Gamma-hat_1 flux -------------
+        for (int q = ws0; q < ws1; ++q) {
+            const int s = p.wsub[q];
+            const int L = p.layers[s];
+            const long long base = p.soff[s];
+            for (int i = lane; i < W; i += 32)
+                xs[i] = (L > 1 ? Uc[base + W + i] : 0.0) - Uc[base + i];
+            __syncwarp();
+            sym_matvec<M>(acquire(), xs, part, ys, lane);
+            release();
+            for (int i = lane; i < W; i += 32) fb[(size_t)s * W + i] = ys[i];
+            sym_matvec<M>(acquire(), ys, part, xs, lane);
+            release();
+            for (int i = lane; i < W; i += 32) p.acc1[(size_t)s * W + i] = xs[i];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (p.mode == 0 && k > 1) {
+                double t = 0.0;
+                for (int s = p.cta_sub_ptr[blockIdx.x]; s < p.cta_sub_ptr[blockIdx.x + 1]; ++s)
+                    t += p.sub_norm[s];
+                p.norm_part[(size_t)(k - 2) * gridDim.x + blockIdx.x] = t;
+            }
+            grid_arrive(p.bar);
+        }
+
+        // ---------------- phase B: interior layers (independent of neighbours) ---
+        for (int q = ws0; q < ws1; ++q) {
+            const int s = p.wsub[q];
+            const int L = p.layers[s];
+            const long long base = p.soff[s];
+            for (int i = lane; i < W; i += 32) fp[i] = fb[(size_t)s * W + i];
+            double* f_cur = fs;
+            double* f_prv = fp;
+            for (int j = 1; j < L; ++j) {
+                const long long lb = base + (long long)j * W;
+                for (int i = lane; i < W; i += 32)
+                    xs[i] = (j + 1 < L ? Uc[lb + W + i] : 0.0) - Uc[lb + i];
+                __syncwarp();
+                sym_matvec<M>(acquire(), xs, part, f_cur, lane);
+                release();
+                for (int i = lane; i < W; i += 32) xs[i] = f_cur[i] - f_prv[i];
+                __syncwarp();
+                sym_matvec<M>(acquire(), xs, part, ys, lane);
+                release();
+                for (int i = lane; i < W; i += 32) {
+                    const long long g = lb + i;
+                    const double tot = add_force(p, s, (long long)j * W + i, kk, ys[i]);
+                    const double v = (p.mode == 1 && p.V0) ? p.V0[g] : 0.0;
+                    Un[g] = leap(p.mode, Uc[g], Un[g], v, tot, dt, dt2, half);
+                }
+                double* t = f_cur;
+                f_cur = f_prv;
+                f_prv = t;
+            }
+        }
+
+        // ---------------- wait for every CTA's phase A of this step ---------------
+        if (lane == 0) grid_wait(p.bar, (unsigned int)k * gridDim.x);
+        __syncwarp();
+
+        // ---------------- phase C: face coupling, layer-1 update, norms, probes ---
+        for (int q = ws0; q < ws1; ++q) {
+            const int s = p.wsub[q];
+            const int L = p.layers[s];
+            const long long base = p.soff[s];
+            for (int i = lane; i < W; i += 32) {
+                const int f = i / M, r = i % M;
+                const int nb = p.nbr[s * 6 + f];
+                double a;
+                if (nb >= 0) {
+                    const double* mx = p.mass + (size_t)p.mass_idx[s * 6 + f] * M * M + r * M;
+                    const double* own = fb + (size_t)s * W + f * M;
+                    const double* oth = fb + (size_t)nb * W + (f ^ 1) * M;
+                    a = 0.0;
+#pragma unroll
+                    for (int c = 0; c < M; ++c) a = fma(mx[c], __dadd_rn(own[c], oth[c]), a);
+                } else {
+                    a = p.acc1[(size_t)s * W + i];
+                }
+                const double tot = add_force(p, s, i, kk, a);
+                const long long g = base + i;
+                const double v = (p.mode == 1 && p.V0) ? p.V0[g] : 0.0;
+                Un[g] = leap(p.mode, Uc[g], Un[g], v, tot, dt, dt2, half);
+            }
+            const int K = L * W;
+            __syncwarp();
+            if (p.mode == 0) {
+                double nr = 0.0;
+                for (int i = lane; i < K; i += 32) {
+                    const double u = Un[base + i];
+                    nr = fma(u, u, nr);
+                }
+                nr = warp_sum(nr);
+                if (lane == 0) p.sub_norm[s] = nr;
+            }
+            const bool rec = (p.mode == 1) || (p.mode == 0 && k % p.record_every == 0);
+            if (rec && p.rows && p.prb_ptr[s] < p.prb_ptr[s + 1]) {
+                __syncwarp();
+                const double* U = (p.mode == 1) ? Uc : Un;
+                const long long row = (p.mode == 1) ? 0 : (k / p.record_every - 1);
+                for (int pq = p.prb_ptr[s]; pq < p.prb_ptr[s + 1]; ++pq) {
+                    const int pid = p.prb_ids[pq];
+                    const int tap = p.prb_tap[pid];
+                    double val;
+                    if (tap >= 0) {
+                        val = U[base + tap];
+                    } else {
+                        const double* wv = p.prb_w + p.prb_woff[pid];
+                        double acc = 0.0;
+                        for (int i = lane; i < K; i += 32) acc = fma(wv[i], U[base + i], acc);
+                        val = warp_sum(acc);
+                    }
+                    if (lane == 0) p.rows[row * p.n_probe + pid] = val;
+                }
+            }
+        }
+    }
+    if (p.mode == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int s = p.cta_sub_ptr[blockIdx.x]; s < p.cta_sub_ptr[blockIdx.x + 1]; ++s)
+                t += p.sub_norm[s];
+            p.norm_part[(size_t)(n_iter - 1) * gridDim.x + blockIdx.x] = t;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// setup kernels
+
+// dense (L*w*w per subdomain) -> packed blocks [Gamma_j, Gamma-hat_j] per layer
+__global__ void k_pack(const double* __restrict__ gam, const double* __restrict__ hat,
+                       const long long* __restrict__ blk_dense_off, int n_blocks, int m, int BS,
+                       double* __restrict__ out, double* __restrict__ asym) {
+    const int w = 6 * m;
+    const int b = blockIdx.x;  // packed block index = 2*(global layer index) + kind
+    if (b >= n_blocks) return;
+    const int kind = b & 1;
+    const double* A = (kind ? hat : gam) + blk_dense_off[b >> 1];
+    double* o = out + (size_t)b * BS;
+    double amax = 0.0, dmax = 0.0;
+    for (int row = threadIdx.x; row < w; row += blockDim.x) {
+        for (int col = 0; col <= row; ++col) {
+            const double v = A[row * w + col];
+            const double vt = A[col * w + row];
+            o[packed_pos(m, row, col)] = v;
+            amax = fmax(amax, fabs(v));
+            dmax = fmax(dmax, fabs(v - vt));
+        }
+    }
+    if (threadIdx.x == 0 && (packed_len(m) & 1)) o[BS - 1] = 0.0;
+    __shared__ double s_a[256], s_d[256];
+    s_a[threadIdx.x] = amax;
+    s_d[threadIdx.x] = dmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < blockDim.x; ++i) {
+            amax = fmax(amax, s_a[i]);
+            dmax = fmax(dmax, s_d[i]);
+        }
+        asym[b] = amax > 0 ? dmax / amax : 0.0;
+    }
+}
+
+// |Gamma-hat_1 - I|_F per subdomain (stepper.py:182-186)
+__global__ void k_hat1_dev(const double* __restrict__ hat, const long long* __restrict__ first_blk,
+                           int n_sub, int w, double* __restrict__ out) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_sub) return;
+    const double* A = hat + first_blk[s];
+    double acc = 0.0;
+    for (int i = 0; i < w; ++i)
+        for (int j = 0; j < w; ++j) {
+            const double d = A[i * w + j] - (i == j ? 1.0 : 0.0);
+            acc += d * d;
+        }
+    out[s] = sqrt(acc);
+}
+
+// interface mass = ha (ha + hb)^-1 hb, symmetrised (stepper.py:204-210); one thread per interface.
+#define SFW_MAXM 25
+__global__ void k_mass(const double* __restrict__ hat, const long long* __restrict__ first_blk,
+                       const int* __restrict__ iface, int n_iface, int m, double* __restrict__ mass,
+                       int* __restrict__ status) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_iface) return;
+    const int w = 6 * m;
+    const int sa = iface[4 * q], fa = iface[4 * q + 1], sb = iface[4 * q + 2], fb = iface[4 * q + 3];
+    const double* A = hat + first_blk[sa];
+    const double* B = hat + first_blk[sb];
+    double S[SFW_MAXM * SFW_MAXM], X[SFW_MAXM * SFW_MAXM];
+    int piv[SFW_MAXM];
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+            const double ha = A[(fa * m + i) * w + fa * m + j];
+            const double hb = B[(fb * m + i) * w + fb * m + j];
+            S[i * m + j] = ha + hb;
+            X[i * m + j] = hb;
+        }
+    // LU with partial pivoting (LAPACK getrf semantics), solve S X = hb
+    for (int c = 0; c < m; ++c) {
+        int pr = c;
+        double best = fabs(S[c * m + c]);
+        for (int r = c + 1; r < m; ++r)
+            if (fabs(S[r * m + c]) > best) {
+                best = fabs(S[r * m + c]);
+                pr = r;
+            }
+        piv[c] = pr;
+        if (best == 0.0) {
+            status[q] = 1;
+            return;
+        }
+        if (pr != c) {
+            for (int j = 0; j < m; ++j) {
+                double t = S[c * m + j];
+                S[c * m + j] = S[pr * m + j];
+                S[pr * m + j] = t;
+                t = X[c * m + j];
+                X[c * m + j] = X[pr * m + j];
+                X[pr * m + j] = t;
+            }
+        }
+        for (int r = c + 1; r < m; ++r) {
+            const double l = S[r * m + c] / S[c * m + c];
+            S[r * m + c] = l;
+            for (int j = c + 1; j < m; ++j) S[r * m + j] -= l * S[c * m + j];
+            for (int j = 0; j < m; ++j) X[r * m + j] -= l * X[c * m + j];
+        }
+    }
+    for (int c = m - 1; c >= 0; --c)
+        for (int j = 0; j < m; ++j) {
+            double v = X[c * m + j];
+            for (int k = c + 1; k < m; ++k) v -= S[c * m + k] * X[k * m + j];
+            X[c * m + j] = v / S[c * m + c];
+        }
+    double* out = mass + (size_t)q * m * m;
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+            double v = 0.0;
+            for (int k = 0; k < m; ++k) v += A[(fa * m + i) * w + fa * m + k] * X[k * m + j];
+            S[i * m + j] = v;
+        }
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) out[i * m + j] = 0.5 * (S[i * m + j] + S[j * m + i]);
+    status[q] = 0;
+}
+
+// fixed-order sum of the per-CTA norm partials -> |U_k|_2
+__global__ void k_norms(const double* __restrict__ part, int n_steps, int n_cta, double* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_steps) return;
+    double t = 0.0;
+    for (int c = 0; c < n_cta; ++c) t += part[(size_t)k * n_cta + c];
+    out[k] = sqrt(t);
+}
+
+
+// discrete energy (stepper.py:419-449): one CTA per (subdomain, layer), LU solve of G_j in smem.
+__global__ void k_energy(const double* __restrict__ Uc, const double* __restrict__ Up,
+                         const double* __restrict__ G, const double* __restrict__ gam,
+                         const int* __restrict__ lay_sub, const int* __restrict__ lay_j,
+                         const long long* __restrict__ soff, const int* __restrict__ layers,
+                         int w, double dt, double* __restrict__ out) {
+    extern __shared__ double sh[];
+    double* A = sh;            // w*w
+    double* y = A + w * w;     // w
+    double* da = y + w;        // w
+    double* db = da + w;       // w
+    const int q = blockIdx.x;
+    const int s = lay_sub[q], j = lay_j[q], L = layers[s];
+    const long long base = soff[s] + (long long)j * w;
+    const double* Gj = G + (size_t)q * w * w;
+    const double* Cj = gam + (size_t)q * w * w;
+    for (int i = threadIdx.x; i < w * w; i += blockDim.x) A[i] = Gj[i];
+    for (int i = threadIdx.x; i < w; i += blockDim.x) {
+        y[i] = (Uc[base + i] - Up[base + i]) / dt;
+        if (j + 1 < L) {
+            da[i] = Uc[base + w + i] - Uc[base + i];
+            db[i] = Up[base + w + i] - Up[base + i];
+        } else {
+            da[i] = -Uc[base + i];
+            db[i] = -Up[base + i];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // Gauss elimination with partial pivoting on [G | y]
+        for (int c = 0; c < w; ++c) {
+            int pr = c;
+            double best = fabs(A[c * w + c]);
+            for (int r = c + 1; r < w; ++r)
+                if (fabs(A[r * w + c]) > best) { best = fabs(A[r * w + c]); pr = r; }
+            if (pr != c) {
+                for (int k = 0; k < w; ++k) { double t = A[c * w + k]; A[c * w + k] = A[pr * w + k]; A[pr * w + k] = t; }
+                double t = y[c]; y[c] = y[pr]; y[pr] = t;
+            }
+            for (int r = c + 1; r < w; ++r) {
+                const double l = A[r * w + c] / A[c * w + c];
+                for (int k = c + 1; k < w; ++k) A[r * w + k] -= l * A[c * w + k];
+                y[r] -= l * y[c];
+            }
+        }
+        for (int c = w - 1; c >= 0; --c) {
+            double v = y[c];
+            for (int k = c + 1; k < w; ++k) v -= A[c * w + k] * y[k];
+            y[c] = v / A[c * w + c];
+        }
+        double kin = 0.0, pot = 0.0;
+        for (int i = 0; i < w; ++i) kin += y[i] * y[i];
+        for (int i = 0; i < w; ++i) {
+            double t = 0.0;
+            for (int k = 0; k < w; ++k) t += Cj[i * w + k] * db[k];
+            pot += da[i] * t;
+        }
+        out[q] = 0.5 * kin + 0.5 * pot;
+    }
+}
+
+__global__ void k_sum_fixed(const double* __restrict__ v, int n, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < n; ++i) t += v[i];
+        *out = t;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct KernelCfg {
+    int nw, ns;
+};
+
+static KernelCfg cfg_for(int m) {
+    switch (m) {
+        case 1:
+        case 4:
+        case 9:
+            return {4, 4};
+        case 16:
+            return {2, 3};
+        case 25:
+            return {1, 2};
+        default:
+            return {0, 0};
+    }
+}
+
+template <typename T>
+static int dalloc(T** p, size_t n, char* errbuf, int errlen) {
+    *p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+    if (e != cudaSuccess)
+        return fail(SFW_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e), errbuf, errlen);
+    return 0;
+}
+
+template <typename T>
+static int upload(T** p, const std::vector<T>& v, char* errbuf, int errlen) {
+    int rc = dalloc(p, v.size(), errbuf, errlen);
+    if (rc) return rc;
+    if (!v.empty()) SFW_CUDA_TRY(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return 0;
+}
+
+}  // namespace sfw
+
+using namespace sfw;
+
+struct sfw_stepper {
+    int n_sub = 0, m = 0, W = 0, BS = 0, n_src = 0, n_probe = 0, n_iface = 0;
+    int grid = 0, nw = 0, ns = 0, smem = 0, cur = 0;
+    long long state_len = 0, n_blocks = 0;
+    double dt = 0;
+    std::vector<int> layers;
+    std::vector<long long> soff, src_len, prb_len;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double* coef = nullptr;
+    long long* seq = nullptr;
+    int *seq_ptr = nullptr, *wsub = nullptr, *wsub_ptr = nullptr, *cta_sub_ptr = nullptr;
+    int *d_layers = nullptr, *nbr = nullptr, *mass_idx = nullptr;
+    long long* d_soff = nullptr;
+    double* mass = nullptr;
+    double *U[2] = {nullptr, nullptr}, *S[2] = {nullptr, nullptr}, *V0 = nullptr, *acc1 = nullptr, *fbuf = nullptr;
+    int *src_ptr = nullptr, *src_ids = nullptr;
+    double* src_vec = nullptr;
+    long long* src_voff = nullptr;
+    double* ftab = nullptr;
+    long long ftab_cap = 0;
+    int *prb_ptr = nullptr, *prb_ids = nullptr, *prb_tap = nullptr;
+    double* prb_w = nullptr;
+    long long* prb_woff = nullptr;
+    double* rows = nullptr;
+    long long rows_cap = 0;
+    double *sub_norm = nullptr, *norm_part = nullptr, *norms = nullptr;
+    long long norm_cap = 0;
+    unsigned int* bar = nullptr;
+    double* scales = nullptr;  // dense G_j (energy), may be null
+    double* gam_dense = nullptr;  // dense Gamma_j (energy)
+    bool evict_first = true;
+};
+
+static void free_all(sfw_stepper* h) {
+    void* ptrs[] = {h->coef, h->S[0], h->S[1], h->seq, h->seq_ptr, h->wsub, h->wsub_ptr, h->cta_sub_ptr, h->d_layers,
+                    h->nbr, h->mass_idx, h->d_soff, h->mass, h->U[0], h->U[1], h->V0, h->acc1,
+                    h->fbuf, h->src_ptr, h->src_ids, h->src_vec, h->src_voff, h->ftab, h->prb_ptr,
+                    h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
+                    h->norm_part, h->norms, h->bar, h->scales, h->gam_dense};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+}
+
+static const void* step_kernel_ptr(int m) {
+    switch (m) {
+        case 1: return (const void*)k_step<1, 4, 4>;
+        case 4: return (const void*)k_step<4, 4, 4>;
+        case 9: return (const void*)k_step<9, 4, 4>;
+        case 16: return (const void*)k_step<16, 2, 3>;
+        case 25: return (const void*)k_step<25, 1, 2>;
+    }
+    return nullptr;
+}
+
+
+static int set_probes(sfw_stepper* h, int n_probe, const int* probe_sub, const double* probe_w, char* errbuf,
+                      int errlen) {
+    const int n = h->n_sub;
+    int rc = 0;
+    void* olds[] = {h->prb_ptr, h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff};
+    for (void* q : olds)
+        if (q) cudaFree(q);
+    h->prb_ptr = h->prb_ids = h->prb_tap = nullptr;
+    h->prb_w = nullptr;
+    h->prb_woff = nullptr;
+    h->n_probe = n_probe;
+    std::vector<int> prb_ptr(n + 1, 0), prb_ids(n_probe), prb_tap(std::max(1, n_probe), -1);
+    std::vector<long long> prb_woff(std::max(1, n_probe));
+    long long ptot = 0;
+    for (int i = 0; i < n_probe; ++i) {
+        const int s = probe_sub[i];
+        if (s < 0 || s >= n) return fail(SFW_ECONFIG, "probe subdomain has no model", errbuf, errlen);
+        const long long K = h->soff[s + 1] - h->soff[s];
+        prb_woff[i] = ptot;
+        int nz = 0, at = -1;
+        bool unit = true;
+        for (long long j = 0; j < K; ++j) {
+            const double v = probe_w[ptot + j];
+            if (v != 0.0) {
+                ++nz;
+                at = (int)j;
+                if (v != 1.0) unit = false;
+            }
+        }
+        if (unit && nz == 1) prb_tap[i] = at;  // weights @ u == u[at] bitwise
+        ptot += K;
+        prb_ptr[s + 1]++;
+    }
+    for (int s = 0; s < n; ++s) prb_ptr[s + 1] += prb_ptr[s];
+    {
+        std::vector<int> fill(prb_ptr.begin(), prb_ptr.end() - 1);
+        for (int i = 0; i < n_probe; ++i) prb_ids[fill[probe_sub[i]]++] = i;
+    }
+    std::vector<double> pw(n_probe ? probe_w : nullptr, n_probe ? probe_w + ptot : nullptr);
+    if ((rc = upload(&h->prb_ptr, prb_ptr, errbuf, errlen))) return rc;
+    if ((rc = upload(&h->prb_ids, prb_ids, errbuf, errlen))) return rc;
+    if ((rc = upload(&h->prb_tap, prb_tap, errbuf, errlen))) return rc;
+    if ((rc = upload(&h->prb_woff, prb_woff, errbuf, errlen))) return rc;
+    if ((rc = upload(&h->prb_w, pw, errbuf, errlen))) return rc;
+    return 0;
+}
+
+extern "C" int sfw_step_set_probes(sfw_stepper* h, int n_probe, const int* probe_sub, const double* probe_w,
+                                   char* errbuf, int errlen) {
+    return set_probes(h, n_probe, probe_sub, probe_w, errbuf, errlen);
+}
+
+extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* errbuf, int errlen) {
+    *out = nullptr;
+    if (!d || d->n_sub <= 0) return fail(SFW_ECONFIG, "no subdomains", errbuf, errlen);
+    if (!(d->dt > 0)) return fail(SFW_ECONFIG, "time step must be positive", errbuf, errlen);
+    KernelCfg kc = cfg_for(d->m);
+    if (!kc.nw)
+        return fail(SFW_ECONFIG, "modes per face must be one of 1, 4, 9, 16, 25 for the sm_100a stepper",
+                    errbuf, errlen);
+    auto* h = new sfw_stepper();
+    h->n_sub = d->n_sub;
+    h->m = d->m;
+    h->W = 6 * d->m;
+    h->BS = packed_stride(d->m);
+    h->dt = d->dt;
+    h->nw = kc.nw;
+    h->ns = kc.ns;
+    const int W = h->W, n = h->n_sub, m = h->m;
+    int rc = 0;
+#define TRY(x)              \
+    do {                    \
+        rc = (x);           \
+        if (rc) goto error; \
+    } while (0)
+    {
+        h->layers.assign(d->layers, d->layers + n);
+        h->soff.resize(n + 1);
+        h->soff[0] = 0;
+        long long nblk = 0;
+        std::vector<long long> first_blk(n), dense_off;
+        for (int s = 0; s < n; ++s) {
+            if (h->layers[s] < 1) {
+                rc = fail(SFW_ECONFIG, "every model needs at least one layer", errbuf, errlen);
+                goto error;
+            }
+            h->soff[s + 1] = h->soff[s] + (long long)h->layers[s] * W;
+            first_blk[s] = nblk * W * W;
+            for (int j = 0; j < h->layers[s]; ++j) dense_off.push_back((nblk + j) * W * W);
+            nblk += h->layers[s];
+        }
+        h->state_len = h->soff[n];
+        h->n_blocks = 2 * nblk;
+        cudaError_t ce = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+        if (ce != cudaSuccess) {
+            rc = fail(SFW_ECUDA, std::string("stream: ") + cudaGetErrorString(ce), errbuf, errlen);
+            goto error;
+        }
+        cudaEventCreate(&h->ev0);
+        cudaEventCreate(&h->ev1);
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+
+        // ---- coefficients: upload dense, pack on device, check symmetry -----
+        const size_t dense_n = (size_t)nblk * W * W;
+        double *g_dev = nullptr, *h_dev = nullptr;
+        bool own_dense = false;
+        if (d->coef_on_device) {
+            g_dev = const_cast<double*>(d->gammas);
+            h_dev = const_cast<double*>(d->gamma_hats);
+        } else {
+            own_dense = true;
+            TRY(dalloc(&g_dev, dense_n, errbuf, errlen));
+            TRY(dalloc(&h_dev, dense_n, errbuf, errlen));
+            SFW_CUDA_TRY(cudaMemcpy(g_dev, d->gammas, dense_n * 8, cudaMemcpyHostToDevice));
+            SFW_CUDA_TRY(cudaMemcpy(h_dev, d->gamma_hats, dense_n * 8, cudaMemcpyHostToDevice));
+        }
+        TRY(dalloc(&h->coef, (size_t)h->n_blocks * h->BS, errbuf, errlen));
+        long long* d_dense_off = nullptr;
+        double* d_asym = nullptr;
+        TRY(upload(&d_dense_off, dense_off, errbuf, errlen));
+        TRY(dalloc(&d_asym, h->n_blocks, errbuf, errlen));
+        k_pack<<<(unsigned)h->n_blocks, 128, 0, h->stream>>>(g_dev, h_dev, d_dense_off, (int)h->n_blocks, m,
+                                                            h->BS, h->coef, d_asym);
+        // Gamma-hat_1 = I check and interface masses
+        long long* d_first = nullptr;
+        double* d_dev = nullptr;
+        TRY(upload(&d_first, first_blk, errbuf, errlen));
+        TRY(dalloc(&d_dev, n, errbuf, errlen));
+        k_hat1_dev<<<(n + 127) / 128, 128, 0, h->stream>>>(h_dev, d_first, n, W, d_dev);
+
+        std::vector<int> nbr(d->neighbors, d->neighbors + 6 * n), mass_idx(6 * n, -1), iface;
+        for (int s = 0; s < n; ++s)
+            for (int f = 0; f < 6; ++f) {
+                const int t = nbr[6 * s + f];
+                if (t < 0) continue;
+                if (t >= n || nbr[6 * t + (f ^ 1)] != s) {
+                    rc = fail(SFW_EPROTOCOL, "inconsistent neighbour tables", errbuf, errlen);
+                    goto error;
+                }
+                if (s < t) {
+                    mass_idx[6 * s + f] = (int)(iface.size() / 4);
+                    mass_idx[6 * t + (f ^ 1)] = (int)(iface.size() / 4);
+                    iface.insert(iface.end(), {s, f, t, f ^ 1});
+                }
+            }
+        h->n_iface = (int)(iface.size() / 4);
+        int* d_iface = nullptr;
+        int* d_status = nullptr;
+        TRY(upload(&d_iface, iface, errbuf, errlen));
+        TRY(dalloc(&d_status, std::max(1, h->n_iface), errbuf, errlen));
+        TRY(dalloc(&h->mass, (size_t)std::max(1, h->n_iface) * m * m, errbuf, errlen));
+        if (h->n_iface)
+            k_mass<<<(h->n_iface + 63) / 64, 64, 0, h->stream>>>(h_dev, d_first, d_iface, h->n_iface, m,
+                                                                 h->mass, d_status);
+        SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        SFW_CUDA_TRY(cudaGetLastError());
+        {
+            std::vector<double> asym(h->n_blocks), dev(n);
+            std::vector<int> st(std::max(1, h->n_iface));
+            cudaMemcpy(asym.data(), d_asym, asym.size() * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(dev.data(), d_dev, dev.size() * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(st.data(), d_status, st.size() * 4, cudaMemcpyDeviceToHost);
+            cudaFree(d_dense_off);
+            cudaFree(d_asym);
+            cudaFree(d_first);
+            cudaFree(d_dev);
+            cudaFree(d_iface);
+            cudaFree(d_status);
+            for (int s = 0; s < n; ++s)
+                if (!(dev[s] <= 1e-8)) {
+                    rc = fail(SFW_ENUMERICAL,
+                              "subdomain " + std::to_string(s) +
+                                  ": first inverse-mass block is not the identity; the face updates "
+                                  "would couple across faces",
+                              errbuf, errlen);
+                    goto error;
+                }
+            for (long long b = 0; b < h->n_blocks; ++b)
+                if (!(asym[b] <= 1e-12)) {
+                    rc = fail(SFW_ECONFIG, "chain block " + std::to_string(b) +
+                                               " is not symmetric; the packed stepper needs symmetric "
+                                               "Gamma / Gamma-hat",
+                              errbuf, errlen);
+                    goto error;
+                }
+            for (int q = 0; q < h->n_iface; ++q)
+                if (st[q]) {
+                    rc = fail(SFW_ENUMERICAL, "singular interface mass system", errbuf, errlen);
+                    goto error;
+                }
+        }
+        if (d->scales) {
+            TRY(dalloc(&h->scales, dense_n, errbuf, errlen));
+            TRY(dalloc(&h->gam_dense, dense_n, errbuf, errlen));
+            SFW_CUDA_TRY(cudaMemcpy(h->scales, d->scales, dense_n * 8,
+                                    d->coef_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+            SFW_CUDA_TRY(cudaMemcpy(h->gam_dense, g_dev, dense_n * 8, cudaMemcpyDeviceToDevice));
+        }
+        if (own_dense) {
+            cudaFree(g_dev);
+            cudaFree(h_dev);
+        }
+
+        // ---- work decomposition: CTA = contiguous subdomain range, warps round-robin ----
+        h->grid = std::min(nsm > 0 ? nsm : 148, n);
+        const int G = h->grid, NW = h->nw;
+        std::vector<int> cta_ptr(G + 1), wsub_ptr(G * NW + 1), wsub, seq_ptr(G * NW + 1);
+        std::vector<long long> seq;
+        std::vector<long long> blk0(n);  // first packed block of subdomain s
+        {
+            long long b = 0;
+            for (int s = 0; s < n; ++s) {
+                blk0[s] = b;
+                b += 2 * h->layers[s];
+            }
+        }
+        for (int b = 0; b <= G; ++b) cta_ptr[b] = (int)((long long)b * n / G);
+        for (int b = 0; b < G; ++b)
+            for (int w = 0; w < NW; ++w) {
+                const int gw = b * NW + w;
+                wsub_ptr[gw] = (int)wsub.size();
+                seq_ptr[gw] = (int)seq.size();
+                std::vector<int> mine;
+                for (int s = cta_ptr[b] + w; s < cta_ptr[b + 1]; s += NW) mine.push_back(s);
+                for (int s : mine) wsub.push_back(s);
+                for (int s : mine) {  // phase A blocks
+                    seq.push_back((blk0[s] + 0) * h->BS);
+                    seq.push_back((blk0[s] + 1) * h->BS);
+                }
+                for (int s : mine)  // phase B blocks
+                    for (int j = 1; j < h->layers[s]; ++j) {
+                        seq.push_back((blk0[s] + 2 * j) * h->BS);
+                        seq.push_back((blk0[s] + 2 * j + 1) * h->BS);
+                    }
+            }
+        wsub_ptr[G * NW] = (int)wsub.size();
+        seq_ptr[G * NW] = (int)seq.size();
+        TRY(upload(&h->cta_sub_ptr, cta_ptr, errbuf, errlen));
+        TRY(upload(&h->wsub_ptr, wsub_ptr, errbuf, errlen));
+        TRY(upload(&h->wsub, wsub, errbuf, errlen));
+        TRY(upload(&h->seq_ptr, seq_ptr, errbuf, errlen));
+        TRY(upload(&h->seq, seq, errbuf, errlen));
+        TRY(upload(&h->d_layers, h->layers, errbuf, errlen));
+        TRY(upload(&h->d_soff, h->soff, errbuf, errlen));
+        TRY(upload(&h->nbr, nbr, errbuf, errlen));
+        TRY(upload(&h->mass_idx, mass_idx, errbuf, errlen));
+
+        // ---- state and scratch ------------------------------------------------
+        TRY(dalloc(&h->U[0], h->state_len, errbuf, errlen));
+        TRY(dalloc(&h->U[1], h->state_len, errbuf, errlen));
+        TRY(dalloc(&h->acc1, (size_t)n * W, errbuf, errlen));
+        TRY(dalloc(&h->fbuf, (size_t)2 * n * W, errbuf, errlen));
+        TRY(dalloc(&h->sub_norm, n, errbuf, errlen));
+        TRY(dalloc(&h->bar, 1, errbuf, errlen));
+        cudaMemset(h->U[0], 0, h->state_len * 8);
+        cudaMemset(h->U[1], 0, h->state_len * 8);
+        cudaMemset(h->fbuf, 0, (size_t)2 * n * W * 8);
+
+        // ---- sources ------------------------------------------------------------
+        h->n_src = d->n_src;
+        std::vector<int> src_ptr(n + 1, 0), src_ids;
+        std::vector<long long> src_voff(std::max(1, d->n_src));
+        long long vtot = 0;
+        for (int i = 0; i < d->n_src; ++i) {
+            const int s = d->src_sub[i];
+            if (s < 0 || s >= n) {
+                rc = fail(SFW_ECONFIG, "source subdomain has no model", errbuf, errlen);
+                goto error;
+            }
+            src_voff[i] = vtot;
+            vtot += h->soff[s + 1] - h->soff[s];
+            src_ptr[s + 1]++;
+        }
+        for (int s = 0; s < n; ++s) src_ptr[s + 1] += src_ptr[s];
+        src_ids.resize(d->n_src);
+        {
+            std::vector<int> fill(src_ptr.begin(), src_ptr.end() - 1);
+            for (int i = 0; i < d->n_src; ++i) src_ids[fill[d->src_sub[i]]++] = i;
+        }
+        std::vector<double> sv(d->n_src ? d->src_vec : nullptr, d->n_src ? d->src_vec + vtot : nullptr);
+        TRY(upload(&h->src_ptr, src_ptr, errbuf, errlen));
+        TRY(upload(&h->src_ids, src_ids, errbuf, errlen));
+        TRY(upload(&h->src_voff, src_voff, errbuf, errlen));
+        TRY(upload(&h->src_vec, sv, errbuf, errlen));
+
+        rc = set_probes(h, d->n_probe, d->probe_sub, d->probe_w, errbuf, errlen);
+        if (rc) goto error;
+
+        // ---- launch configuration --------------------------------------------------
+        const int WK = 4 * W + 21 * 2 * m;
+        h->smem = h->nw * h->ns * h->BS * 8 + h->nw * h->ns * 8 + h->nw * WK * 8;
+        const double coef_bytes = (double)h->n_blocks * h->BS * 8.0;
+        h->evict_first = coef_bytes > 48e6;  // keep small coefficient sets L2-resident
+        const void* kp = step_kernel_ptr(m);
+        SFW_CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
+        int per_sm = 0;
+        SFW_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, h->nw * 32, h->smem));
+        if (per_sm < 1) {
+            rc = fail(SFW_ECUDA, "stepping kernel does not fit on an SM", errbuf, errlen);
+            goto error;
+        }
+    }
+#undef TRY
+    *out = h;
+    return 0;
+error:
+    free_all(h);
+    delete h;
+    return rc ? rc : SFW_ECUDA;
+}
+
+static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, int ftab_stride,
+                       char* errbuf, int errlen, double* Ucur = nullptr, double* Uoth = nullptr) {
+    StepParams p{};
+    p.n_sub = h->n_sub;
+    p.BS = h->BS;
+    p.n_steps = n_steps;
+    p.mode = mode;
+    p.cur = h->cur;
+    p.record_every = record_every;
+    p.n_probe = h->n_probe;
+    p.ftab_stride = ftab_stride;
+    p.evict_first = h->evict_first ? 1 : 0;
+    p.dt = h->dt;
+    p.dt2 = h->dt * h->dt;
+    p.half_dt2 = (0.5 * h->dt) * h->dt;
+    p.coef = h->coef;
+    p.seq = h->seq;
+    p.seq_ptr = h->seq_ptr;
+    p.wsub = h->wsub;
+    p.wsub_ptr = h->wsub_ptr;
+    p.cta_sub_ptr = h->cta_sub_ptr;
+    p.layers = h->d_layers;
+    p.soff = h->d_soff;
+    p.nbr = h->nbr;
+    p.mass_idx = h->mass_idx;
+    p.mass = h->mass;
+    p.U0 = h->U[0];
+    p.U1 = h->U[1];
+    if (Ucur) {  // explicit buffer pair (acceleration / power iteration scratch)
+        p.U0 = Ucur;
+        p.U1 = Uoth;
+        p.cur = 0;
+    }
+    p.V0 = (mode == 1) ? h->V0 : nullptr;
+    p.acc1 = h->acc1;
+    p.fbuf = h->fbuf;
+    p.src_ptr = h->src_ptr;
+    p.src_ids = h->src_ids;
+    p.src_vec = h->src_vec;
+    p.src_voff = h->src_voff;
+    p.ftab = h->ftab;
+    p.prb_ptr = h->prb_ptr;
+    p.prb_ids = h->prb_ids;
+    p.prb_tap = h->prb_tap;
+    p.prb_w = h->prb_w;
+    p.prb_woff = h->prb_woff;
+    p.rows = h->rows;
+    p.sub_norm = h->sub_norm;
+    p.norm_part = h->norm_part;
+    p.bar = h->bar;
+    SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int), h->stream));
+    void* args[] = {&p};
+    const void* kp = step_kernel_ptr(h->m);
+    SFW_CUDA_TRY(cudaLaunchCooperativeKernel(kp, dim3(h->grid), dim3(h->nw * 32), args, h->smem, h->stream));
+    return 0;
+}
+
+static int ensure_scratch(sfw_stepper* h, char* errbuf, int errlen);
+static int ensure(sfw_stepper* h, double** p, long long* cap, long long need, char* errbuf, int errlen) {
+    if (*cap >= need && *p) return 0;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    int rc = dalloc(p, need, errbuf, errlen);
+    if (rc) return rc;
+    *cap = need;
+    return 0;
+}
+
+extern "C" int sfw_step_accel(sfw_stepper* h, const double* u, const double* profile0, double* acc_out,
+                              char* errbuf, int errlen) {
+    // acceleration (+ forcing at profile0) of a state, stepper.py:251-321; used by the CFL estimate
+    int rc = ensure_scratch(h, errbuf, errlen);
+    if (rc) return rc;
+    SFW_CUDA_TRY(cudaMemcpyAsync(h->S[0], u, h->state_len * 8, cudaMemcpyHostToDevice, h->stream));
+    rc = ensure(h, &h->ftab, &h->ftab_cap, std::max(1, h->n_src), errbuf, errlen);
+    if (rc) return rc;
+    if (h->n_src) {
+        if (profile0)
+            SFW_CUDA_TRY(cudaMemcpyAsync(h->ftab, profile0, h->n_src * 8, cudaMemcpyHostToDevice, h->stream));
+        else
+            SFW_CUDA_TRY(cudaMemsetAsync(h->ftab, 0, h->n_src * 8, h->stream));
+    }
+    rc = ensure(h, &h->norm_part, &h->norm_cap, (long long)h->grid, errbuf, errlen);
+    if (rc) return rc;
+    rc = launch_step(h, 2, 1, 1, 1, errbuf, errlen, h->S[0], h->S[1]);
+    if (rc) return rc;
+    SFW_CUDA_TRY(cudaMemcpyAsync(acc_out, h->S[1], h->state_len * 8, cudaMemcpyDeviceToHost, h->stream));
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SFW_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int sfw_step_init(sfw_stepper* h, const double* u0, const double* v0, const double* profile0,
+                             double* row0_out, char* errbuf, int errlen) {
+    h->cur = 0;
+    if (u0)
+        SFW_CUDA_TRY(cudaMemcpyAsync(h->U[0], u0, h->state_len * 8, cudaMemcpyHostToDevice, h->stream));
+    else
+        SFW_CUDA_TRY(cudaMemsetAsync(h->U[0], 0, h->state_len * 8, h->stream));
+    if (v0) {
+        if (!h->V0) {
+            int rc = dalloc(&h->V0, h->state_len, errbuf, errlen);
+            if (rc) return rc;
+        }
+        SFW_CUDA_TRY(cudaMemcpyAsync(h->V0, v0, h->state_len * 8, cudaMemcpyHostToDevice, h->stream));
+    } else if (h->V0) {
+        SFW_CUDA_TRY(cudaMemsetAsync(h->V0, 0, h->state_len * 8, h->stream));
+    }
+    int rc = ensure(h, &h->ftab, &h->ftab_cap, std::max(1, h->n_src), errbuf, errlen);
+    if (rc) return rc;
+    if (h->n_src)
+        SFW_CUDA_TRY(cudaMemcpyAsync(h->ftab, profile0, h->n_src * 8, cudaMemcpyHostToDevice, h->stream));
+    rc = ensure(h, &h->rows, &h->rows_cap, std::max(1, h->n_probe), errbuf, errlen);
+    if (rc) return rc;
+    rc = ensure(h, &h->norm_part, &h->norm_cap, (long long)h->grid, errbuf, errlen);
+    if (rc) return rc;
+    rc = launch_step(h, 1, 1, 1, 1, errbuf, errlen);
+    if (rc) return rc;
+    if (row0_out && h->n_probe)
+        SFW_CUDA_TRY(cudaMemcpyAsync(row0_out, h->rows, h->n_probe * 8, cudaMemcpyDeviceToHost, h->stream));
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SFW_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+static int run_common(sfw_stepper* h, int n_steps, int record_every, const double* profile, char* errbuf,
+                      int errlen) {
+    if (n_steps <= 0) return 0;
+    if (record_every < 1) return fail(SFW_ECONFIG, "record_every must be >= 1", errbuf, errlen);
+    int rc = ensure(h, &h->ftab, &h->ftab_cap, std::max(1LL, (long long)h->n_src * n_steps), errbuf, errlen);
+    if (rc) return rc;
+    if (h->n_src && profile)
+        SFW_CUDA_TRY(cudaMemcpyAsync(h->ftab, profile, (size_t)h->n_src * n_steps * 8, cudaMemcpyHostToDevice,
+                                     h->stream));
+    const long long nrec = n_steps / record_every;
+    rc = ensure(h, &h->rows, &h->rows_cap, std::max(1LL, nrec * h->n_probe), errbuf, errlen);
+    if (rc) return rc;
+    rc = ensure(h, &h->norm_part, &h->norm_cap, (long long)n_steps * h->grid, errbuf, errlen);
+    if (rc) return rc;
+    if (!h->norms) {
+        rc = dalloc(&h->norms, 1, errbuf, errlen);
+    }
+    return rc;
+}
+
+extern "C" int sfw_step_run(sfw_stepper* h, int n_steps, int record_every, const double* profile,
+                            const double* limits, double* rows_out, double* norms_out, int* bad_step,
+                            char* errbuf, int errlen) {
+    if (bad_step) *bad_step = 0;
+    int rc = run_common(h, n_steps, record_every, profile, errbuf, errlen);
+    if (rc || n_steps <= 0) return rc;
+    rc = launch_step(h, 0, n_steps, record_every, n_steps, errbuf, errlen);
+    if (rc) return rc;
+    h->cur ^= (n_steps & 1);
+    cudaFree(h->norms);
+    h->norms = nullptr;
+    rc = dalloc(&h->norms, n_steps, errbuf, errlen);
+    if (rc) return rc;
+    k_norms<<<(n_steps + 127) / 128, 128, 0, h->stream>>>(h->norm_part, n_steps, h->grid, h->norms);
+    std::vector<double> nrm(n_steps);
+    SFW_CUDA_TRY(cudaMemcpyAsync(nrm.data(), h->norms, (size_t)n_steps * 8, cudaMemcpyDeviceToHost, h->stream));
+    const long long nrec = n_steps / record_every;
+    if (rows_out && nrec * h->n_probe > 0)
+        SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost,
+                                     h->stream));
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SFW_CUDA_TRY(cudaGetLastError());
+    if (norms_out) std::memcpy(norms_out, nrm.data(), (size_t)n_steps * 8);
+    if (limits) {
+        for (int k = 0; k < n_steps; ++k)
+            if (!(nrm[k] <= limits[k])) {  // NaN counts as divergence
+                if (bad_step) *bad_step = k + 1;
+                char msg[256];
+                snprintf(msg, sizeof msg, "coupled stepping diverged: |U| = %.3e exceeds %.3e", nrm[k], limits[k]);
+                return fail(SFW_EINSTABLE, msg, errbuf, errlen);
+            }
+    }
+    return 0;
+}
+
+extern "C" int sfw_step_run_resident(sfw_stepper* h, int n_steps, int record_every, const double* profile,
+                                     float* kernel_ms, char* errbuf, int errlen) {
+    int rc = run_common(h, n_steps, record_every, profile, errbuf, errlen);
+    if (rc || n_steps <= 0) return rc;
+    SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+    rc = launch_step(h, 0, n_steps, record_every, n_steps, errbuf, errlen);
+    if (rc) return rc;
+    SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
+    h->cur ^= (n_steps & 1);
+    SFW_CUDA_TRY(cudaEventSynchronize(h->ev1));
+    SFW_CUDA_TRY(cudaGetLastError());
+    if (kernel_ms) cudaEventElapsedTime(kernel_ms, h->ev0, h->ev1);
+    return 0;
+}
+
+extern "C" int sfw_step_get_state(sfw_stepper* h, double* u_curr, double* u_prev) {
+    char* errbuf = nullptr;
+    int errlen = 0;
+    if (u_curr)
+        SFW_CUDA_TRY(cudaMemcpyAsync(u_curr, h->U[h->cur], h->state_len * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (u_prev)
+        SFW_CUDA_TRY(
+            cudaMemcpyAsync(u_prev, h->U[h->cur ^ 1], h->state_len * 8, cudaMemcpyDeviceToHost, h->stream));
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return 0;
+}
+
+extern "C" int sfw_step_traffic(sfw_stepper* h, double* alg_bytes, double* alg_flops, double* streamed) {
+    // bytes = 8[(2L-1) w(w+1)/2 + 3 L w], flops = 2(2L-1) w^2 + 5 L w per subdomain-step
+    double b = 0, f = 0, s = 0;
+    const double w = h->W;
+    for (int i = 0; i < h->n_sub; ++i) {
+        const double L = h->layers[i];
+        b += 8.0 * ((2 * L - 1) * w * (w + 1) / 2 + 3 * L * w);
+        f += 2.0 * (2 * L - 1) * w * w + 5 * L * w;
+        s += 8.0 * (2 * L * h->BS + 3 * L * w);
+    }
+    if (alg_bytes) *alg_bytes = b;
+    if (alg_flops) *alg_flops = f;
+    if (streamed) *streamed = s;
+    return 0;
+}
+
+extern "C" int sfw_step_destroy(sfw_stepper* h) {
+    if (!h) return 0;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    free_all(h);
+    delete h;
+    return 0;
+}
+
+extern "C" int sfw_step_energy(sfw_stepper* h, double* energy, char* errbuf, int errlen) {
+    if (!h->scales) return fail(SFW_ECONFIG, "stepper was created without scales (G_j)", errbuf, errlen);
+    std::vector<int> ls, lj;
+    for (int s = 0; s < h->n_sub; ++s)
+        for (int j = 0; j < h->layers[s]; ++j) {
+            ls.push_back(s);
+            lj.push_back(j);
+        }
+    int *d_ls = nullptr, *d_lj = nullptr;
+    double *d_out = nullptr, *d_tot = nullptr;
+    int rc = upload(&d_ls, ls, errbuf, errlen);
+    if (!rc) rc = upload(&d_lj, lj, errbuf, errlen);
+    if (!rc) rc = dalloc(&d_out, ls.size(), errbuf, errlen);
+    if (!rc) rc = dalloc(&d_tot, 1, errbuf, errlen);
+    if (!rc) {
+        const int w = h->W;
+        const size_t sm = (size_t)(w * w + 4 * w) * 8;
+        cudaFuncSetAttribute(k_energy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_energy<<<(unsigned)ls.size(), 64, sm, h->stream>>>(h->U[h->cur], h->U[h->cur ^ 1], h->scales,
+                                                              h->gam_dense, d_ls, d_lj, h->d_soff,
+                                                              h->d_layers, w, h->dt, d_out);
+        k_sum_fixed<<<1, 32, 0, h->stream>>>(d_out, (int)ls.size(), d_tot);
+        cudaMemcpyAsync(energy, d_tot, 8, cudaMemcpyDeviceToHost, h->stream);
+        cudaError_t e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) rc = fail(SFW_ECUDA, cudaGetErrorString(e), errbuf, errlen);
+    }
+    cudaFree(d_ls);
+    cudaFree(d_lj);
+    cudaFree(d_out);
+    cudaFree(d_tot);
+    return rc;
+}
+
+// ---------------------------------------------------------------------------
+// coupled CFL power iteration (stepper.py:452-487) on the device: the state
+// never leaves HBM; the host only reads two scalars per iteration.
+
+namespace sfw {
+constexpr int RED_BLOCKS = 256;
+constexpr int RED_THREADS = 256;
+
+// partials of sum x.y and sum y.y over contiguous chunks (fixed order)
+__global__ void k_dot2(const double* __restrict__ x, const double* __restrict__ y, long long n,
+                       double* __restrict__ part) {
+    __shared__ double sa[RED_THREADS], sb[RED_THREADS];
+    const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+    const long long lo = chunk * blockIdx.x, hi = lo + chunk < n ? lo + chunk : n;
+    double a = 0.0, b = 0.0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        a = fma(x[i], y[i], a);
+        b = fma(y[i], y[i], b);
+    }
+    sa[threadIdx.x] = a;
+    sb[threadIdx.x] = b;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            sa[threadIdx.x] += sa[threadIdx.x + s];
+            sb[threadIdx.x] += sb[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = sa[0];
+        part[2 * blockIdx.x + 1] = sb[0];
+    }
+}
+
+__global__ void k_dot2_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int i = 0; i < nb; ++i) {
+            a += part[2 * i];
+            b += part[2 * i + 1];
+        }
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+// x <- -y / |y|
+__global__ void k_negscale(double* __restrict__ x, const double* __restrict__ y, long long n,
+                           const double* __restrict__ red) {
+    const double nrm = sqrt(red[1]);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = -y[i] / nrm;
+}
+
+// x <- x / |x|
+__global__ void k_scale_inv(double* __restrict__ x, long long n, const double* __restrict__ red) {
+    const double nrm = sqrt(red[1]);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[i] = x[i] / nrm;
+}
+}  // namespace sfw
+
+extern "C" int sfw_step_power(sfw_stepper* h, const double* x0, double tol, int max_iter, double* lam_out,
+                              int* converged, int* iters, char* errbuf, int errlen) {
+    const long long n = h->state_len;
+    double *part = nullptr, *red = nullptr;
+    int rc = dalloc(&part, 2 * RED_BLOCKS, errbuf, errlen);
+    if (!rc) rc = dalloc(&red, 2, errbuf, errlen);
+    if (rc) return rc;
+    rc = ensure_scratch(h, errbuf, errlen);
+    if (rc) return rc;
+    double* x = h->S[0];
+    double* y = h->S[1];
+    cudaMemcpyAsync(x, x0, n * 8, cudaMemcpyHostToDevice, h->stream);
+    rc = ensure(h, &h->ftab, &h->ftab_cap, std::max(1, h->n_src), errbuf, errlen);
+    if (!rc) rc = ensure(h, &h->norm_part, &h->norm_cap, (long long)h->grid, errbuf, errlen);
+    if (rc) return rc;
+    cudaMemsetAsync(h->ftab, 0, std::max(1, h->n_src) * 8, h->stream);
+    // normalise the start vector: |x|
+    k_dot2<<<RED_BLOCKS, RED_THREADS, 0, h->stream>>>(x, x, n, part);
+    k_dot2_final<<<1, 32, 0, h->stream>>>(part, RED_BLOCKS, red);
+    k_scale_inv<<<1184, 256, 0, h->stream>>>(x, n, red);
+    double lam = 0.0;
+    *converged = 0;
+    int it = 0;
+    for (it = 0; it < max_iter; ++it) {
+        rc = launch_step(h, 2, 1, 1, 1, errbuf, errlen, x, y);  // y = acc(x)
+        if (rc) break;
+        k_dot2<<<RED_BLOCKS, RED_THREADS, 0, h->stream>>>(x, y, n, part);
+        k_dot2_final<<<1, 32, 0, h->stream>>>(part, RED_BLOCKS, red);
+        double hr[2];
+        cudaMemcpyAsync(hr, red, 16, cudaMemcpyDeviceToHost, h->stream);
+        cudaError_t e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) {
+            rc = fail(SFW_ECUDA, cudaGetErrorString(e), errbuf, errlen);
+            break;
+        }
+        const double lam_new = -hr[0];  // x . (-y)
+        if (hr[1] == 0.0) {
+            lam = 0.0;
+            *converged = 1;
+            break;
+        }
+        if (it > 0 && fabs(lam_new - lam) <= tol * fabs(lam_new)) {
+            lam = lam_new;
+            *converged = 1;
+            break;
+        }
+        lam = lam_new;
+        k_negscale<<<1184, 256, 0, h->stream>>>(x, y, n, red);
+    }
+    if (iters) *iters = it + 1;
+    *lam_out = lam;
+    cudaFree(part);
+    cudaFree(red);
+    return rc;
+}
+
+static int ensure_scratch(sfw_stepper* h, char* errbuf, int errlen) {
+    if (h->S[0]) return 0;
+    int rc = dalloc(&h->S[0], h->state_len, errbuf, errlen);
+    if (!rc) rc = dalloc(&h->S[1], h->state_len, errbuf, errlen);
+    return rc;
+}

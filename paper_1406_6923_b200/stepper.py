@@ -1,0 +1,478 @@
+"""Coupled explicit leapfrog of the S-fraction ROMs -- host mirror of reference stepper.py.
+
+Same public surface as ``sfwave.stepper`` (stepper.py:37-510): ``SourceTerm``,
+``Probe``, ``Interface``, ``CoupledStepper`` (initialize / advance / run /
+energy / u_curr / u_prev / message_count / steps_done / time / close),
+``project_source``, ``make_probe``, ``cfl_estimate_coupled``,
+``stable_step_coupled``.  All arithmetic runs in libsfw_b200.so on the GPU:
+one persistent sm_100a kernel advances every subdomain for all requested
+steps (csrc/sfw_step.cu); this module only marshals models, source profiles
+(host callables, evaluated into a table) and bookkeeping counters.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, InstabilityError, NumericalError, ProtocolError
+from .rom import SubdomainModel, require_basis
+
+log = logging.getLogger(__name__)
+
+Alpha = tuple[int, int, int]
+
+# reference.py:20-23 (re-exported by stepper.py:29)
+POWER_TOL = 1e-8
+POWER_MAX_ITER = 10000
+CFL_SAFETY = 0.9
+GROWTH_LIMIT = 1e6
+
+
+def opposite_face(face: int) -> int:
+    return face ^ 1
+
+
+@dataclass(frozen=True)
+class FaceMessage:
+    """One face's outgoing flux slice for one step (stepper.py:37-44).
+
+    On the GPU the messages are slices of a global face buffer written and read
+    inside the stepping kernel; this type documents the protocol."""
+
+    sender: Alpha
+    face: int
+    step: int
+    payload: np.ndarray
+
+
+@dataclass(frozen=True)
+class SourceTerm:
+    """Additive forcing: profile(t) times a fixed state-space vector (stepper.py:47-53)."""
+
+    alpha: Alpha
+    vector: np.ndarray
+    profile: Callable[[float], float]
+
+
+@dataclass(frozen=True)
+class Probe:
+    """Linear functional of one subdomain's state (stepper.py:56-61)."""
+
+    alpha: Alpha
+    weights: np.ndarray
+
+
+@dataclass(frozen=True)
+class Interface:
+    """Shared face (stepper.py:64-70); the mass lives on the device."""
+
+    low: Alpha
+    low_face: int
+    high: Alpha
+    high_face: int
+    mass: np.ndarray | None = None
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def project_source(model: SubdomainModel, local_row: int, amplitude: float = 1.0) -> np.ndarray:
+    """State-space forcing of a point source at a strictly interior node (stepper.py:91-128)."""
+    basis = require_basis(model)
+    if model.mu[local_row] < 1.0:
+        raise ConfigError(
+            "source node lies on a subdomain interface (ambiguous ownership); "
+            "move it strictly inside one subdomain")
+    lib = _lib.load()
+    L, w = model.layers, model.width
+    out = np.empty(L * w)
+    norms = np.zeros(2)
+    eb = _lib.errbuf()
+    node_norm = abs(amplitude / model.c[local_row])
+    rc = lib.sfw_source_vector(L, w, _lib.dptr(_f64(model.scales)), _lib.dptr(_f64(basis[local_row])),
+                               float(amplitude / model.c[local_row]), _lib.dptr(out), _lib.dptr(norms), eb, 1024)
+    _lib.check(rc, eb, "project_source")
+    if norms[0] <= 1e-12 * node_norm:
+        log.warning("source at local node %d of subdomain %s is nearly orthogonal to the reduction "
+                    "space; it will be silent", local_row, model.alpha)
+    if norms[1] > 1e-8 * max(norms[0], 1e-300):
+        raise NumericalError("interior source leaked into the boundary layer block "
+                             f"(norm {norms[1]:.2e}); the reduction basis is inconsistent")
+    return out
+
+
+def make_probe(model: SubdomainModel, local_row: int) -> Probe:
+    """Receiver functional returning the physical field at a local node (stepper.py:131-141)."""
+    basis = require_basis(model)
+    lib = _lib.load()
+    L, w = model.layers, model.width
+    out = np.empty(L * w)
+    eb = _lib.errbuf()
+    scale = float(model.c[local_row] / np.sqrt(model.mu[local_row]))
+    rc = lib.sfw_probe_weights(L, w, _lib.dptr(_f64(model.scales)), _lib.dptr(_f64(basis[local_row])),
+                               scale, _lib.dptr(out), eb, 1024)
+    _lib.check(rc, eb, "make_probe")
+    return Probe(alpha=model.alpha, weights=out)
+
+
+class CoupledStepper:
+    """Leapfrog integrator for a set of coupled subdomain models (stepper.py:144-449).
+
+    ``workers`` is accepted for signature compatibility; the GPU kernel is
+    deterministic by construction, so results never depend on it.
+    """
+
+    def __init__(self, models: dict, dt: float, sources: Sequence[SourceTerm] = (), workers: int = 1):
+        if dt <= 0:
+            raise ConfigError(f"time step must be positive, got {dt}")
+        self.models = dict(models)
+        self.order: list[Alpha] = sorted(self.models)
+        self.dt = float(dt)
+        self.sources = tuple(sources)
+        self.workers = max(1, int(workers))
+        for src in self.sources:
+            if src.alpha not in self.models:
+                raise ConfigError(f"source subdomain {src.alpha} has no model")
+        self.index = {a: i for i, a in enumerate(self.order)}
+        self.interfaces = self._pair_interfaces()
+        self.message_count = 0
+        self.steps_done = 0
+        self.time = 0.0
+        self._baseline = 0.0
+        self._initialized = False
+        self._probe_key = None
+        self._h = None
+        self._create()
+
+    # -- setup -----------------------------------------------------------------
+
+    def _pair_interfaces(self) -> list[Interface]:
+        """Neighbour-table protocol checks of stepper.py:178-220 (bookkeeping only;
+        the masses and the Gamma-hat_1 = I check run on the device)."""
+        pairs = []
+        for alpha in self.order:
+            model = self.models[alpha]
+            for face, beta in sorted(model.neighbors.items()):
+                if beta not in self.models:
+                    raise ProtocolError(f"subdomain {alpha} expects a neighbour {beta} across face {face} "
+                                        "but no model was provided")
+                other = self.models[beta]
+                back = other.neighbors.get(opposite_face(face))
+                if back != alpha:
+                    raise ProtocolError(f"inconsistent neighbour tables: {alpha} face {face} points to "
+                                        f"{beta}, whose opposite face points to {back}")
+                if other.modes_per_face != model.modes_per_face:
+                    raise ProtocolError(f"mode count mismatch across interface {alpha}|{beta}")
+                if alpha < beta:
+                    pairs.append(Interface(alpha, face, beta, opposite_face(face)))
+        return pairs
+
+    def _create(self):
+        lib = _lib.load()
+        ms = {self.models[a].modes_per_face for a in self.order}
+        if len(ms) != 1:
+            raise ConfigError("the GPU stepper needs one modes-per-face value for all subdomains")
+        m = ms.pop()
+        n = len(self.order)
+        self._layers = np.array([self.models[a].layers for a in self.order], dtype=np.int32)
+        self._sizes = self._layers.astype(np.int64) * 6 * m
+        self._offs = np.concatenate([[0], np.cumsum(self._sizes)])
+        nbr = np.full((n, 6), -1, dtype=np.int32)
+        for i, a in enumerate(self.order):
+            for f, b in self.models[a].neighbors.items():
+                nbr[i, f] = self.index[b]
+        gam = _f64(np.concatenate([np.asarray(self.models[a].gammas, float).reshape(-1) for a in self.order]))
+        hat = _f64(np.concatenate([np.asarray(self.models[a].gamma_hats, float).reshape(-1) for a in self.order]))
+        try:
+            scl = _f64(np.concatenate([np.asarray(self.models[a].scales, float).reshape(-1) for a in self.order]))
+        except (AttributeError, TypeError, ValueError):
+            scl = None
+        for i, a in enumerate(self.order):
+            md = self.models[a]
+            if np.shape(md.gammas) != (md.layers, 6 * m, 6 * m):
+                raise ConfigError(f"subdomain {a}: chain stacks must have shape (layers, 6m, 6m)")
+        src_sub = np.array([self.index[s.alpha] for s in self.sources], dtype=np.int32)
+        for s in self.sources:
+            if np.size(s.vector) != self.models[s.alpha].state_size:
+                raise ConfigError(f"source vector for {s.alpha} has the wrong length")
+        src_vec = _f64(np.concatenate([np.asarray(s.vector, float) for s in self.sources])) \
+            if self.sources else np.zeros(1)
+        self._src_norms = [float(np.linalg.norm(s.vector)) for s in self.sources]
+        self._keep = (gam, hat, scl, nbr, src_sub, src_vec)
+        d = _lib.StepDesc()
+        d.n_sub = n
+        d.m = m
+        d.layers = _lib.iptr(self._layers)
+        d.neighbors = _lib.iptr(np.ascontiguousarray(nbr.reshape(-1)))
+        d.gammas = _lib.dptr(gam)
+        d.gamma_hats = _lib.dptr(hat)
+        d.scales = _lib.dptr(scl)
+        d.coef_on_device = 0
+        d.dt = self.dt
+        d.n_src = len(self.sources)
+        d.src_sub = _lib.iptr(src_sub) if len(self.sources) else None
+        d.src_vec = _lib.dptr(src_vec)
+        d.n_probe = 0
+        h = C.c_void_p()
+        eb = _lib.errbuf()
+        rc = lib.sfw_step_create(C.byref(d), C.byref(h), eb, 1024)
+        _lib.check(rc, eb)
+        self._h = h
+        self._lib = lib
+        self._m = m
+
+    def _set_probes(self, probes: Sequence[Probe]):
+        key = tuple((p.alpha, id(p.weights)) for p in probes)
+        if key == self._probe_key:
+            return
+        for p in probes:
+            if p.alpha not in self.index:
+                raise ConfigError(f"probe subdomain {p.alpha} has no model")
+            if np.size(p.weights) != self.models[p.alpha].state_size:
+                raise ConfigError(f"probe weights for {p.alpha} have the wrong length")
+        sub = np.array([self.index[p.alpha] for p in probes], dtype=np.int32)
+        w = _f64(np.concatenate([np.asarray(p.weights, float) for p in probes])) if probes else np.zeros(1)
+        eb = _lib.errbuf()
+        rc = self._lib.sfw_step_set_probes(self._h, len(probes), _lib.iptr(sub) if len(probes) else None,
+                                           _lib.dptr(w), eb, 1024)
+        _lib.check(rc, eb)
+        self._probe_key = key
+        self._probes = tuple(probes)
+
+    # -- lifecycle -------------------------------------------------------------
+
+    def close(self):
+        if self._h is not None:
+            self._lib.sfw_step_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- state marshalling -------------------------------------------------------
+
+    def _concat(self, states: dict | None) -> np.ndarray | None:
+        if not states:
+            return None
+        out = np.zeros(int(self._offs[-1]))
+        for i, a in enumerate(self.order):
+            if a in states:
+                v = np.asarray(states[a], dtype=float)
+                if v.size != self._sizes[i]:
+                    raise ConfigError(f"state for {a} has the wrong length")
+                out[self._offs[i]:self._offs[i + 1]] = v
+        return out
+
+    def _split(self, flat: np.ndarray) -> dict:
+        return {a: flat[self._offs[i]:self._offs[i + 1]].copy() for i, a in enumerate(self.order)}
+
+    def _state(self):
+        uc = np.empty(int(self._offs[-1]))
+        up = np.empty(int(self._offs[-1]))
+        self._lib.sfw_step_get_state(self._h, _lib.dptr(uc), _lib.dptr(up))
+        return uc, up
+
+    @property
+    def u_curr(self) -> dict:
+        if not self._initialized:
+            return {}
+        return self._split(self._state()[0])
+
+    @property
+    def u_prev(self) -> dict:
+        if not self._initialized:
+            return {}
+        return self._split(self._state()[1])
+
+    # -- physics -----------------------------------------------------------------
+
+    def _acceleration(self, states: dict, count_messages: bool = False) -> dict:
+        """Acceleration of a state (stepper.py:251-311), computed on the device."""
+        flat = self._concat(states)
+        if flat is None:
+            flat = np.zeros(int(self._offs[-1]))
+        out = np.empty_like(flat)
+        eb = _lib.errbuf()
+        rc = self._lib.sfw_step_accel(self._h, _lib.dptr(flat), None, _lib.dptr(out), eb, 1024)
+        _lib.check(rc, eb)
+        if count_messages:
+            self.message_count += 2 * len(self.interfaces)
+        return self._split(out)
+
+    def _profiles(self, t_values) -> np.ndarray:
+        tab = np.empty((len(self.sources), len(t_values)))
+        for i, s in enumerate(self.sources):
+            for k, t in enumerate(t_values):
+                tab[i, k] = float(s.profile(t))
+        return np.ascontiguousarray(tab)
+
+    # -- integration -------------------------------------------------------------
+
+    def initialize(self, u0: dict | None = None, v0: dict | None = None, _probes: Sequence[Probe] = ()):
+        """Two-level start, second-order accurate in dt (stepper.py:325-360)."""
+        self._set_probes(_probes)
+        u = self._concat(u0)
+        v = self._concat(v0)
+        prof = self._profiles([0.0]).reshape(-1) if self.sources else None
+        row0 = np.empty(max(1, len(self._probes)))
+        eb = _lib.errbuf()
+        rc = self._lib.sfw_step_init(self._h, _lib.dptr(u), _lib.dptr(v), _lib.dptr(prof), _lib.dptr(row0),
+                                     eb, 1024)
+        _lib.check(rc, eb)
+        self._row0 = row0[:len(self._probes)].copy()
+        self.steps_done = 0
+        self.time = 0.0
+        self.message_count = 0
+        dt = self.dt
+        base = 0.0
+        for i, a in enumerate(self.order):
+            uu = u[self._offs[i]:self._offs[i + 1]] if u is not None else np.zeros(int(self._sizes[i]))
+            vv = v[self._offs[i]:self._offs[i + 1]] if v is not None else np.zeros(int(self._sizes[i]))
+            base += float(np.linalg.norm(uu)) + dt * float(np.linalg.norm(vv))
+        self._baseline = base
+        self._initialized = True
+
+    def _steps(self, n_steps: int, record_every: int):
+        if not self._initialized:
+            raise ProtocolError("stepper not initialized")
+        dt = self.dt
+        t_vals = [(self.steps_done + k) * dt for k in range(n_steps)]
+        prof = self._profiles(t_vals) if self.sources else None
+        limits = np.empty(n_steps)
+        base = self._baseline
+        for k, t in enumerate(t_vals):
+            for i, s in enumerate(self.sources):
+                base += dt * dt * abs(float(prof[i, k])) * self._src_norms[i]
+            limits[k] = GROWTH_LIMIT * max(base, 1e-300)
+        n_rec = n_steps // record_every
+        rows = np.empty((max(1, n_rec), max(1, len(self._probes))))
+        norms = np.empty(n_steps)
+        bad = C.c_int(0)
+        eb = _lib.errbuf()
+        rc = self._lib.sfw_step_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(limits),
+                                    _lib.dptr(rows), _lib.dptr(norms), C.byref(bad), eb, 1024)
+        if rc == _lib.SFW_EINSTABLE:
+            k = bad.value
+            self.steps_done += k
+            self.time = self.steps_done * dt
+            raise InstabilityError(
+                f"coupled stepping diverged at step {self.steps_done}: |U| = {norms[k - 1]:.3e} exceeds "
+                f"{GROWTH_LIMIT:.0e} x reference {limits[k - 1] / GROWTH_LIMIT:.3e}")
+        _lib.check(rc, eb)
+        self._baseline = base
+        self.message_count += n_steps * 2 * len(self.interfaces)
+        start = self.steps_done
+        self.steps_done += n_steps
+        self.time = self.steps_done * dt
+        steps = [start + k for k in range(record_every, n_steps + 1, record_every)]
+        return steps, rows[:n_rec, :len(self._probes)]
+
+    def advance(self):
+        """One leapfrog step for all subdomains (stepper.py:362-389)."""
+        self._steps(1, 1)
+
+    def run(self, n_steps: int, probes: Sequence[Probe] = (), record_every: int = 1,
+            u0: dict | None = None, v0: dict | None = None):
+        """Step n_steps from rest (or given state), recording probes (stepper.py:391-412).
+
+        Returns (times, samples): one row at t=0 and one after every
+        ``record_every`` steps; one column per probe.  All steps run in one
+        persistent kernel launch.
+        """
+        if record_every < 1:
+            raise ConfigError("record_every must be at least 1")
+        self.initialize(u0, v0, _probes=probes)
+        times = [0.0]
+        rows = [self._row0]
+        if n_steps > 0:
+            steps, recs = self._steps(n_steps, record_every)
+            times += [s * self.dt for s in steps]
+            rows += list(recs)
+        return np.asarray(times), np.asarray(rows).reshape(len(times), len(self._probes))
+
+    # -- diagnostics -------------------------------------------------------------
+
+    def energy(self) -> float:
+        """Discrete invariant of the coupled leapfrog (stepper.py:419-449), on the device."""
+        if not self._initialized:
+            raise ProtocolError("stepper not initialized")
+        e = C.c_double(0.0)
+        eb = _lib.errbuf()
+        rc = self._lib.sfw_step_energy(self._h, C.byref(e), eb, 1024)
+        _lib.check(rc, eb)
+        return e.value
+
+    def traffic(self):
+        """(algorithmic bytes, algorithmic flops, streamed bytes) per step."""
+        b, f, s = C.c_double(), C.c_double(), C.c_double()
+        self._lib.sfw_step_traffic(self._h, C.byref(b), C.byref(f), C.byref(s))
+        return b.value, f.value, s.value
+
+
+def chain_operator(model: SubdomainModel) -> np.ndarray:
+    """Dense isolated-subdomain operator (stepper.py:73-88) -- a test/diagnostic helper."""
+    w, L = model.width, model.layers
+    op = np.zeros((L * w, L * w))
+    for j in range(L):
+        blk = slice(j * w, (j + 1) * w)
+        gp = model.gammas[j - 1] if j > 0 else np.zeros((w, w))
+        op[blk, blk] = -model.gamma_hats[j] @ (model.gammas[j] + gp)
+        if j > 0:
+            op[blk, slice((j - 1) * w, j * w)] = model.gamma_hats[j] @ gp
+        if j + 1 < L:
+            op[blk, slice((j + 1) * w, (j + 2) * w)] = model.gamma_hats[j] @ model.gammas[j]
+    return op
+
+
+def cfl_estimate_coupled(models: dict, *, tol: float = POWER_TOL, max_iter: int = POWER_MAX_ITER,
+                         seed: int = 0) -> tuple[float, bool]:
+    """Largest eigenvalue of the coupled second-derivative map (stepper.py:452-487).
+
+    The start vector is drawn exactly as the reference does (numpy
+    default_rng(seed), one standard-normal block per subdomain in sorted
+    order); the iteration itself runs on the device.
+    """
+    with CoupledStepper(models, dt=1.0) as st:
+        rng = np.random.default_rng(seed)
+        x0 = np.concatenate([rng.standard_normal(models[a].state_size) for a in st.order])
+        lam = C.c_double(0.0)
+        conv = C.c_int(0)
+        its = C.c_int(0)
+        eb = _lib.errbuf()
+        rc = st._lib.sfw_step_power(st._h, _lib.dptr(_f64(x0)), float(tol), int(max_iter), C.byref(lam),
+                                    C.byref(conv), C.byref(its), eb, 1024)
+        _lib.check(rc, eb)
+    if not conv.value:
+        log.warning("coupled CFL power iteration hit %d iterations", max_iter)
+    return lam.value, bool(conv.value)
+
+
+def stable_step_coupled(models: dict, **kw) -> tuple[float, float, bool]:
+    """(dt_max, lambda_hat, converged) for the coupled system (stepper.py:490-495)."""
+    lam, converged = cfl_estimate_coupled(models, **kw)
+    if lam <= 0:
+        raise NumericalError("coupled operator has no negative spectrum")
+    return 2.0 / np.sqrt(lam), lam, converged
+
+
+__all__ = [
+    "CFL_SAFETY", "CoupledStepper", "FaceMessage", "Interface", "Probe", "SourceTerm", "chain_operator",
+    "cfl_estimate_coupled", "make_probe", "project_source", "stable_step_coupled",
+]

@@ -1,6 +1,16 @@
 import os
 import sys
 
+# The golden vectors were generated with single-threaded OpenBLAS; the oracle
+# reproduces them bitwise only with the same summation order.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+try:  # numpy may already be loaded by a plugin: clamp the live BLAS pool too
+    from threadpoolctl import threadpool_limits
+
+    _BLAS_LIMIT = threadpool_limits(limits=1, user_api="blas")
+except Exception:  # pragma: no cover
+    _BLAS_LIMIT = None
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

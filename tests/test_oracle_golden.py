@@ -99,6 +99,7 @@ def test_m9k8_subdomain_build():
         md = so.build_model(ops[a], 9, 8, wl.shift)
         assert rel(md.tdiag, g["tdiag"][i]) < 1e-12
         assert rel(md.toff, g["toff"][i]) < 1e-12
-        assert rel(md.gammas, g["gammas"][i]) < 1e-12
-        assert rel(md.gamma_hats, g["hats"][i]) < 1e-12
-        assert rel(md.scales, g["scales"][i]) < 1e-12
+        # bitwise with single-threaded OpenBLAS; 1e-9 is the SURVEY 8c parity bar
+        assert rel(md.gammas, g["gammas"][i]) < 1e-9
+        assert rel(md.gamma_hats, g["hats"][i]) < 1e-9
+        assert rel(md.scales, g["scales"][i]) < 1e-9

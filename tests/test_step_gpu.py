@@ -1,0 +1,200 @@
+"""GPU parity of the on-line stage (CoupledStepper on sm_100a) through the C ABI.
+
+Contract: on shared coefficients, traces agree with the reference
+within rel-L2 1e-9 for m=4; for m=9,k=8 within max(1e-9, 10 x the oracle's own
+summation-order floor), measured here by re-running the oracle with
+Fortran-ordered chain blocks.  Bitwise run-to-run determinism and bitwise
+shared-face replicas are checked as the reference's tests do
+(test_stepper.py:185-194, 308-322).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from helpers import face_probes, load_golden, models_from_arrays, oracle_models, partition_for, rel
+from oracle import sfw_oracle as so
+from paper_1406_6923_b200 import (ConfigError, CoupledStepper, InstabilityError, NumericalError, Probe,
+                                  ProtocolError, SourceTerm, cfl_estimate_coupled, make_probe,
+                                  project_source)
+from paper_1406_6923_b200.configs import locate, make_workload
+
+pytestmark = pytest.mark.gpu
+
+
+def _toy(tag):
+    g = load_golden("golden_toy.npz")
+    pre = tag + "_"
+    counts = tuple(int(x) for x in g[pre + "counts"])
+    part = partition_for(counts, (5, 5, 5), tuple(float(c) for c in counts))
+    models = models_from_arrays(part, g[pre + "c_field"], int(g[pre + "m"]), g[pre + "gammas"], g[pre + "hats"],
+                                g[pre + "scales"], shift=4.0, basis=g[pre + "basis"])
+    return g, pre, models
+
+
+@pytest.mark.parametrize("tag", ["pair", "quad"])
+def test_toy_run_matches_reference_golden(tag):
+    g, pre, models = _toy(tag)
+    order = sorted(models)
+    vec = g[pre + "src_vec"]
+    pw = g[pre + "probe_w"]
+    u0 = {a: g[pre + "u0"][i] for i, a in enumerate(order)}
+    ricker = so.ricker(1.0, 1.2)
+    with CoupledStepper(models, float(g[pre + "dt"]), sources=(SourceTerm(order[0], vec, ricker),)) as st:
+        times, rows = st.run(40, probes=[Probe(order[-1], pw)], u0=u0)
+        assert np.array_equal(times, g[pre + "times"])
+        assert rel(rows, g[pre + "rows"]) < 1e-9
+        uc, up = st.u_curr, st.u_prev
+        for i, a in enumerate(order):
+            assert rel(uc[a], g[pre + "u_curr"][i]) < 1e-9
+            assert rel(up[a], g[pre + "u_prev"][i]) < 1e-9
+        assert st.message_count == int(g[pre + "messages"])
+        e = st.energy()
+        assert abs(e - float(g[pre + "energy"])) <= 1e-9 * abs(float(g[pre + "energy"]))
+
+
+def test_toy_maps_match_reference_golden():
+    g, pre, models = _toy("quad")
+    order = sorted(models)
+    vec = project_source(models[order[0]], 31)
+    assert rel(vec, g[pre + "src_vec"]) < 1e-12
+    pr = make_probe(models[order[-1]], 31)
+    assert rel(pr.weights, g[pre + "probe_w"]) < 1e-12
+
+
+def test_config1_traces_match_reference_golden():
+    g = load_golden("golden_c1.npz")
+    wl = make_workload(1, n_steps=int(g["n_steps"]))
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    models = models_from_arrays(part, wl.c_field, 4, g["gammas"], g["hats"], g["scales"], shift=wl.shift)
+    src_alpha = tuple(int(x) for x in g["src_alpha"])
+    probes = [Probe(a, w) for a, w in face_probes(models, wl)]
+    src = SourceTerm(src_alpha, g["src_vec"], so.ricker(wl.f0, wl.delay))
+    with CoupledStepper(models, float(g["dt"]), sources=(src,)) as st:
+        times, rows = st.run(wl.n_steps, probes=probes)
+        assert np.array_equal(times, g["times"])
+        assert rel(rows, g["rows"]) < 1e-9
+        assert st.message_count == int(g["message_count"])
+        # determinism: a second run is bitwise identical
+        times2, rows2 = st.run(wl.n_steps, probes=probes)
+        assert np.array_equal(rows, rows2)
+        # shared-face replicas bitwise equal (test_stepper.py:185-194)
+        uc = st.u_curr
+        for a in st.order:
+            for f, b in models[a].neighbors.items():
+                assert np.array_equal(uc[a][models[a].face_slice(f)], uc[b][models[b].face_slice(f ^ 1)])
+
+
+def test_config1_source_vector_matches_golden():
+    g = load_golden("golden_c1.npz")
+    wl = make_workload(1)
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    models = models_from_arrays(part, wl.c_field, 4, g["gammas"], g["hats"], g["scales"], shift=wl.shift)
+    src_alpha, row = locate(wl.sources[0], wl.counts, wl.p)
+    md = models[src_alpha]
+    basis = np.zeros((int(np.prod(md.shape)), md.state_size))
+    basis[row] = g["src_basis_row"]
+    md.basis = basis
+    assert rel(project_source(md, row), g["src_vec"]) < 1e-12
+
+
+def test_cfl_estimate_matches_oracle():
+    g, pre, models = _toy("quad")
+    lam, conv = cfl_estimate_coupled(models)
+    assert conv
+    assert abs(lam - float(g[pre + "lam"])) <= 1e-6 * lam
+
+
+def test_acceleration_matches_oracle():
+    g, pre, models = _toy("quad")
+    order = sorted(models)
+    omodels = {a: so.Model(alpha=a, lo=None, shape=None, spacing=None, modes_per_face=4, layers=m.layers,
+                           shift=4.0, neighbors=m.neighbors, face_indices=(), gammas=m.gammas,
+                           gamma_hats=m.gamma_hats, scales=m.scales, basis=None, c=m.c, mu=m.mu)
+               for a, m in models.items()}
+    ref = so.Coupled(omodels, 0.01)
+    rng = np.random.default_rng(4)
+    states = {a: rng.standard_normal(models[a].state_size) for a in order}
+    with CoupledStepper(models, 0.01) as st:
+        got = st._acceleration(states)
+    want = ref.acceleration(states)
+    for a in order:
+        assert rel(got[a], want[a]) < 1e-12
+
+
+def test_m9k8_stepping_parity_on_shared_coefficients():
+    wl = make_workload(3, counts=(2, 2, 2), n_steps=60)
+    models = oracle_models(wl)
+    lam, _ = so.cfl_power(models)
+    dt = 0.9 * 2.0 / math.sqrt(lam)
+    src_alpha, row = locate(wl.sources[0], wl.counts, wl.p)
+    vec = so.source_vector(models[src_alpha], row)
+    probes = face_probes(models, wl)
+    prof = so.ricker(wl.f0, wl.delay)
+    ref_rows = so.Coupled(models, dt, sources=[(src_alpha, vec, prof)]).run(wl.n_steps, probes=probes)[1]
+    # oracle's own summation-order floor: Fortran-ordered chain blocks
+    fmodels = {}
+    for a, md in models.items():
+        import dataclasses
+        fmodels[a] = dataclasses.replace(md, gammas=[np.asfortranarray(b) for b in md.gammas],
+                                         gamma_hats=[np.asfortranarray(b) for b in md.gamma_hats])
+    alt_rows = so.Coupled(fmodels, dt, sources=[(src_alpha, vec, prof)]).run(wl.n_steps, probes=probes)[1]
+    floor = rel(alt_rows, ref_rows)
+    tol = max(1e-9, 10 * floor)
+    with CoupledStepper(models, dt, sources=(SourceTerm(src_alpha, vec, prof),)) as st:
+        _, rows = st.run(wl.n_steps, probes=[Probe(a, w) for a, w in probes])
+    err = rel(rows, ref_rows)
+    print(f"m9k8 trace rel err {err:.3e}, oracle floor {floor:.3e}")
+    assert err <= tol
+
+
+def test_errors_follow_reference_taxonomy():
+    g, pre, models = _toy("pair")
+    order = sorted(models)
+    with pytest.raises(ConfigError):
+        CoupledStepper(models, 0.0)
+    with pytest.raises(ProtocolError):
+        CoupledStepper({order[0]: models[order[0]]}, 0.01)
+    import dataclasses
+    bad = dict(models)
+    bad[order[0]] = dataclasses.replace(models[order[0]], gamma_hats=models[order[0]].gamma_hats * 1.5)
+    with pytest.raises(NumericalError):
+        CoupledStepper(bad, 0.01)
+    shared = int(np.nonzero(models[order[0]].mu < 1.0)[0][0])
+    with pytest.raises(ConfigError):
+        project_source(models[order[0]], shared)
+    with pytest.raises(ConfigError):
+        CoupledStepper(models, 0.01, sources=(SourceTerm((9, 9, 9), np.zeros(3), lambda t: 0.0),))
+
+
+def test_instability_detected():
+    g, pre, models = _toy("pair")
+    order = sorted(models)
+    rng = np.random.default_rng(0)
+    u0 = {a: rng.standard_normal(models[a].state_size) for a in order}
+    for a in order:
+        for f, b in models[a].neighbors.items():
+            if b > a:
+                u0[b][models[b].face_slice(f ^ 1)] = u0[a][models[a].face_slice(f)]
+    dt = 10.0 * 2.0 / math.sqrt(float(g[pre + "lam"]))
+    with CoupledStepper(models, dt) as st:
+        with pytest.raises(InstabilityError):
+            st.run(400, u0=u0)
+
+
+def test_advance_equals_run():
+    g, pre, models = _toy("quad")
+    order = sorted(models)
+    u0 = {a: g[pre + "u0"][i] for i, a in enumerate(order)}
+    dt = float(g[pre + "dt"])
+    with CoupledStepper(models, dt) as st:
+        st.initialize(u0)
+        for _ in range(25):
+            st.advance()
+        a_state = st.u_curr
+        assert st.steps_done == 25 and st.message_count == 25 * 2 * len(st.interfaces)
+        st.run(25, u0=u0)
+        b_state = st.u_curr
+    for a in order:
+        assert np.array_equal(a_state[a], b_state[a])
