@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -87,11 +88,39 @@ __host__ __device__ inline int packed_pos(int m, int row, int col) {
     return 15 * m * m + e * 6 + I;
 }
 
+// Per-lane smem offsets of the 6 partials that sum to each output row the lane
+// owns (rows i = lane + 32 e).  Order per row R: row partials of tiles (R, K<R),
+// the diagonal tile R, column partials of tiles (I>R, R) -- fixed, so the
+// result is bitwise reproducible.  Computed once per kernel (registers).
+template <int M>
+struct RedOff {
+    static constexpr int W = 6 * M, EPL = (W + 31) / 32;
+    int o[EPL][6];
+    __device__ __forceinline__ explicit RedOff(int lane) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            const int i = lane + 32 * e;
+            const int R = i < W ? i / M : 0, r = i < W ? i % M : 0;
+#pragma unroll
+            for (int t = 0; t < 6; ++t) {
+                int off;
+                if (t < R)
+                    off = off_tile(R, t) * 2 * M + r;
+                else if (t == R)
+                    off = (15 + R) * 2 * M + r;
+                else
+                    off = off_tile(t, R) * 2 * M + M + r;
+                o[e][t] = off;
+            }
+        }
+    }
+};
+
 // y = A x for one packed symmetric block, computed by one warp.
 // blk, x, part, y in shared memory; x must be visible to the warp on entry.
 template <int M>
 __device__ __forceinline__ void sym_matvec(const double* __restrict__ blk, const double* x,
-                                           double* part, double* y, int lane) {
+                                           double* part, double* y, int lane, const RedOff<M>& ro) {
     constexpr int W = 6 * M;
     if (lane < 15) {
         const int I = off_I(lane), K = off_K(lane);
@@ -143,13 +172,15 @@ __device__ __forceinline__ void sym_matvec(const double* __restrict__ blk, const
         for (int i = 0; i < M; ++i) pp[i] = P[i];
     }
     __syncwarp();
-    for (int i = lane; i < W; i += 32) {
-        const int R = i / M, r = i % M;
-        double s = 0.0;
-        for (int K = 0; K < R; ++K) s += part[off_tile(R, K) * 2 * M + r];
-        s += part[(15 + R) * 2 * M + r];
-        for (int I = R + 1; I < 6; ++I) s += part[off_tile(I, R) * 2 * M + M + r];
-        y[i] = s;
+#pragma unroll
+    for (int e = 0; e < RedOff<M>::EPL; ++e) {
+        const int i = lane + 32 * e;
+        if (i < W) {
+            double s = part[ro.o[e][0]];
+#pragma unroll
+            for (int t = 1; t < 6; ++t) s += part[ro.o[e][t]];
+            y[i] = s;
+        }
     }
     __syncwarp();
 }
@@ -157,6 +188,10 @@ __device__ __forceinline__ void sym_matvec(const double* __restrict__ blk, const
 struct StepParams {
     int n_sub, BS, n_steps, mode, cur, record_every, n_probe, ftab_stride;
     int evict_first;
+    int L;               // uniform layer count (k_step2)
+    long long state_len;
+    double* flux;        // [2][state_len] per-layer fluxes (k_step2)
+    double* sq;          // [n_sub*L] per-layer |U_next|^2 (k_step2)
     double dt, dt2, half_dt2;
     const double* coef;
     const long long* seq;
@@ -220,6 +255,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step(const StepParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gw = blockIdx.x * NW + warp;
+    const RedOff<M> ro(lane);
     double* stages = reinterpret_cast<double*>(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)NW * NS * p.BS);
     double* wk = reinterpret_cast<double*>(bars + NW * NS) + (size_t)warp * WK;
@@ -241,15 +277,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step(const StepParams p) {
     const int seq0 = p.seq_ptr[gw];
     const int seqlen = p.seq_ptr[gw + 1] - seq0;
     const int n_iter = (p.mode == 0) ? p.n_steps : 1;  // init / accel: one pass
-    const long long total = (long long)seqlen * n_iter;
+    const int total = seqlen * n_iter;
     const uint32_t bytes = (uint32_t)p.BS * 8u;
-    long long issued = 0, consumed = 0;
+    int issued = 0, consumed = 0, pr_pos = 0;
 
     auto issue = [&]() {
         if (lane == 0) {
             while (issued < total && issued < consumed + NS) {
-                const int st = (int)(issued % NS);
-                const long long off = p.seq[seq0 + (int)(issued % seqlen)];
+                const int st = issued % NS;
+                const long long off = p.seq[seq0 + pr_pos];
+                if (++pr_pos == seqlen) pr_pos = 0;
                 fence_proxy_async();
                 mbar_arrive_expect_tx(&my_bar[st], bytes);
                 bulk_g2s(my_stage + (size_t)st * p.BS, p.coef + off, bytes, &my_bar[st], pol);
@@ -288,10 +325,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step(const StepParams p) {
             for (int i = lane; i < W; i += 32)
                 xs[i] = (L > 1 ? Uc[base + W + i] : 0.0) - Uc[base + i];
             __syncwarp();
-            sym_matvec<M>(acquire(), xs, part, ys, lane);
+            sym_matvec<M>(acquire(), xs, part, ys, lane, ro);
             release();
             for (int i = lane; i < W; i += 32) fb[(size_t)s * W + i] = ys[i];
-            sym_matvec<M>(acquire(), ys, part, xs, lane);
+            sym_matvec<M>(acquire(), ys, part, xs, lane, ro);
             release();
             for (int i = lane; i < W; i += 32) p.acc1[(size_t)s * W + i] = xs[i];
         }
@@ -319,11 +356,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step(const StepParams p) {
                 for (int i = lane; i < W; i += 32)
                     xs[i] = (j + 1 < L ? Uc[lb + W + i] : 0.0) - Uc[lb + i];
                 __syncwarp();
-                sym_matvec<M>(acquire(), xs, part, f_cur, lane);
+                sym_matvec<M>(acquire(), xs, part, f_cur, lane, ro);
                 release();
                 for (int i = lane; i < W; i += 32) xs[i] = f_cur[i] - f_prv[i];
                 __syncwarp();
-                sym_matvec<M>(acquire(), xs, part, ys, lane);
+                sym_matvec<M>(acquire(), xs, part, ys, lane, ro);
                 release();
                 for (int i = lane; i < W; i += 32) {
                     const long long g = lb + i;
@@ -404,6 +441,264 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step(const StepParams p) {
             double t = 0.0;
             for (int s = p.cta_sub_ptr[blockIdx.x]; s < p.cta_sub_ptr[blockIdx.x + 1]; ++s)
                 t += p.sub_norm[s];
+            p.norm_part[(size_t)(n_iter - 1) * gridDim.x + blockIdx.x] = t;
+        }
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// k_step2: uniform layer count.  Per step and CTA the work is split into
+//   round 1: items (s, j) -> flux_j = Gamma_j (U_{j+1} - U_j)            (all layers at once)
+//   round 2: items (s, j) -> acc_j = Gamma-hat_j (flux_j - flux_{j-1}), leapfrog (j >= 2)
+//            or acc_1 = Gamma-hat_1 flux_1 (j = 1)
+//   round 3: per subdomain: face coupling + layer-1 leapfrog, |U|^2, probes
+// Items are dealt round-robin to the warps; every item's vector inputs are
+// prefetched into registers one item ahead, its coefficient block is streamed
+// by the TMA engine NS blocks ahead, so the warps never wait on a dependent
+// global load.  All addressing is arithmetic (no tables).
+template <int M, int NW, int NS>
+__global__ void __launch_bounds__(NW * 32, 1) k_step2(const StepParams p) {
+    constexpr int W = 6 * M;
+    constexpr int EPL = (W + 31) / 32;
+    constexpr int WK = 2 * W + 21 * 2 * M;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const RedOff<M> ro(lane);
+    double* stages = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)NW * NS * p.BS);
+    double* wk = reinterpret_cast<double*>(bars + NW * NS) + (size_t)warp * WK;
+    double* xs = wk;
+    double* ys = xs + W;
+    double* part = ys + W;
+    double* my_stage = stages + (size_t)warp * NS * p.BS;
+    uint64_t* my_bar = bars + warp * NS;
+    if (lane == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&my_bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    const int L = p.L;
+    const long long K = (long long)L * W;
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int nit = (s1 - s0) * L;
+    const int n1 = nit > warp ? (nit - warp + NW - 1) / NW : 0;  // items of this warp per round
+    const int n_iter = (p.mode == 0) ? p.n_steps : 1;
+    const int total = 2 * n1 * n_iter;
+    const uint64_t pol = p.evict_first ? l2_policy_evict_first() : l2_policy_evict_last();
+    const uint32_t bytes = (uint32_t)p.BS * 8u;
+    int issued = 0, consumed = 0;
+    int pr_t = 0, pr_r = 0;  // producer position: item index within round, round (0 = Gamma, 1 = Gamma-hat)
+    const double* coef_base = p.coef + (size_t)(s0 * L + warp) * 2 * p.BS;
+
+    auto issue = [&]() {
+        if (lane == 0) {
+            while (issued < total && issued < consumed + NS) {
+                const int st = issued % NS;
+                const double* src_blk = coef_base + ((size_t)pr_t * NW * 2 + pr_r) * p.BS;
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&my_bar[st], bytes);
+                bulk_g2s(my_stage + (size_t)st * p.BS, src_blk, bytes, &my_bar[st], pol);
+                ++issued;
+                if (++pr_t == n1) {
+                    pr_t = 0;
+                    pr_r ^= 1;
+                }
+            }
+        }
+    };
+    auto acquire = [&]() -> const double* {
+        const int st = (int)(consumed % NS);
+        mbar_wait(&my_bar[st], (uint32_t)((consumed / NS) & 1));
+        return my_stage + (size_t)st * p.BS;
+    };
+    auto release = [&]() {
+        __syncwarp();
+        ++consumed;
+        issue();
+    };
+    issue();
+    const double dt = p.dt, dt2 = p.dt2, half = p.half_dt2;
+
+    for (int k = 1; k <= n_iter; ++k) {
+        const int par = k & 1;
+        const int cb = p.cur ^ ((k - 1) & 1);
+        const double* Uc = cb ? p.U1 : p.U0;
+        double* Un = cb ? p.U0 : p.U1;
+        double* fx = p.flux + (size_t)par * p.state_len;
+        const int kk = k - 1;
+
+        // ---------------- round 1: all layer fluxes ------------------------------
+        {
+            double a[EPL], b[EPL];
+            auto load = [&](int t) {
+                const int q = warp + t * NW;
+                const int s = s0 + q / L, j = q % L;
+                const long long o = (long long)s * K + (long long)j * W;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const int i = lane + 32 * e;
+                    a[e] = (i < W && j + 1 < L) ? Uc[o + W + i] : 0.0;
+                    b[e] = (i < W) ? Uc[o + i] : 0.0;
+                }
+            };
+            if (n1 > 0) load(0);
+            for (int t = 0; t < n1; ++t) {
+                const int q = warp + t * NW;
+                const int s = s0 + q / L, j = q % L;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const int i = lane + 32 * e;
+                    if (i < W) xs[i] = a[e] - b[e];
+                }
+                if (t + 1 < n1) load(t + 1);
+                __syncwarp();
+                sym_matvec<M>(acquire(), xs, part, ys, lane, ro);
+                release();
+                const long long o = (long long)s * K + (long long)j * W;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const int i = lane + 32 * e;
+                    if (i < W) fx[o + i] = ys[i];
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (p.mode == 0 && k > 1) {
+                double t = 0.0;
+                for (int s = s0; s < s1; ++s) t += p.sub_norm[s];
+                p.norm_part[(size_t)(k - 2) * gridDim.x + blockIdx.x] = t;
+            }
+            grid_arrive(p.bar);
+        }
+
+        // ---------------- round 2: accelerations + leapfrog of layers >= 2 -------
+        {
+            double fa[EPL], fb_[EPL], uc[EPL], uo[EPL];
+            auto load = [&](int t) {
+                const int q = warp + t * NW;
+                const int s = s0 + q / L, j = q % L;
+                const long long o = (long long)s * K + (long long)j * W;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const int i = lane + 32 * e;
+                    fa[e] = (i < W) ? fx[o + i] : 0.0;
+                    fb_[e] = (i < W && j > 0) ? fx[o - W + i] : 0.0;
+                    uc[e] = (i < W && j > 0) ? Uc[o + i] : 0.0;
+                    uo[e] = (i < W && j > 0 && p.mode != 2) ? ((p.mode == 1) ? (p.V0 ? p.V0[o + i] : 0.0) : Un[o + i]) : 0.0;
+                }
+            };
+            if (n1 > 0) load(0);
+            for (int t = 0; t < n1; ++t) {
+                const int q = warp + t * NW;
+                const int s = s0 + q / L, j = q % L;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const int i = lane + 32 * e;
+                    if (i < W) xs[i] = (j > 0) ? fa[e] - fb_[e] : fa[e];
+                }
+                double ucur[EPL], uold[EPL];
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    ucur[e] = uc[e];
+                    uold[e] = uo[e];
+                }
+                if (t + 1 < n1) load(t + 1);
+                __syncwarp();
+                sym_matvec<M>(acquire(), xs, part, ys, lane, ro);
+                release();
+                const long long o = (long long)s * K + (long long)j * W;
+                if (j == 0) {
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) {
+                        const int i = lane + 32 * e;
+                        if (i < W) p.acc1[(size_t)s * W + i] = ys[i];
+                    }
+                } else {
+                    double sq = 0.0;
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) {
+                        const int i = lane + 32 * e;
+                        if (i < W) {
+                            const double tot = add_force(p, s, (long long)j * W + i, kk, ys[i]);
+                            const double un = leap(p.mode, ucur[e], uold[e], uold[e], tot, dt, dt2, half);
+                            Un[o + i] = un;
+                            sq = fma(un, un, sq);
+                        }
+                    }
+                    if (p.mode == 0) {
+                        sq = warp_sum(sq);
+                        if (lane == 0) p.sq[(size_t)s * L + j] = sq;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) grid_wait(p.bar, (unsigned int)k * gridDim.x);
+        __syncthreads();
+
+        // ---------------- round 3: face coupling, layer-1 leapfrog, norms, probes --
+        for (int s = s0 + warp; s < s1; s += NW) {
+            const long long base = (long long)s * K;
+            double sq = 0.0;
+            for (int i = lane; i < W; i += 32) {
+                const int f = i / M, r = i % M;
+                const int nb = p.nbr[s * 6 + f];
+                double a;
+                if (nb >= 0) {
+                    const double* mx = p.mass + (size_t)p.mass_idx[s * 6 + f] * M * M + r * M;
+                    const double* own = fx + base + f * M;
+                    const double* oth = fx + (long long)nb * K + (f ^ 1) * M;
+                    a = 0.0;
+#pragma unroll
+                    for (int c = 0; c < M; ++c) a = fma(mx[c], __dadd_rn(own[c], oth[c]), a);
+                } else {
+                    a = p.acc1[(size_t)s * W + i];
+                }
+                const double tot = add_force(p, s, i, kk, a);
+                const long long g = base + i;
+                const double v = (p.mode == 1) ? (p.V0 ? p.V0[g] : 0.0) : (p.mode == 0 ? Un[g] : 0.0);
+                const double un = leap(p.mode, Uc[g], v, v, tot, dt, dt2, half);
+                Un[g] = un;
+                sq = fma(un, un, sq);
+            }
+            if (p.mode == 0) {
+                sq = warp_sum(sq);
+                if (lane == 0) {
+                    double t = sq;
+                    for (int j = 1; j < L; ++j) t += p.sq[(size_t)s * L + j];
+                    p.sub_norm[s] = t;
+                }
+            }
+            const bool rec = (p.mode == 1) || (p.mode == 0 && k % p.record_every == 0);
+            if (rec && p.rows && p.prb_ptr[s] < p.prb_ptr[s + 1]) {
+                __syncwarp();
+                const double* U = (p.mode == 1) ? Uc : Un;
+                const long long row = (p.mode == 1) ? 0 : (k / p.record_every - 1);
+                for (int pq = p.prb_ptr[s]; pq < p.prb_ptr[s + 1]; ++pq) {
+                    const int pid = p.prb_ids[pq];
+                    const int tap = p.prb_tap[pid];
+                    double val;
+                    if (tap >= 0) {
+                        val = U[base + tap];
+                    } else {
+                        const double* wv = p.prb_w + p.prb_woff[pid];
+                        double acc = 0.0;
+                        for (int i = lane; i < K; i += 32) acc = fma(wv[i], U[base + i], acc);
+                        val = warp_sum(acc);
+                    }
+                    if (lane == 0) p.rows[row * p.n_probe + pid] = val;
+                }
+            }
+        }
+    }
+    if (p.mode == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int s = s0; s < s1; ++s) t += p.sub_norm[s];
             p.norm_part[(size_t)(n_iter - 1) * gridDim.x + blockIdx.x] = t;
         }
     }
@@ -614,21 +909,34 @@ __global__ void k_sum_fixed(const double* __restrict__ v, int n, double* __restr
 
 struct KernelCfg {
     int nw, ns;
+    const void* fn;
 };
 
-static KernelCfg cfg_for(int m) {
-    switch (m) {
-        case 1:
-        case 4:
-        case 9:
-            return {4, 4};
-        case 16:
-            return {2, 3};
-        case 25:
-            return {1, 2};
-        default:
-            return {0, 0};
+// launch variants: (modes per face, warps per CTA, TMA stages per warp)
+static KernelCfg pick_kernel(int m, bool uniform, int want_nw) {
+    if (!uniform) {
+        switch (m) {
+            case 1: return {4, 4, (const void*)k_step<1, 4, 4>};
+            case 4: return {4, 4, (const void*)k_step<4, 4, 4>};
+            case 9: return {4, 4, (const void*)k_step<9, 4, 4>};
+            case 16: return {2, 3, (const void*)k_step<16, 2, 3>};
+            case 25: return {1, 2, (const void*)k_step<25, 1, 2>};
+        }
+        return {0, 0, nullptr};
     }
+    switch (m) {
+        case 1: return {8, 4, (const void*)k_step2<1, 8, 4>};
+        case 4:
+            if (want_nw == 16) return {16, 4, (const void*)k_step2<4, 16, 4>};
+            return {8, 4, (const void*)k_step2<4, 8, 4>};
+        case 9:
+            if (want_nw == 4) return {4, 4, (const void*)k_step2<9, 4, 4>};
+            if (want_nw == 6) return {6, 3, (const void*)k_step2<9, 6, 3>};
+            return {8, 2, (const void*)k_step2<9, 8, 2>};
+        case 16: return {2, 3, (const void*)k_step2<16, 2, 3>};
+        case 25: return {1, 2, (const void*)k_step2<25, 1, 2>};
+    }
+    return {0, 0, nullptr};
 }
 
 template <typename T>
@@ -685,6 +993,11 @@ struct sfw_stepper {
     double* scales = nullptr;  // dense G_j (energy), may be null
     double* gam_dense = nullptr;  // dense Gamma_j (energy)
     bool evict_first = true;
+    bool uniform = false;
+    int L = 0;
+    const void* kfn = nullptr;
+    double* flux = nullptr;
+    double* sq = nullptr;
 };
 
 static void free_all(sfw_stepper* h) {
@@ -692,7 +1005,7 @@ static void free_all(sfw_stepper* h) {
                     h->nbr, h->mass_idx, h->d_soff, h->mass, h->U[0], h->U[1], h->V0, h->acc1,
                     h->fbuf, h->src_ptr, h->src_ids, h->src_vec, h->src_voff, h->ftab, h->prb_ptr,
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
-                    h->norm_part, h->norms, h->bar, h->scales, h->gam_dense};
+                    h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -700,16 +1013,6 @@ static void free_all(sfw_stepper* h) {
     if (h->stream) cudaStreamDestroy(h->stream);
 }
 
-static const void* step_kernel_ptr(int m) {
-    switch (m) {
-        case 1: return (const void*)k_step<1, 4, 4>;
-        case 4: return (const void*)k_step<4, 4, 4>;
-        case 9: return (const void*)k_step<9, 4, 4>;
-        case 16: return (const void*)k_step<16, 2, 3>;
-        case 25: return (const void*)k_step<25, 1, 2>;
-    }
-    return nullptr;
-}
 
 
 static int set_probes(sfw_stepper* h, int n_probe, const int* probe_sub, const double* probe_w, char* errbuf,
@@ -768,7 +1071,11 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
     *out = nullptr;
     if (!d || d->n_sub <= 0) return fail(SFW_ECONFIG, "no subdomains", errbuf, errlen);
     if (!(d->dt > 0)) return fail(SFW_ECONFIG, "time step must be positive", errbuf, errlen);
-    KernelCfg kc = cfg_for(d->m);
+    bool uniform = true;
+    for (int s = 1; s < d->n_sub; ++s) uniform = uniform && (d->layers[s] == d->layers[0]);
+    int want_nw = 0;
+    if (const char* e = getenv("SFW_STEP_NW")) want_nw = atoi(e);
+    KernelCfg kc = pick_kernel(d->m, uniform, want_nw);
     if (!kc.nw)
         return fail(SFW_ECONFIG, "modes per face must be one of 1, 4, 9, 16, 25 for the sm_100a stepper",
                     errbuf, errlen);
@@ -780,6 +1087,9 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
     h->dt = d->dt;
     h->nw = kc.nw;
     h->ns = kc.ns;
+    h->kfn = kc.fn;
+    h->uniform = uniform;
+    h->L = d->layers[0];
     const int W = h->W, n = h->n_sub, m = h->m;
     int rc = 0;
 #define TRY(x)              \
@@ -1003,11 +1313,15 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
         if (rc) goto error;
 
         // ---- launch configuration --------------------------------------------------
-        const int WK = 4 * W + 21 * 2 * m;
+        const int WK = (h->uniform ? 2 * W : 4 * W) + 21 * 2 * m;
+        if (h->uniform) {
+            TRY(dalloc(&h->flux, (size_t)2 * h->state_len, errbuf, errlen));
+            TRY(dalloc(&h->sq, (size_t)n * h->L, errbuf, errlen));
+        }
         h->smem = h->nw * h->ns * h->BS * 8 + h->nw * h->ns * 8 + h->nw * WK * 8;
         const double coef_bytes = (double)h->n_blocks * h->BS * 8.0;
         h->evict_first = coef_bytes > 48e6;  // keep small coefficient sets L2-resident
-        const void* kp = step_kernel_ptr(m);
+        const void* kp = h->kfn;
         SFW_CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
         int per_sm = 0;
         SFW_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, h->nw * 32, h->smem));
@@ -1076,8 +1390,12 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
     p.norm_part = h->norm_part;
     p.bar = h->bar;
     SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int), h->stream));
+    p.L = h->L;
+    p.state_len = h->state_len;
+    p.flux = h->flux;
+    p.sq = h->sq;
     void* args[] = {&p};
-    const void* kp = step_kernel_ptr(h->m);
+    const void* kp = h->kfn;
     SFW_CUDA_TRY(cudaLaunchCooperativeKernel(kp, dim3(h->grid), dim3(h->nw * 32), args, h->smem, h->stream));
     return 0;
 }
