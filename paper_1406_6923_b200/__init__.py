@@ -13,14 +13,14 @@ from .errors import (ConfigError, DataError, DeviceError, InstabilityError, Nume
                      ProtocolError, SfwaveError)
 from .grid import (DomainPartition, DomainSpec, SubdomainOperator, assemble_subdomain_operator,  # noqa: F401
                    build_partition, opposite_face)
-from .rom import SubdomainModel  # noqa: F401
+from .rom import SubdomainModel, build_models, build_subdomain_model  # noqa: F401
 from .stepper import (CoupledStepper, Probe, SourceTerm, cfl_estimate_coupled, make_probe,  # noqa: F401
                       project_source, stable_step_coupled)
 
 __all__ = [
     "ConfigError", "CoupledStepper", "DataError", "DeviceError", "DomainPartition", "DomainSpec",
     "InstabilityError", "NumericalError", "Probe", "ProtocolError", "SfwaveError", "SourceTerm",
-    "SubdomainModel", "SubdomainOperator", "assemble_subdomain_operator", "build_partition",
+    "SubdomainModel", "SubdomainOperator", "build_models", "build_subdomain_model", "assemble_subdomain_operator", "build_partition",
     "cfl_estimate_coupled", "make_probe", "opposite_face", "project_source", "stable_step_coupled",
     "__version__",
 ]
