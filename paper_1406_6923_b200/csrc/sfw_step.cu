@@ -693,6 +693,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step2(const StepParams p) {
                 }
             }
         }
+        // round 3 wrote layer 1 of U_next from the subdomain's warp; the next step's
+        // round 1 reads it from whichever warp owns the item
+        __syncthreads();
     }
     if (p.mode == 0) {
         __syncthreads();
@@ -1229,6 +1232,7 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
 
         // ---- work decomposition: CTA = contiguous subdomain range, warps round-robin ----
         h->grid = std::min(nsm > 0 ? nsm : 148, n);
+        if (const char* e = getenv("SFW_STEP_MAXGRID")) h->grid = std::max(1, std::min(h->grid, atoi(e)));  // test hook
         const int G = h->grid, NW = h->nw;
         std::vector<int> cta_ptr(G + 1), wsub_ptr(G * NW + 1), wsub, seq_ptr(G * NW + 1);
         std::vector<long long> seq;

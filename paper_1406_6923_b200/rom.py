@@ -43,6 +43,7 @@ class SubdomainModel:
     truncated: bool = False
     tdiag: np.ndarray | None = None
     toff: np.ndarray | None = None
+    basis_rows: dict | None = None
 
     @property
     def width(self) -> int:
@@ -55,6 +56,18 @@ class SubdomainModel:
     @property
     def state_size(self) -> int:
         return self.layers * self.width
+
+
+def basis_row(model, row: int) -> np.ndarray:
+    """Row ``row`` of the node-space basis V Q: from the full basis, or from the
+    rows a batched build materialised (``build_models(rows=...)``)."""
+    b = getattr(model, "basis", None)
+    if b is not None:
+        return np.asarray(b[row])
+    rows = getattr(model, "basis_rows", None)
+    if rows and int(row) in rows:
+        return rows[int(row)]
+    raise NumericalError("model was loaded without its node-space basis")
 
 
 def require_basis(model) -> np.ndarray:

@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from .errors import ConfigError, InstabilityError, NumericalError, ProtocolError
-from .rom import SubdomainModel, require_basis
+from .rom import SubdomainModel, basis_row
 
 log = logging.getLogger(__name__)
 
@@ -85,7 +85,7 @@ def _f64(a) -> np.ndarray:
 
 def project_source(model: SubdomainModel, local_row: int, amplitude: float = 1.0) -> np.ndarray:
     """State-space forcing of a point source at a strictly interior node (stepper.py:91-128)."""
-    basis = require_basis(model)
+    brow = basis_row(model, local_row)
     if model.mu[local_row] < 1.0:
         raise ConfigError(
             "source node lies on a subdomain interface (ambiguous ownership); "
@@ -96,7 +96,7 @@ def project_source(model: SubdomainModel, local_row: int, amplitude: float = 1.0
     norms = np.zeros(2)
     eb = _lib.errbuf()
     node_norm = abs(amplitude / model.c[local_row])
-    rc = lib.sfw_source_vector(L, w, _lib.dptr(_f64(model.scales)), _lib.dptr(_f64(basis[local_row])),
+    rc = lib.sfw_source_vector(L, w, _lib.dptr(_f64(model.scales)), _lib.dptr(_f64(brow)),
                                float(amplitude / model.c[local_row]), _lib.dptr(out), _lib.dptr(norms), eb, 1024)
     _lib.check(rc, eb, "project_source")
     if norms[0] <= 1e-12 * node_norm:
@@ -110,13 +110,13 @@ def project_source(model: SubdomainModel, local_row: int, amplitude: float = 1.0
 
 def make_probe(model: SubdomainModel, local_row: int) -> Probe:
     """Receiver functional returning the physical field at a local node (stepper.py:131-141)."""
-    basis = require_basis(model)
+    brow = basis_row(model, local_row)
     lib = _lib.load()
     L, w = model.layers, model.width
     out = np.empty(L * w)
     eb = _lib.errbuf()
     scale = float(model.c[local_row] / np.sqrt(model.mu[local_row]))
-    rc = lib.sfw_probe_weights(L, w, _lib.dptr(_f64(model.scales)), _lib.dptr(_f64(basis[local_row])),
+    rc = lib.sfw_probe_weights(L, w, _lib.dptr(_f64(model.scales)), _lib.dptr(_f64(brow)),
                                scale, _lib.dptr(out), eb, 1024)
     _lib.check(rc, eb, "make_probe")
     return Probe(alpha=model.alpha, weights=out)
@@ -129,7 +129,12 @@ class CoupledStepper:
     deterministic by construction, so results never depend on it.
     """
 
-    def __init__(self, models: dict, dt: float, sources: Sequence[SourceTerm] = (), workers: int = 1):
+    def __init__(self, models: dict, dt: float, sources: Sequence[SourceTerm] = (), workers: int = 1,
+                 device_coefficients=None):
+        """``device_coefficients``: optional (gammas, gamma_hats, scales) device
+        addresses holding the chain stacks of all models in sorted(alpha) order
+        (as ``build_models(..., device_out=...)`` writes them); the host arrays
+        of the models are then not needed."""
         if dt <= 0:
             raise ConfigError(f"time step must be positive, got {dt}")
         self.models = dict(models)
@@ -149,6 +154,7 @@ class CoupledStepper:
         self._initialized = False
         self._probe_key = None
         self._h = None
+        self._devcoef = device_coefficients
         self._create()
 
     # -- setup -----------------------------------------------------------------
@@ -188,16 +194,23 @@ class CoupledStepper:
         for i, a in enumerate(self.order):
             for f, b in self.models[a].neighbors.items():
                 nbr[i, f] = self.index[b]
-        gam = _f64(np.concatenate([np.asarray(self.models[a].gammas, float).reshape(-1) for a in self.order]))
-        hat = _f64(np.concatenate([np.asarray(self.models[a].gamma_hats, float).reshape(-1) for a in self.order]))
-        try:
-            scl = _f64(np.concatenate([np.asarray(self.models[a].scales, float).reshape(-1) for a in self.order]))
-        except (AttributeError, TypeError, ValueError):
-            scl = None
-        for i, a in enumerate(self.order):
-            md = self.models[a]
-            if np.shape(md.gammas) != (md.layers, 6 * m, 6 * m):
-                raise ConfigError(f"subdomain {a}: chain stacks must have shape (layers, 6m, 6m)")
+        if self._devcoef is None:
+            gam = _f64(np.concatenate([np.asarray(self.models[a].gammas, float).reshape(-1) for a in self.order]))
+            hat = _f64(np.concatenate([np.asarray(self.models[a].gamma_hats, float).reshape(-1)
+                                       for a in self.order]))
+            try:
+                scl = _f64(np.concatenate([np.asarray(self.models[a].scales, float).reshape(-1)
+                                           for a in self.order]))
+            except (AttributeError, TypeError, ValueError):
+                scl = None
+            for i, a in enumerate(self.order):
+                md = self.models[a]
+                if np.shape(md.gammas) != (md.layers, 6 * m, 6 * m):
+                    raise ConfigError(f"subdomain {a}: chain stacks must have shape (layers, 6m, 6m)")
+            gptr, hptr, sptr = _lib.dptr(gam), _lib.dptr(hat), _lib.dptr(scl)
+        else:
+            gam = hat = scl = None
+            gptr, hptr, sptr = (C.cast(C.c_void_p(int(x)), _lib.PD) if x else None for x in self._devcoef)
         src_sub = np.array([self.index[s.alpha] for s in self.sources], dtype=np.int32)
         for s in self.sources:
             if np.size(s.vector) != self.models[s.alpha].state_size:
@@ -211,10 +224,10 @@ class CoupledStepper:
         d.m = m
         d.layers = _lib.iptr(self._layers)
         d.neighbors = _lib.iptr(np.ascontiguousarray(nbr.reshape(-1)))
-        d.gammas = _lib.dptr(gam)
-        d.gamma_hats = _lib.dptr(hat)
-        d.scales = _lib.dptr(scl)
-        d.coef_on_device = 0
+        d.gammas = gptr
+        d.gamma_hats = hptr
+        d.scales = sptr
+        d.coef_on_device = 0 if self._devcoef is None else 1
         d.dt = self.dt
         d.n_src = len(self.sources)
         d.src_sub = _lib.iptr(src_sub) if len(self.sources) else None
@@ -442,14 +455,14 @@ def chain_operator(model: SubdomainModel) -> np.ndarray:
 
 
 def cfl_estimate_coupled(models: dict, *, tol: float = POWER_TOL, max_iter: int = POWER_MAX_ITER,
-                         seed: int = 0) -> tuple[float, bool]:
+                         seed: int = 0, device_coefficients=None) -> tuple[float, bool]:
     """Largest eigenvalue of the coupled second-derivative map (stepper.py:452-487).
 
     The start vector is drawn exactly as the reference does (numpy
     default_rng(seed), one standard-normal block per subdomain in sorted
     order); the iteration itself runs on the device.
     """
-    with CoupledStepper(models, dt=1.0) as st:
+    with CoupledStepper(models, dt=1.0, device_coefficients=device_coefficients) as st:
         rng = np.random.default_rng(seed)
         x0 = np.concatenate([rng.standard_normal(models[a].state_size) for a in st.order])
         lam = C.c_double(0.0)

@@ -86,6 +86,22 @@ def test_config1_traces_match_reference_golden():
                 assert np.array_equal(uc[a][models[a].face_slice(f)], uc[b][models[b].face_slice(f ^ 1)])
 
 
+@pytest.mark.parametrize("grid", ["1", "3"])
+def test_config1_traces_with_many_subdomains_per_cta(grid, monkeypatch):
+    """Force several subdomains (and layer items) per CTA so cross-warp hand-offs are exercised."""
+    monkeypatch.setenv("SFW_STEP_MAXGRID", grid)
+    g = load_golden("golden_c1.npz")
+    wl = make_workload(1, n_steps=int(g["n_steps"]))
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    models = models_from_arrays(part, wl.c_field, 4, g["gammas"], g["hats"], g["scales"], shift=wl.shift)
+    src_alpha = tuple(int(x) for x in g["src_alpha"])
+    probes = [Probe(a, w) for a, w in face_probes(models, wl)]
+    src = SourceTerm(src_alpha, g["src_vec"], so.ricker(wl.f0, wl.delay))
+    with CoupledStepper(models, float(g["dt"]), sources=(src,)) as st:
+        _, rows = st.run(wl.n_steps, probes=probes)
+    assert rel(rows, g["rows"]) < 1e-9
+
+
 def test_config1_source_vector_matches_golden():
     g = load_golden("golden_c1.npz")
     wl = make_workload(1)
