@@ -122,6 +122,22 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def reduce_max(x: float, device="cuda") -> float:
+    """Max over ranks (device-timed seconds); identity on one process."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_value(n_sub: int, steps: int, world: int, t_max: float) -> float:
+    """Whole-job subdomain-steps/s of ``world`` independent replicas."""
+    return world * n_sub * steps / t_max
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -242,6 +258,8 @@ def run_ours(args):
     t0 = time.perf_counter()
     lam, conv = cfl_estimate_coupled(models, device_coefficients=ptrs)
     cfl_s = time.perf_counter() - t0
+    from paper_1406_6923_b200.stepper import LAST_CFL
+    cfl_iters = LAST_CFL.get("iterations")
     dt = 0.9 * 2.0 / math.sqrt(lam)
     vec = project_source(models[src_alpha], src_row)
     probes = []
@@ -277,12 +295,8 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     kernel_s = ms.value * 1e-3
-    t_max = kernel_s
-    if ws > 1:
-        tt = torch.tensor([kernel_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-    value = ws * n_sub * K / t_max
+    t_max = reduce_max(kernel_s)
+    value = replica_value(n_sub, K, ws, t_max)
     alg_bytes, alg_flops, streamed = st.traffic()
     # e2e through the public API: host profile/limit tables in, probe rows + norms out, every step
     torch.cuda.synchronize()
@@ -290,12 +304,8 @@ def run_ours(args):
     times, trace = st.run(K, probes=probes)
     torch.cuda.synchronize()
     e2e_wall = time.perf_counter() - t0
-    e2e_t = e2e_wall
-    if ws > 1:
-        tt = torch.tensor([e2e_wall], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_t = float(tt.item())
-    e2e_value = ws * n_sub * K / e2e_t
+    e2e_t = reduce_max(e2e_wall)
+    e2e_value = replica_value(n_sub, K, ws, e2e_t)
     h2d = 8 * (1 + len(st.sources))  # growth limit + profile value per source
     d2h = 8 * (len(probes) + 1)      # probe row + |U|
     if rank != 0:
@@ -355,7 +365,8 @@ def run_ours(args):
         "gpu_launches": 1,
         "kernel_ms": ms.value, "wall_ms": wall * 1e3,
         "rom_build": {"seconds": build_s, "subdomains_per_s": n_sub / build_s, "stages_s": build_stats,
-                      "cfl_seconds": cfl_s},
+                      "cfl_seconds": cfl_s, "cfl_iterations": cfl_iters,
+                      "k_step2_launches_before_timed": (cfl_iters or 0) + 2},
     }
     print(json.dumps(line), flush=True)
     st.close()

@@ -106,6 +106,30 @@ __device__ __forceinline__ void grid_wait(const unsigned int* ctr, unsigned int 
     __threadfence();
 }
 
+// neighbour-only step flags: CTA c publishes "phase A of step k done" as flags[c] = k
+// (release, gpu scope); a CTA waits only for the CTAs that own its subdomains'
+// face neighbours (acquire).  Double-buffered face data make this sufficient.
+__device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void flag_publish(unsigned int* flags, unsigned int k) {
+    __threadfence();
+    st_release(flags + blockIdx.x, k);
+}
+
+// called by one full warp
+__device__ __forceinline__ void flags_wait(const unsigned int* flags, const int* list, int n, unsigned int k,
+                                           int lane) {
+    for (int i = lane; i < n; i += 32) {
+        const unsigned int* f = flags + list[i];
+        while (ld_acquire(f) < k) {
+        }
+    }
+    __syncwarp();
+    __threadfence();
+}
+
 // fixed-order warp sum (butterfly; identical order on every call -> deterministic)
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -222,7 +222,9 @@ struct StepParams {
     double* rows;
     double* sub_norm;
     double* norm_part;  // [n_steps][gridDim.x]
-    unsigned int* bar;
+    unsigned int* bar;       // per-CTA step flags [gridDim.x]
+    const int* ncta_ptr;     // CSR: CTAs owning face neighbours of this CTA's subdomains
+    const int* ncta;
 };
 
 __device__ __forceinline__ double leap(int mode, double uc, double uo, double v, double tot,
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step(const StepParams p) {
                     t += p.sub_norm[s];
                 p.norm_part[(size_t)(k - 2) * gridDim.x + blockIdx.x] = t;
             }
-            grid_arrive(p.bar);
+            flag_publish(p.bar, (unsigned int)k);
         }
 
         // ---------------- phase B: interior layers (independent of neighbours) ---
@@ -375,8 +377,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step(const StepParams p) {
         }
 
         // ---------------- wait for every CTA's phase A of this step ---------------
-        if (lane == 0) grid_wait(p.bar, (unsigned int)k * gridDim.x);
-        __syncwarp();
+        flags_wait(p.bar, p.ncta + p.ncta_ptr[blockIdx.x], p.ncta_ptr[blockIdx.x + 1] - p.ncta_ptr[blockIdx.x],
+                   (unsigned int)k, lane);
 
         // ---------------- phase C: face coupling, layer-1 update, norms, probes ---
         for (int q = ws0; q < ws1; ++q) {
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step2(const StepParams p) {
                 for (int s = s0; s < s1; ++s) t += p.sub_norm[s];
                 p.norm_part[(size_t)(k - 2) * gridDim.x + blockIdx.x] = t;
             }
-            grid_arrive(p.bar);
+            flag_publish(p.bar, (unsigned int)k);
         }
 
         // ---------------- round 2: accelerations + leapfrog of layers >= 2 -------
@@ -636,7 +638,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step2(const StepParams p) {
             }
         }
         __syncthreads();
-        if (threadIdx.x == 0) grid_wait(p.bar, (unsigned int)k * gridDim.x);
+        if (warp == 0)
+            flags_wait(p.bar, p.ncta + p.ncta_ptr[blockIdx.x], p.ncta_ptr[blockIdx.x + 1] - p.ncta_ptr[blockIdx.x],
+                       (unsigned int)k, lane);
         __syncthreads();
 
         // ---------------- round 3: face coupling, layer-1 leapfrog, norms, probes --
@@ -930,8 +934,8 @@ static KernelCfg pick_kernel(int m, bool uniform, int want_nw) {
     switch (m) {
         case 1: return {8, 4, (const void*)k_step2<1, 8, 4>};
         case 4:
-            if (want_nw == 16) return {16, 4, (const void*)k_step2<4, 16, 4>};
-            return {8, 4, (const void*)k_step2<4, 8, 4>};
+            if (want_nw == 8) return {8, 4, (const void*)k_step2<4, 8, 4>};
+            return {16, 4, (const void*)k_step2<4, 16, 4>};
         case 9:
             if (want_nw == 4) return {4, 4, (const void*)k_step2<9, 4, 4>};
             if (want_nw == 6) return {6, 3, (const void*)k_step2<9, 6, 3>};
@@ -976,7 +980,7 @@ struct sfw_stepper {
     double* coef = nullptr;
     long long* seq = nullptr;
     int *seq_ptr = nullptr, *wsub = nullptr, *wsub_ptr = nullptr, *cta_sub_ptr = nullptr;
-    int *d_layers = nullptr, *nbr = nullptr, *mass_idx = nullptr;
+    int *d_layers = nullptr, *nbr = nullptr, *mass_idx = nullptr, *ncta_ptr = nullptr, *ncta = nullptr;
     long long* d_soff = nullptr;
     double* mass = nullptr;
     double *U[2] = {nullptr, nullptr}, *S[2] = {nullptr, nullptr}, *V0 = nullptr, *acc1 = nullptr, *fbuf = nullptr;
@@ -1008,7 +1012,7 @@ static void free_all(sfw_stepper* h) {
                     h->nbr, h->mass_idx, h->d_soff, h->mass, h->U[0], h->U[1], h->V0, h->acc1,
                     h->fbuf, h->src_ptr, h->src_ids, h->src_vec, h->src_voff, h->ftab, h->prb_ptr,
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
-                    h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq};
+                    h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -1265,6 +1269,25 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
             }
         wsub_ptr[G * NW] = (int)wsub.size();
         seq_ptr[G * NW] = (int)seq.size();
+        {
+            std::vector<int> owner(n), nptr(G + 1, 0), nlist;
+            for (int b = 0; b < G; ++b)
+                for (int s = cta_ptr[b]; s < cta_ptr[b + 1]; ++s) owner[s] = b;
+            for (int b = 0; b < G; ++b) {
+                std::vector<int> mine;
+                for (int s = cta_ptr[b]; s < cta_ptr[b + 1]; ++s)
+                    for (int f = 0; f < 6; ++f) {
+                        const int t = nbr[6 * s + f];
+                        if (t >= 0 && owner[t] != b) mine.push_back(owner[t]);
+                    }
+                std::sort(mine.begin(), mine.end());
+                mine.erase(std::unique(mine.begin(), mine.end()), mine.end());
+                nlist.insert(nlist.end(), mine.begin(), mine.end());
+                nptr[b + 1] = (int)nlist.size();
+            }
+            TRY(upload(&h->ncta_ptr, nptr, errbuf, errlen));
+            TRY(upload(&h->ncta, nlist, errbuf, errlen));
+        }
         TRY(upload(&h->cta_sub_ptr, cta_ptr, errbuf, errlen));
         TRY(upload(&h->wsub_ptr, wsub_ptr, errbuf, errlen));
         TRY(upload(&h->wsub, wsub, errbuf, errlen));
@@ -1281,7 +1304,7 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
         TRY(dalloc(&h->acc1, (size_t)n * W, errbuf, errlen));
         TRY(dalloc(&h->fbuf, (size_t)2 * n * W, errbuf, errlen));
         TRY(dalloc(&h->sub_norm, n, errbuf, errlen));
-        TRY(dalloc(&h->bar, 1, errbuf, errlen));
+        TRY(dalloc(&h->bar, (size_t)h->grid, errbuf, errlen));
         cudaMemset(h->U[0], 0, h->state_len * 8);
         cudaMemset(h->U[1], 0, h->state_len * 8);
         cudaMemset(h->fbuf, 0, (size_t)2 * n * W * 8);
@@ -1393,7 +1416,9 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
     p.sub_norm = h->sub_norm;
     p.norm_part = h->norm_part;
     p.bar = h->bar;
-    SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int), h->stream));
+    SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int) * h->grid, h->stream));
+    p.ncta_ptr = h->ncta_ptr;
+    p.ncta = h->ncta;
     p.L = h->L;
     p.state_len = h->state_len;
     p.flux = h->flux;

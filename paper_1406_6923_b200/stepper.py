@@ -454,6 +454,9 @@ def chain_operator(model: SubdomainModel) -> np.ndarray:
     return op
 
 
+LAST_CFL: dict = {}
+
+
 def cfl_estimate_coupled(models: dict, *, tol: float = POWER_TOL, max_iter: int = POWER_MAX_ITER,
                          seed: int = 0, device_coefficients=None) -> tuple[float, bool]:
     """Largest eigenvalue of the coupled second-derivative map (stepper.py:452-487).
@@ -472,6 +475,8 @@ def cfl_estimate_coupled(models: dict, *, tol: float = POWER_TOL, max_iter: int 
         rc = st._lib.sfw_step_power(st._h, _lib.dptr(_f64(x0)), float(tol), int(max_iter), C.byref(lam),
                                     C.byref(conv), C.byref(its), eb, 1024)
         _lib.check(rc, eb)
+    LAST_CFL.clear()
+    LAST_CFL.update(iterations=its.value, converged=bool(conv.value))
     if not conv.value:
         log.warning("coupled CFL power iteration hit %d iterations", max_iter)
     return lam.value, bool(conv.value)

@@ -1,0 +1,121 @@
+"""CPU-side checks: the C-ABI library loads and exports its header, host bookkeeping
+mirrors the reference/oracle, and the product path fails loudly without a GPU."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from helpers import load_golden, models_from_arrays, partition_for
+from oracle import sfw_oracle as so
+from paper_1406_6923_b200 import (ConfigError, CoupledStepper, DeviceError, ProtocolError, _lib, grid,
+                                  project_source)
+from paper_1406_6923_b200.configs import locate, make_workload
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load(require_device=False)
+    hdr = open(os.path.join(ROOT, "include", "sfw_b200.h")).read()
+    names = set(re.findall(r"^\s*(?:int|const char\*)\s+(sfw_\w+)\s*\(", hdr, flags=re.M))
+    assert len(names) >= 14
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES or name == "sfw_rom_build", name
+    import paper_1406_6923_b200.rom  # noqa: F401  registers sfw_rom_build
+    assert hasattr(lib, "sfw_rom_build")
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>/dev/null").read()
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("mask", range(64))
+def test_face_windows_match_oracle(mask):
+    nbr = {f: None for f in range(6) if (mask >> f) & 1}
+    for shape in [(17, 17, 17), (5, 6, 7)]:
+        for f in range(6):
+            mine = grid.face_window(shape, f, nbr)
+            idx, ps = so.face_window(shape, f, nbr)
+            assert np.array_equal(mine.indices, idx)
+            assert tuple(mine.plane_shape) == tuple(ps)
+
+
+def test_operator_matches_oracle_and_golden():
+    g = load_golden("golden_toy.npz")
+    part = partition_for((2, 1, 1), (5, 5, 5), (2.0, 1.0, 1.0))
+    op = grid.assemble_subdomain_operator(part, (0, 0, 0), g["pair_c_field"], with_matrix=True)
+    assert np.allclose(op.matrix.toarray(), g["pair_matrix0"], rtol=0, atol=1e-13)
+    oop = so.make_subops((2, 1, 1), (5, 5, 5), (0.25, 0.25, 0.25), g["pair_c_field"])[(0, 0, 0)]
+    assert np.array_equal(op.mu, oop.mu) and np.array_equal(op.c, oop.c)
+
+
+def test_kronecker_factorisation_of_the_operator():
+    """A = -C (X_x (+) X_y (+) X_z) C: the identity the GPU solver relies on (csrc/sfw_rom.cu)."""
+    wl = make_workload(3, counts=(3, 3, 3))
+    ext = tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing))
+    part = grid.build_partition(grid.DomainSpec(ext, wl.counts, wl.p))
+    op = grid.assemble_subdomain_operator(part, (1, 0, 2), wl.c_field, with_matrix=True)
+    P, h = 17, 10.0
+
+    def X1(lo, hi):
+        L1 = np.diag(np.r_[1.0, 2.0 * np.ones(P - 2), 1.0]) - np.eye(P, k=1) - np.eye(P, k=-1)
+        s = np.ones(P)
+        s[0] = np.sqrt(2) if lo else 1
+        s[-1] = np.sqrt(2) if hi else 1
+        return (s[:, None] * L1 * s[None, :]) / h ** 2
+    Xs = [X1((2 * a) in op.neighbors, (2 * a + 1) in op.neighbors) for a in range(3)]
+    I = np.eye(P)
+    S = np.kron(np.kron(Xs[0], I), I) + np.kron(np.kron(I, Xs[1]), I) + np.kron(np.kron(I, I), Xs[2])
+    A = -(op.c[:, None] * S * op.c[None, :])
+    Ad = op.matrix.toarray()
+    assert np.abs(A - Ad).max() <= 1e-14 * np.abs(Ad).max()
+
+
+def test_configs_are_seeded_and_sources_interior():
+    for cfg in (1, 2, 3, 5):
+        a = make_workload(cfg, counts=(2, 2, 2))
+        b = make_workload(cfg, counts=(2, 2, 2))
+        assert np.array_equal(a.c_field, b.c_field)
+        assert a.c_field.min() >= 1500 and a.c_field.max() <= 5500
+    wl = make_workload(4, counts=(2, 2, 2))
+    assert len(wl.sources) == 32
+    for ijk in wl.sources:
+        assert all(x % 16 != 0 for x in ijk)
+    wl = make_workload(2)
+    alpha, row = locate(wl.sources[0], wl.counts, wl.p)
+    assert alpha == (3, 3, 3)
+    assert np.unravel_index(row, wl.p) == (15, 15, 15)
+
+
+def test_protocol_and_config_errors_before_any_device_work():
+    g = load_golden("golden_toy.npz")
+    part = partition_for((2, 1, 1), (5, 5, 5), (2.0, 1.0, 1.0))
+    models = models_from_arrays(part, g["pair_c_field"], 1, g["pair_gammas"], g["pair_hats"], g["pair_scales"])
+    order = sorted(models)
+    with pytest.raises(ConfigError):
+        CoupledStepper(models, -1.0)
+    with pytest.raises(ProtocolError):
+        CoupledStepper({order[0]: models[order[0]]}, 0.01)
+
+
+def test_product_path_fails_loudly_without_gpu():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except Exception:
+        pass
+    g = load_golden("golden_toy.npz")
+    part = partition_for((2, 1, 1), (5, 5, 5), (2.0, 1.0, 1.0))
+    models = models_from_arrays(part, g["pair_c_field"], 1, g["pair_gammas"], g["pair_hats"], g["pair_scales"],
+                                basis=g["pair_basis"])
+    with pytest.raises(DeviceError):
+        CoupledStepper(models, 0.01)
+    with pytest.raises(DeviceError):
+        project_source(models[sorted(models)[0]], 31)
