@@ -113,8 +113,9 @@ __device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Called by one thread after a __syncthreads(): bar.sync orders the CTA's prior
+// writes before this thread's release store (cumulativity), so no extra fence.
 __device__ __forceinline__ void flag_publish(unsigned int* flags, unsigned int k) {
-    __threadfence();
     st_release(flags + blockIdx.x, k);
 }
 
@@ -126,8 +127,7 @@ __device__ __forceinline__ void flags_wait(const unsigned int* flags, const int*
         while (ld_acquire(f) < k) {
         }
     }
-    __syncwarp();
-    __threadfence();
+    __syncwarp();  // acquire loads above; the caller's __syncthreads() publishes them to the CTA
 }
 
 // fixed-order warp sum (butterfly; identical order on every call -> deterministic)

@@ -103,13 +103,13 @@ struct RedOff {
             const int R = i < W ? i / M : 0, r = i < W ? i % M : 0;
 #pragma unroll
             for (int t = 0; t < 6; ++t) {
-                int off;
+                int off;  // partial (slot, tile) lives at slot * 21 + tile (conflict-free lane writes)
                 if (t < R)
-                    off = off_tile(R, t) * 2 * M + r;
+                    off = r * 21 + off_tile(R, t);
                 else if (t == R)
-                    off = (15 + R) * 2 * M + r;
+                    off = r * 21 + 15 + R;
                 else
-                    off = off_tile(t, R) * 2 * M + M + r;
+                    off = (M + r) * 21 + off_tile(t, R);
                 o[e][t] = off;
             }
         }
@@ -140,11 +140,10 @@ __device__ __forceinline__ void sym_matvec(const double* __restrict__ blk, const
             P[r] = fma(a, xk[c], P[r]);
             Q[c] = fma(a, xi[r], Q[c]);
         }
-        double* pp = part + lane * 2 * M;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            pp[i] = P[i];
-            pp[M + i] = Q[i];
+            part[i * 21 + lane] = P[i];
+            part[(M + i) * 21 + lane] = Q[i];
         }
     }
     if (lane < 6) {
@@ -167,9 +166,8 @@ __device__ __forceinline__ void sym_matvec(const double* __restrict__ blk, const
                 if (d != 0) P[c] = fma(a, xi[r], P[c]);
             }
         }
-        double* pp = part + (15 + lane) * 2 * M;
 #pragma unroll
-        for (int i = 0; i < M; ++i) pp[i] = P[i];
+        for (int i = 0; i < M; ++i) part[i * 21 + 15 + lane] = P[i];
     }
     __syncwarp();
 #pragma unroll
@@ -179,6 +177,105 @@ __device__ __forceinline__ void sym_matvec(const double* __restrict__ blk, const
             double s = part[ro.o[e][0]];
 #pragma unroll
             for (int t = 1; t < 6; ++t) s += part[ro.o[e][t]];
+            y[i] = s;
+        }
+    }
+    __syncwarp();
+}
+
+
+// ---- SMEM-resident block format (k_step_res): 21 full m x m tiles, element e of
+// tile t at e*21 + t.  Tiles 0..14 are the off-diagonal tiles (I > K); tile 15+d is
+// diagonal tile d stored as (strict lower + diag/2), upper part zero, so that
+// P (row partials) + Q (column partials) of a diagonal tile is its symmetric
+// product.  All 21 lanes then run the same loop (no divergent diagonal pass).
+template <int M>
+__device__ __forceinline__ void expand_block_full(const double* __restrict__ packed, double* __restrict__ out,
+                                                  int tid, int nthr) {
+    for (int idx = tid; idx < 21 * M * M; idx += nthr) {
+        const int t = idx % 21, e = idx / 21;
+        const int r = e % M, c = (e / M + r) % M;
+        double v;
+        if (t < 15) {
+            v = packed[e * 15 + t];
+        } else if (r < c) {
+            v = 0.0;
+        } else {
+            const int d = r - c;
+            const int ep = d * M - d * (d - 1) / 2 + c;
+            v = packed[15 * M * M + ep * 6 + (t - 15)];
+            if (d == 0) v = 0.5 * v;
+        }
+        out[idx] = v;
+    }
+}
+
+template <int M>
+struct RedOff7 {
+    static constexpr int W = 6 * M, EPL = (W + 31) / 32;
+    int o[EPL][7];
+    __device__ __forceinline__ explicit RedOff7(int lane) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            const int i = lane + 32 * e;
+            const int R = i < W ? i / M : 0, r = i < W ? i % M : 0;
+            int n = 0;
+#pragma unroll
+            for (int t = 0; t < 6; ++t) {
+                if (t < R) {
+                    o[e][n] = r * 21 + off_tile(R, t);
+                } else if (t == R) {
+                    o[e][n] = r * 21 + 15 + R;
+                } else {
+                    o[e][n] = (M + r) * 21 + off_tile(t, R);
+                }
+                n = n + 1;
+                if (t == R) {
+                    o[e][n] = (M + r) * 21 + 15 + R;
+                    n = n + 1;
+                }
+            }
+        }
+    }
+};
+
+template <int M>
+__device__ __forceinline__ void sym_matvec_full(const double* __restrict__ blk, const double* x, double* part,
+                                                double* y, int lane, const RedOff7<M>& ro) {
+    constexpr int W = 6 * M;
+    if (lane < 21) {
+        const int I = lane < 15 ? off_I(lane) : lane - 15;
+        const int K = lane < 15 ? off_K(lane) : lane - 15;
+        double xk[M], xi[M], P[M], Q[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            xk[i] = x[K * M + i];
+            xi[i] = x[I * M + i];
+            P[i] = 0.0;
+            Q[i] = 0.0;
+        }
+        const double* b = blk + lane;
+#pragma unroll
+        for (int e = 0; e < M * M; ++e) {
+            const int r = e % M, c = (e / M + r) % M;
+            const double a = b[e * 21];
+            P[r] = fma(a, xk[c], P[r]);
+            Q[c] = fma(a, xi[r], Q[c]);
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            part[i * 21 + lane] = P[i];
+            part[(M + i) * 21 + lane] = Q[i];
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < RedOff7<M>::EPL; ++e) {
+        const int i = lane + 32 * e;
+        if (i < W) {
+            double s = part[ro.o[e][0]];
+#pragma unroll
+            for (int t = 1; t < 7; ++t) s += part[ro.o[e][t]];
             y[i] = s;
         }
     }
@@ -225,6 +322,7 @@ struct StepParams {
     unsigned int* bar;       // per-CTA step flags [gridDim.x]
     const int* ncta_ptr;     // CSR: CTAs owning face neighbours of this CTA's subdomains
     const int* ncta;
+    unsigned long long* tprof;  // debug: [gridDim.x][n_steps][5] globaltimer stamps or null
 };
 
 __device__ __forceinline__ double leap(int mode, double uc, double uo, double v, double tot,
@@ -711,6 +809,208 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step2(const StepParams p) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_step_res: SMEM-resident variant for small configurations (e.g. config 2:
+// 512 x m4k6, <= 4 subdomains / CTA).  The CTA's chain coefficients, both state
+// levels, layer fluxes and interface masses stay in shared memory for the whole
+// launch; per step only the layer-1 face slices (global mailbox, double
+// buffered) and one step flag per CTA go through L2.  Blocks are expanded to
+// 21 full tiles in SMEM (see expand_block_full); same physics as k_step2.
+template <int M, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
+    constexpr int W = 6 * M;
+    constexpr int WK = 2 * W + 21 * 2 * M;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const RedOff7<M> ro(lane);
+    constexpr int FB = 21 * M * M;  // resident (expanded) block size
+    const int L = p.L;
+    const int K = L * W;
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int ns = s1 - s0;
+    const int nit = ns * L;
+    const int BS = p.BS;
+    double* cf = reinterpret_cast<double*>(smem_raw);          // ns * 2L * FB
+    double* U = cf + (size_t)ns * 2 * L * FB;                  // [2][ns][K]
+    double* fl = U + (size_t)2 * ns * K;                       // [ns][K] layer fluxes
+    double* a1 = fl + (size_t)ns * K;                          // [ns][W]
+    double* ms = a1 + (size_t)ns * W;                          // [ns][6][M*M]
+    double* sqv = ms + (size_t)ns * 6 * M * M;                 // [ns][L]
+    double* wk = sqv + (size_t)ns * L + (size_t)warp * WK;
+    double* xs = wk;
+    double* ys = xs + W;
+    double* part = ys + W;
+
+    // ---- one-time loads -----------------------------------------------------
+    {
+        for (int bk = threadIdx.x >> 5; bk < ns * 2 * L; bk += NW)
+            expand_block_full<M>(p.coef + ((size_t)s0 * 2 * L + bk) * BS, cf + (size_t)bk * FB, threadIdx.x & 31, 32);
+        const double* Ug0 = p.cur ? p.U1 : p.U0;
+        const double* Ug1 = p.cur ? p.U0 : p.U1;
+        for (int i = threadIdx.x; i < ns * K; i += blockDim.x) {
+            U[i] = Ug0[(size_t)s0 * K + i];
+            U[ns * K + i] = Ug1[(size_t)s0 * K + i];
+        }
+        for (int i = threadIdx.x; i < ns * 6 * M * M; i += blockDim.x) {
+            const int sl = i / (6 * M * M), f = (i / (M * M)) % 6, e = i % (M * M);
+            const int mi = p.mass_idx[(s0 + sl) * 6 + f];
+            ms[i] = mi >= 0 ? p.mass[(size_t)mi * M * M + e] : 0.0;
+        }
+    }
+    __syncthreads();
+    const double dt2 = p.dt2;
+
+    for (int k = 1; k <= p.n_steps; ++k) {
+        const int par = k & 1;
+        const int cb = (k - 1) & 1;  // U[cb] = current, U[cb^1] = previous -> next
+        double* Uc = U + (size_t)cb * ns * K;
+        double* Un = U + (size_t)(cb ^ 1) * ns * K;
+        double* fb = p.fbuf + (size_t)par * p.n_sub * W;
+        const int kk = k - 1;
+        auto stamp = [&](int ph) {
+            if (p.tprof && threadIdx.x == 0) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                p.tprof[((size_t)blockIdx.x * p.n_steps + kk) * 5 + ph] = t;
+            }
+        };
+        stamp(0);
+
+        // round 1: every layer flux.  Item order puts the layer-1 fluxes (the only
+        // data neighbours need) first: warps 0..ns-1 compute them, meet on a named
+        // barrier, and the step flag is published before the remaining items.
+        for (int q = warp; q < nit; q += NW) {
+            const int sl = q < ns ? q : (q - ns) / (L - 1);
+            const int j = q < ns ? 0 : 1 + (q - ns) % (L - 1);
+            const double* u = Uc + (size_t)sl * K + j * W;
+            for (int i = lane; i < W; i += 32) xs[i] = (j + 1 < L ? u[W + i] : 0.0) - u[i];
+            __syncwarp();
+            sym_matvec_full<M>(cf + ((size_t)(sl * L + j) * 2) * FB, xs, part, ys, lane, ro);
+            double* fo = fl + (size_t)sl * K + j * W;
+            for (int i = lane; i < W; i += 32) {
+                fo[i] = ys[i];
+                if (j == 0) fb[(size_t)(s0 + sl) * W + i] = ys[i];
+            }
+            __syncwarp();
+            if (q < ns) {  // this warp produced a layer-1 flux (warps 0..ns-1, first pass)
+                asm volatile("bar.sync 1, %0;" ::"r"(ns * 32) : "memory");
+                if (threadIdx.x == 0) flag_publish(p.bar, (unsigned int)k);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && k > 1) {
+            double t = 0.0;
+            for (int s = s0; s < s1; ++s) t += p.sub_norm[s];
+            p.norm_part[(size_t)(k - 2) * gridDim.x + blockIdx.x] = t;
+        }
+        stamp(1);
+        // round 2: accelerations + leapfrog of layers >= 2
+        for (int q = warp; q < nit; q += NW) {
+            const int sl = q < ns ? q : (q - ns) / (L - 1);
+            const int j = q < ns ? 0 : 1 + (q - ns) % (L - 1);
+            const double* fj = fl + (size_t)sl * K + j * W;
+            for (int i = lane; i < W; i += 32) xs[i] = (j > 0) ? fj[i] - fj[i - W] : fj[i];
+            __syncwarp();
+            sym_matvec_full<M>(cf + ((size_t)(sl * L + j) * 2 + 1) * FB, xs, part, ys, lane, ro);
+            if (j == 0) {
+                for (int i = lane; i < W; i += 32) a1[sl * W + i] = ys[i];
+            } else {
+                double sq = 0.0;
+                const int s = s0 + sl;
+                for (int i = lane; i < W; i += 32) {
+                    const int g = sl * K + j * W + i;
+                    const double tot = add_force(p, s, (long long)j * W + i, kk, ys[i]);
+                    const double un = __dadd_rn(__dsub_rn(__dmul_rn(2.0, Uc[g]), Un[g]), __dmul_rn(dt2, tot));
+                    Un[g] = un;
+                    sq = fma(un, un, sq);
+                }
+                sq = warp_sum(sq);
+                if (lane == 0) sqv[sl * L + j] = sq;
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        stamp(2);
+        if (warp == 0)
+            flags_wait(p.bar, p.ncta + p.ncta_ptr[blockIdx.x], p.ncta_ptr[blockIdx.x + 1] - p.ncta_ptr[blockIdx.x],
+                       (unsigned int)k, lane);
+        __syncthreads();
+        stamp(3);
+        // round 3: face coupling, layer-1 leapfrog, norms, probes
+        for (int sl = warp; sl < ns; sl += NW) {
+            const int s = s0 + sl;
+            double sq = 0.0;
+            for (int i = lane; i < W; i += 32) {
+                const int f = i / M, r = i % M;
+                const int nb = p.nbr[s * 6 + f];
+                double a;
+                if (nb >= 0) {
+                    const double* mx = ms + (sl * 6 + f) * M * M + r * M;
+                    const double* own = fl + (size_t)sl * K + f * M;
+                    const double* oth = fb + (size_t)nb * W + (f ^ 1) * M;
+                    a = 0.0;
+#pragma unroll
+                    for (int c = 0; c < M; ++c) a = fma(mx[c], __dadd_rn(own[c], oth[c]), a);
+                } else {
+                    a = a1[sl * W + i];
+                }
+                const double tot = add_force(p, s, i, kk, a);
+                const int g = sl * K + i;
+                const double un = __dadd_rn(__dsub_rn(__dmul_rn(2.0, Uc[g]), Un[g]), __dmul_rn(dt2, tot));
+                Un[g] = un;
+                sq = fma(un, un, sq);
+            }
+            sq = warp_sum(sq);
+            if (lane == 0) {
+                double t = sq;
+                for (int j = 1; j < L; ++j) t += sqv[sl * L + j];
+                p.sub_norm[s] = t;
+            }
+            if (k % p.record_every == 0 && p.rows && p.prb_ptr[s] < p.prb_ptr[s + 1]) {
+                __syncwarp();
+                const double* Us = Un + (size_t)sl * K;
+                const long long row = k / p.record_every - 1;
+                for (int pq = p.prb_ptr[s]; pq < p.prb_ptr[s + 1]; ++pq) {
+                    const int pid = p.prb_ids[pq];
+                    const int tap = p.prb_tap[pid];
+                    double val;
+                    if (tap >= 0) {
+                        val = Us[tap];
+                    } else {
+                        const double* wv = p.prb_w + p.prb_woff[pid];
+                        double acc = 0.0;
+                        for (int i = lane; i < K; i += 32) acc = fma(wv[i], Us[i], acc);
+                        val = warp_sum(acc);
+                    }
+                    if (lane == 0) p.rows[row * p.n_probe + pid] = val;
+                }
+            }
+        }
+        // No CTA barrier here: the only next-step consumer of round 3's output
+        // (layer 1 of U) is the layer-1 flux item of the same subdomain, which the
+        // item order maps to this same warp; other warps may start interior-layer
+        // fluxes of the next step while round 3 finishes.
+        stamp(4);
+    }
+    __syncthreads();
+    // write both time levels back (global layout as k_step2: U[cur ^ (n & 1)] is current)
+    {
+        const int cb = p.n_steps & 1;  // U[cb] holds the current level after n steps
+        double* Gc = (p.cur ^ (p.n_steps & 1)) ? p.U1 : p.U0;
+        double* Go = (p.cur ^ (p.n_steps & 1)) ? p.U0 : p.U1;
+        for (int i = threadIdx.x; i < ns * K; i += blockDim.x) {
+            Gc[(size_t)s0 * K + i] = U[(size_t)cb * ns * K + i];
+            Go[(size_t)s0 * K + i] = U[(size_t)(cb ^ 1) * ns * K + i];
+        }
+    }
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int s = s0; s < s1; ++s) t += p.sub_norm[s];
+        p.norm_part[(size_t)(p.n_steps - 1) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // setup kernels
 
@@ -1003,6 +1303,11 @@ struct sfw_stepper {
     bool uniform = false;
     int L = 0;
     const void* kfn = nullptr;
+    const void* kres = nullptr;
+    int res_smem = 0, res_nw = 0;
+    std::vector<int> cta_ptr_h;
+    unsigned long long* tprof = nullptr;
+    size_t tprof_n = 0;
     double* flux = nullptr;
     double* sq = nullptr;
 };
@@ -1021,6 +1326,8 @@ static void free_all(sfw_stepper* h) {
 }
 
 
+
+static int cta_res_ns(const sfw_stepper* h, int b) { return h->cta_ptr_h[b + 1] - h->cta_ptr_h[b]; }
 
 static int set_probes(sfw_stepper* h, int n_probe, const int* probe_sub, const double* probe_w, char* errbuf,
                       int errlen) {
@@ -1289,6 +1596,7 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
             TRY(upload(&h->ncta, nlist, errbuf, errlen));
         }
         TRY(upload(&h->cta_sub_ptr, cta_ptr, errbuf, errlen));
+        h->cta_ptr_h = cta_ptr;
         TRY(upload(&h->wsub_ptr, wsub_ptr, errbuf, errlen));
         TRY(upload(&h->wsub, wsub, errbuf, errlen));
         TRY(upload(&h->seq_ptr, seq_ptr, errbuf, errlen));
@@ -1348,6 +1656,26 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
         h->smem = h->nw * h->ns * h->BS * 8 + h->nw * h->ns * 8 + h->nw * WK * 8;
         const double coef_bytes = (double)h->n_blocks * h->BS * 8.0;
         h->evict_first = coef_bytes > 48e6;  // keep small coefficient sets L2-resident
+        // SMEM-resident variant when a CTA's coefficients + state fit on chip
+        if (h->uniform && !getenv("SFW_NO_RESIDENT")) {
+            int maxns = 0;
+            for (int b = 0; b < h->grid; ++b) maxns = std::max(maxns, cta_res_ns(h, b));
+            const int L = h->L, K = L * W;
+            const int nwr = (m <= 4) ? 16 : 8;
+            const size_t need = 8 * ((size_t)maxns * 2 * L * 21 * m * m + (size_t)2 * maxns * K + (size_t)maxns * K +
+                                     (size_t)maxns * W + (size_t)maxns * 6 * m * m + (size_t)maxns * L +
+                                     (size_t)nwr * (2 * W + 42 * m));
+            const void* kr = nullptr;
+            if (m == 1) kr = (const void*)k_step_res<1, 16>;
+            if (m == 4) kr = (const void*)k_step_res<4, 16>;
+            if (m == 9) kr = (const void*)k_step_res<9, 8>;
+            if (kr && need <= 220 * 1024 && maxns <= nwr) {  // layer-1 flux items map to warps 0..ns-1
+                h->kres = kr;
+                h->res_smem = (int)need;
+                h->res_nw = nwr;
+                SFW_CUDA_TRY(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+            }
+        }
         const void* kp = h->kfn;
         SFW_CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
         int per_sm = 0;
@@ -1421,9 +1749,28 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
     p.ncta = h->ncta;
     p.L = h->L;
     p.state_len = h->state_len;
+    p.tprof = nullptr;
+    if (mode == 0 && getenv("SFW_STEP_PROF")) {
+        static unsigned long long* tp = nullptr;
+        static size_t tpn = 0;
+        const size_t need = (size_t)h->grid * n_steps * 5;
+        if (need > tpn) {
+            if (tp) cudaFree(tp);
+            cudaMalloc(&tp, need * 8);
+            tpn = need;
+        }
+        p.tprof = tp;
+        h->tprof = tp;
+        h->tprof_n = need;
+    }
     p.flux = h->flux;
     p.sq = h->sq;
     void* args[] = {&p};
+    if (mode == 0 && h->kres && !Ucur) {
+        SFW_CUDA_TRY(cudaLaunchCooperativeKernel(h->kres, dim3(h->grid), dim3(h->res_nw * 32), args, h->res_smem,
+                                                 h->stream));
+        return 0;
+    }
     const void* kp = h->kfn;
     SFW_CUDA_TRY(cudaLaunchCooperativeKernel(kp, dim3(h->grid), dim3(h->nw * 32), args, h->smem, h->stream));
     return 0;
@@ -1761,4 +2108,11 @@ static int ensure_scratch(sfw_stepper* h, char* errbuf, int errlen) {
     int rc = dalloc(&h->S[0], h->state_len, errbuf, errlen);
     if (!rc) rc = dalloc(&h->S[1], h->state_len, errbuf, errlen);
     return rc;
+}
+
+extern "C" int sfw_step_debug_prof(sfw_stepper* h, unsigned long long* out, long long n) {
+    if (!h->tprof) return -1;
+    cudaStreamSynchronize(h->stream);
+    cudaMemcpy(out, h->tprof, std::min((size_t)n, h->tprof_n) * 8, cudaMemcpyDeviceToHost);
+    return (int)h->grid;
 }
