@@ -127,6 +127,28 @@ int sfw_step_accel(sfw_stepper* h, const double* u, const double* profile0, doub
 int sfw_step_power(sfw_stepper* h, const double* x0, double tol, int max_iter,
                    double* lam_out, int* converged, int* iters, char* errbuf, int errlen);
 
+/* Multi-shot mode (BASELINE config 4): S = 32 independent wavefields stepped
+ * together, every chain-block product a (w x w)(w x S) DMMA GEMM.  Shot q is the
+ * reference's CoupledStepper(models, dt, sources=(shot_q,)).run(...) from rest.
+ * shot_sub: HOST [32] source subdomain (-1 = no source); shot_vec: HOST concat
+ * of the source vectors (length L*w of shot_sub[q], skipped when -1). */
+int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub, const double* shot_vec,
+                    char* errbuf, int errlen);
+
+/* Run all shots from rest for n_steps in one persistent launch.  profile0: HOST
+ * [S] f_q(0); profile: HOST [S][n_steps] f_q(k dt); rows_out: HOST
+ * [n_steps/record_every][n_probe][S] or NULL; norms_out: HOST [n_steps][S]
+ * |U_q| after each step or NULL; *kernel_ms: CUDA-event time of the launch. */
+int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, const double* profile0,
+                  const double* profile, double* rows_out, double* norms_out, float* kernel_ms,
+                  char* errbuf, int errlen);
+
+/* State of shot q after the last sfw_shots_run (HOST concat of L_s*w). */
+int sfw_shots_state(sfw_stepper* h, int q, double* u_curr, double* u_prev);
+
+/* Algorithmic bytes / flops per step of the multi-shot launch, and bytes streamed. */
+int sfw_shots_traffic(sfw_stepper* h, double* alg_bytes, double* alg_flops, double* streamed_bytes);
+
 /* Copy the current/previous state (HOST concat of L_s*w per subdomain). */
 int sfw_step_get_state(sfw_stepper* h, double* u_curr, double* u_prev);
 

@@ -155,7 +155,7 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 }
 
 // C = op(A) op(B), all n x n row-major in smem; C must not alias A or B.
-__device__ void sm_matmul(const double* A, bool ta, const double* B, bool tb, double* C, int n) {
+__device__ inline void sm_matmul(const double* A, bool ta, const double* B, bool tb, double* C, int n) {
     for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
         const int i = idx / n, j = idx % n;
         double s = 0.0;
@@ -170,7 +170,7 @@ __device__ void sm_matmul(const double* A, bool ta, const double* B, bool tb, do
 }
 
 // In-place LU with partial pivoting (getrf); returns false if exactly singular.
-__device__ bool sm_lu(double* A, int* piv, int n, int* flag) {
+__device__ inline bool sm_lu(double* A, int* piv, int n, int* flag) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     for (int c = 0; c < n; ++c) {
@@ -212,7 +212,7 @@ __device__ bool sm_lu(double* A, int* piv, int n, int* flag) {
 }
 
 // Solve (LU) X = B in place, B is n x nrhs row-major (getrs).
-__device__ void sm_lu_solve(const double* LU, const int* piv, double* B, int n, int nrhs) {
+__device__ inline void sm_lu_solve(const double* LU, const int* piv, double* B, int n, int nrhs) {
     for (int j = threadIdx.x; j < nrhs; j += blockDim.x) {
         for (int c = 0; c < n; ++c) {
             const int pr = piv[c];
@@ -240,7 +240,7 @@ __device__ void sm_lu_solve(const double* LU, const int* piv, double* B, int n, 
 // untouched) by one-sided Jacobi SVD on a copy W (n x n workspace).  Columns
 // are orthogonalised pairwise in a fixed round-robin order; returns +inf for a
 // (numerically) singular matrix.
-__device__ double sm_cond2(const double* A, double* W, int n, double* red, int* flag) {
+__device__ inline double sm_cond2(const double* A, double* W, int n, double* red, int* flag) {
     for (int i = threadIdx.x; i < n * n; i += blockDim.x) W[i] = A[i];
     __syncthreads();
     const int m = (n % 2) ? n + 1 : n;  // tournament size (dummy player if n is odd)

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "sfw_common.cuh"
+#include "sfw_step_internal.cuh"
 
 namespace sfw {
 
@@ -1246,78 +1247,19 @@ static KernelCfg pick_kernel(int m, bool uniform, int want_nw) {
     return {0, 0, nullptr};
 }
 
-template <typename T>
-static int dalloc(T** p, size_t n, char* errbuf, int errlen) {
-    *p = nullptr;
-    if (n == 0) n = 1;
-    cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
-    if (e != cudaSuccess)
-        return fail(SFW_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e), errbuf, errlen);
-    return 0;
-}
-
-template <typename T>
-static int upload(T** p, const std::vector<T>& v, char* errbuf, int errlen) {
-    int rc = dalloc(p, v.size(), errbuf, errlen);
-    if (rc) return rc;
-    if (!v.empty()) SFW_CUDA_TRY(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-    return 0;
-}
-
 }  // namespace sfw
 
 using namespace sfw;
 
-struct sfw_stepper {
-    int n_sub = 0, m = 0, W = 0, BS = 0, n_src = 0, n_probe = 0, n_iface = 0;
-    int grid = 0, nw = 0, ns = 0, smem = 0, cur = 0;
-    long long state_len = 0, n_blocks = 0;
-    double dt = 0;
-    std::vector<int> layers;
-    std::vector<long long> soff, src_len, prb_len;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    double* coef = nullptr;
-    long long* seq = nullptr;
-    int *seq_ptr = nullptr, *wsub = nullptr, *wsub_ptr = nullptr, *cta_sub_ptr = nullptr;
-    int *d_layers = nullptr, *nbr = nullptr, *mass_idx = nullptr, *ncta_ptr = nullptr, *ncta = nullptr;
-    long long* d_soff = nullptr;
-    double* mass = nullptr;
-    double *U[2] = {nullptr, nullptr}, *S[2] = {nullptr, nullptr}, *V0 = nullptr, *acc1 = nullptr, *fbuf = nullptr;
-    int *src_ptr = nullptr, *src_ids = nullptr;
-    double* src_vec = nullptr;
-    long long* src_voff = nullptr;
-    double* ftab = nullptr;
-    long long ftab_cap = 0;
-    int *prb_ptr = nullptr, *prb_ids = nullptr, *prb_tap = nullptr;
-    double* prb_w = nullptr;
-    long long* prb_woff = nullptr;
-    double* rows = nullptr;
-    long long rows_cap = 0;
-    double *sub_norm = nullptr, *norm_part = nullptr, *norms = nullptr;
-    long long norm_cap = 0;
-    unsigned int* bar = nullptr;
-    double* scales = nullptr;  // dense G_j (energy), may be null
-    double* gam_dense = nullptr;  // dense Gamma_j (energy)
-    bool evict_first = true;
-    bool uniform = false;
-    int L = 0;
-    const void* kfn = nullptr;
-    const void* kres = nullptr;
-    int res_smem = 0, res_nw = 0;
-    std::vector<int> cta_ptr_h;
-    unsigned long long* tprof = nullptr;
-    size_t tprof_n = 0;
-    double* flux = nullptr;
-    double* sq = nullptr;
-};
 
 static void free_all(sfw_stepper* h) {
     void* ptrs[] = {h->coef, h->S[0], h->S[1], h->seq, h->seq_ptr, h->wsub, h->wsub_ptr, h->cta_sub_ptr, h->d_layers,
                     h->nbr, h->mass_idx, h->d_soff, h->mass, h->U[0], h->U[1], h->V0, h->acc1,
                     h->fbuf, h->src_ptr, h->src_ids, h->src_vec, h->src_voff, h->ftab, h->prb_ptr,
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
-                    h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta};
+                    h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta, h->tcoef, h->UM[0], h->UM[1],
+                    h->mfb, h->macc1, h->mnorm, h->mrows, h->shot_vec, h->shot_sub, h->shot_voff,
+                    h->shot_ftab};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);

@@ -420,6 +420,85 @@ class CoupledStepper:
             rows += list(recs)
         return np.asarray(times), np.asarray(rows).reshape(len(times), len(self._probes))
 
+    # -- independent shots (BASELINE config 4) ------------------------------------
+
+    SHOTS = 32
+
+    def run_shots(self, n_steps: int, shots: Sequence[SourceTerm], probes: Sequence[Probe] = (),
+                  record_every: int = 1, return_norms: bool = False):
+        """Step up to 32 independent wavefields from rest in one launch.
+
+        Shot q is exactly ``CoupledStepper(models, dt, sources=(shots[q],)).run(
+        n_steps, probes, record_every)`` of the reference (SURVEY 8d config 4:
+        32 separate runs); on the GPU all shots share one persistent kernel whose
+        block products are (w x w)(w x 32) DMMA GEMMs.  Returns (times, rows) with
+        rows[k, q, p] = probe p of shot q after the k-th recorded step (row 0 at t=0).
+        """
+        if record_every < 1:
+            raise ConfigError("record_every must be at least 1")
+        S = self.SHOTS
+        if not 1 <= len(shots) <= S:
+            raise ConfigError(f"run_shots takes 1..{S} shots")
+        for sh in shots:
+            if sh.alpha not in self.index:
+                raise ConfigError(f"source subdomain {sh.alpha} has no model")
+            if np.size(sh.vector) != self.models[sh.alpha].state_size:
+                raise ConfigError(f"source vector for {sh.alpha} has the wrong length")
+        self._set_probes(probes)
+        sub = np.full(S, -1, dtype=np.int32)
+        vecs = []
+        for q, sh in enumerate(shots):
+            sub[q] = self.index[sh.alpha]
+            vecs.append(np.asarray(sh.vector, float))
+        vec = _f64(np.concatenate(vecs))
+        eb = _lib.errbuf()
+        rc = self._lib.sfw_shots_setup(self._h, S, _lib.iptr(sub), _lib.dptr(vec), eb, 1024)
+        _lib.check(rc, eb)
+        dt = self.dt
+        prof = np.zeros((S, n_steps))
+        prof0 = np.zeros(S)
+        for q, sh in enumerate(shots):
+            prof0[q] = float(sh.profile(0.0))
+            for k in range(n_steps):
+                prof[q, k] = float(sh.profile(k * dt))
+        n_rec = n_steps // record_every
+        rows = np.zeros((max(n_rec, 1), max(len(self._probes), 1), S))
+        norms = np.zeros((n_steps, S))
+        ms = C.c_float(0.0)
+        rc = self._lib.sfw_shots_run(self._h, n_steps, record_every, _lib.dptr(prof0), _lib.dptr(_f64(prof)),
+                                     _lib.dptr(rows), _lib.dptr(norms), C.byref(ms), eb, 1024)
+        _lib.check(rc, eb)
+        self.last_kernel_ms = ms.value
+        # growth detector per shot (stepper.py:379-389), from rest: baseline = sum dt^2 |f| |vec|
+        for q, sh in enumerate(shots):
+            base = 0.0
+            nv = float(np.linalg.norm(sh.vector))
+            for k in range(n_steps):
+                base += dt * dt * abs(float(prof[q, k])) * nv
+                if not norms[k, q] <= GROWTH_LIMIT * max(base, 1e-300):
+                    raise InstabilityError(f"shot {q}: coupled stepping diverged at step {k + 1}: "
+                                           f"|U| = {norms[k, q]:.3e}")
+        self._initialized = False  # the single-wavefield state was not advanced
+        times = np.array([0.0] + [k * dt for k in range(record_every, n_steps + 1, record_every)])
+        out = np.zeros((n_rec + 1, len(shots), len(self._probes)))
+        if len(self._probes):
+            out[1:] = rows[:n_rec, :len(self._probes), :len(shots)].transpose(0, 2, 1)
+        if return_norms:
+            return times, out, norms[:, :len(shots)]
+        return times, out
+
+    def shot_state(self, q: int):
+        """(u_curr, u_prev) dicts of shot q after run_shots."""
+        uc = np.empty(int(self._offs[-1]))
+        up = np.empty(int(self._offs[-1]))
+        self._lib.sfw_shots_state(self._h, int(q), _lib.dptr(uc), _lib.dptr(up))
+        return self._split(uc), self._split(up)
+
+    def shots_traffic(self):
+        b, f, s = C.c_double(), C.c_double(), C.c_double()
+        self._lib.sfw_shots_traffic(self._h, C.byref(b), C.byref(f), C.byref(s))
+        return b.value, f.value, s.value
+
     # -- diagnostics -------------------------------------------------------------
 
     def energy(self) -> float:
