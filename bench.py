@@ -278,6 +278,9 @@ def run_ours(args):
     if len(wl.sources) > 1:
         return _run_shots(args, wl, models, ptrs, dt, lam, conv, probes, ws, rank, build_s, build_stats, cfl_s,
                           cfl_iters)
+    if args.precision == "fp32":
+        return _run_fp32(args, wl, models, ptrs, dt, lam, conv, src, probes, ws, rank, build_s, build_stats, cfl_s,
+                         cfl_iters)
     st = CoupledStepper(models, dt, sources=(src,), device_coefficients=ptrs)
     st.initialize(_probes=probes)
     lib = st._lib
@@ -381,6 +384,57 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _run_fp32(args, wl, models, ptrs, dt, lam, conv, src, probes, ws, rank, build_s, build_stats, cfl_s, cfl_iters):
+    """Config 5 fp32 variant: W-form stepping (U_j = G_j W_j), fp32 blocks."""
+    import ctypes as C
+
+    import torch
+    from paper_1406_6923_b200 import CoupledStepper, _lib
+    n_sub = len(models)
+    w, L = wl.width, wl.layers
+    st = CoupledStepper(models, dt, sources=(src,), device_coefficients=ptrs, precision="fp32")
+    st.run(max(args.warmup, 1), probes=probes)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    flush.fill_(1.0)
+    torch.cuda.synchronize()
+    K = args.steps
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        t0 = time.perf_counter()
+        times, rows = st.run(K, probes=probes)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    kernel_s = st.last_kernel_ms * 1e-3
+    t_max = reduce_max(kernel_s)
+    value = replica_value(n_sub, K, ws, t_max)
+    e2e_value = replica_value(n_sub, K, ws, reduce_max(wall))
+    b, st_b = C.c_double(), C.c_double()
+    st._lib.sfw_wform_traffic(st._h, C.byref(b), C.byref(st_b))
+    st.close()
+    if rank != 0:
+        return
+    peak, peak_kind = _peaks()
+    achieved = b.value * K / kernel_s / 1e9
+    line = {
+        "metric": METRIC.replace("fp64", "fp32 W-form"), "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_max / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded medium, SURVEY 8d); models built on the GPU",
+        "config": {"workload": _describe(wl) + ", fp32 W-form variant", "subdomains": n_sub,
+                   "rom_dof_per_subdomain": L * w, "dt": dt, "lambda_hat": lam, "cfl_converged": conv,
+                   "probes": len(probes), "l2": "flushed before the timed launch", "parallelism": "1 GPU"},
+        "dof_updates_per_s": value * L * w,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16, "d2h_bytes_per_step": 8 * (len(probes) + 1),
+                "api": "CoupledStepper(precision='fp32').run(K, probes)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_step": b.value,
+                     "streamed_bytes_per_step": st_b.value,
+                     "formula": "4[(2L-1)w(w+1)/2 + 3Lw] bytes per subdomain-step (SURVEY 8d fp32)"},
+        "cpu_baseline": None, "clocks": clk.summary(), "gpu_launches": 2, "kernel_ms": kernel_s * 1e3,
+        "rom_build": {"seconds": build_s, "subdomains_per_s": n_sub / build_s, "stages_s": build_stats,
+                      "cfl_seconds": cfl_s, "cfl_iterations": cfl_iters},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def _run_shots(args, wl, models, ptrs, dt, lam, conv, probes, ws, rank, build_s, build_stats, cfl_s, cfl_iters):
     """Config 4: 32 independent sources stepped together (DMMA path)."""
     import torch
@@ -451,6 +505,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()

@@ -149,6 +149,28 @@ int sfw_shots_state(sfw_stepper* h, int q, double* u_curr, double* u_prev);
 /* Algorithmic bytes / flops per step of the multi-shot launch, and bytes streamed. */
 int sfw_shots_traffic(sfw_stepper* h, double* alg_bytes, double* alg_flops, double* streamed_bytes);
 
+/* fp32 W-form variant: U_j = G_j W_j turns the chain
+ * into the Lanczos block-tridiagonal operator (A_j symmetric, B_j triangular,
+ * computed on the device from G_j, Gamma_j) with interface mass 1/2; blocks are
+ * fp32 (half the bytes).  Requires scales at create. */
+int sfw_wform_setup(sfw_stepper* h, char* errbuf, int errlen);
+/* Convert the handle's U-form sources (G^-1 s) and probe weights (G^T p) to W-form.
+ * src_vec / probe_w: HOST U-form arrays as passed to create / set_probes;
+ * src_norms: HOST [n_src] |G^-1 s| or NULL. */
+int sfw_wform_vectors(sfw_stepper* h, const double* src_vec, const double* probe_w, double* src_norms,
+                      char* errbuf, int errlen);
+/* Two-level start in W-form (u0/v0: HOST U-form or NULL). */
+int sfw_wform_init(sfw_stepper* h, const double* u0, const double* v0, const double* profile0,
+                   double* row0_out, char* errbuf, int errlen);
+/* n_steps fp32 W-form steps in one launch; rows are physical probe values (fp64),
+ * norms_out |W| per step; *kernel_ms the launch's CUDA-event time. */
+int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, const double* profile,
+                  double* rows_out, double* norms_out, float* kernel_ms, char* errbuf, int errlen);
+/* Current/previous state mapped back to U-form (fp64). */
+int sfw_wform_state(sfw_stepper* h, double* u_curr, double* u_prev, char* errbuf, int errlen);
+int sfw_wform_traffic(sfw_stepper* h, double* alg_bytes, double* streamed_bytes);
+int sfw_wform_destroy(sfw_stepper* h);
+
 /* Copy the current/previous state (HOST concat of L_s*w per subdomain). */
 int sfw_step_get_state(sfw_stepper* h, double* u_curr, double* u_prev);
 

@@ -55,6 +55,13 @@ SIGNATURES = {
     "sfw_shots_run": (C.c_int, [C.c_void_p, C.c_int, C.c_int, PD, PD, PD, PD, PF, C.c_char_p, C.c_int]),
     "sfw_shots_state": (C.c_int, [C.c_void_p, C.c_int, PD, PD]),
     "sfw_shots_traffic": (C.c_int, [C.c_void_p, PD, PD, PD]),
+    "sfw_wform_setup": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
+    "sfw_wform_vectors": (C.c_int, [C.c_void_p, PD, PD, PD, C.c_char_p, C.c_int]),
+    "sfw_wform_init": (C.c_int, [C.c_void_p, PD, PD, PD, PD, C.c_char_p, C.c_int]),
+    "sfw_wform_run": (C.c_int, [C.c_void_p, C.c_int, C.c_int, PD, PD, PD, PF, C.c_char_p, C.c_int]),
+    "sfw_wform_state": (C.c_int, [C.c_void_p, PD, PD, C.c_char_p, C.c_int]),
+    "sfw_wform_traffic": (C.c_int, [C.c_void_p, PD, PD]),
+    "sfw_wform_destroy": (C.c_int, [C.c_void_p]),
     "sfw_source_vector": (C.c_int, [C.c_int, C.c_int, PD, PD, C.c_double, PD, PD, C.c_char_p, C.c_int]),
     "sfw_probe_weights": (C.c_int, [C.c_int, C.c_int, PD, PD, C.c_double, PD, C.c_char_p, C.c_int]),
 }

@@ -130,11 +130,18 @@ class CoupledStepper:
     """
 
     def __init__(self, models: dict, dt: float, sources: Sequence[SourceTerm] = (), workers: int = 1,
-                 device_coefficients=None):
+                 device_coefficients=None, precision: str = "fp64"):
         """``device_coefficients``: optional (gammas, gamma_hats, scales) device
         addresses holding the chain stacks of all models in sorted(alpha) order
         (as ``build_models(..., device_out=...)`` writes them); the host arrays
-        of the models are then not needed."""
+        of the models are then not needed.
+
+        ``precision``: "fp64" (U-form, the reference's arithmetic) or "fp32"
+        (the W-form variant of SURVEY 8c.4: U_j = G_j W_j, Lanczos block-
+        tridiagonal operator, half the bytes; within 1e-4 of fp64)."""
+        if precision not in ("fp64", "fp32"):
+            raise ConfigError("precision must be 'fp64' or 'fp32'")
+        self.precision = precision
         if dt <= 0:
             raise ConfigError(f"time step must be positive, got {dt}")
         self.models = dict(models)
@@ -240,6 +247,12 @@ class CoupledStepper:
         self._h = h
         self._lib = lib
         self._m = m
+        self._src_vec_u = src_vec
+        self._probe_w_u = None
+        if self.precision == "fp32":
+            rc = lib.sfw_wform_setup(h, eb, 1024)
+            _lib.check(rc, eb)
+            self._wform_vectors()
 
     def _set_probes(self, probes: Sequence[Probe]):
         key = tuple((p.alpha, id(p.weights)) for p in probes)
@@ -258,11 +271,24 @@ class CoupledStepper:
         _lib.check(rc, eb)
         self._probe_key = key
         self._probes = tuple(probes)
+        self._probe_w_u = w
+        if self.precision == "fp32":
+            self._wform_vectors()
+
+    def _wform_vectors(self):
+        norms = np.zeros(max(1, len(self.sources)))
+        eb = _lib.errbuf()
+        rc = self._lib.sfw_wform_vectors(self._h, _lib.dptr(self._src_vec_u), _lib.dptr(self._probe_w_u),
+                                         _lib.dptr(norms), eb, 1024)
+        _lib.check(rc, eb)
+        self._src_norms_w = norms[:len(self.sources)].tolist()
 
     # -- lifecycle -------------------------------------------------------------
 
     def close(self):
         if self._h is not None:
+            if self.precision == "fp32":
+                self._lib.sfw_wform_destroy(self._h)
             self._lib.sfw_step_destroy(self._h)
             self._h = None
 
@@ -299,7 +325,11 @@ class CoupledStepper:
     def _state(self):
         uc = np.empty(int(self._offs[-1]))
         up = np.empty(int(self._offs[-1]))
-        self._lib.sfw_step_get_state(self._h, _lib.dptr(uc), _lib.dptr(up))
+        if self.precision == "fp32":
+            eb = _lib.errbuf()
+            _lib.check(self._lib.sfw_wform_state(self._h, _lib.dptr(uc), _lib.dptr(up), eb, 1024), eb)
+        else:
+            self._lib.sfw_step_get_state(self._h, _lib.dptr(uc), _lib.dptr(up))
         return uc, up
 
     @property
@@ -318,6 +348,8 @@ class CoupledStepper:
 
     def _acceleration(self, states: dict, count_messages: bool = False) -> dict:
         """Acceleration of a state (stepper.py:251-311), computed on the device."""
+        if self.precision != "fp64":
+            raise ConfigError("_acceleration is defined for the fp64 U-form stepper")
         flat = self._concat(states)
         if flat is None:
             flat = np.zeros(int(self._offs[-1]))
@@ -346,8 +378,8 @@ class CoupledStepper:
         prof = self._profiles([0.0]).reshape(-1) if self.sources else None
         row0 = np.empty(max(1, len(self._probes)))
         eb = _lib.errbuf()
-        rc = self._lib.sfw_step_init(self._h, _lib.dptr(u), _lib.dptr(v), _lib.dptr(prof), _lib.dptr(row0),
-                                     eb, 1024)
+        init = self._lib.sfw_wform_init if self.precision == "fp32" else self._lib.sfw_step_init
+        rc = init(self._h, _lib.dptr(u), _lib.dptr(v), _lib.dptr(prof), _lib.dptr(row0), eb, 1024)
         _lib.check(rc, eb)
         self._row0 = row0[:len(self._probes)].copy()
         self.steps_done = 0
@@ -379,8 +411,25 @@ class CoupledStepper:
         norms = np.empty(n_steps)
         bad = C.c_int(0)
         eb = _lib.errbuf()
-        rc = self._lib.sfw_step_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(limits),
-                                    _lib.dptr(rows), _lib.dptr(norms), C.byref(bad), eb, 1024)
+        if self.precision == "fp32":
+            # W-form: |W| against the same detector rule with W-form source norms
+            base = self._baseline
+            for k in range(n_steps):
+                for i in range(len(self.sources)):
+                    base += dt * dt * abs(float(prof[i, k])) * self._src_norms_w[i]
+                limits[k] = GROWTH_LIMIT * max(base, 1e-300)
+            ms = C.c_float(0.0)
+            rc = self._lib.sfw_wform_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(rows),
+                                         _lib.dptr(norms), C.byref(ms), eb, 1024)
+            self.last_kernel_ms = ms.value
+            if rc == 0:
+                over = np.nonzero(~(norms <= limits))[0]
+                if over.size:
+                    rc = _lib.SFW_EINSTABLE
+                    bad.value = int(over[0]) + 1
+        else:
+            rc = self._lib.sfw_step_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(limits),
+                                        _lib.dptr(rows), _lib.dptr(norms), C.byref(bad), eb, 1024)
         if rc == _lib.SFW_EINSTABLE:
             k = bad.value
             self.steps_done += k
@@ -505,6 +554,8 @@ class CoupledStepper:
         """Discrete invariant of the coupled leapfrog (stepper.py:419-449), on the device."""
         if not self._initialized:
             raise ProtocolError("stepper not initialized")
+        if self.precision != "fp64":
+            raise ConfigError("energy() is defined for the fp64 U-form stepper")
         e = C.c_double(0.0)
         eb = _lib.errbuf()
         rc = self._lib.sfw_step_energy(self._h, C.byref(e), eb, 1024)
