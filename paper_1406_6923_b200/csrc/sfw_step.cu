@@ -324,6 +324,7 @@ struct StepParams {
     const int* ncta_ptr;     // CSR: CTAs owning face neighbours of this CTA's subdomains
     const int* ncta;
     unsigned long long* tprof;  // debug: [gridDim.x][n_steps][5] globaltimer stamps or null
+    int res_pmax, res_pdense;   // k_step_res: probes / dense probe weight vectors staged per CTA
 };
 
 __device__ __forceinline__ double leap(int mode, double uc, double uo, double v, double tot,
@@ -839,6 +840,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
     double* ms = a1 + (size_t)ns * W;                          // [ns][6][M*M]
     double* sqv = ms + (size_t)ns * 6 * M * M;                 // [ns][L]
     double* wk = sqv + (size_t)ns * L + (size_t)warp * WK;
+    // probes of this CTA (contiguous in the CSR): ids/taps and dense weights staged in SMEM
+    double* pwv = sqv + (size_t)ns * L + (size_t)NW * WK;     // [npd][K] dense weights
+    int* pmeta = reinterpret_cast<int*>(pwv + (size_t)p.res_pdense * K);  // [np][2]: id, tap-or-dense-slot
+    // per-subdomain metadata kept in SMEM: the per-step flag acquire invalidates L1
+    __shared__ int s_nbr[4 * 6 * 8];     // [ns][6] (ns <= 32 supported; checked on the host)
+    __shared__ int s_src[32 + 1];        // source range begin per local subdomain (CSR)
+    __shared__ int s_prb[32 + 1];        // probe range begin per local subdomain (CSR)
     double* xs = wk;
     double* ys = xs + W;
     double* part = ys + W;
@@ -852,6 +860,38 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
         for (int i = threadIdx.x; i < ns * K; i += blockDim.x) {
             U[i] = Ug0[(size_t)s0 * K + i];
             U[ns * K + i] = Ug1[(size_t)s0 * K + i];
+        }
+        {
+            const int pa = p.prb_ptr[s0], pb = p.prb_ptr[s1];
+            if (threadIdx.x == 0) {
+                int nd = 0;
+                for (int q = pa; q < pb && q - pa < p.res_pmax; ++q) {
+                    const int pid = p.prb_ids[q];
+                    const int tap = p.prb_tap[pid];
+                    pmeta[2 * (q - pa)] = pid;
+                    if (tap >= 0) {
+                        pmeta[2 * (q - pa) + 1] = tap;
+                    } else if (nd < p.res_pdense) {
+                        pmeta[2 * (q - pa) + 1] = -1 - nd;  // dense slot
+                        ++nd;
+                    } else {
+                        pmeta[2 * (q - pa) + 1] = -1000000;  // dense, weights from global
+                    }
+                }
+            }
+            __syncthreads();
+            for (int q = pa + warp; q < pb && q - pa < p.res_pmax; q += NW) {
+                const int slot = pmeta[2 * (q - pa) + 1];
+                if (slot < 0 && slot > -1000000) {
+                    const double* wv = p.prb_w + p.prb_woff[pmeta[2 * (q - pa)]];
+                    for (int i = lane; i < K; i += 32) pwv[(size_t)(-1 - slot) * K + i] = wv[i];
+                }
+            }
+        }
+        for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nbr[i] = p.nbr[s0 * 6 + i];
+        for (int i = threadIdx.x; i <= ns; i += blockDim.x) {
+            s_src[i] = p.src_ptr[s0 + i];
+            s_prb[i] = p.prb_ptr[s0 + i];
         }
         for (int i = threadIdx.x; i < ns * 6 * M * M; i += blockDim.x) {
             const int sl = i / (6 * M * M), f = (i / (M * M)) % 6, e = i % (M * M);
@@ -921,7 +961,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
                 const int s = s0 + sl;
                 for (int i = lane; i < W; i += 32) {
                     const int g = sl * K + j * W + i;
-                    const double tot = add_force(p, s, (long long)j * W + i, kk, ys[i]);
+                    const double tot = (s_src[sl] == s_src[sl + 1]) ? ys[i] : add_force(p, s, (long long)j * W + i, kk, ys[i]);
                     const double un = __dadd_rn(__dsub_rn(__dmul_rn(2.0, Uc[g]), Un[g]), __dmul_rn(dt2, tot));
                     Un[g] = un;
                     sq = fma(un, un, sq);
@@ -944,7 +984,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
             double sq = 0.0;
             for (int i = lane; i < W; i += 32) {
                 const int f = i / M, r = i % M;
-                const int nb = p.nbr[s * 6 + f];
+                const int nb = s_nbr[sl * 6 + f];
                 double a;
                 if (nb >= 0) {
                     const double* mx = ms + (sl * 6 + f) * M * M + r * M;
@@ -956,7 +996,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
                 } else {
                     a = a1[sl * W + i];
                 }
-                const double tot = add_force(p, s, i, kk, a);
+                const double tot = (s_src[sl] == s_src[sl + 1]) ? a : add_force(p, s, i, kk, a);
                 const int g = sl * K + i;
                 const double un = __dadd_rn(__dsub_rn(__dmul_rn(2.0, Uc[g]), Un[g]), __dmul_rn(dt2, tot));
                 Un[g] = un;
@@ -968,18 +1008,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
                 for (int j = 1; j < L; ++j) t += sqv[sl * L + j];
                 p.sub_norm[s] = t;
             }
-            if (k % p.record_every == 0 && p.rows && p.prb_ptr[s] < p.prb_ptr[s + 1]) {
+            if (k % p.record_every == 0 && p.rows && s_prb[sl] < s_prb[sl + 1]) {
                 __syncwarp();
                 const double* Us = Un + (size_t)sl * K;
                 const long long row = k / p.record_every - 1;
-                for (int pq = p.prb_ptr[s]; pq < p.prb_ptr[s + 1]; ++pq) {
-                    const int pid = p.prb_ids[pq];
-                    const int tap = p.prb_tap[pid];
+                const int pa = s_prb[0];
+                for (int pq = s_prb[sl]; pq < s_prb[sl + 1]; ++pq) {
+                    const bool staged = pq - pa < p.res_pmax;
+                    const int pid = staged ? pmeta[2 * (pq - pa)] : p.prb_ids[pq];
+                    const int tap = staged ? pmeta[2 * (pq - pa) + 1] : p.prb_tap[pid];
                     double val;
                     if (tap >= 0) {
                         val = Us[tap];
                     } else {
-                        const double* wv = p.prb_w + p.prb_woff[pid];
+                        const double* wv = (tap > -1000000) ? pwv + (size_t)(-1 - tap) * K : p.prb_w + p.prb_woff[pid];
                         double acc = 0.0;
                         for (int i = lane; i < K; i += 32) acc = fma(wv[i], Us[i], acc);
                         val = warp_sum(acc);
@@ -1604,14 +1646,17 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
             for (int b = 0; b < h->grid; ++b) maxns = std::max(maxns, cta_res_ns(h, b));
             const int L = h->L, K = L * W;
             const int nwr = (m <= 4) ? 16 : 8;
+            h->res_pmax = 1024;
+            h->res_pdense = 8;
             const size_t need = 8 * ((size_t)maxns * 2 * L * 21 * m * m + (size_t)2 * maxns * K + (size_t)maxns * K +
                                      (size_t)maxns * W + (size_t)maxns * 6 * m * m + (size_t)maxns * L +
-                                     (size_t)nwr * (2 * W + 42 * m));
+                                     (size_t)nwr * (2 * W + 42 * m) + (size_t)h->res_pdense * K) +
+                                4 * 2 * (size_t)h->res_pmax;
             const void* kr = nullptr;
             if (m == 1) kr = (const void*)k_step_res<1, 16>;
             if (m == 4) kr = (const void*)k_step_res<4, 16>;
             if (m == 9) kr = (const void*)k_step_res<9, 8>;
-            if (kr && need <= 220 * 1024 && maxns <= nwr) {  // layer-1 flux items map to warps 0..ns-1
+            if (kr && need <= 220 * 1024 && maxns <= nwr && maxns <= 32) {  // layer-1 flux items map to warps 0..ns-1
                 h->kres = kr;
                 h->res_smem = (int)need;
                 h->res_nw = nwr;
@@ -1692,6 +1737,8 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
     p.L = h->L;
     p.state_len = h->state_len;
     p.tprof = nullptr;
+    p.res_pmax = h->res_pmax;
+    p.res_pdense = h->res_pdense;
     if (mode == 0 && getenv("SFW_STEP_PROF")) {
         static unsigned long long* tp = nullptr;
         static size_t tpn = 0;

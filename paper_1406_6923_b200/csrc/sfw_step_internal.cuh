@@ -66,7 +66,7 @@ struct sfw_stepper {
     int L = 0;
     const void* kfn = nullptr;
     const void* kres = nullptr;
-    int res_smem = 0, res_nw = 0;
+    int res_smem = 0, res_nw = 0, res_pmax = 0, res_pdense = 0;
     std::vector<int> cta_ptr_h;
     unsigned long long* tprof = nullptr;
     size_t tprof_n = 0;
