@@ -378,10 +378,53 @@ def run_ours(args):
                       "cfl_seconds": cfl_s, "cfl_iterations": cfl_iters,
                       "k_step2_launches_before_timed": (cfl_iters or 0) + 2},
     }
-    print(json.dumps(line), flush=True)
     st.close()
+    if args.extra and args.config == 2:
+        try:
+            line["extra"] = _extra_config3(args)
+        except Exception as exc:  # the headline line must still print
+            line["extra"] = {"config3": {"error": str(exc)[:200]}}
+    print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def _extra_config3(args):
+    """Kernel-only stepping of config 3 (4096 x m9k8, the HBM-bound case) for the roofline picture."""
+    import ctypes as C
+
+    import torch
+    from paper_1406_6923_b200 import CoupledStepper, _lib, build_models, cfl_estimate_coupled
+    wl, ops, alphas, _, _ = _workload(3)
+    n_sub, w, L = len(ops), wl.width, wl.layers
+    dev = [torch.empty(n_sub * L * w * w, dtype=torch.float64, device="cuda") for _ in range(3)]
+    ptrs = tuple(t.data_ptr() for t in dev)
+    t0 = time.perf_counter()
+    models = build_models(ops, wl.modes_per_face, wl.n, wl.shift, device_out=ptrs)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    lam, conv = cfl_estimate_coupled(models, device_coefficients=ptrs)
+    dt = 0.9 * 2.0 / math.sqrt(lam)
+    st = CoupledStepper(models, dt, device_coefficients=ptrs)
+    st.initialize()
+    ms = C.c_float(0.0)
+    eb = _lib.errbuf()
+    _lib.check(st._lib.sfw_step_run_resident(st._h, 5, 1, None, C.byref(ms), eb, 1024), eb)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    flush.fill_(1.0)
+    torch.cuda.synchronize()
+    K3 = 300
+    _lib.check(st._lib.sfw_step_run_resident(st._h, K3, 1, None, C.byref(ms), eb, 1024), eb)
+    b, f, sb = st.traffic()
+    st.close()
+    peak, _ = _peaks()
+    sec = ms.value * 1e-3
+    return {"config3": {"workload": _describe(wl), "subdomains": n_sub, "steps": K3, "ms_per_step": ms.value / K3,
+                        "value": n_sub * K3 / sec, "unit": UNIT,
+                        "roofline": {"bound": "hbm", "achieved": b * K3 / sec / 1e9, "peak": peak, "unit": "GB/s",
+                                     "frac": b * K3 / sec / 1e9 / peak},
+                        "rom_build_seconds": build_s, "rom_build_subdomains_per_s": n_sub / build_s,
+                        "cfl_converged": conv}}
 
 
 def _run_fp32(args, wl, models, ptrs, dt, lam, conv, src, probes, ws, rank, build_s, build_stats, cfl_s, cfl_iters):
@@ -507,6 +550,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--extra", type=int, default=1, help="also measure config 3 kernel-only stepping (default on)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":
