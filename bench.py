@@ -331,8 +331,8 @@ def run_ours(args):
         try:
             tj = json.load(open(tfile))
             ent = tj.get(f"config{args.config}")
-            if ent:
-                traffic = ent.get("dram_bytes_per_step")
+            if ent:  # per launch, like achieved: ncu DRAM bytes per step x the K steps of this launch
+                traffic = ent.get("dram_bytes_per_step") * K
         except Exception:
             traffic = None
     # CPU baseline: the oracle (reference algorithm) stepping the same models, bounded sample
@@ -367,6 +367,7 @@ def run_ours(args):
                 "api": "CoupledStepper.run(K, probes) incl. init, profile/limit upload, trace/norm download"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "alg_bytes_per_launch": alg_bytes * K,
                      "alg_bytes_per_step": alg_bytes, "streamed_bytes_per_step": streamed,
                      "alg_flops_per_step": alg_flops,
                      "formula": "8[(2L-1)w(w+1)/2 + 3Lw] bytes per subdomain-step (SURVEY 8d)"},
