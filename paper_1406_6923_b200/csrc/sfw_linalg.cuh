@@ -312,4 +312,28 @@ __device__ inline double sm_cond2(const double* A, double* W, int n, double* red
     return smax / smin;
 }
 
+// Condition check for "cond2(A) > limit" (numpy.linalg.cond semantics) from an existing
+// LU factorisation of A (or A^T): cond_F = |A|_F |A^-1|_F satisfies cond_F/n <= cond2 <= cond_F,
+// so the decision is exact unless cond_F falls in [limit, n*limit], where the exact one-sided
+// Jacobi SVD of A decides.  Returns a value on the same side of limit as cond2(A).
+// Wk, Wk2: n x n workspaces; A is left untouched.
+__device__ inline double sm_cond2_check(const double* A, const double* LU, const int* piv, double* Wk, double* Wk2,
+                                        int n, double limit, double* red, int* flag) {
+    double fa = 0.0;
+    for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+        fa = fma(A[i], A[i], fa);
+        Wk[i] = (i / n == i % n) ? 1.0 : 0.0;
+    }
+    fa = block_sum(fa, red);
+    sm_lu_solve(LU, piv, Wk, n, n);  // Wk = A^-1 (or A^-T): same Frobenius norm
+    double fi = 0.0;
+    for (int i = threadIdx.x; i < n * n; i += blockDim.x) fi = fma(Wk[i], Wk[i], fi);
+    fi = block_sum(fi, red);
+    const double cf = sqrt(fa) * sqrt(fi);
+    if (!(cf == cf) || isinf(cf)) return __longlong_as_double(0x7ff0000000000000LL);
+    if (cf <= limit) return cf;
+    if (cf / n > limit) return cf / n;
+    return sm_cond2(A, Wk2, n, red, flag);
+}
+
 }  // namespace sfw

@@ -194,7 +194,11 @@ template <int PT>
 __device__ __forceinline__ void line_pass(double* z, const double* Q, int n, int nlines, int stride, int lstride_a,
                                           int lstride_b, int nb_inner, bool fwd) {
     // line l -> base = (l / nb_inner) * lstride_a + (l % nb_inner) * lstride_b
+    // PT > 0: Q points at the direction-specific compact table Qd[i][k] (row stride QS = PT+1,
+    //         16-B aligned rows) with y[k] = sum_i Qd[i][k] v[i]  -> 128-bit loads of Q pairs.
+    // PT = 0: generic n <= PMAX, Q is the PMAX x PMAX table (forward Q[i][k], backward Q[k][i]).
     constexpr int PN = PT > 0 ? PT : PMAX;
+    constexpr int QS = PT > 0 ? ((PT + 1) & ~1) : PMAX;
     for (int l = threadIdx.x; l < nlines; l += blockDim.x) {
         const int base = (l / nb_inner) * lstride_a + (l % nb_inner) * lstride_b;
         double v[PN], y[PN];
@@ -204,9 +208,16 @@ __device__ __forceinline__ void line_pass(double* z, const double* Q, int n, int
 #pragma unroll
             for (int k = 0; k < PN; ++k) y[k] = 0.0;
 #pragma unroll
-            for (int i = 0; i < PN; ++i)
+            for (int i = 0; i < PN; ++i) {
+                const double* qr = Q + i * QS;
 #pragma unroll
-                for (int k = 0; k < PN; ++k) y[k] = fma(fwd ? Q[i * PN + k] : Q[k * PN + i], v[i], y[k]);
+                for (int k = 0; k + 1 < PN; k += 2) {
+                    const double2 q = *reinterpret_cast<const double2*>(qr + k);
+                    y[k] = fma(q.x, v[i], y[k]);
+                    y[k + 1] = fma(q.y, v[i], y[k + 1]);
+                }
+                if (PN & 1) y[PN - 1] = fma(qr[PN - 1], v[i], y[PN - 1]);
+            }
 #pragma unroll
             for (int k = 0; k < PN; ++k) z[base + k * stride] = y[k];
         } else {
@@ -226,13 +237,15 @@ template <int PT>
 __global__ void __launch_bounds__(512, 1) k_pcg(const PcgArgs a) {
     extern __shared__ __align__(16) double sh[];
     const int N = a.N, px = PT > 0 ? PT : a.px, py = PT > 0 ? PT : a.py, pz = PT > 0 ? PT : a.pz;
+    constexpr int QS = PT > 0 ? ((PT + 1) & ~1) : PMAX;        // compact row stride
+    constexpr int QT = PT > 0 ? PT * QS : PMAX * PMAX;        // one table
     double* c = sh;
-    double* x = c + N;
-    double* r = x + N;
+    double* ic = c + N;                // 1/c
+    double* r = ic + N;
     double* p = r + N;
     double* z = p + N;
-    double* Q = z + N;                 // 3 * PMAX*PMAX
-    double* lam = Q + 3 * PMAX * PMAX; // 3 * PMAX
+    double* Q = sh + ((5 * N + 1) & ~1);  // 16-B aligned;  PT > 0: [3 axes][fwd, bwd][PT][QS];  PT = 0: [3][PMAX*PMAX]
+    double* lam = Q + (PT > 0 ? 6 : 3) * QT;
     double* dd = lam + 3 * PMAX;
     double* ee = dd + 3 * PMAX;
     double* red = ee + 3 * PMAX;       // 40
@@ -242,7 +255,16 @@ __global__ void __launch_bounds__(512, 1) k_pcg(const PcgArgs a) {
     for (int ax = 0; ax < 3; ++ax) {
         const int pat = ((mask >> (2 * ax)) & 1) | (((mask >> (2 * ax + 1)) & 1) << 1);
         const int n = P[ax];
-        for (int i = threadIdx.x; i < n * n; i += blockDim.x) Q[ax * PMAX * PMAX + i] = a.Qt[(ax * 4 + pat) * PMAX * PMAX + i];
+        const double* Qg = a.Qt + (size_t)(ax * 4 + pat) * PMAX * PMAX;  // compact n x n, row-major
+        if (PT > 0) {
+            for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+                const int i = idx / n, k = idx % n;
+                Q[(2 * ax) * QT + i * QS + k] = Qg[idx];          // forward:  Qd[i][k] = Q[i][k]
+                Q[(2 * ax + 1) * QT + k * QS + i] = Qg[idx];      // backward: Qd[i][k] = Q[k][i]
+            }
+        } else {
+            for (int i = threadIdx.x; i < n * n; i += blockDim.x) Q[ax * QT + i] = Qg[i];
+        }
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             lam[ax * PMAX + i] = a.lamt[(ax * 4 + pat) * PMAX + i];
             dd[ax * PMAX + i] = a.dt[(ax * 4 + pat) * PMAX + i];
@@ -251,15 +273,17 @@ __global__ void __launch_bounds__(512, 1) k_pcg(const PcgArgs a) {
     }
     const double* cg = a.c + (size_t)b * N;
     const double* bg = a.rhs + (size_t)b * a.sR + (size_t)j * a.ldn;
+    double* og = a.out + (size_t)b * a.sO + (size_t)j * a.ldn;  // accumulates -x
     double cmin = 1e308, cmax = 0.0, bb = 0.0;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         const double ci = cg[i];
         c[i] = ci;
+        ic[i] = 1.0 / ci;
         cmin = fmin(cmin, ci);
         cmax = fmax(cmax, ci);
         const double bi = bg[i];
         r[i] = bi;
-        x[i] = 0.0;
+        og[i] = 0.0;
         bb = fma(bi, bi, bb);
     }
     cmax = block_max(cmax, red);
@@ -268,22 +292,24 @@ __global__ void __launch_bounds__(512, 1) k_pcg(const PcgArgs a) {
     const double sigma = a.shift / (cmin * cmax);
     const double s = a.shift;
     const int sy = pz, sx = py * pz;
+    auto Qf = [&](int ax) { return PT > 0 ? Q + (2 * ax) * QT : Q + ax * QT; };
+    auto Qb = [&](int ax) { return PT > 0 ? Q + (2 * ax + 1) * QT : Q + ax * QT; };
 
     auto precond = [&]() {  // z = P^-1 r
-        for (int i = threadIdx.x; i < N; i += blockDim.x) z[i] = r[i] / c[i];
+        for (int i = threadIdx.x; i < N; i += blockDim.x) z[i] = r[i] * ic[i];
         __syncthreads();
-        line_pass<PT>(z, Q + 0 * PMAX * PMAX, px, py * pz, sx, 1, 1, py * pz, true);      // x lines: base = l
-        line_pass<PT>(z, Q + 1 * PMAX * PMAX, py, px * pz, sy, sx, 1, pz, true);          // y lines
-        line_pass<PT>(z, Q + 2 * PMAX * PMAX, pz, px * py, 1, pz, 0, 1, true);            // z lines: base = l*pz
+        line_pass<PT>(z, Qf(0), px, py * pz, sx, 1, 1, py * pz, true);      // x lines: base = l
+        line_pass<PT>(z, Qf(1), py, px * pz, sy, sx, 1, pz, true);          // y lines
+        line_pass<PT>(z, Qf(2), pz, px * py, 1, pz, 0, 1, true);            // z lines: base = l*pz
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
             const int ix = i / sx, iy = (i / sy) % py, iz = i % pz;
-            z[i] = z[i] / (((lam[ix] + lam[PMAX + iy]) + lam[2 * PMAX + iz]) + sigma);
+            z[i] = z[i] * __drcp_rn(((lam[ix] + lam[PMAX + iy]) + lam[2 * PMAX + iz]) + sigma);
         }
         __syncthreads();
-        line_pass<PT>(z, Q + 2 * PMAX * PMAX, pz, px * py, 1, pz, 0, 1, false);
-        line_pass<PT>(z, Q + 1 * PMAX * PMAX, py, px * pz, sy, sx, 1, pz, false);
-        line_pass<PT>(z, Q + 0 * PMAX * PMAX, px, py * pz, sx, 1, 1, py * pz, false);
-        for (int i = threadIdx.x; i < N; i += blockDim.x) z[i] = z[i] / c[i];
+        line_pass<PT>(z, Qb(2), pz, px * py, 1, pz, 0, 1, false);
+        line_pass<PT>(z, Qb(1), py, px * pz, sy, sx, 1, pz, false);
+        line_pass<PT>(z, Qb(0), px, py * pz, sx, 1, 1, py * pz, false);
+        for (int i = threadIdx.x; i < N; i += blockDim.x) z[i] = z[i] * ic[i];
         __syncthreads();
     };
 
@@ -322,7 +348,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(const PcgArgs a) {
         const double alpha = rho / pq;
         double rr = 0.0;
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
-            x[i] = fma(alpha, p[i], x[i]);
+            og[i] = fma(-alpha, p[i], og[i]);  // og = -x
             const double ri = fma(-alpha, z[i], r[i]);
             r[i] = ri;
             rr = fma(ri, ri, rr);
@@ -341,8 +367,6 @@ __global__ void __launch_bounds__(512, 1) k_pcg(const PcgArgs a) {
         for (int i = threadIdx.x; i < N; i += blockDim.x) p[i] = fma(beta, p[i], z[i]);
         __syncthreads();
     }
-    double* og = a.out + (size_t)b * a.sO + (size_t)j * a.ldn;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) og[i] = -x[i];
     if (threadIdx.x == 0) a.iters[blockIdx.x] = status;
 }
 
@@ -534,7 +558,15 @@ __global__ void k_sfraction(const double* __restrict__ Td, const double* __restr
     }
     __syncthreads();
     for (int j = 0; j < L; ++j) {
-        const double cg = sm_cond2(G, Wk, w, red, &flag);
+        // LU of G^T (used by the congruence below) also gives the condition check
+        for (int idx = threadIdx.x; idx < ww; idx += blockDim.x) {
+            const int i = idx / w, k = idx % w;
+            LU[idx] = G[k * w + i];
+        }
+        __syncthreads();
+        const bool lu_ok = sm_lu(LU, piv, w, &flag);
+        const double cg = lu_ok ? sm_cond2_check(G, LU, piv, Wk, Y, w, 1e12, red, &flag)
+                                : __longlong_as_double(0x7ff0000000000000LL);
         if (threadIdx.x == 0) condv[(size_t)b * 2 * Ls + 2 * j] = cg;
         if (!(cg <= 1e12)) {
             st = 10 + j;
@@ -544,16 +576,8 @@ __global__ void k_sfraction(const double* __restrict__ Td, const double* __restr
         sm_matmul(G, false, G, true, Wk, w);  // hat = G G^T
         for (int idx = threadIdx.x; idx < ww; idx += blockDim.x) hb[(size_t)j * ww + idx] = Wk[idx];
         // congruence: y = solve(G^T, A_j); z = solve(G^T, y^T)^T; sym   (rom.py:265-269)
-        for (int idx = threadIdx.x; idx < ww; idx += blockDim.x) {
-            const int i = idx / w, k = idx % w;
-            LU[idx] = G[k * w + i];
-            Y[idx] = Tb[(size_t)j * ww + idx];
-        }
+        for (int idx = threadIdx.x; idx < ww; idx += blockDim.x) Y[idx] = Tb[(size_t)j * ww + idx];
         __syncthreads();
-        if (!sm_lu(LU, piv, w, &flag)) {
-            st = 30;
-            break;
-        }
         sm_lu_solve(LU, piv, Y, w, w);
         for (int idx = threadIdx.x; idx < ww; idx += blockDim.x) {
             const int i = idx / w, k = idx % w;
@@ -569,7 +593,11 @@ __global__ void k_sfraction(const double* __restrict__ Td, const double* __restr
         __syncthreads();
         for (int idx = threadIdx.x; idx < ww; idx += blockDim.x) gb[(size_t)j * ww + idx] = Gm[idx];
         if (j + 1 < L) {
-            const double cl = sm_cond2(Gm, Wk, w, red, &flag);
+            for (int idx = threadIdx.x; idx < ww; idx += blockDim.x) Y[idx] = Gm[idx];
+            __syncthreads();
+            const bool gl_ok = sm_lu(Y, piv, w, &flag);
+            const double cl = gl_ok ? sm_cond2_check(Gm, Y, piv, Wk, LU, w, 1e12, red, &flag)
+                                    : __longlong_as_double(0x7ff0000000000000LL);
             if (threadIdx.x == 0) condv[(size_t)b * 2 * Ls + 2 * j + 1] = cl;
             if (!(cl <= 1e12)) {
                 st = 20 + j;
@@ -708,7 +736,9 @@ extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf
                  d->shift, hint);
         return fail(SFW_ENUMERICAL, msg, errbuf, errlen);
     }
-    const size_t pcg_smem = (size_t)(5 * N + 3 * PMAX * PMAX + 9 * PMAX + 40) * 8;
+    const bool p17 = (px == 17 && py == 17 && pz == 17);
+    const size_t pcg_smem = p17 ? (size_t)(5 * N + 1 + 6 * 17 * 18 + 9 * PMAX + 40) * 8
+                                : (size_t)(5 * N + 1 + 3 * PMAX * PMAX + 9 * PMAX + 40) * 8;
     if (pcg_smem > 227 * 1024)
         return fail(SFW_ECONFIG, "subdomain too large for the shared-memory PCG (N <= ~5100 nodes)", errbuf, errlen);
 
@@ -794,7 +824,6 @@ extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf
     pa.dt = ddt;
     pa.et = det;
     pa.iters = it;
-    const bool p17 = (px == 17 && py == 17 && pz == 17);
     const void* pcg_fn = p17 ? (const void*)k_pcg<17> : (const void*)k_pcg<0>;
     cudaFuncSetAttribute(pcg_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem);
     const size_t cq_smem = 2 * ww * 8;
