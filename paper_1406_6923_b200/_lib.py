@@ -14,7 +14,7 @@ import numpy as np
 
 from .errors import (ConfigError, DeviceError, InstabilityError, NumericalError, ProtocolError)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsfw_b200.so")
+LIB_PATH = os.environ.get("SFW_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsfw_b200.so")
 
 SFW_ECONFIG, SFW_ENUMERICAL, SFW_EINSTABLE, SFW_EPROTOCOL, SFW_ECUDA = -1, -2, -3, -4, -5
 

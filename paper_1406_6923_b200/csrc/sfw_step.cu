@@ -220,21 +220,13 @@ struct RedOff7 {
         for (int e = 0; e < EPL; ++e) {
             const int i = lane + 32 * e;
             const int R = i < W ? i / M : 0, r = i < W ? i % M : 0;
-            int n = 0;
+            // slot n (compile-time): tiles t < R (row partials), the diagonal tile's row
+            // and column partials, then tiles t > R (column partials)
 #pragma unroll
-            for (int t = 0; t < 6; ++t) {
-                if (t < R) {
-                    o[e][n] = r * 21 + off_tile(R, t);
-                } else if (t == R) {
-                    o[e][n] = r * 21 + 15 + R;
-                } else {
-                    o[e][n] = (M + r) * 21 + off_tile(t, R);
-                }
-                n = n + 1;
-                if (t == R) {
-                    o[e][n] = (M + r) * 21 + 15 + R;
-                    n = n + 1;
-                }
+            for (int n = 0; n < 7; ++n) {
+                const int pr = r * 21 + (n < R ? off_tile(R, n) : 15 + R);
+                const int qr = (M + r) * 21 + (n == R + 1 ? 15 + R : off_tile(n > 0 ? n - 1 : 0, R));
+                o[e][n] = n <= R ? pr : qr;
             }
         }
     }
@@ -283,6 +275,46 @@ __device__ __forceinline__ void sym_matvec_full(const double* __restrict__ blk, 
     __syncwarp();
 }
 
+// w <= 32 variant: lane i returns y[i] in a register (no y staging in SMEM).
+template <int M>
+__device__ __forceinline__ double sym_matvec_lane(const double* __restrict__ blk, const double* x, double* part,
+                                                  int lane, const RedOff7<M>& ro) {
+    static_assert(6 * M <= 32, "one lane per row");
+    if (lane < 21) {
+        const int I = lane < 15 ? off_I(lane) : lane - 15;
+        const int K = lane < 15 ? off_K(lane) : lane - 15;
+        double xk[M], xi[M], P[M], Q[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            xk[i] = x[K * M + i];
+            xi[i] = x[I * M + i];
+            P[i] = 0.0;
+            Q[i] = 0.0;
+        }
+        const double* b = blk + lane;
+#pragma unroll
+        for (int e = 0; e < M * M; ++e) {
+            const int r = e % M, c = (e / M + r) % M;
+            const double a = b[e * 21];
+            P[r] = fma(a, xk[c], P[r]);
+            Q[c] = fma(a, xi[r], Q[c]);
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            part[i * 21 + lane] = P[i];
+            part[(M + i) * 21 + lane] = Q[i];
+        }
+    }
+    __syncwarp();
+    double y = 0.0;
+    if (lane < 6 * M) {
+        y = part[ro.o[0][0]];
+#pragma unroll
+        for (int t = 1; t < 7; ++t) y += part[ro.o[0][t]];
+    }
+    return y;
+}
+
 struct StepParams {
     int n_sub, BS, n_steps, mode, cur, record_every, n_probe, ftab_stride;
     int evict_first;
@@ -325,6 +357,9 @@ struct StepParams {
     const int* ncta;
     unsigned long long* tprof;  // debug: [gridDim.x][n_steps][5] globaltimer stamps or null
     int res_pmax, res_pdense;   // k_step_res: probes / dense probe weight vectors staged per CTA
+    unsigned long long* mbox;   // k_step_lw: tagged face mailbox [2][n_sub][W] x {lo|tag, hi|tag}
+    unsigned int tag_base;      // k_step_lw: step tag of this launch's step 0
+    int groups;                 // k_step_lw: subdomain groups (norm partials) per CTA
 };
 
 __device__ __forceinline__ double leap(int mode, double uc, double uo, double v, double tot,
@@ -335,6 +370,8 @@ __device__ __forceinline__ double leap(int mode, double uc, double uo, double v,
     if (mode == 2) return tot;
     return __dadd_rn(__dsub_rn(uc, __dmul_rn(dt, v)), __dmul_rn(half, tot));
 }
+
+__device__ __noinline__ double add_force_cold(const StepParams& p, int s, long long idx, int k, double acc);
 
 // total = acc + sum_src vec * f(t)   (stepper.py:313-321 superposes in list order)
 __device__ __forceinline__ double add_force(const StepParams& p, int s, long long idx, int k,
@@ -348,6 +385,11 @@ __device__ __forceinline__ double add_force(const StepParams& p, int s, long lon
         f = (q == a) ? term : __dadd_rn(f, term);
     }
     return __dadd_rn(acc, f);
+}
+
+// out-of-line copy for the resident kernels' rare > 2-sources case (keeps their loop small)
+__device__ __noinline__ double add_force_cold(const StepParams& p, int s, long long idx, int k, double acc) {
+    return add_force(p, s, idx, k, acc);
 }
 
 template <int M, int NW, int NS>
@@ -937,6 +979,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
             if (q < ns) {  // this warp produced a layer-1 flux (warps 0..ns-1, first pass)
                 asm volatile("bar.sync 1, %0;" ::"r"(ns * 32) : "memory");
                 if (threadIdx.x == 0) flag_publish(p.bar, (unsigned int)k);
+                stamp(4);  // debug: publish time
             }
         }
         __syncthreads();
@@ -1034,7 +1077,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
         // (layer 1 of U) is the layer-1 flux item of the same subdomain, which the
         // item order maps to this same warp; other warps may start interior-layer
         // fluxes of the next step while round 3 finishes.
-        stamp(4);
     }
     __syncthreads();
     // write both time levels back (global layout as k_step2: U[cur ^ (n & 1)] is current)
@@ -1051,6 +1093,645 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
         double t = 0.0;
         for (int s = s0; s < s1; ++s) t += p.sub_norm[s];
         p.norm_part[(size_t)(p.n_steps - 1) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// k_step_lw: layer-warp SMEM-resident variant for small-m configurations
+// (config 2: 512 x m4k6, <= 4 subdomains per CTA, w = 24 <= 32).
+//
+// Warp (g, j) owns layer j of the CTA's g-th subdomain for the whole launch:
+// U_j (current, previous) live in its registers, its two chain blocks in SMEM.
+// Per step: phase 1 flux_j = Gamma_j (U_{j+1} - U_j); phase 2 acc_j =
+// Gamma-hat_j (flux_j - flux_{j-1}) and the leapfrog.  The two phases of one
+// subdomain meet on two named barriers (the layer-1 warp only arrives on the
+// first, the last-layer warp only on the second), so groups run independently.
+//
+// Face exchange goes through a tagged mailbox instead of a flag + data pair:
+// each fp64 face value is stored as two 64-bit words {32 data bits | step tag}
+// (single-copy atomic 8-byte accesses), so one poll both detects and fetches
+// the neighbour's value.  Slots are double-buffered by step parity; a producer
+// overwrites slot (k & 1) at step k+2 only after it has consumed the
+// consumer's step-(k+1) values, which depend on the consumer's step-k read.
+// Same arithmetic, in the same order, as k_step2 / k_step_res.
+__device__ __forceinline__ void mbox_put(unsigned long long* slot, double v, unsigned int tag) {
+    const unsigned long long t = (unsigned long long)tag << 32;
+    const unsigned long long a = t | (unsigned int)__double2loint(v);
+    const unsigned long long b = t | (unsigned int)__double2hiint(v);
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(a), "l"(b) : "memory");
+}
+
+// warp-collective poll: every lane re-reads until all lanes hold their tagged value, so
+// the loop never diverges (a divergent spin leaves the warp split for the rest of the
+// step: shuffles then take the slow path, ~500 cycles each, measured)
+__device__ __forceinline__ double mbox_take_warp(const unsigned long long* slot, unsigned int tag, bool want) {
+    unsigned long long a = 0, b = 0;
+    bool ok;
+    do {
+        if (want)
+            asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(slot) : "memory");
+        ok = !want || ((unsigned int)(a >> 32) == tag && (unsigned int)(b >> 32) == tag);
+    } while (!__all_sync(0xffffffffu, ok));
+    return __hiloint2double((int)(unsigned int)b, (int)(unsigned int)a);
+}
+
+__device__ __forceinline__ double mbox_take(const unsigned long long* slot, unsigned int tag) {
+    unsigned long long a, b;
+    do {
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(slot) : "memory");
+    } while ((unsigned int)(a >> 32) != tag || (unsigned int)(b >> 32) != tag);
+    return __hiloint2double((int)(unsigned int)b, (int)(unsigned int)a);
+}
+
+template <int M, int NT>
+__global__ void __launch_bounds__(NT, 1) k_step_lw(const StepParams p) {
+    constexpr int W = 6 * M;
+    static_assert(W <= 32, "one lane per chain row");
+    constexpr int WK = W + 21 * 2 * M;
+    constexpr int FB = 21 * M * M;
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const RedOff7<M> ro(lane);
+    const int L = p.L;
+    const int K = L * W;
+    const int G = p.groups;
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int ns = s1 - s0;
+    const int BS = p.BS;
+    double* cf = reinterpret_cast<double*>(smem_raw);          // [G][2L][FB]
+    double* Us = cf + (size_t)G * 2 * L * FB;                  // [G][L][W] current U
+    double* Fl = Us + (size_t)G * K;                           // [G][L][W] layer fluxes
+    double* ms = Fl + (size_t)G * K;                           // [G][6][M*M]
+    double* sqv = ms + (size_t)G * 6 * M * M;                  // [G][L]
+    double* wk = sqv + (size_t)G * L + (size_t)warp * WK;      // per-warp matvec scratch
+    double* pwv = sqv + (size_t)G * L + (size_t)nwarps * WK;   // [npd][K] dense probe weights
+    int* pmeta = reinterpret_cast<int*>(pwv + (size_t)p.res_pdense * K);
+    __shared__ int s_nbr[8 * 6];
+    __shared__ int s_src[8 + 1];
+    __shared__ int s_prb[8 + 1];
+    double* xs = wk;
+    double* part = xs + W;
+    const int g = warp / L, j = warp % L;  // subdomain group, layer
+    const bool live = g < ns;
+    const bool act = lane < W;
+
+    // ---- one-time loads (whole CTA) ----------------------------------------
+    for (int bk = warp; bk < ns * 2 * L; bk += nwarps)
+        expand_block_full<M>(p.coef + ((size_t)s0 * 2 * L + bk) * BS, cf + (size_t)bk * FB, lane, 32);
+    {
+        const int pa = p.prb_ptr[s0], pb = p.prb_ptr[s1];
+        if (threadIdx.x == 0) {
+            int nd = 0;
+            for (int q = pa; q < pb && q - pa < p.res_pmax; ++q) {
+                const int pid = p.prb_ids[q];
+                const int tap = p.prb_tap[pid];
+                pmeta[2 * (q - pa)] = pid;
+                if (tap >= 0) {
+                    pmeta[2 * (q - pa) + 1] = tap;
+                } else if (nd < p.res_pdense) {
+                    pmeta[2 * (q - pa) + 1] = -1 - nd;
+                    ++nd;
+                } else {
+                    pmeta[2 * (q - pa) + 1] = -1000000;
+                }
+            }
+        }
+        __syncthreads();
+        for (int q = pa + warp; q < pb && q - pa < p.res_pmax; q += nwarps) {
+            const int slot = pmeta[2 * (q - pa) + 1];
+            if (slot < 0 && slot > -1000000) {
+                const double* wv = p.prb_w + p.prb_woff[pmeta[2 * (q - pa)]];
+                for (int i = lane; i < K; i += 32) pwv[(size_t)(-1 - slot) * K + i] = wv[i];
+            }
+        }
+    }
+    for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nbr[i] = p.nbr[s0 * 6 + i];
+    for (int i = threadIdx.x; i <= ns; i += blockDim.x) {
+        s_src[i] = p.src_ptr[s0 + i];
+        s_prb[i] = p.prb_ptr[s0 + i];
+    }
+    for (int i = threadIdx.x; i < ns * 6 * M * M; i += blockDim.x) {
+        const int sl = i / (6 * M * M), f = (i / (M * M)) % 6, e = i % (M * M);
+        const int mi = p.mass_idx[(s0 + sl) * 6 + f];
+        ms[i] = mi >= 0 ? p.mass[(size_t)mi * M * M + e] : 0.0;
+    }
+    double uc = 0.0, up = 0.0;
+    const double* Ug0 = p.cur ? p.U1 : p.U0;
+    const double* Ug1 = p.cur ? p.U0 : p.U1;
+    if (live && act) {
+        const size_t gi = (size_t)(s0 + g) * K + j * W + lane;
+        uc = Ug0[gi];
+        up = Ug1[gi];
+        Us[(g * L + j) * W + lane] = uc;
+    }
+    __syncthreads();
+    if (!live) {  // empty group slot: zero norm partials, then leave
+        if (j == 0 && lane == 0)
+            for (int k = 0; k < p.n_steps; ++k) p.norm_part[((size_t)k * gridDim.x + blockIdx.x) * G + g] = 0.0;
+        return;
+    }
+    const int s = s0 + g;
+    // sources of this subdomain (<= 2) staged in registers: a dependent chain of global
+    // loads per step would sit on the critical path of the whole coupled grid
+    const int src_a = s_src[g], nsrc = s_src[g + 1] - s_src[g];
+    double sv0 = 0.0, sv1 = 0.0;
+    const double *ft0 = p.ftab, *ft1 = p.ftab;
+    if (nsrc >= 1 && nsrc <= 2 && act) {
+        const int q0 = p.src_ids[src_a];
+        sv0 = p.src_vec[p.src_voff[q0] + (long long)j * W + lane];
+        ft0 = p.ftab + (long long)q0 * p.ftab_stride;
+        if (nsrc == 2) {
+            const int q1 = p.src_ids[src_a + 1];
+            sv1 = p.src_vec[p.src_voff[q1] + (long long)j * W + lane];
+            ft1 = p.ftab + (long long)q1 * p.ftab_stride;
+        }
+    }
+    const int pa0 = s_prb[0], pq0 = s_prb[g], pq1 = s_prb[g + 1];
+    const double dt2 = p.dt2;
+    const int barA = 1 + 2 * g, barB = 2 + 2 * g, nthr = L * 32;
+    const double* cfj = cf + (size_t)(g * L + j) * 2 * FB;
+    double* Usj = Us + (g * L + j) * W;
+    double* Flj = Fl + (g * L + j) * W;
+    // face of this lane (layer-1 warp only)
+    const int f = lane / M, r = lane % M;
+    const int nb = (j == 0 && act) ? s_nbr[g * 6 + f] : -1;
+    unsigned long long* mb_out = p.mbox + ((size_t)s * W + lane) * 2;
+    const unsigned long long* mb_in = p.mbox + ((size_t)(nb < 0 ? 0 : nb) * W + (f ^ 1) * M + r) * 2;
+    const size_t mb_par = (size_t)p.n_sub * W * 2;
+    const double* mrow = ms + (g * 6 + (f < 6 ? f : 0)) * M * M + r * M;
+
+#ifdef SFW_LW_CLK  // debug: per-warp cycle accounting of the step phases
+    long long clk_prev = clock64(), clk_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#define LW_CLK(ph)                          \
+    {                                       \
+        const long long c_ = clock64();     \
+        clk_acc[ph] += c_ - clk_prev;       \
+        clk_prev = c_;                      \
+    }
+#else
+#define LW_CLK(ph)
+#endif
+    int rec_cnt = p.record_every;
+    long long row = -1;
+    for (int k = 1; k <= p.n_steps; ++k) {
+        const int par = k & 1;
+        const unsigned int tag = p.tag_base + (unsigned int)k;
+        const int kk = k - 1;
+        const bool rec = (--rec_cnt == 0) && p.rows;
+        if (rec_cnt == 0) {
+            rec_cnt = p.record_every;
+            ++row;
+        }
+        // this step's source amplitudes, loaded early (consumed after phase 2)
+        const double fa0 = (nsrc >= 1 && nsrc <= 2) ? ft0[kk] : 0.0;
+        const double fa1 = (nsrc == 2) ? ft1[kk] : 0.0;
+        // ---- phase 1: flux_j = Gamma_j (U_{j+1} - U_j) ----------------------
+        if (act) xs[lane] = (j + 1 < L ? Usj[W + lane] : 0.0) - uc;
+        __syncwarp();
+        LW_CLK(0);
+        const double fl = sym_matvec_lane<M>(cfj, xs, part, lane, ro);
+        if (act) Flj[lane] = fl;
+        if (nb >= 0) mbox_put(mb_out + par * mb_par, fl, tag);
+        LW_CLK(1);
+        if (j == 0)
+            asm volatile("bar.arrive %0, %1;" ::"r"(barA), "r"(nthr) : "memory");
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(barA), "r"(nthr) : "memory");
+        LW_CLK(2);
+        // ---- phase 2: acc_j = Gamma-hat_j (flux_j - flux_{j-1}), leapfrog -----
+        if (act) xs[lane] = j > 0 ? fl - Flj[lane - W] : fl;
+        __syncwarp();
+        double a = sym_matvec_lane<M>(cfj + FB, xs, part, lane, ro);
+        LW_CLK(3);
+        if (j == 0) {
+            // interface faces: seg = mass (own + nbr)  (stepper.py:283-300)
+            const double oth = mbox_take_warp(mb_in + par * mb_par, tag, nb >= 0);
+            // face values regrouped through SMEM, not shuffles: right after the divergent
+            // poll loop a shuffle takes the warp-divergent slow path (~1 us per step measured)
+            if (nb >= 0) xs[lane] = oth;
+            __syncwarp();
+            LW_CLK(4);
+            double acc_if = 0.0;
+#pragma unroll
+            for (int c = 0; c < M; ++c) acc_if = fma(mrow[c], __dadd_rn(Flj[f * M + c], xs[f * M + c]), acc_if);
+            if (nb >= 0) a = acc_if;
+        }
+        double un = 0.0;
+        if (act) {
+            double tot = a;
+            if (nsrc == 1) {  // add_force order: f = term_0 (+ term_1); tot = acc + f
+                tot = __dadd_rn(a, __dmul_rn(sv0, fa0));
+            } else if (nsrc == 2) {
+                tot = __dadd_rn(a, __dadd_rn(__dmul_rn(sv0, fa0), __dmul_rn(sv1, fa1)));
+            } else if (nsrc > 2) {
+                tot = add_force(p, s, (long long)j * W + lane, kk, a);
+            }
+            un = __dadd_rn(__dsub_rn(__dmul_rn(2.0, uc), up), __dmul_rn(dt2, tot));
+            up = uc;
+            uc = un;
+            Usj[lane] = un;
+        }
+        __syncwarp();
+        LW_CLK(5);
+        const double sq = warp_sum(act ? un * un : 0.0);
+        if (lane == 0) sqv[g * L + j] = sq;
+        if (rec) {  // tap probes on this layer, straight from registers
+            for (int q = pq0; q < pq1; ++q) {
+                const bool staged = q - pa0 < p.res_pmax;
+                const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
+                const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
+                if (tap >= j * W && tap < (j + 1) * W) {
+                    const double v = __shfl_sync(FULL, un, tap - j * W);
+                    if (lane == 0) p.rows[row * p.n_probe + pid] = v;
+                }
+            }
+        }
+        LW_CLK(6);
+        if (j == L - 1 && L > 1)
+            asm volatile("bar.arrive %0, %1;" ::"r"(barB), "r"(nthr) : "memory");
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(barB), "r"(nthr) : "memory");
+        LW_CLK(7);
+        if (j == 0) {
+            if (lane == 0) {
+                double t = sqv[g * L];
+                for (int jj = 1; jj < L; ++jj) t += sqv[g * L + jj];
+                p.norm_part[((size_t)kk * gridDim.x + blockIdx.x) * G + g] = t;
+            }
+            if (rec) {  // dense probes: whole subdomain state (all layers published by barrier B)
+                const double* Ug = Us + (size_t)g * K;
+                for (int q = pq0; q < pq1; ++q) {
+                    const bool staged = q - pa0 < p.res_pmax;
+                    const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
+                    const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
+                    if (tap >= 0) continue;
+                    const double* wv = (tap > -1000000) ? pwv + (size_t)(-1 - tap) * K : p.prb_w + p.prb_woff[pid];
+                    double acc = 0.0;
+                    for (int i = lane; i < K; i += 32) acc = fma(wv[i], Ug[i], acc);
+                    const double v = warp_sum(acc);
+                    if (lane == 0) p.rows[row * p.n_probe + pid] = v;
+                }
+            }
+        }
+        LW_CLK(8);
+    }
+#ifdef SFW_LW_CLK
+    if (p.tprof && lane < 10) {
+        long long v = 0;
+#pragma unroll
+        for (int q = 0; q < 10; ++q)
+            if (lane == q) v = clk_acc[q];
+        p.tprof[((size_t)blockIdx.x * nwarps + warp) * 16 + lane] = v;
+    }
+#endif
+#undef LW_CLK
+    // write both time levels back (global layout as k_step2: U[cur ^ (n & 1)] is current)
+    if (act) {
+        double* Gc = (p.cur ^ (p.n_steps & 1)) ? p.U1 : p.U0;
+        double* Go = (p.cur ^ (p.n_steps & 1)) ? p.U0 : p.U1;
+        const size_t gi = (size_t)s * K + j * W + lane;
+        Gc[gi] = uc;
+        Go[gi] = up;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// k_step_sw: one warp per subdomain, SMEM-resident (small-m configurations,
+// config 2: 512 x m4k6 on 148 SMs, <= 4 subdomains per CTA, w = 24 <= 32).
+//
+// Lane i holds row i of every layer's state U_j (current, previous) in
+// registers; the 2L chain blocks live in SMEM in the 21-tile format with
+// element pairs adjacent (128-bit loads).  A step is two phases of L
+// independent block mat-vecs (ILP across layers, no intra-CTA barriers):
+//   phase 1: flux_j = Gamma_j (U_{j+1} - U_j)            -> layer-1 faces to the mailbox
+//   phase 2: acc_j  = Gamma-hat_j (flux_j - flux_{j-1})   -> leapfrog of layers >= 2,
+//            then the neighbours' face fluxes (tagged mailbox poll) -> layer-1 leapfrog.
+// Same arithmetic, in the same order, as k_step2 / k_step_res.
+template <int M>
+__device__ __forceinline__ void expand_block_pairs(const double* __restrict__ packed, double* __restrict__ out,
+                                                   int tid, int nthr) {
+    // element e of tile t at ((e / 2) * 21 + t) * 2 + (e & 1)   (M * M even)
+    for (int idx = tid; idx < 21 * M * M; idx += nthr) {
+        const int t = idx % 21, e = idx / 21;
+        const int r = e % M, c = (e / M + r) % M;
+        double v;
+        if (t < 15) {
+            v = packed[e * 15 + t];
+        } else if (r < c) {
+            v = 0.0;
+        } else {
+            const int d = r - c;
+            const int ep = d * M - d * (d - 1) / 2 + c;
+            v = packed[15 * M * M + ep * 6 + (t - 15)];
+            if (d == 0) v = 0.5 * v;
+        }
+        out[((e >> 1) * 21 + t) * 2 + (e & 1)] = v;
+    }
+}
+
+// NL independent symmetric block mat-vecs y_j = B_j x_j (tile lanes 0..20), results in
+// registers of lanes 0..w-1.  B_j at blk + j * bstride (pair layout), x_j at xw + j * W,
+// partials at pw + j * 42 * M.
+template <int M, int NL>
+__device__ __forceinline__ void sym_matvec_multi(const double* __restrict__ blk, int bstride, const double* xw,
+                                                 double* pw, double (&y)[NL], int lane, const RedOff7<M>& ro) {
+    constexpr int W = 32;  // x_j at xw + 32 j (rows >= 6M are padding)
+    static_assert((M * M) % 2 == 0, "pair layout");
+    if (lane < 21) {
+        const int I = lane < 15 ? off_I(lane) : lane - 15;
+        const int K = lane < 15 ? off_K(lane) : lane - 15;
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            double xk[M], xi[M], P[M], Q[M];
+#pragma unroll
+            for (int i = 0; i < M; i += 2) {
+                const double2 a = *reinterpret_cast<const double2*>(xw + j * W + K * M + i);
+                const double2 b = *reinterpret_cast<const double2*>(xw + j * W + I * M + i);
+                xk[i] = a.x;
+                xk[i + 1] = a.y;
+                xi[i] = b.x;
+                xi[i + 1] = b.y;
+                P[i] = P[i + 1] = Q[i] = Q[i + 1] = 0.0;
+            }
+            const double* b = blk + (size_t)j * bstride + lane * 2;
+#pragma unroll
+            for (int ep = 0; ep < M * M / 2; ++ep) {
+                const double2 a2 = *reinterpret_cast<const double2*>(b + ep * 42);
+                const int e0 = 2 * ep, e1 = 2 * ep + 1;
+                const int r0 = e0 % M, c0 = (e0 / M + r0) % M;
+                const int r1 = e1 % M, c1 = (e1 / M + r1) % M;
+                P[r0] = fma(a2.x, xk[c0], P[r0]);
+                Q[c0] = fma(a2.x, xi[r0], Q[c0]);
+                P[r1] = fma(a2.y, xk[c1], P[r1]);
+                Q[c1] = fma(a2.y, xi[r1], Q[c1]);
+            }
+            double* pj = pw + j * 42 * M;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                pj[i * 21 + lane] = P[i];
+                pj[(M + i) * 21 + lane] = Q[i];
+            }
+        }
+    }
+    __syncwarp();
+    // branch-free reduction (lanes >= 6M read valid dummy offsets), so the layers interleave
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        const double* pj = pw + j * 42 * M;
+        double t = pj[ro.o[0][0]];
+#pragma unroll
+        for (int q = 1; q < 7; ++q) t += pj[ro.o[0][q]];
+        y[j] = lane < 6 * M ? t : 0.0;
+    }
+    __syncwarp();
+}
+
+template <int M, int L>
+__global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
+    constexpr int W = 6 * M;
+    static_assert(W <= 32, "one lane per chain row");
+    constexpr int K = L * W;
+    constexpr int FB = 21 * M * M;
+    constexpr int PW = 42 * M;                 // partials per layer
+    constexpr int WS = L * 32 + L * PW + 32;   // per-warp scratch: x (stride 32), partials, face regroup
+    constexpr unsigned FULL = 0xffffffffu;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const RedOff7<M> ro(lane);
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int ns = s1 - s0;
+    const int BS = p.BS;
+    double* cf = reinterpret_cast<double*>(smem_raw);          // [nwarps][2L][FB]
+    double* ms = cf + (size_t)nwarps * 2 * L * FB;             // [nwarps][6][M*M]
+    double* wsb = ms + (size_t)nwarps * 6 * M * M;             // [nwarps][WS]
+    double* pwv = wsb + (size_t)nwarps * WS;                   // [npd][K] dense probe weights
+    int* pmeta = reinterpret_cast<int*>(pwv + (size_t)p.res_pdense * K);
+    __shared__ int s_nbr[8 * 6];
+    __shared__ int s_src[8 + 1];
+    __shared__ int s_prb[8 + 1];
+    const int g = warp;
+    const bool live = g < ns;
+    const bool act = lane < W;
+
+    // ---- one-time loads (whole CTA) ----------------------------------------
+    for (int bk = warp; bk < ns * 2 * L; bk += nwarps)
+        expand_block_pairs<M>(p.coef + ((size_t)s0 * 2 * L + bk) * BS, cf + (size_t)bk * FB, lane, 32);
+    {
+        const int pa = p.prb_ptr[s0], pb = p.prb_ptr[s1];
+        if (threadIdx.x == 0) {
+            int nd = 0;
+            for (int q = pa; q < pb && q - pa < p.res_pmax; ++q) {
+                const int pid = p.prb_ids[q];
+                const int tap = p.prb_tap[pid];
+                pmeta[2 * (q - pa)] = pid;
+                if (tap >= 0) {
+                    pmeta[2 * (q - pa) + 1] = tap;
+                } else if (nd < p.res_pdense) {
+                    pmeta[2 * (q - pa) + 1] = -1 - nd;
+                    ++nd;
+                } else {
+                    pmeta[2 * (q - pa) + 1] = -1000000;
+                }
+            }
+        }
+        __syncthreads();
+        for (int q = pa + warp; q < pb && q - pa < p.res_pmax; q += nwarps) {
+            const int slot = pmeta[2 * (q - pa) + 1];
+            if (slot < 0 && slot > -1000000) {
+                const double* wv = p.prb_w + p.prb_woff[pmeta[2 * (q - pa)]];
+                for (int i = lane; i < K; i += 32) pwv[(size_t)(-1 - slot) * K + i] = wv[i];
+            }
+        }
+    }
+    for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nbr[i] = p.nbr[s0 * 6 + i];
+    for (int i = threadIdx.x; i <= ns; i += blockDim.x) {
+        s_src[i] = p.src_ptr[s0 + i];
+        s_prb[i] = p.prb_ptr[s0 + i];
+    }
+    for (int i = threadIdx.x; i < ns * 6 * M * M; i += blockDim.x) {
+        const int sl = i / (6 * M * M), f = (i / (M * M)) % 6, e = i % (M * M);
+        const int mi = p.mass_idx[(s0 + sl) * 6 + f];
+        ms[i] = mi >= 0 ? p.mass[(size_t)mi * M * M + e] : 0.0;
+    }
+    __syncthreads();
+    if (!live) {  // no subdomain for this warp: zero its norm partials
+        if (lane == 0)
+            for (int k = 0; k < p.n_steps; ++k) p.norm_part[((size_t)k * gridDim.x + blockIdx.x) * p.groups + g] = 0.0;
+        return;
+    }
+    const int s = s0 + g;
+    double uc[L], up[L];
+    {
+        const double* Ug0 = p.cur ? p.U1 : p.U0;
+        const double* Ug1 = p.cur ? p.U0 : p.U1;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            uc[j] = act ? Ug0[(size_t)s * K + j * W + lane] : 0.0;
+            up[j] = act ? Ug1[(size_t)s * K + j * W + lane] : 0.0;
+        }
+    }
+    // sources of this subdomain (<= 2 staged in registers; more use add_force)
+    const int src_a = s_src[g], nsrc = s_src[g + 1] - s_src[g];
+    double sv0[L], sv1[L];
+    const double *ft0 = p.ftab, *ft1 = p.ftab;
+#pragma unroll
+    for (int j = 0; j < L; ++j) sv0[j] = sv1[j] = 0.0;
+    if (nsrc >= 1 && nsrc <= 2) {
+        const int q0 = p.src_ids[src_a];
+        ft0 = p.ftab + (long long)q0 * p.ftab_stride;
+#pragma unroll
+        for (int j = 0; j < L; ++j) sv0[j] = act ? p.src_vec[p.src_voff[q0] + (long long)j * W + lane] : 0.0;
+        if (nsrc == 2) {
+            const int q1 = p.src_ids[src_a + 1];
+            ft1 = p.ftab + (long long)q1 * p.ftab_stride;
+#pragma unroll
+            for (int j = 0; j < L; ++j) sv1[j] = act ? p.src_vec[p.src_voff[q1] + (long long)j * W + lane] : 0.0;
+        }
+    }
+    const int pa0 = s_prb[0], pq0 = s_prb[g], pq1 = s_prb[g + 1];
+    const double dt2 = p.dt2;
+    const double* cfg = cf + (size_t)g * 2 * L * FB;
+    double* xw = wsb + (size_t)g * WS;
+    double* pw = xw + L * 32;
+    double* ob = pw + L * PW;
+    const int f = lane / M, r = lane % M;
+    const int nb = act ? s_nbr[g * 6 + f] : -1;
+    unsigned long long* mb_out = p.mbox + ((size_t)s * W + lane) * 2;
+    const unsigned long long* mb_in = p.mbox + ((size_t)(nb < 0 ? 0 : nb) * W + (f ^ 1) * M + r) * 2;
+    const size_t mb_par = (size_t)p.n_sub * W * 2;
+    const double* mrow = ms + (g * 6 + (f < 6 ? f : 0)) * M * M + r * M;
+
+#ifdef SFW_LW_CLK
+    long long clk_prev = clock64(), clk_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#define SW_CLK(ph)                          \
+    {                                       \
+        const long long c_ = clock64();     \
+        clk_acc[ph] += c_ - clk_prev;       \
+        clk_prev = c_;                      \
+    }
+#else
+#define SW_CLK(ph)
+#endif
+    int rec_cnt = p.record_every;
+    long long row = -1;
+    for (int k = 1; k <= p.n_steps; ++k) {
+        const int par = k & 1;
+        const unsigned int tag = p.tag_base + (unsigned int)k;
+        const int kk = k - 1;
+        const bool rec = (--rec_cnt == 0) && p.rows;
+        if (rec_cnt == 0) {
+            rec_cnt = p.record_every;
+            ++row;
+        }
+        const double fa0 = (nsrc >= 1 && nsrc <= 2) ? ft0[kk] : 0.0;
+        const double fa1 = (nsrc == 2) ? ft1[kk] : 0.0;
+        // ---- phase 1: flux_j = Gamma_j (U_{j+1} - U_j) --------------------------
+#pragma unroll
+        for (int j = 0; j < L; ++j) xw[j * 32 + lane] = (j + 1 < L ? uc[j + 1] : 0.0) - uc[j];
+        __syncwarp();
+        SW_CLK(0);
+        double fl[L];
+        sym_matvec_multi<M, L>(cfg, 2 * FB, xw, pw, fl, lane, ro);
+        SW_CLK(1);
+        if (nb >= 0) mbox_put(mb_out + par * mb_par, fl[0], tag);
+        // ---- phase 2: acc_j = Gamma-hat_j (flux_j - flux_{j-1}) ------------------
+#pragma unroll
+        for (int j = 0; j < L; ++j) xw[j * 32 + lane] = j > 0 ? fl[j] - fl[j - 1] : fl[0];
+        __syncwarp();
+        SW_CLK(2);
+        double acc[L];
+        sym_matvec_multi<M, L>(cfg + FB, 2 * FB, xw, pw, acc, lane, ro);
+        SW_CLK(3);
+        // interior layers first (independent of the exchange), then layer 1
+        double sq[L];
+#pragma unroll
+        for (int j = L - 1; j >= 0; --j) {
+            double a = acc[j];
+            if (j == 0) {
+                // interface faces: seg = mass (own + nbr)  (stepper.py:283-300); the own
+                // layer-1 flux is phase 2's layer-1 input, still in xw[0..W)
+                SW_CLK(4);
+                const double oth = mbox_take_warp(mb_in + par * mb_par, tag, nb >= 0);
+                if (nb >= 0) ob[lane] = oth;
+                __syncwarp();
+                SW_CLK(5);
+                double acc_if = 0.0;
+#pragma unroll
+                for (int c = 0; c < M; ++c) acc_if = fma(mrow[c], __dadd_rn(xw[f * M + c], ob[f * M + c]), acc_if);
+                if (nb >= 0) a = acc_if;
+            }
+            // branch-free (lanes >= w carry zeros) so the layers interleave
+            double tot = a;
+            if (nsrc == 1) {  // add_force order: f = term_0 (+ term_1); tot = acc + f
+                tot = __dadd_rn(a, __dmul_rn(sv0[j], fa0));
+            } else if (nsrc == 2) {
+                tot = __dadd_rn(a, __dadd_rn(__dmul_rn(sv0[j], fa0), __dmul_rn(sv1[j], fa1)));
+            } else if (nsrc > 2 && act) {
+                tot = add_force_cold(p, s, (long long)j * W + lane, kk, a);
+            }
+            const double un = act ? __dadd_rn(__dsub_rn(__dmul_rn(2.0, uc[j]), up[j]), __dmul_rn(dt2, tot)) : 0.0;
+            up[j] = uc[j];
+            uc[j] = un;
+            sq[j] = un * un;
+        }
+        __syncwarp();
+        SW_CLK(6);
+        // |U|^2 of the subdomain: per-layer lane sums, then layers in order (k_step2 order)
+        double t = warp_sum(sq[0]);
+#pragma unroll
+        for (int j = 1; j < L; ++j) t += warp_sum(sq[j]);
+        if (lane == 0) p.norm_part[((size_t)kk * gridDim.x + blockIdx.x) * p.groups + g] = t;
+        SW_CLK(7);
+        if (rec) {
+            for (int q = pq0; q < pq1; ++q) {
+                const bool staged = q - pa0 < p.res_pmax;
+                const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
+                const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
+                double v;
+                if (tap >= 0) {  // one state entry: layer tap / W, row tap % W
+                    const int jt = tap / W;
+                    double u = 0.0;
+#pragma unroll
+                    for (int j = 0; j < L; ++j)
+                        if (j == jt) u = uc[j];
+                    v = __shfl_sync(FULL, u, tap - jt * W);
+                } else {  // dense weights: lane-local partial over the layers, then the warp
+                    const double* wv = (tap > -1000000) ? pwv + (size_t)(-1 - tap) * K : p.prb_w + p.prb_woff[pid];
+                    double a = 0.0;
+#pragma unroll
+                    for (int j = 0; j < L; ++j)
+                        if (act) a = fma(wv[j * W + lane], uc[j], a);
+                    v = warp_sum(a);
+                }
+                if (lane == 0) p.rows[row * p.n_probe + pid] = v;
+            }
+        }
+        SW_CLK(8);
+    }
+#ifdef SFW_LW_CLK
+    if (p.tprof && lane < 10) {
+        long long v = 0;
+#pragma unroll
+        for (int q = 0; q < 10; ++q)
+            if (lane == q) v = clk_acc[q];
+        p.tprof[((size_t)blockIdx.x * nwarps + warp) * 16 + lane] = v;
+    }
+#endif
+#undef SW_CLK
+    // write both time levels back (global layout as k_step2: U[cur ^ (n & 1)] is current)
+    if (act) {
+        double* Gc = (p.cur ^ (p.n_steps & 1)) ? p.U1 : p.U0;
+        double* Go = (p.cur ^ (p.n_steps & 1)) ? p.U0 : p.U1;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            Gc[(size_t)s * K + j * W + lane] = uc[j];
+            Go[(size_t)s * K + j * W + lane] = up[j];
+        }
     }
 }
 
@@ -1176,11 +1857,18 @@ __global__ void k_mass(const double* __restrict__ hat, const long long* __restri
 }
 
 // fixed-order sum of the per-CTA norm partials -> |U_k|_2
-__global__ void k_norms(const double* __restrict__ part, int n_steps, int n_cta, double* __restrict__ out) {
+__global__ void k_norms(const double* __restrict__ part, int n_steps, int n_cta, int groups,
+                        double* __restrict__ out) {
+    // part[k][cta][groups]: per-CTA subtotal over its groups (subdomain order), then over CTAs
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n_steps) return;
     double t = 0.0;
-    for (int c = 0; c < n_cta; ++c) t += part[(size_t)k * n_cta + c];
+    for (int c = 0; c < n_cta; ++c) {
+        const double* q = part + ((size_t)k * n_cta + c) * groups;
+        double tc = q[0];
+        for (int g = 1; g < groups; ++g) tc += q[g];
+        t += tc;
+    }
     out[k] = sqrt(t);
 }
 
@@ -1301,7 +1989,7 @@ static void free_all(sfw_stepper* h) {
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
                     h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta, h->tcoef, h->UM[0], h->UM[1],
                     h->mfb, h->macc1, h->mnorm, h->mrows, h->shot_vec, h->shot_sub, h->shot_voff,
-                    h->shot_ftab};
+                    h->shot_ftab, h->mbox};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -1663,6 +2351,63 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
                 SFW_CUDA_TRY(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
             }
         }
+        // warp-per-subdomain resident variant (m = 4, 2 <= L <= 8, <= 8 subdomains per CTA)
+        if (h->uniform && !getenv("SFW_NO_RESIDENT") && !getenv("SFW_NO_SW") && m == 4 && h->L >= 2 && h->L <= 8) {
+            int maxns = 0;
+            for (int b = 0; b < h->grid; ++b) maxns = std::max(maxns, cta_res_ns(h, b));
+            const int L = h->L, K = L * W;
+            const int pmax = 256, pdense = 2;
+            const size_t ws = (size_t)L * 32 + (size_t)L * 42 * m + 32;
+            const size_t need = 8 * ((size_t)maxns * 2 * L * 21 * m * m + (size_t)maxns * 6 * m * m + (size_t)maxns * ws +
+                                     (size_t)pdense * K) +
+                                4 * 2 * (size_t)pmax;
+            static const void* const ksw[9] = {nullptr, nullptr, (const void*)k_step_sw<4, 2>, (const void*)k_step_sw<4, 3>,
+                                               (const void*)k_step_sw<4, 4>, (const void*)k_step_sw<4, 5>, (const void*)k_step_sw<4, 6>,
+                                               (const void*)k_step_sw<4, 7>, (const void*)k_step_sw<4, 8>};
+            if (getenv("SFW_STEP_VERBOSE"))
+                fprintf(stderr, "[sfw] k_step_sw: maxns=%d L=%d smem=%zu\n", maxns, L, need);
+            if (maxns >= 1 && maxns <= 8 && need <= 220 * 1024) {
+                h->klw = ksw[L];
+                h->lw_smem = (int)need;
+                h->lw_threads = 32 * maxns;
+                h->lw_groups = maxns;
+                h->res_pmax = pmax;
+                h->res_pdense = pdense;
+                SFW_CUDA_TRY(cudaFuncSetAttribute(h->klw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+                SFW_CUDA_TRY(cudaMalloc(&h->mbox, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
+                SFW_CUDA_TRY(cudaMemset(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
+                h->tag_base = 0;
+            }
+        }
+        // layer-warp resident variant: one warp per (subdomain, layer), w <= 32
+        if (!h->klw && h->uniform && !getenv("SFW_NO_RESIDENT") && !getenv("SFW_NO_LW") && (m == 1 || m == 4)) {
+            int maxns = 0;
+            for (int b = 0; b < h->grid; ++b) maxns = std::max(maxns, cta_res_ns(h, b));
+            const int L = h->L, K = L * W, nthr = maxns * L * 32;
+            const int pmax = 256, pdense = 2;
+            const size_t need = 8 * ((size_t)maxns * 2 * L * 21 * m * m + (size_t)2 * maxns * K +
+                                     (size_t)maxns * 6 * m * m + (size_t)maxns * L +
+                                     (size_t)(nthr / 32) * (W + 42 * m) + (size_t)pdense * K) +
+                                4 * 2 * (size_t)pmax;
+            const void* kl = nullptr;
+            if (nthr <= 768) kl = (m == 1) ? (const void*)k_step_lw<1, 768> : (const void*)k_step_lw<4, 768>;
+            else if (nthr <= 896) kl = (m == 1) ? (const void*)k_step_lw<1, 896> : (const void*)k_step_lw<4, 896>;
+            else if (nthr <= 1024) kl = (m == 1) ? (const void*)k_step_lw<1, 1024> : (const void*)k_step_lw<4, 1024>;
+            if (getenv("SFW_STEP_VERBOSE"))
+                fprintf(stderr, "[sfw] k_step_lw: maxns=%d L=%d nthr=%d smem=%zu\n", maxns, L, nthr, need);
+            if (kl && maxns >= 1 && maxns <= 7 && need <= 220 * 1024) {
+                h->klw = kl;
+                h->lw_smem = (int)need;
+                h->lw_threads = nthr;
+                h->lw_groups = maxns;
+                h->res_pmax = pmax;
+                h->res_pdense = pdense;
+                SFW_CUDA_TRY(cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+                SFW_CUDA_TRY(cudaMalloc(&h->mbox, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
+                SFW_CUDA_TRY(cudaMemset(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
+                h->tag_base = 0;
+            }
+        }
         const void* kp = h->kfn;
         SFW_CUDA_TRY(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem));
         int per_sm = 0;
@@ -1755,6 +2500,34 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
     p.flux = h->flux;
     p.sq = h->sq;
     void* args[] = {&p};
+    if (mode == 0 && h->klw && !Ucur) {
+        if ((unsigned long long)h->tag_base + (unsigned long long)n_steps >= 0xFFFFFF00ull) {  // tag wrap
+            SFW_CUDA_TRY(cudaMemsetAsync(h->mbox, 0, (size_t)2 * h->n_sub * h->W * 2 * 8, h->stream));
+            h->tag_base = 0;
+        }
+        p.mbox = h->mbox;
+        p.tag_base = h->tag_base;
+        p.groups = h->lw_groups;
+        p.tprof = nullptr;
+        if (getenv("SFW_STEP_PROF")) {
+            static unsigned long long* tp = nullptr;
+            static size_t tpn = 0;
+            const size_t need = (size_t)h->grid * (h->lw_threads / 32) * 16;  // SFW_LW_CLK cycle sums
+            if (need > tpn) {
+                if (tp) cudaFree(tp);
+                cudaMalloc(&tp, need * 8);
+                tpn = need;
+            }
+            cudaMemsetAsync(tp, 0, need * 8, h->stream);
+            p.tprof = tp;
+            h->tprof = tp;
+            h->tprof_n = need;
+        }
+        SFW_CUDA_TRY(cudaLaunchCooperativeKernel(h->klw, dim3(h->grid), dim3(h->lw_threads), args, h->lw_smem,
+                                                 h->stream));
+        h->tag_base += (unsigned int)n_steps;
+        return 0;
+    }
     if (mode == 0 && h->kres && !Ucur) {
         SFW_CUDA_TRY(cudaLaunchCooperativeKernel(h->kres, dim3(h->grid), dim3(h->res_nw * 32), args, h->res_smem,
                                                  h->stream));
@@ -1846,7 +2619,8 @@ static int run_common(sfw_stepper* h, int n_steps, int record_every, const doubl
     const long long nrec = n_steps / record_every;
     rc = ensure(h, &h->rows, &h->rows_cap, std::max(1LL, nrec * h->n_probe), errbuf, errlen);
     if (rc) return rc;
-    rc = ensure(h, &h->norm_part, &h->norm_cap, (long long)n_steps * h->grid, errbuf, errlen);
+    rc = ensure(h, &h->norm_part, &h->norm_cap, (long long)n_steps * h->grid * (h->klw ? h->lw_groups : 1), errbuf,
+                errlen);
     if (rc) return rc;
     if (!h->norms) {
         rc = dalloc(&h->norms, 1, errbuf, errlen);
@@ -1867,7 +2641,8 @@ extern "C" int sfw_step_run(sfw_stepper* h, int n_steps, int record_every, const
     h->norms = nullptr;
     rc = dalloc(&h->norms, n_steps, errbuf, errlen);
     if (rc) return rc;
-    k_norms<<<(n_steps + 127) / 128, 128, 0, h->stream>>>(h->norm_part, n_steps, h->grid, h->norms);
+    k_norms<<<(n_steps + 127) / 128, 128, 0, h->stream>>>(h->norm_part, n_steps, h->grid,
+                                                          h->klw ? h->lw_groups : 1, h->norms);
     std::vector<double> nrm(n_steps);
     SFW_CUDA_TRY(cudaMemcpyAsync(nrm.data(), h->norms, (size_t)n_steps * 8, cudaMemcpyDeviceToHost, h->stream));
     const long long nrec = n_steps / record_every;

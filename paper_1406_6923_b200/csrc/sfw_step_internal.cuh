@@ -67,6 +67,11 @@ struct sfw_stepper {
     const void* kfn = nullptr;
     const void* kres = nullptr;
     int res_smem = 0, res_nw = 0, res_pmax = 0, res_pdense = 0;
+    // k_step_lw (layer-warp resident kernel): launch shape + tagged face mailbox
+    const void* klw = nullptr;
+    int lw_smem = 0, lw_threads = 0, lw_groups = 1;
+    unsigned long long* mbox = nullptr;
+    unsigned int tag_base = 0;
     std::vector<int> cta_ptr_h;
     unsigned long long* tprof = nullptr;
     size_t tprof_n = 0;
