@@ -371,8 +371,6 @@ __device__ __forceinline__ double leap(int mode, double uc, double uo, double v,
     return __dadd_rn(__dsub_rn(uc, __dmul_rn(dt, v)), __dmul_rn(half, tot));
 }
 
-__device__ __noinline__ double add_force_cold(const StepParams& p, int s, long long idx, int k, double acc);
-
 // total = acc + sum_src vec * f(t)   (stepper.py:313-321 superposes in list order)
 __device__ __forceinline__ double add_force(const StepParams& p, int s, long long idx, int k,
                                             double acc) {
@@ -385,11 +383,6 @@ __device__ __forceinline__ double add_force(const StepParams& p, int s, long lon
         f = (q == a) ? term : __dadd_rn(f, term);
     }
     return __dadd_rn(acc, f);
-}
-
-// out-of-line copy for the resident kernels' rare > 2-sources case (keeps their loop small)
-__device__ __noinline__ double add_force_cold(const StepParams& p, int s, long long idx, int k, double acc) {
-    return add_force(p, s, idx, k, acc);
 }
 
 template <int M, int NW, int NS>
@@ -1594,6 +1587,42 @@ __global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
         }
     }
     const int pa0 = s_prb[0], pq0 = s_prb[g], pq1 = s_prb[g + 1];
+    // probes of this subdomain, resolved once: tap probes are stored by the lane that
+    // owns the entry (<= 2 per lane), dense probes (<= 2, weights staged in SMEM) are
+    // reduced together with the norm; anything else takes the generic loop
+    int tj0 = -1, tp0 = -1, tj1 = -1, tp1 = -1;
+    int dp0 = -1, dp1 = -1;
+    const double *dw0 = pwv, *dw1 = pwv;
+    bool generic = false;
+    for (int q = pq0; q < pq1; ++q) {
+        const bool staged = q - pa0 < p.res_pmax;
+        const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
+        const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
+        if (tap < 0) {
+            if (!staged || tap <= -1000000) {
+                generic = true;
+            } else if (dp0 < 0) {
+                dp0 = pid;
+                dw0 = pwv + (size_t)(-1 - tap) * K;
+            } else if (dp1 < 0) {
+                dp1 = pid;
+                dw1 = pwv + (size_t)(-1 - tap) * K;
+            } else {
+                generic = true;
+            }
+        } else if (tap % W == lane) {
+            if (tp0 < 0) {
+                tj0 = tap / W;
+                tp0 = pid;
+            } else if (tp1 < 0) {
+                tj1 = tap / W;
+                tp1 = pid;
+            } else {
+                generic = true;
+            }
+        }
+    }
+    generic = __any_sync(FULL, generic);
     const double dt2 = p.dt2;
     const double* cfg = cf + (size_t)g * 2 * L * FB;
     double* xw = wsb + (size_t)g * WS;
@@ -1617,49 +1646,123 @@ __global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
 #else
 #define SW_CLK(ph)
 #endif
-    int rec_cnt = p.record_every;
-    long long row = -1;
+    // norm + probe rows of the state after step kd (1-based), read from uc; runs
+    // right after the next step's layer-1 put, i.e. off the exchange critical path
+    auto record = [&](int kd) {
+        const bool rows_now = (kd % p.record_every == 0) && p.rows;
+        const long long row = kd / p.record_every - 1;
+        double sq = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < L; ++j) sq = fma(uc[j], uc[j], sq);  // lanes >= w hold zeros
+        if (rows_now && !generic && dp0 >= 0) {
+#pragma unroll
+            for (int j = 0; j < L; ++j)
+                if (act) d0 = fma(dw0[j * W + lane], uc[j], d0);
+            if (dp1 >= 0) {
+#pragma unroll
+                for (int j = 0; j < L; ++j)
+                    if (act) d1 = fma(dw1[j * W + lane], uc[j], d1);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // one interleaved butterfly for the three sums
+            sq += __shfl_xor_sync(FULL, sq, o);
+            d0 += __shfl_xor_sync(FULL, d0, o);
+            d1 += __shfl_xor_sync(FULL, d1, o);
+        }
+        if (lane == 0) p.norm_part[((size_t)(kd - 1) * gridDim.x + blockIdx.x) * p.groups + g] = sq;
+        if (!rows_now) return;
+        if (!generic) {
+            if (lane == 0 && dp0 >= 0) p.rows[row * p.n_probe + dp0] = d0;
+            if (lane == 0 && dp1 >= 0) p.rows[row * p.n_probe + dp1] = d1;
+            if (tp0 >= 0) {
+                double u = 0.0;
+#pragma unroll
+                for (int j = 0; j < L; ++j)
+                    if (j == tj0) u = uc[j];
+                p.rows[row * p.n_probe + tp0] = u;
+            }
+            if (tp1 >= 0) {
+                double u = 0.0;
+#pragma unroll
+                for (int j = 0; j < L; ++j)
+                    if (j == tj1) u = uc[j];
+                p.rows[row * p.n_probe + tp1] = u;
+            }
+            return;
+        }
+        for (int q = pq0; q < pq1; ++q) {
+            const bool staged = q - pa0 < p.res_pmax;
+            const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
+            const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
+            double v;
+            if (tap >= 0) {  // one state entry: layer tap / W, row tap % W
+                const int jt = tap / W;
+                double u = 0.0;
+#pragma unroll
+                for (int j = 0; j < L; ++j)
+                    if (j == jt) u = uc[j];
+                v = __shfl_sync(FULL, u, tap - jt * W);
+            } else {  // dense weights: lane-local partial over the layers, then the warp
+                const double* wv = (tap > -1000000) ? pwv + (size_t)(-1 - tap) * K : p.prb_w + p.prb_woff[pid];
+                double acc = 0.0;
+#pragma unroll
+                for (int j = 0; j < L; ++j)
+                    if (act) acc = fma(wv[j * W + lane], uc[j], acc);
+                v = warp_sum(acc);
+            }
+            if (lane == 0) p.rows[row * p.n_probe + pid] = v;
+        }
+    };
+
     for (int k = 1; k <= p.n_steps; ++k) {
         const int par = k & 1;
         const unsigned int tag = p.tag_base + (unsigned int)k;
         const int kk = k - 1;
-        const bool rec = (--rec_cnt == 0) && p.rows;
-        if (rec_cnt == 0) {
-            rec_cnt = p.record_every;
-            ++row;
-        }
         const double fa0 = (nsrc >= 1 && nsrc <= 2) ? ft0[kk] : 0.0;
         const double fa1 = (nsrc == 2) ? ft1[kk] : 0.0;
-        // ---- phase 1: flux_j = Gamma_j (U_{j+1} - U_j) --------------------------
+        // ---- phase 1: flux_j = Gamma_j (U_{j+1} - U_j); layer 1 first, its faces
+        // go to the mailbox before anything else (the inter-CTA critical path) -----
 #pragma unroll
         for (int j = 0; j < L; ++j) xw[j * 32 + lane] = (j + 1 < L ? uc[j + 1] : 0.0) - uc[j];
         __syncwarp();
         SW_CLK(0);
         double fl[L];
-        sym_matvec_multi<M, L>(cfg, 2 * FB, xw, pw, fl, lane, ro);
-        SW_CLK(1);
+        {
+            double f0[1];
+            sym_matvec_multi<M, 1>(cfg, 2 * FB, xw, pw, f0, lane, ro);
+            fl[0] = f0[0];
+        }
         if (nb >= 0) mbox_put(mb_out + par * mb_par, fl[0], tag);
+        SW_CLK(1);
+        if (k > 1) record(k - 1);
+        SW_CLK(2);
+        {
+            double fr[L - 1];
+            sym_matvec_multi<M, L - 1>(cfg + 2 * FB, 2 * FB, xw + 32, pw + PW, fr, lane, ro);
+#pragma unroll
+            for (int j = 1; j < L; ++j) fl[j] = fr[j - 1];
+        }
         // ---- phase 2: acc_j = Gamma-hat_j (flux_j - flux_{j-1}) ------------------
+        SW_CLK(3);
 #pragma unroll
         for (int j = 0; j < L; ++j) xw[j * 32 + lane] = j > 0 ? fl[j] - fl[j - 1] : fl[0];
         __syncwarp();
-        SW_CLK(2);
         double acc[L];
         sym_matvec_multi<M, L>(cfg + FB, 2 * FB, xw, pw, acc, lane, ro);
-        SW_CLK(3);
+        SW_CLK(4);
         // interior layers first (independent of the exchange), then layer 1
-        double sq[L];
 #pragma unroll
         for (int j = L - 1; j >= 0; --j) {
             double a = acc[j];
             if (j == 0) {
                 // interface faces: seg = mass (own + nbr)  (stepper.py:283-300); the own
                 // layer-1 flux is phase 2's layer-1 input, still in xw[0..W)
-                SW_CLK(4);
+                SW_CLK(5);
                 const double oth = mbox_take_warp(mb_in + par * mb_par, tag, nb >= 0);
                 if (nb >= 0) ob[lane] = oth;
                 __syncwarp();
-                SW_CLK(5);
+                SW_CLK(6);
                 double acc_if = 0.0;
 #pragma unroll
                 for (int c = 0; c < M; ++c) acc_if = fma(mrow[c], __dadd_rn(xw[f * M + c], ob[f * M + c]), acc_if);
@@ -1669,50 +1772,17 @@ __global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
             double tot = a;
             if (nsrc == 1) {  // add_force order: f = term_0 (+ term_1); tot = acc + f
                 tot = __dadd_rn(a, __dmul_rn(sv0[j], fa0));
-            } else if (nsrc == 2) {
+            } else if (nsrc == 2) {  // (> 2 sources per subdomain: host picks another kernel)
                 tot = __dadd_rn(a, __dadd_rn(__dmul_rn(sv0[j], fa0), __dmul_rn(sv1[j], fa1)));
-            } else if (nsrc > 2 && act) {
-                tot = add_force_cold(p, s, (long long)j * W + lane, kk, a);
             }
             const double un = act ? __dadd_rn(__dsub_rn(__dmul_rn(2.0, uc[j]), up[j]), __dmul_rn(dt2, tot)) : 0.0;
             up[j] = uc[j];
             uc[j] = un;
-            sq[j] = un * un;
         }
         __syncwarp();
-        SW_CLK(6);
-        // |U|^2 of the subdomain: per-layer lane sums, then layers in order (k_step2 order)
-        double t = warp_sum(sq[0]);
-#pragma unroll
-        for (int j = 1; j < L; ++j) t += warp_sum(sq[j]);
-        if (lane == 0) p.norm_part[((size_t)kk * gridDim.x + blockIdx.x) * p.groups + g] = t;
         SW_CLK(7);
-        if (rec) {
-            for (int q = pq0; q < pq1; ++q) {
-                const bool staged = q - pa0 < p.res_pmax;
-                const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
-                const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
-                double v;
-                if (tap >= 0) {  // one state entry: layer tap / W, row tap % W
-                    const int jt = tap / W;
-                    double u = 0.0;
-#pragma unroll
-                    for (int j = 0; j < L; ++j)
-                        if (j == jt) u = uc[j];
-                    v = __shfl_sync(FULL, u, tap - jt * W);
-                } else {  // dense weights: lane-local partial over the layers, then the warp
-                    const double* wv = (tap > -1000000) ? pwv + (size_t)(-1 - tap) * K : p.prb_w + p.prb_woff[pid];
-                    double a = 0.0;
-#pragma unroll
-                    for (int j = 0; j < L; ++j)
-                        if (act) a = fma(wv[j * W + lane], uc[j], a);
-                    v = warp_sum(a);
-                }
-                if (lane == 0) p.rows[row * p.n_probe + pid] = v;
-            }
-        }
-        SW_CLK(8);
     }
+    if (p.n_steps > 0) record(p.n_steps);
 #ifdef SFW_LW_CLK
     if (p.tprof && lane < 10) {
         long long v = 0;
@@ -2304,6 +2374,8 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
             vtot += h->soff[s + 1] - h->soff[s];
             src_ptr[s + 1]++;
         }
+        h->max_src_sub = 0;
+        for (int s = 0; s < n; ++s) h->max_src_sub = std::max(h->max_src_sub, src_ptr[s + 1]);
         for (int s = 0; s < n; ++s) src_ptr[s + 1] += src_ptr[s];
         src_ids.resize(d->n_src);
         {
@@ -2352,7 +2424,8 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
             }
         }
         // warp-per-subdomain resident variant (m = 4, 2 <= L <= 8, <= 8 subdomains per CTA)
-        if (h->uniform && !getenv("SFW_NO_RESIDENT") && !getenv("SFW_NO_SW") && m == 4 && h->L >= 2 && h->L <= 8) {
+        if (h->uniform && !getenv("SFW_NO_RESIDENT") && !getenv("SFW_NO_SW") && m == 4 && h->L >= 2 && h->L <= 8 &&
+            h->max_src_sub <= 2) {
             int maxns = 0;
             for (int b = 0; b < h->grid; ++b) maxns = std::max(maxns, cta_res_ns(h, b));
             const int L = h->L, K = L * W;

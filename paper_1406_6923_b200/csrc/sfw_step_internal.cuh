@@ -72,6 +72,7 @@ struct sfw_stepper {
     int lw_smem = 0, lw_threads = 0, lw_groups = 1;
     unsigned long long* mbox = nullptr;
     unsigned int tag_base = 0;
+    int max_src_sub = 0;  // most sources injected into one subdomain
     std::vector<int> cta_ptr_h;
     unsigned long long* tprof = nullptr;
     size_t tprof_n = 0;
