@@ -102,6 +102,8 @@ struct MsParams {
     const int* ncta_ptr;
     const int* ncta;
     int evict_first;
+    unsigned long long* dbg;  // debug cycle counters (SFW_MS_CLK builds) or null
+    const double* mblk;       // [n_sub][6][M*M] interface mass per face (0 for outer faces)
 };
 
 constexpr int MS_NW = 16;  // warp = (row tile I = warp/2, column half = warp%2)
@@ -539,6 +541,563 @@ __global__ void __launch_bounds__((MS_NW + 1) * 32, 1) k_step_ms(const MsParams 
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_step_ms2: shot-column-parallel multi-shot stepping.  8 compute warps: warp
+// (c, hh) owns shots 8c..8c+7 and output row tiles [hh*RH, hh*RH+RH) of every
+// layer GEMM B X (B = Gamma_j or Gamma-hat_j, 56 x 56 symmetric, X 56 x 8), two
+// warps per SMSP (the FP64 tensor pipe needs two LDS-fed DMMA streams per SMSP:
+// measured 1 DMMA / 4.0 SM cycles with 8 warps vs 5.3 with 4).  Shots are
+// independent: the two warps of a column pair exchange only their X rows
+// (double-buffered, one 64-thread named barrier per GEMM); all warps share the
+// TMA-streamed chain blocks and state blocks (full/empty mbarriers, 8 consumer
+// arrivals per stage).  The lane's output fragment (row 8I + l/4, shots q0, q0+1)
+// is also the slice of U / flux it owns in registers across the layer sweep.
+//   per subdomain (A+B): F_0 = G_0 (U_1 - U_0) -> face buffer; acc_0 = H_0 F_0;
+//     j = 1..L-1: F_j = G_j (U_{j+1} - U_j); A_j = H_j (F_j - F_{j-1}); leapfrog.
+//   after all subdomains: step flag; neighbour flags; C: layer-1 coupling + leapfrog.
+constexpr int M2_NC = 4;    // chain-block stages
+constexpr int M2_NSS = 8;   // state-block stages
+constexpr int M2_LDX = 12;  // X row stride (conflict-free B-fragment reads)
+constexpr int M2_NQ = 4;    // warps per shot column tile (row-tile groups)
+constexpr int M2_NW = 4 * M2_NQ;  // compute warps
+
+template <int M, int HH>  // HH: row-tile group of this warp (0..M2_NQ-1)
+__device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst, const double* sst, double* Xpair,
+                                            uint64_t* cfull, uint64_t* cempty, uint64_t* sfull, uint64_t* sempty,
+                                            uint64_t* stepdone, const int* ssub, const int* s_nb, int s0, int ns,
+                                            int cw, int lane) {
+    constexpr int S = 32;
+    constexpr int RT = (6 * M + 7) / 8;
+    constexpr int RH = (RT + M2_NQ - 1) / M2_NQ;  // row tiles per group
+    constexpr int I0 = HH * RH;                   // first row tile of this warp
+    constexpr int NI = (RT - I0 >= RH) ? RH : (RT - I0 > 0 ? RT - I0 : 1);  // row tiles of this warp (>= 1 slot)
+    constexpr int WP = 8 * RT;
+    constexpr int W = 6 * M;
+    const int TB = p.TB, L = p.L;
+    const long long K = p.K;
+    const long long WS = (long long)W * S, KS = K * S;
+    const int barP = 2 + cw;                    // named barrier of the column group (NQ warps)
+    int tr[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int r = 4 * h + (lane & 3), c = lane >> 2;
+        tr[h] = (c >> 2) * 32 + r * 4 + (c & 3);
+    }
+    long long c_con = 0, s_con = 0;
+    int xb = 0;  // X double buffer
+#ifdef SFW_MS_CLK
+    long long clk[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // c-wait, s-wait, gemm, total, flags, C, tail
+    const long long clk_start = clock64();
+#define MS_T0 const long long t0_ = clock64();
+#define MS_T1(i) clk[i] += clock64() - t0_;
+#else
+#define MS_T0
+#define MS_T1(i)
+#endif
+    auto c_acquire = [&]() -> const double* {
+        const int st = (int)(c_con % M2_NC);
+        MS_T0
+        mbar_wait(&cfull[st], (uint32_t)((c_con / M2_NC) & 1));
+        MS_T1(0)
+        return cst + (size_t)st * TB;
+    };
+    auto c_release = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[c_con % M2_NC]);
+        ++c_con;
+    };
+    auto s_acquire_at = [&](int o) -> const double* {  // o-th stage after the next unreleased one
+        const long long c = s_con + o;
+        const int st = (int)(c % M2_NSS);
+        MS_T0
+        mbar_wait(&sfull[st], (uint32_t)((c / M2_NSS) & 1));
+        MS_T1(1)
+        return sst + (size_t)st * WS;
+    };
+    auto s_release = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[s_con % M2_NSS]);
+        ++s_con;
+    };
+    const int r0 = lane >> 2;              // fragment row within a row tile
+    const int q0 = 8 * cw + 2 * (lane & 3);  // first of the lane's two shots
+    auto load_slice = [&](const double* blk, double (&v)[NI][2]) {
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int row = 8 * (I0 + i) + r0;
+            if (row < W) {
+                const double2 t = *reinterpret_cast<const double2*>(blk + (size_t)row * S + q0);
+                v[i][0] = t.x;
+                v[i][1] = t.y;
+            } else {
+                v[i][0] = v[i][1] = 0.0;
+            }
+        }
+    };
+    // write this warp's rows of X into the pair's next buffer, then meet the partner
+    auto put_x = [&](const double (&v)[NI][2]) -> const double* {
+        xb ^= 1;
+        double* Xw = Xpair + (size_t)xb * WP * M2_LDX;
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+            if (I0 + i < RT)
+                *reinterpret_cast<double2*>(Xw + (8 * (I0 + i) + r0) * M2_LDX + 2 * (lane & 3)) =
+                    make_double2(v[i][0], v[i][1]);
+        asm volatile("bar.sync %0, %1;" ::"r"(barP), "r"(M2_NQ * 32) : "memory");
+        return Xw;
+    };
+    // acc = B X over this warp's row tiles, B symmetric (lower tiles, fragment order)
+    auto gemm = [&](const double* tiles, const double* Xw, double (&acc)[NI][2]) {
+        MS_T0
+#pragma unroll
+        for (int i = 0; i < NI; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+        for (int kap = 0; kap < 2 * RT; ++kap) {
+            const int Kt = kap >> 1, h = kap & 1;
+            const double b = Xw[(4 * kap + (lane & 3)) * M2_LDX + r0];
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int I = I0 + i;
+                if (I >= RT) break;
+                const double a = (I >= Kt) ? tiles[(I * (I + 1) / 2 + Kt) * 64 + h * 32 + lane]
+                                           : tiles[(Kt * (Kt + 1) / 2 + I) * 64 + tr[h]];
+                dmma8x8x4(acc[i], a, b);
+            }
+        }
+#ifdef SFW_MS_CLK
+        for (int i = 0; i < NI; ++i) asm volatile("" ::"d"(acc[i][0]), "d"(acc[i][1]));
+#endif
+        MS_T1(2)
+    };
+    auto store_global = [&](double* blk, const double (&v)[NI][2]) {
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int row = 8 * (I0 + i) + r0;
+            if (row < W) *reinterpret_cast<double2*>(blk + (size_t)row * S + q0) = make_double2(v[i][0], v[i][1]);
+        }
+    };
+    const double dt2 = p.dt2;
+    const bool src0 = ssub[q0] >= 0, src1 = ssub[q0 + 1] >= 0;
+
+    for (int k = 1; k <= p.n_steps; ++k) {
+        const int par = k & 1;
+        const int cb = (k - 1) & 1;
+        double* Un = cb ? p.U0 : p.U1;
+        double* fx = p.flux + (size_t)par * p.n_sub * WS;
+        const int kk = k - 1;
+        const double f0 = src0 ? p.ftab[(size_t)q0 * p.ftab_stride + kk] : 0.0;
+        const double f1 = src1 ? p.ftab[(size_t)(q0 + 1) * p.ftab_stride + kk] : 0.0;
+        double sq0 = 0.0, sq1 = 0.0;
+        auto force = [&](int s, long long idx, int e) -> double {  // shot source term (ssub[q] == s)
+            const int q = q0 + e;
+            return __dmul_rn(p.shot_vec[p.shot_voff[q] + idx], e ? f1 : f0);
+        };
+
+        // ---------------- A + B: every subdomain's layer sweep --------------------------
+        for (int sl = 0; sl < ns; ++sl) {
+            const int s = s0 + sl;
+            double ua[NI][2], ub[NI][2], fp[NI][2], acc[NI][2];
+            const double* Xw;
+            {
+                double u0[NI][2];
+                load_slice(s_acquire_at(0), u0);
+                load_slice(s_acquire_at(1), ua);  // U_1
+                s_release();
+                s_release();
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    u0[i][0] = ua[i][0] - u0[i][0];
+                    u0[i][1] = ua[i][1] - u0[i][1];
+                }
+                Xw = put_x(u0);
+            }
+            gemm(c_acquire(), Xw, fp);  // F_0
+            c_release();
+            store_global(fx + (size_t)s * WS, fp);
+            Xw = put_x(fp);
+            gemm(c_acquire(), Xw, acc);  // acc_0 = H_0 F_0 (boundary faces)
+            c_release();
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {  // only rows of outer faces are ever read back
+                const int row = 8 * (I0 + i) + r0;
+                if (row < W && s_nb[sl * 6 + row / M] < 0)
+                    *reinterpret_cast<double2*>(p.acc1 + ((size_t)s * W + row) * S + q0) =
+                        make_double2(acc[i][0], acc[i][1]);
+            }
+            for (int j = 1; j < L; ++j) {
+                if (j + 1 < L) {
+                    load_slice(s_acquire_at(0), ub);  // U_{j+1}
+                    s_release();
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NI; ++i) ub[i][0] = ub[i][1] = 0.0;
+                }
+                {
+                    double x[NI][2];
+#pragma unroll
+                    for (int i = 0; i < NI; ++i) {
+                        x[i][0] = ub[i][0] - ua[i][0];
+                        x[i][1] = ub[i][1] - ua[i][1];
+                    }
+                    Xw = put_x(x);
+                }
+                gemm(c_acquire(), Xw, acc);  // F_j
+                c_release();
+                {
+                    double x[NI][2];
+#pragma unroll
+                    for (int i = 0; i < NI; ++i) {
+                        x[i][0] = acc[i][0] - fp[i][0];
+                        x[i][1] = acc[i][1] - fp[i][1];
+                        fp[i][0] = acc[i][0];
+                        fp[i][1] = acc[i][1];
+                    }
+                    Xw = put_x(x);
+                }
+                double uo[NI][2];
+                load_slice(s_acquire_at(0), uo);  // Uprev_j
+                s_release();
+                gemm(c_acquire(), Xw, acc);  // A_j
+                c_release();
+                double* un = Un + (size_t)s * KS + (size_t)j * WS;
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const int row = 8 * (I0 + i) + r0;
+                    double v[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        double tot = acc[i][e];
+                        if ((e ? src1 : src0) && row < W && ssub[q0 + e] == s)
+                            tot = __dadd_rn(tot, force(s, (long long)j * W + row, e));
+                        v[e] = __dadd_rn(__dsub_rn(__dmul_rn(2.0, ua[i][e]), uo[i][e]), __dmul_rn(dt2, tot));
+                    }
+                    if (row < W) {
+                        *reinterpret_cast<double2*>(un + (size_t)row * S + q0) = make_double2(v[0], v[1]);
+                        sq0 = fma(v[0], v[0], sq0);
+                        sq1 = fma(v[1], v[1], sq1);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    ua[i][0] = ub[i][0];
+                    ua[i][1] = ub[i][1];
+                }
+            }
+        }
+        // ---------------- step flag, neighbour flags ------------------------------------
+#ifdef SFW_MS_CLK
+        long long tf0 = clock64();
+#endif
+        asm volatile("bar.sync 1, %0;" ::"r"(M2_NW * 32) : "memory");
+        if (cw == 0 && HH == 0 && lane == 0) flag_publish(p.flags, (unsigned int)k);
+        if (cw == 0 && HH == 0)
+            flags_wait(p.flags, p.ncta + p.ncta_ptr[blockIdx.x], p.ncta_ptr[blockIdx.x + 1] - p.ncta_ptr[blockIdx.x],
+                       (unsigned int)k, lane);
+        asm volatile("bar.sync 1, %0;" ::"r"(M2_NW * 32) : "memory");
+#ifdef SFW_MS_CLK
+        clk[4] += clock64() - tf0;
+        tf0 = clock64();
+#endif
+        // ---------------- C: layer-1 face coupling + leapfrog ---------------------------
+        for (int sl = 0; sl < ns; ++sl) {
+            const int s = s0 + sl;
+            const double* mb = s_acquire_at(0);  // [6][M][M] interface mass
+            // own + neighbour layer-1 flux of every face row, the pair's 8 shots; each warp
+            // of the pair stages half of the rows (independent loads: one L2 round trip)
+            xb ^= 1;
+            double* T = Xpair + (size_t)xb * WP * M2_LDX;
+            {
+                constexpr int NROW = (6 * M + M2_NQ - 1) / M2_NQ;  // rows per warp
+                constexpr int NIT = (NROW * 4 + 31) / 32;
+                double2 ow[NIT], ot[NIT];
+#pragma unroll
+                for (int t = 0; t < NIT; ++t) {
+                    const int it = lane + 32 * t, row = HH * NROW + (it >> 2), pr = it & 3;
+                    ow[t] = ot[t] = make_double2(0.0, 0.0);
+                    if ((it >> 2) < NROW && row < 6 * M) {
+                        const int f = row / M, c = row % M, nb = s_nb[sl * 6 + f];
+                        if (nb >= 0) {
+                            ow[t] = __ldcg(reinterpret_cast<const double2*>(fx + ((size_t)s * W + row) * S + 8 * cw + 2 * pr));
+                            ot[t] = __ldcg(reinterpret_cast<const double2*>(fx + ((size_t)nb * W + (f ^ 1) * M + c) * S +
+                                                                           8 * cw + 2 * pr));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < NIT; ++t) {
+                    const int it = lane + 32 * t, row = HH * NROW + (it >> 2), pr = it & 3;
+                    if ((it >> 2) < NROW && row < 6 * M)
+                        *reinterpret_cast<double2*>(T + row * M2_LDX + 2 * pr) =
+                            make_double2(__dadd_rn(ow[t].x, ot[t].x), __dadd_rn(ow[t].y, ot[t].y));
+                }
+            }
+            double a1[NI][2];
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {  // boundary-face accelerations (prefetch)
+                const int row = 8 * (I0 + i) + r0;
+                a1[i][0] = a1[i][1] = 0.0;
+                if (row < W && s_nb[sl * 6 + row / M] < 0) {
+                    const double2 t = __ldcg(reinterpret_cast<const double2*>(p.acc1 + ((size_t)s * W + row) * S + q0));
+                    a1[i][0] = t.x;
+                    a1[i][1] = t.y;
+                }
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(barP), "r"(M2_NQ * 32) : "memory");
+            double u0[NI][2], uo[NI][2];
+            load_slice(s_acquire_at(1), u0);
+            load_slice(s_acquire_at(2), uo);
+            double* un = Un + (size_t)s * KS;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const int row = 8 * (I0 + i) + r0;
+                if (row >= W) continue;
+                const int f = row / M, r = row % M;
+                double a[2] = {a1[i][0], a1[i][1]};
+                if (s_nb[sl * 6 + f] >= 0) {
+                    a[0] = a[1] = 0.0;
+                    const double* mx = mb + (f * M + r) * M;
+                    const double* tx = T + (f * M) * M2_LDX + 2 * (lane & 3);
+#pragma unroll
+                    for (int c = 0; c < M; ++c) {
+                        const double mc = mx[c];
+                        const double2 t = *reinterpret_cast<const double2*>(tx + c * M2_LDX);
+                        a[0] = fma(mc, t.x, a[0]);
+                        a[1] = fma(mc, t.y, a[1]);
+                    }
+                }
+                double v[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    double tot = a[e];
+                    if ((e ? src1 : src0) && ssub[q0 + e] == s) tot = __dadd_rn(tot, force(s, row, e));
+                    v[e] = __dadd_rn(__dsub_rn(__dmul_rn(2.0, u0[i][e]), uo[i][e]), __dmul_rn(dt2, tot));
+                }
+                *reinterpret_cast<double2*>(un + (size_t)row * S + q0) = make_double2(v[0], v[1]);
+                sq0 = fma(v[0], v[0], sq0);
+                sq1 = fma(v[1], v[1], sq1);
+            }
+            s_release();  // mass
+            s_release();  // U_0
+            s_release();  // Uprev_0
+        }
+#ifdef SFW_MS_CLK
+        clk[5] += clock64() - tf0;
+        tf0 = clock64();
+#endif
+        // per-shot |U|^2 of this warp's rows: lanes with equal (lane & 3) hold the same shots;
+        // the pair's two halves go to separate partial slots (k_ms_norms sums them)
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            sq0 += __shfl_xor_sync(0xffffffffu, sq0, o);
+            sq1 += __shfl_xor_sync(0xffffffffu, sq1, o);
+        }
+        if (lane < 4) {
+            double* np = p.norm_part + (((size_t)kk * gridDim.x + blockIdx.x) * M2_NQ + HH) * S + q0;
+            np[0] = sq0;
+            np[1] = sq1;
+        }
+        // probes (this warp: its pair's 8 shots, every other probe): rows of U after the step
+        if (k % p.record_every == 0 && p.rows) {
+            asm volatile("bar.sync %0, %1;" ::"r"(barP), "r"(M2_NQ * 32) : "memory");  // group's U rows written
+            const long long row = k / p.record_every - 1;
+            const int q = 8 * cw + (lane & 7);
+            for (int s = s0; s < s0 + ns; ++s) {
+                const double* us = Un + (size_t)s * KS;
+                for (int pq = p.prb_ptr[s] + M2_NQ * (lane >> 3) + HH; pq < p.prb_ptr[s + 1]; pq += 4 * M2_NQ) {
+                    const int pid = p.prb_ids[pq];
+                    const int tap = p.prb_tap[pid];
+                    double val;
+                    if (tap >= 0) {
+                        val = us[(size_t)tap * S + q];
+                    } else {
+                        const double* wv = p.prb_w + p.prb_woff[pid];
+                        val = 0.0;
+                        for (long long i = 0; i < K; ++i) val = fma(wv[i], us[i * S + q], val);
+                    }
+                    p.rows[(row * p.n_probe + pid) * S + q] = val;
+                }
+            }
+        }
+        // this step's state writes feed the next step's TMA reads (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(stepdone);
+#ifdef SFW_MS_CLK
+        clk[6] += clock64() - tf0;
+#endif
+    }
+#ifdef SFW_MS_CLK
+    clk[3] = clock64() - clk_start;
+    if (lane < 8 && p.dbg) {
+        long long v = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (lane == i) v = clk[i];
+        p.dbg[(blockIdx.x * M2_NW + M2_NQ * cw + HH) * 8 + lane] = v;
+    }
+#endif
+#undef MS_T0
+#undef MS_T1
+}
+
+template <int M>
+__global__ void __launch_bounds__((M2_NW + 1) * 32, 1) k_step_ms2(const MsParams p) {
+    constexpr int S = 32;
+    constexpr int RT = (6 * M + 7) / 8;
+    constexpr int WP = 8 * RT;
+    constexpr int W = 6 * M;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L = p.L, TB = p.TB;
+    const long long K = p.K;
+    const long long WS = (long long)W * S, KS = K * S;
+    double* cst = reinterpret_cast<double*>(smem_raw);   // [NC][TB]
+    double* sst = cst + (size_t)M2_NC * TB;              // [NSS][W*S]
+    double* Xall = sst + (size_t)M2_NSS * WS;            // [4 column groups][2][WP][LDX]
+    uint64_t* cfull = reinterpret_cast<uint64_t*>(Xall + (size_t)4 * 2 * WP * M2_LDX);
+    uint64_t* cempty = cfull + M2_NC;
+    uint64_t* sfull = cempty + M2_NC;
+    uint64_t* sempty = sfull + M2_NSS;
+    uint64_t* stepdone = sempty + M2_NSS;
+    int* ssub = reinterpret_cast<int*>(stepdone + 1);
+    int* s_nb = ssub + S;  // [ns][6] face neighbours of the CTA's subdomains
+
+    for (int q = threadIdx.x; q < S; q += blockDim.x) ssub[q] = p.shot_sub[q];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < M2_NC; ++i) {
+            mbar_init(&cfull[i], 1);
+            mbar_init(&cempty[i], M2_NW);
+        }
+        for (int i = 0; i < M2_NSS; ++i) {
+            mbar_init(&sfull[i], 1);
+            mbar_init(&sempty[i], M2_NW);
+        }
+        mbar_init(stepdone, M2_NW);
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < 4 * 2 * WP * M2_LDX; i += blockDim.x) Xall[i] = 0.0;
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int ns = s1 - s0;
+    for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nb[i] = p.nbr[s0 * 6 + i];
+    __syncthreads();
+
+    // ======== producer warp: chain blocks (ungated) and state blocks (gated per step) ====
+    if (warp == M2_NW) {
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            const uint64_t pol_state = l2_policy_evict_last();
+            const int cper = ns * 2 * L;
+            const long long ctotal = (long long)cper * p.n_steps;
+            const int sper = ns * (2 * L - 1) + 3 * ns;
+            const uint32_t mbytes = (uint32_t)(6 * M * M * 8);
+            const long long stotal = (long long)sper * p.n_steps;
+            const uint32_t sbytes = (uint32_t)(WS * 8), cbytes = (uint32_t)TB * 8u;
+            long long c_iss = 0, s_iss = 0;
+            int cpos = 0, spos = 0, sstep = 0;
+            while (c_iss < ctotal || s_iss < stotal) {
+                if (c_iss < ctotal) {
+                    const int st = (int)(c_iss % M2_NC);
+                    if (mbar_test_wait(&cempty[st], (uint32_t)(((c_iss / M2_NC) & 1) ^ 1))) {
+                        mbar_arrive_expect_tx(&cfull[st], cbytes);
+                        bulk_g2s(cst + (size_t)st * TB, p.tcoef + ((long long)s0 * 2 * L + cpos) * TB, cbytes, &cfull[st],
+                                 pol);
+                        ++c_iss;
+                        if (++cpos == cper) cpos = 0;
+                    }
+                }
+                if (s_iss < stotal) {
+                    // step k >= 2 reads what step k-1 wrote: wait for all compute warps
+                    const bool ready = spos > 0 || sstep == 0 || mbar_test_wait(stepdone, (uint32_t)((sstep - 1) & 1));
+                    const int st = (int)(s_iss % M2_NSS);
+                    if (ready && mbar_test_wait(&sempty[st], (uint32_t)(((s_iss / M2_NSS) & 1) ^ 1))) {
+                        const int cb = sstep & 1;
+                        const double* cur = cb ? p.U1 : p.U0;
+                        const double* prv = cb ? p.U0 : p.U1;
+                        const double* src;
+                        uint32_t bytes = sbytes;
+                        const int nab = 2 * L - 1;
+                        if (spos < ns * nab) {
+                            const int sl = spos / nab, r = spos % nab;
+                            const long long base = (long long)(s0 + sl) * KS;
+                            if (r < 2) {
+                                src = cur + base + r * WS;  // U_0, U_1
+                            } else {
+                                const int rp = r - 2;   // j = 1..L-1: [U_{j+1}], Uprev_j
+                                if (rp < 2 * (L - 2)) {
+                                    const int j = 1 + rp / 2;
+                                    src = (rp & 1) ? prv + base + j * WS : cur + base + (j + 1) * WS;
+                                } else {
+                                    src = prv + base + (L - 1) * WS;
+                                }
+                            }
+                        } else {
+                            const int r = spos - ns * nab, sl = r / 3, w3 = r % 3;
+                            if (w3 == 0) {  // interface mass of the 6 faces
+                                src = p.mblk + (size_t)(s0 + sl) * 6 * M * M;
+                                bytes = mbytes;
+                            } else {
+                                src = ((w3 == 2) ? prv : cur) + (long long)(s0 + sl) * KS;  // U_0, Uprev_0
+                            }
+                        }
+                        mbar_arrive_expect_tx(&sfull[st], bytes);
+                        bulk_g2s(sst + (size_t)st * WS, src, bytes, &sfull[st], pol_state);
+                        ++s_iss;
+                        if (++spos == sper) {
+                            spos = 0;
+                            ++sstep;
+                        }
+                    }
+                }
+            }
+        }
+        return;
+    }
+    // ======== compute warps: (column tile cw, row half hh) ========
+    // SMSP (warp % 4) hosts one warp of every row-tile group -> equal DMMA work per SMSP
+    const int cw = warp / M2_NQ, hh = (warp / M2_NQ + warp) % M2_NQ;
+    double* Xpair = Xall + (size_t)cw * 2 * WP * M2_LDX;
+    switch (hh) {
+        case 0: ms2_compute<M, 0>(p, cst, sst, Xpair, cfull, cempty, sfull, sempty, stepdone, ssub, s_nb, s0, ns, cw, lane); break;
+        case 1: ms2_compute<M, 1>(p, cst, sst, Xpair, cfull, cempty, sfull, sempty, stepdone, ssub, s_nb, s0, ns, cw, lane); break;
+        case 2: ms2_compute<M, 2>(p, cst, sst, Xpair, cfull, cempty, sfull, sempty, stepdone, ssub, s_nb, s0, ns, cw, lane); break;
+        default: ms2_compute<M, 3>(p, cst, sst, Xpair, cfull, cempty, sfull, sempty, stepdone, ssub, s_nb, s0, ns, cw, lane); break;
+    }
+}
+
+static size_t ms2_smem_bytes(int RT, int TB, int W, int nsmax) {
+    return 8 * ((size_t)M2_NC * TB + (size_t)M2_NSS * W * 32 + (size_t)4 * 2 * 8 * RT * M2_LDX + 2 * M2_NC +
+                2 * M2_NSS + 1) +
+           4 * (32 + 6 * (size_t)nsmax) + 64;
+}
+
+// per-subdomain interface mass blocks [n_sub][6][m*m] (zeros on outer faces)
+__global__ void k_ms_massblocks(const double* __restrict__ mass, const int* __restrict__ mass_idx, int n_sub, int m,
+                                double* __restrict__ out) {
+    const long long total = (long long)n_sub * 6 * m * m;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long sf = i / (m * m);
+        const int e = (int)(i % (m * m));
+        const int mi = mass_idx[sf];
+        out[i] = mi >= 0 ? mass[(size_t)mi * m * m + e] : 0.0;
+    }
+}
+
+static const void* ms2_kernel(int m) {
+    static const void* const tab[10] = {nullptr,
+                                        (const void*)k_step_ms2<1>,
+                                        (const void*)k_step_ms2<2>,
+                                        (const void*)k_step_ms2<3>,
+                                        (const void*)k_step_ms2<4>,
+                                        (const void*)k_step_ms2<5>,
+                                        (const void*)k_step_ms2<6>,
+                                        (const void*)k_step_ms2<7>,
+                                        (const void*)k_step_ms2<8>,
+                                        (const void*)k_step_ms2<9>};
+    return (m >= 1 && m <= 9) ? tab[m] : nullptr;
+}
+
 // shots start from rest (u0 = v0 = 0): U_curr = 0, U_prev = ((0.5 dt) dt) (vec_q f_q(0))  (stepper.py:347-353)
 __global__ void k_ms_init(double* U0, double* U1, long long total, int S, const int* shot_sub,
                           const double* shot_vec, const long long* shot_voff, const double* f0, double half,
@@ -623,6 +1182,20 @@ extern "C" int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub,
     if (L < 2) return fail(SFW_ECONFIG, "multi-shot stepping needs at least 2 layers", errbuf, errlen);
     SFW_CUDA_TRY(cudaFuncSetAttribute((const void*)k_step_ms<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       h->shot_smem));
+    if (ms2_kernel(h->m) && !getenv("SFW_MS_V1")) {
+        const void* k2 = ms2_kernel(h->m);
+        int nsmax = 0;
+        for (int b = 0; b < h->grid; ++b) nsmax = std::max(nsmax, h->cta_ptr_h[b + 1] - h->cta_ptr_h[b]);
+        h->shot_smem2 = (int)ms2_smem_bytes(RT, h->TB, W, nsmax);
+        if (!h->mmass && (rc = dalloc(&h->mmass, (size_t)h->n_sub * 6 * h->m * h->m, errbuf, errlen))) return rc;
+        k_ms_massblocks<<<592, 256, 0, h->stream>>>(h->mass, h->mass_idx, h->n_sub, h->m, h->mmass);
+        if (h->shot_smem2 <= 220 * 1024)
+            SFW_CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, h->shot_smem2));
+        else
+            h->shot_smem2 = 0;
+    } else {
+        h->shot_smem2 = 0;
+    }
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
     SFW_CUDA_TRY(cudaGetLastError());
     return 0;
@@ -646,7 +1219,8 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
                                  h->stream));
     const long long nrec = n_steps / record_every;
     if ((rc = ms_ensure(&h->mrows, &h->mrows_cap, std::max(1LL, nrec * h->n_probe * S), errbuf, errlen))) return rc;
-    if ((rc = ms_ensure(&h->mnorm, &h->mnorm_cap, (long long)n_steps * h->grid * S + (long long)n_steps * S, errbuf,
+    const int nparts = h->shot_smem2 ? M2_NQ * h->grid : h->grid;  // ms2: one partial per row-tile group
+    if ((rc = ms_ensure(&h->mnorm, &h->mnorm_cap, (long long)n_steps * nparts * S + (long long)n_steps * S, errbuf,
                         errlen)))
         return rc;
     const long long total = (long long)h->n_sub * L * W * S;
@@ -692,13 +1266,29 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
     p.ncta_ptr = h->ncta_ptr;
     p.ncta = h->ncta;
     p.evict_first = 1;
+    p.dbg = nullptr;
+    p.mblk = h->mmass;
+    if (getenv("SFW_STEP_PROF")) {
+        const size_t need = (size_t)h->grid * M2_NW * 8;
+        if (h->tprof_n < need) {
+            if (h->tprof) cudaFree(h->tprof);
+            cudaMalloc(&h->tprof, need * 8);
+            h->tprof_n = need;
+        }
+        cudaMemsetAsync(h->tprof, 0, need * 8, h->stream);
+        p.dbg = h->tprof;
+    }
     void* args[] = {&p};
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
-    SFW_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_step_ms<32>, dim3(h->grid), dim3((MS_NW + 1) * 32), args,
-                                             h->shot_smem, h->stream));
+    if (h->shot_smem2)
+        SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ms2_kernel(h->m), dim3(h->grid), dim3((M2_NW + 1) * 32), args,
+                                                 h->shot_smem2, h->stream));
+    else
+        SFW_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_step_ms<32>, dim3(h->grid), dim3((MS_NW + 1) * 32),
+                                                 args, h->shot_smem, h->stream));
     SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
-    double* dn = h->mnorm + (size_t)n_steps * h->grid * S;
-    k_ms_norms<<<(unsigned)((n_steps * S + 255) / 256), 256, 0, h->stream>>>(h->mnorm, n_steps, h->grid, S, dn);
+    double* dn = h->mnorm + (size_t)n_steps * nparts * S;
+    k_ms_norms<<<(unsigned)((n_steps * S + 255) / 256), 256, 0, h->stream>>>(h->mnorm, n_steps, nparts, S, dn);
     if (norms_out)
         SFW_CUDA_TRY(cudaMemcpyAsync(norms_out, dn, (size_t)n_steps * S * 8, cudaMemcpyDeviceToHost, h->stream));
     if (rows_out && nrec * h->n_probe > 0)

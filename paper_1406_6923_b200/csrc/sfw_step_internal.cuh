@@ -79,7 +79,8 @@ struct sfw_stepper {
     double* flux = nullptr;
     double* sq = nullptr;
     // multi-shot mode (sfw_shots_*): S independent wavefields, DMMA tile-packed chain blocks
-    int n_shots = 0, shot_smem = 0;
+    int n_shots = 0, shot_smem = 0, shot_smem2 = 0;
+    double* mmass = nullptr;  // multi-shot: per-subdomain interface mass blocks
     double* tcoef = nullptr;          // [n_blocks][TB] fragment-ordered 8x8 lower tiles
     int TB = 0;
     double *UM[2] = {nullptr, nullptr};
