@@ -7,7 +7,13 @@ SRC := $(wildcard $(PKG)/csrc/*.cu)
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 LIB := $(PKG)/libsfw_b200.so
 
-all: $(LIB)
+all: $(LIB) tools
+
+tools: build/fp64_peak
+
+build/fp64_peak: tools/fp64_peak.cu
+	@mkdir -p build
+	$(NVCC) -O3 $(ARCH) -o $@ $<
 
 build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/sfw_b200.h
 	@mkdir -p build
@@ -21,4 +27,4 @@ oracle: oracle/_ref/.stamp
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean oracle
+.PHONY: all clean oracle tools

@@ -37,185 +37,170 @@ __host__ __device__ constexpr int off_I(int t) { return t < 1 ? 1 : t < 3 ? 2 : 
 __host__ __device__ constexpr int off_K(int t) { return t - off_I(t) * (off_I(t) - 1) / 2; }
 __host__ __device__ constexpr int off_tile(int I, int K) { return I * (I - 1) / 2 + K; }
 
-// same 6-group lower-packed layout as the fp64 stepper (sfw_step.cu packed_pos)
+// Packed fp32 block (symmetric A_j, or lower-triangular B_j^T), laid out for 16-B shared loads.
+// A w x w block (w = 6m) is 15 off-diagonal m x m tiles t = (I > K) plus 6 diagonal lower
+// triangles d.  Inside a tile, element e <-> (r, c) = (e % m, (e / m + e % m) % m) (wrapped
+// diagonals: m consecutive e touch m distinct rows and columns).  Inside a triangle, element
+// q = dd*m - dd(dd-1)/2 + c holds row c + dd, column c.  Storage (floats):
+//   [tile chunks]  (e/4)*60 + t*4 + e%4             for e < 4*NC,  NC  = m*m/4
+//   [tri chunks]   60*NC + (q/4)*24 + d*4 + q%4     for q < 4*NC2, NC2 = tri/4
+//   [tile tails]   60*NC + 24*NC2 + (e-4NC)*15 + t
+//   [tri tails]    60*NC + 24*NC2 + 15*(m*m%4) + (q-4NC2)*6 + d
+// so the 15 tile lanes (or 6 triangle lanes) of a warp read one float4 each per LDS.128.
+__host__ __device__ constexpr int nc1(int m) { return (m * m) / 4; }
+__host__ __device__ constexpr int nc2(int m) { return tri_count(m) / 4; }
+__host__ __device__ constexpr int tri_base(int m) { return 60 * nc1(m); }
+__host__ __device__ constexpr int tail1_base(int m) { return 60 * nc1(m) + 24 * nc2(m); }
+__host__ __device__ constexpr int tail2_base(int m) { return tail1_base(m) + 15 * ((m * m) % 4); }
+__host__ __device__ inline int off_pos(int m, int t, int e) {
+    return e < 4 * nc1(m) ? (e / 4) * 60 + t * 4 + (e % 4) : tail1_base(m) + (e - 4 * nc1(m)) * 15 + t;
+}
+__host__ __device__ inline int diag_pos(int m, int d, int q) {
+    return q < 4 * nc2(m) ? tri_base(m) + (q / 4) * 24 + d * 4 + (q % 4) : tail2_base(m) + (q - 4 * nc2(m)) * 6 + d;
+}
+__host__ __device__ constexpr int tri_row0(int m, int dd) { return dd * m - dd * (dd - 1) / 2; }
+__host__ __device__ constexpr int tri_dd(int m, int q) {
+    int dd = 0;
+    while (q >= tri_row0(m, dd + 1)) ++dd;
+    return dd;
+}
 __host__ __device__ inline int packed_pos(int m, int row, int col) {
-    int I = row / m, K = col / m, r = row % m, c = col % m;
-    if (I != K) {
-        const int t = off_tile(I, K);
-        const int q = (c - r + m) % m;
-        return (q * m + r) * 15 + t;
-    }
-    const int d = r - c;
-    int e = 0;
-    for (int dd = 0; dd < d; ++dd) e += m - dd;
-    e += c;
-    return 15 * m * m + e * 6 + I;
+    const int I = row / m, K = col / m, r = row % m, c = col % m;
+    if (I != K) return off_pos(m, off_tile(I, K), ((c - r + m) % m) * m + r);
+    const int dd = r - c;
+    return diag_pos(m, I, dd * m - dd * (dd - 1) / 2 + c);
 }
 }  // namespace wf
 
-// offsets of the partials summed into each output row (conflict-free layout slot*21 + tile)
+// Partial-sum slots of the paired block product (per output row r of a tile group, stride PS):
+//   [0,15)  tile t rows I: A_j + B_j^T row partials      -> p_j
+//   [15,30) tile t rows K: A_j column partials            -> p_j
+//   [30,45) tile t rows K: B_j column partials (B_j W_j)  -> c_{j+1}
+//   [45,51) triangle d:    A_j (both parts) + B_j^T rows  -> p_j
+//   [51,57) triangle d:    B_j column partials            -> c_{j+1}
+//   57      zero
+constexpr int PS = 61;  // 57 zero slot, 58-60 junk slots of idle lanes
+
 template <int M>
-struct WRed {
+struct WRed2 {
     static constexpr int W = 6 * M, EPL = (W + 31) / 32;
-    int sym[EPL][6];  // symmetric product: 6 terms (as sfw_step.cu RedOff)
-    int lo[EPL][6];   // L x   : rows R: tiles (R,K<=R) row partials, -1 padded
-    int up[EPL][6];   // L^T x': rows K: tiles (I>=K,K) column partials, -1 padded
-    __device__ __forceinline__ explicit WRed(int lane) {
+    int po[EPL][6], co[EPL][6];
+    __device__ __forceinline__ explicit WRed2(int lane) {
 #pragma unroll
         for (int e = 0; e < EPL; ++e) {
             const int i = lane + 32 * e;
             const int R = i < W ? i / M : 0, r = i < W ? i % M : 0;
 #pragma unroll
-            for (int t = 0; t < 6; ++t) {
-                sym[e][t] = (t < R) ? r * 21 + wf::off_tile(R, t)
-                                    : (t == R) ? r * 21 + 15 + R : (M + r) * 21 + wf::off_tile(t, R);
-                lo[e][t] = (t < R) ? r * 21 + wf::off_tile(R, t) : (t == R) ? r * 21 + 15 + R : -1;
-                up[e][t] = (t == R) ? (M + r) * 21 + 15 + R : (t > R) ? (M + r) * 21 + wf::off_tile(t, R) : -1;
+            for (int q = 0; q < 6; ++q) {
+                // p_j: tiles (R, K < R) rows, tiles (I > R, R) columns, triangle R
+                po[e][q] = q < R ? r * PS + wf::off_tile(R, q)
+                                 : q < 5 ? r * PS + 15 + wf::off_tile(q + 1, R) : r * PS + 45 + R;
+                // c_{j+1}: tiles (I > R, R) columns of B_j, triangle R, zero slot
+                co[e][q] = q < 5 - R ? r * PS + 30 + wf::off_tile(R + 1 + q, R)
+                                     : q == 5 - R ? r * PS + 51 + R : r * PS + 57;
             }
         }
     }
 };
 
-// y = A x, A symmetric lower-packed (fp32, one warp)
+// One warp, one pass over the pair (A_j, B_j^T) staged in shared memory:
+//   half 0 (lanes 0-15) reads A_j, half 1 (lanes 16-31) reads B_j^T.
+//   p_j = A_j x_j + B_j^T x_{j+1},   c_{j+1} = B_j x_j     (partials into `part`, summed by WRed2)
+// Control flow is warp-uniform: idle lanes (t = 15 in the tile pass, t >= 6 in the triangle
+// pass, half 1 when !hasB) run the same code on finite shared data with x = 0 and store to
+// junk slots, so the warp never splits (a split warp runs each half separately).
 template <int M>
-__device__ __forceinline__ void wsym(const float* __restrict__ blk, const float* x, float* part, float* y, int lane,
-                                     const WRed<M>& ro) {
-    constexpr int W = 6 * M;
-    if (lane < 15) {
-        const int I = wf::off_I(lane), K = wf::off_K(lane);
-        float xk[M], xi[M], P[M], Q[M];
+__device__ __forceinline__ void wpair(const float* __restrict__ blkA, const float* xj, const float* xj1, float* part,
+                                      int lane, bool hasB, int BS) {
+    constexpr int MM = M * M, NC = wf::nc1(M), TRI = wf::tri_count(M), NC2 = wf::nc2(M);
+    const int h = lane >> 4, t = lane & 15;
+    const float* blk = blkA + h * BS;
+    const bool act = (h == 0) || hasB;
+    const float* xv = h ? xj1 : xj;
+    {
+        const int tt = t < 15 ? t : 14;
+        const float xs = (t < 15 && act) ? 1.f : 0.f;
+        const int I = wf::off_I(tt), K = wf::off_K(tt);
+        float P[M], Q[M], xk[M], xi[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            xk[i] = x[K * M + i];
-            xi[i] = x[I * M + i];
+            xk[i] = xv[K * M + i] * xs;
+            xi[i] = xj[I * M + i] * xs;
             P[i] = Q[i] = 0.f;
         }
 #pragma unroll
-        for (int e = 0; e < M * M; ++e) {
+        for (int ch = 0; ch < NC; ++ch) {
+            const float4 a4 = *reinterpret_cast<const float4*>(blk + ch * 60 + tt * 4);
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = ch * 4 + u, r = e % M, c = (e / M + r) % M;
+                P[r] = fmaf(av[u], xk[c], P[r]);
+                Q[c] = fmaf(av[u], xi[r], Q[c]);
+            }
+        }
+#pragma unroll
+        for (int e = 4 * NC; e < MM; ++e) {
             const int r = e % M, c = (e / M + r) % M;
-            const float a = blk[e * 15 + lane];
+            const float a = blk[wf::tail1_base(M) + (e - 4 * NC) * 15 + tt];
             P[r] = fmaf(a, xk[c], P[r]);
             Q[c] = fmaf(a, xi[r], Q[c]);
         }
+        const int sa = t == 15 ? 58 : (h ? 30 + t : t);  // h0: A+B^T rows I; h1: B columns K
+        const int sb = (t == 15 || h) ? 59 : 15 + t;       // h0: A columns K
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            part[i * 21 + lane] = P[i];
-            part[(M + i) * 21 + lane] = Q[i];
+            const float ps = P[i] + __shfl_xor_sync(0xffffffffu, P[i], 16);
+            part[i * PS + sa] = h ? Q[i] : ps;
+            part[i * PS + sb] = Q[i];
         }
     }
-    if (lane < 6) {
-        float xi[M], P[M];
+    {
+        const int d = t < 6 ? t : 5;
+        const float xs = (t < 6 && act) ? 1.f : 0.f;
+        const float qsel = h ? 1.f : 0.f;  // symmetric block: diagonal counted once
+        float P[M], Q[M], xa[M], xb[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            xi[i] = x[lane * M + i];
-            P[i] = 0.f;
-        }
-        const float* b = blk + 15 * M * M + lane;
-#pragma unroll
-        for (int d = 0; d < M; ++d)
-#pragma unroll
-            for (int r = d; r < M; ++r) {
-                const int c = r - d;
-                const float a = b[(d * M - d * (d - 1) / 2 + c) * 6];
-                P[r] = fmaf(a, xi[c], P[r]);
-                if (d != 0) P[c] = fmaf(a, xi[r], P[c]);
-            }
-#pragma unroll
-        for (int i = 0; i < M; ++i) part[i * 21 + 15 + lane] = P[i];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < WRed<M>::EPL; ++e) {
-        const int i = lane + 32 * e;
-        if (i < W) {
-            float s = part[ro.sym[e][0]];
-#pragma unroll
-            for (int t = 1; t < 6; ++t) s += part[ro.sym[e][t]];
-            y[i] = s;
-        }
-    }
-    __syncwarp();
-}
-
-// y1 = Lo x (Lo lower-packed incl. diagonal), y2 = Lo^T x2   (one warp, one pass over Lo)
-template <int M>
-__device__ __forceinline__ void wtri2(const float* __restrict__ blk, const float* x, const float* x2, float* part,
-                                      float* y1, float* y2, int lane, const WRed<M>& ro) {
-    constexpr int W = 6 * M;
-    if (lane < 15) {
-        const int I = wf::off_I(lane), K = wf::off_K(lane);
-        float xk[M], xi[M], P[M], Q[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            xk[i] = x[K * M + i];
-            xi[i] = x2[I * M + i];
+            xa[i] = xv[d * M + i] * xs;
+            xb[i] = xj[d * M + i] * xs;
             P[i] = Q[i] = 0.f;
         }
+        auto term = [&](int q, float a) {
+            const int dd = wf::tri_dd(M, q), c = q - wf::tri_row0(M, dd), r = c + dd;
+            P[r] = fmaf(a, xa[c], P[r]);
+            Q[c] = fmaf(dd == 0 ? a * qsel : a, xb[r], Q[c]);
+        };
 #pragma unroll
-        for (int e = 0; e < M * M; ++e) {
-            const int r = e % M, c = (e / M + r) % M;
-            const float a = blk[e * 15 + lane];
-            P[r] = fmaf(a, xk[c], P[r]);
-            Q[c] = fmaf(a, xi[r], Q[c]);
+        for (int ch = 0; ch < NC2; ++ch) {
+            const float4 a4 = *reinterpret_cast<const float4*>(blk + wf::tri_base(M) + ch * 24 + d * 4);
+            term(ch * 4 + 0, a4.x);
+            term(ch * 4 + 1, a4.y);
+            term(ch * 4 + 2, a4.z);
+            term(ch * 4 + 3, a4.w);
         }
+#pragma unroll
+        for (int q = 4 * NC2; q < TRI; ++q) term(q, blk[wf::tail2_base(M) + (q - 4 * NC2) * 6 + d]);
+        const int sa = t >= 6 ? 60 : (h ? 51 + t : 45 + t);
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-            part[i * 21 + lane] = P[i];
-            part[(M + i) * 21 + lane] = Q[i];
+            float D = h ? P[i] : P[i] + Q[i];
+            D += __shfl_xor_sync(0xffffffffu, D, 16);
+            part[i * PS + sa] = h ? Q[i] : D;
         }
     }
-    if (lane < 6) {
-        float xa[M], xb[M], P[M], Q[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            xa[i] = x[lane * M + i];
-            xb[i] = x2[lane * M + i];
-            P[i] = Q[i] = 0.f;
-        }
-        const float* b = blk + 15 * M * M + lane;
-#pragma unroll
-        for (int d = 0; d < M; ++d)
-#pragma unroll
-            for (int r = d; r < M; ++r) {
-                const int c = r - d;
-                const float a = b[(d * M - d * (d - 1) / 2 + c) * 6];
-                P[r] = fmaf(a, xa[c], P[r]);
-                Q[c] = fmaf(a, xb[r], Q[c]);
-            }
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            part[i * 21 + 15 + lane] = P[i];
-            part[(M + i) * 21 + 15 + lane] = Q[i];
-        }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < WRed<M>::EPL; ++e) {
-        const int i = lane + 32 * e;
-        if (i < W) {
-            float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-            for (int t = 0; t < 6; ++t) {
-                if (ro.lo[e][t] >= 0) s1 += part[ro.lo[e][t]];
-                if (ro.up[e][t] >= 0) s2 += part[ro.up[e][t]];
-            }
-            y1[i] = s1;
-            y2[i] = s2;
-        }
-    }
-    __syncwarp();
 }
 
 struct WParams {
     int n_sub, L, BS, n_steps, record_every, n_probe, ftab_stride, mode;  // mode 0 step, 1 init
+    unsigned int tag0;      // mailbox tag of step k is tag0 + k (monotone across launches)
     double dt;
     float dt2, half;
-    const float* coef;      // [n_sub][2L-1][BS]: A_0, B_0, A_1, B_1, ..., A_{L-1}
-    float* W0;
-    float* W1;
+    const float* coef;      // [n_sub][2L-1][BS]: A_0, B_0^T, A_1, B_1^T, ..., A_{L-1}
+    float* W0;              // current level (read)
+    float* W1;              // previous level, overwritten with the next level
     const float* V0;        // init velocity (W-form) or null
-    float* P;               // [2][n_sub][K] row partials (layer 0 = face mailbox)
-    float* Cc;              // [n_sub][K] carries B_{j-1} W_{j-1}
+    unsigned long long* mbox;  // [2][n_sub][W] tagged layer-0 partials p_0 (face mailbox)
     const int* cta_sub_ptr;
     const int* nbr;
     const int* src_ptr;
@@ -225,16 +210,11 @@ struct WParams {
     const float* ftab;      // [n_src][ftab_stride] profile values
     const int* prb_ptr;
     const int* prb_ids;
-    const int* prb_tap;
     const float* prb_w;     // W-form probe weights
     const long long* prb_woff;
+    const int* prb_rng;     // [n_probe][2]: first element, element count of the nonzero layer range
     double* rows;
-    double* sub_norm;
-    double* sqs;            // [n_sub][L]
-    double* norm_part;
-    unsigned int* flags;
-    const int* ncta_ptr;
-    const int* ncta;
+    double* norm_part;      // [n_steps][grid * NW]
 };
 
 __device__ __forceinline__ float wforce(const WParams& p, int s, long long idx, int k, float acc) {
@@ -252,218 +232,252 @@ __device__ __forceinline__ float wleap(int mode, float u, float uo, float v, flo
     return fmaf(half, tot, u - dt * v);
 }
 
-template <int M, int NW, int NS>
-__global__ void __launch_bounds__(NW * 32, 1) k_wstep(const WParams p) {
+__device__ __forceinline__ void st_tagged(unsigned long long* p, float v, unsigned int tag) {
+    const unsigned long long w = ((unsigned long long)tag << 32) | (unsigned long long)__float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+}
+
+// warp-uniform mbarrier wait: every lane polls, the warp leaves the loop together
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+    while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+    }
+}
+
+// fp32 W-form stepping, persistent (one launch = n_steps steps).  Warp-per-subdomain:
+// each warp owns subdomains s0+warp, s0+warp+NW, ... and sweeps their layers in order,
+// so the carry c_j = B_{j-1} W_{j-1} stays in registers and the leapfrog of layers j >= 1
+// is fused into the block pass.  Layer 0 waits for the neighbours' p_0 face slices,
+// which travel through a tagged mailbox (value and step tag in one 64-bit word): no
+// CTA barrier, no flag round trip.  The (A_j, B_j^T) pair of each item is one TMA bulk
+// copy into a per-warp NS-deep ring.  All control flow inside the step loop is
+// warp-uniform (lane-dependent work is predicated), so the warp never splits.
+template <int M, int NS>
+__global__ void __launch_bounds__(256, 1) k_wstep(const WParams p) {
     constexpr int W = 6 * M;
     constexpr int EPL = (W + 31) / 32;
-    constexpr int WK = 4 * W + 21 * 2 * M;
+    const int NW = blockDim.x >> 5;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const WRed<M> ro(lane);
+    const WRed2<M> ro(lane);
     const int BS = p.BS, L = p.L;
     const long long K = (long long)L * W;
+    const int PAIR = 2 * BS;
     float* stages = reinterpret_cast<float*>(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)NW * NS * BS);
-    float* wk = reinterpret_cast<float*>(bars + NW * NS) + (size_t)warp * WK;
-    float* xa = wk;         // W_j
-    float* xb = xa + W;     // W_{j+1}
-    float* y1 = xb + W;
-    float* y2 = y1 + W;
-    float* part = y2 + W;
-    float* my_stage = stages + (size_t)warp * NS * BS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)NW * NS * PAIR);
+    float* wk = reinterpret_cast<float*>(bars + NW * NS) + (size_t)warp * (2 * W + M * PS);
+    float* buf = wk;           // [2][W]: W_j, W_{j+1} of the current item (ring by layer parity)
+    float* part = wk + 2 * W;  // [M][PS]
+    float* my_stage = stages + (size_t)warp * NS * PAIR;
     uint64_t* my_bar = bars + warp * NS;
+    // stage memory must hold finite values (idle lanes multiply stale data by 0)
+    for (int i = lane; i < NS * PAIR; i += 32) my_stage[i] = 0.f;
+    for (int i = lane; i < M * PS; i += 32) part[i] = 0.f;
+    for (int i = lane; i < 2 * W; i += 32) buf[i] = 0.f;
     if (lane == 0) {
         for (int i = 0; i < NS; ++i) mbar_init(&my_bar[i], 1);
         fence_mbar_init();
     }
     __syncwarp();
     const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
-    const int nit = (s1 - s0) * L;
-    const int n1 = nit > warp ? (nit - warp + NW - 1) / NW : 0;
+    const int n_my = (s1 - s0) > warp ? (s1 - s0 - warp + NW - 1) / NW : 0;
     const int n_iter = p.mode == 0 ? p.n_steps : 1;
-    // blocks per step for this warp: its items, 2 blocks each except the last layer (1)
-    int per = 0;
-    for (int t = 0; t < n1; ++t) per += ((warp + t * NW) % L == L - 1) ? 1 : 2;
-    const int total = per * n_iter;
+    const long long total = (long long)n_my * L * n_iter;
     const uint64_t pol = l2_policy_evict_first();
-    const uint32_t bytes = (uint32_t)BS * 4u;
-    int issued = 0, consumed = 0, pr_t = 0, pr_b = 0;  // producer: item index, block within item
-    auto issue = [&]() {
-        if (lane == 0)
-            while (issued < total && issued < consumed + NS) {
-                const int q = warp + pr_t * NW;
-                const int s = s0 + q / L, j = q % L;
-                const long long blk = (long long)s * (2 * L - 1) + 2 * j + pr_b;
-                const int st = issued % NS;
+    long long issued = 0, consumed = 0;
+    int pr_t = 0, pr_j = 0;
+    auto issue = [&]() {  // warp-uniform bookkeeping, lane 0 issues
+        while (issued < total && issued < consumed + NS) {
+            const int s = s0 + warp + pr_t * NW;
+            const long long blk = (long long)s * (2 * L - 1) + 2 * pr_j;
+            const uint32_t bytes = (uint32_t)((pr_j + 1 < L ? 2 : 1) * BS) * 4u;
+            const int st = (int)(issued % NS);
+            if (lane == 0) {
                 fence_proxy_async();
                 mbar_arrive_expect_tx(&my_bar[st], bytes);
-                bulk_g2s(my_stage + (size_t)st * BS, p.coef + blk * BS, bytes, &my_bar[st], pol);
-                ++issued;
-                if (pr_b == 0 && j < L - 1) {
-                    pr_b = 1;
-                } else {
-                    pr_b = 0;
-                    if (++pr_t == n1) pr_t = 0;
-                }
+                bulk_g2s(my_stage + (size_t)st * PAIR, p.coef + blk * BS, bytes, &my_bar[st], pol);
             }
-    };
-    auto acquire = [&]() -> const float* {
-        const int st = consumed % NS;
-        mbar_wait(&my_bar[st], (uint32_t)((consumed / NS) & 1));
-        return my_stage + (size_t)st * BS;
-    };
-    auto release = [&]() {
-        __syncwarp();
-        ++consumed;
-        issue();
+            ++issued;
+            if (++pr_j == L) {
+                pr_j = 0;
+                if (++pr_t == n_my) pr_t = 0;
+            }
+        }
     };
     issue();
     const float dt = (float)p.dt, dt2 = p.dt2, half = p.half;
+    const int NWG = gridDim.x * NW;
+    bool ok_e[EPL];
+    int ic[EPL];  // this lane's rows (clamped; stores predicated on ok_e)
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+        ok_e[e] = lane + 32 * e < W;
+        ic[e] = ok_e[e] ? lane + 32 * e : W - 1;
+    }
 
     for (int k = 1; k <= n_iter; ++k) {
-        const int par = k & 1;
-        const int cb = (k - 1) & 1;
+        const unsigned int tag = p.tag0 + (unsigned int)k;
+        unsigned long long* mb = p.mbox + (size_t)(tag & 1u) * p.n_sub * W;
+        const int cb = (k - 1) & 1;  // W0 holds the current level at k = 1
         const float* Wc = cb ? p.W1 : p.W0;
         float* Wn = cb ? p.W0 : p.W1;
-        float* Pp = p.P + (size_t)par * p.n_sub * K;
         const int kk = k - 1;
-        // ---------------- round 1: row partials and carries ----------------------
-        {
-            float na[EPL], nb[EPL];  // next item's W_j, W_{j+1} (register prefetch)
-            auto load = [&](int t) {
-                const int q = warp + t * NW;
-                const int s = s0 + q / L, j = q % L;
-                const float* w = Wc + (size_t)s * K + (size_t)j * W;
+        double sq = 0.0;  // this lane's share of |W_next|^2 (fixed order)
+        // ---------------- layers 1..L-1 (fused), layer-0 partials to the mailbox ------------
+        float na[EPL], nb[EPL];  // prefetch for the next item
+        auto prefetch = [&](int t, int j) {
+            const int s = s0 + warp + t * NW;
+            const float* w = Wc + (size_t)s * K;
 #pragma unroll
-                for (int e = 0; e < EPL; ++e) {
-                    const int i = lane + 32 * e;
-                    na[e] = (i < W) ? w[i] : 0.f;
-                    nb[e] = (i < W && j + 1 < L) ? w[W + i] : 0.f;
-                }
-            };
-            if (n1 > 0) load(0);
-            for (int t = 0; t < n1; ++t) {
-                const int q = warp + t * NW;
-                const int s = s0 + q / L, j = q % L;
-#pragma unroll
-                for (int e = 0; e < EPL; ++e) {
-                    const int i = lane + 32 * e;
-                    if (i < W) {
-                        xa[i] = na[e];
-                        xb[i] = nb[e];
-                    }
-                }
-                if (t + 1 < n1) load(t + 1);
-                __syncwarp();
-                wsym<M>(acquire(), xa, part, y1, lane, ro);
-                release();
-                float* pj = Pp + (size_t)s * K + (size_t)j * W;
-                if (j + 1 < L) {
-                    for (int i = lane; i < W; i += 32) y2[i] = y1[i];
-                    __syncwarp();
-                    wtri2<M>(acquire(), xb, xa, part, y1, xb, lane, ro);
-                    release();
-                    float* cj = p.Cc + (size_t)s * K + (size_t)(j + 1) * W;
-                    for (int i = lane; i < W; i += 32) {
-                        pj[i] = y2[i] + y1[i];
-                        cj[i] = xb[i];
-                    }
+            for (int e = 0; e < EPL; ++e) {
+                const int i = ic[e];
+                if (j == 0) {
+                    na[e] = w[i];
+                    nb[e] = L > 1 ? w[W + i] : 0.f;
                 } else {
-                    for (int i = lane; i < W; i += 32) pj[i] = y1[i];
+                    na[e] = j + 1 < L ? w[(size_t)(j + 1) * W + i] : 0.f;
+                    nb[e] = p.mode == 0 ? Wn[(size_t)s * K + (size_t)j * W + i] : 0.f;
+                }
+            }
+        };
+        if (n_my > 0) prefetch(0, 0);
+        float carry[EPL], wprev[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) carry[e] = wprev[e] = 0.f;
+        for (int t = 0; t < n_my; ++t) {
+            const int s = s0 + warp + t * NW;
+            const bool has_src = p.src_ptr[s] != p.src_ptr[s + 1];
+            for (int j = 0; j < L; ++j) {
+                float* xj = buf + (j & 1) * W;
+                float* xj1 = buf + ((j + 1) & 1) * W;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    if (j == 0) {
+                        if (ok_e[e]) {
+                            xj[ic[e]] = na[e];
+                            xj1[ic[e]] = nb[e];
+                        }
+                        carry[e] = 0.f;
+                    } else {
+                        if (ok_e[e]) xj1[ic[e]] = na[e];
+                        wprev[e] = nb[e];
+                    }
+                }
+                __syncwarp();
+                if (j + 1 < L)
+                    prefetch(t, j + 1);
+                else if (t + 1 < n_my)
+                    prefetch(t + 1, 0);
+                const int st = (int)(consumed % NS);
+                mbar_wait_warp(&my_bar[st], (uint32_t)((consumed / NS) & 1));
+                wpair<M>(my_stage + (size_t)st * PAIR, xj, xj1, part, lane, j + 1 < L, BS);
+                __syncwarp();
+                ++consumed;
+                issue();
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    float pj = part[ro.po[e][0]];
+#pragma unroll
+                    for (int q = 1; q < 6; ++q) pj += part[ro.po[e][q]];
+                    float cn = part[ro.co[e][0]];
+#pragma unroll
+                    for (int q = 1; q < 6; ++q) cn += part[ro.co[e][q]];
+                    if (j == 0) {
+                        if (ok_e[e]) st_tagged(mb + (size_t)s * W + ic[e], pj, tag);
+                    } else {
+                        const size_t o = (size_t)s * K + (size_t)j * W + ic[e];
+                        float tot = pj + carry[e];
+                        if (has_src) tot = wforce(p, s, (long long)j * W + ic[e], kk, tot);
+                        const float v = (p.mode == 1 && p.V0) ? p.V0[o] : 0.f;
+                        const float un = wleap(p.mode, xj[ic[e]], wprev[e], v, tot, dt, dt2, half);
+                        if (ok_e[e]) {
+                            Wn[o] = un;
+                            sq = fma((double)un, (double)un, sq);
+                        }
+                    }
+                    carry[e] = cn;
                 }
                 __syncwarp();
             }
         }
-        __syncthreads();
-        if (threadIdx.x == 0) flag_publish(p.flags, (unsigned int)k);
-        double sq = 0.0;  // this thread's share of |W_next|^2 (fixed element order)
-        // ---------------- round 2: interior layers, CTA-wide elementwise ----------
-        {
-            const int per_sub = (L - 1) * W;
-            const int nel = (s1 - s0) * per_sub;
-            constexpr int U = 4;
-            for (int base = threadIdx.x; base < nel; base += U * NW * 32) {
-                float pv[U], cv[U], wc[U], wo[U], vv[U];
-                size_t off[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int idx = base + u * NW * 32;
-                    if (idx < nel) {
-                        const int sl = idx / per_sub, r = idx % per_sub;
-                        off[u] = (size_t)(s0 + sl) * K + W + r;
-                        pv[u] = Pp[off[u]];
-                        cv[u] = p.Cc[off[u]];
-                        wc[u] = Wc[off[u]];
-                        wo[u] = (p.mode == 0) ? Wn[off[u]] : 0.f;
-                        vv[u] = (p.mode == 1 && p.V0) ? p.V0[off[u]] : 0.f;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int idx = base + u * NW * 32;
-                    if (idx < nel) {
-                        const int sl = idx / per_sub, r = idx % per_sub;
-                        const int s = s0 + sl;
-                        const float tot = wforce(p, s, (long long)W + r, kk, pv[u] + cv[u]);
-                        const float un = wleap(p.mode, wc[u], wo[u], vv[u], tot, dt, dt2, half);
-                        Wn[off[u]] = un;
-                        sq = fma((double)un, (double)un, sq);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        if (warp == 0)
-            flags_wait(p.flags, p.ncta + p.ncta_ptr[blockIdx.x], p.ncta_ptr[blockIdx.x + 1] - p.ncta_ptr[blockIdx.x],
-                       (unsigned int)k, lane);
-        __syncthreads();
-        // ---------------- round 3: layer 0 + faces, probes ------------------------
-        for (int s = s0 + warp; s < s1; s += NW) {
+        // ---------------- layer 0: faces (mailbox), leapfrog -------------------------------
+        for (int t = 0; t < n_my; ++t) {
+            const int s = s0 + warp + t * NW;
             const size_t o = (size_t)s * K;
-            for (int i = lane; i < W; i += 32) {
-                const int f = i / M;
+            const bool has_src = p.src_ptr[s] != p.src_ptr[s + 1];
+            const unsigned long long* own[EPL];
+            const unsigned long long* nbp[EPL];
+            float wc[EPL], wo[EPL], v[EPL];
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+                const int i = ic[e], f = i / M;
                 const int nbs = p.nbr[s * 6 + f];
-                float a = Pp[o + i];
-                if (nbs >= 0) a = 0.5f * (a + Pp[(size_t)nbs * K + (f ^ 1) * M + i % M]);
-                const float tot = wforce(p, s, i, kk, a);
-                const float v = (p.mode == 1 && p.V0) ? p.V0[o + i] : 0.f;
-                const float un = wleap(p.mode, Wc[o + i], (p.mode == 0) ? Wn[o + i] : 0.f, v, tot, dt, dt2, half);
-                Wn[o + i] = un;
-                sq = fma((double)un, (double)un, sq);
+                own[e] = mb + (size_t)s * W + i;
+                nbp[e] = nbs >= 0 ? mb + (size_t)nbs * W + (f ^ 1) * M + i % M : own[e];
+                wc[e] = Wc[o + i];
+                wo[e] = (p.mode == 0) ? Wn[o + i] : 0.f;
+                v[e] = (p.mode == 1 && p.V0) ? p.V0[o + i] : 0.f;
+            }
+            float a[EPL], b[EPL];
+            int spins = 0;
+            while (true) {  // warp-uniform poll of the tagged face words
+                bool ok = true;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    const unsigned long long wa = ld_relaxed64(own[e]);
+                    const unsigned long long wb = ld_relaxed64(nbp[e]);
+                    ok = ok && (unsigned int)(wa >> 32) == tag && (unsigned int)(wb >> 32) == tag;
+                    a[e] = __uint_as_float((unsigned int)wa);
+                    b[e] = __uint_as_float((unsigned int)wb);
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+                if (++spins > 2) __nanosleep(100);
+            }
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+                const int i = ic[e];
+                float tot = (nbp[e] != own[e]) ? 0.5f * (a[e] + b[e]) : a[e];
+                if (has_src) tot = wforce(p, s, i, kk, tot);
+                const float un = wleap(p.mode, wc[e], wo[e], v[e], tot, dt, dt2, half);
+                if (ok_e[e]) {
+                    Wn[o + i] = un;
+                    sq = fma((double)un, (double)un, sq);
+                }
             }
         }
-        // per-CTA |W|^2 partial (fixed-order block reduction)
-        {
-            double v = warp_sum(sq);
-            __shared__ double wred[32];
-            if (lane == 0) wred[warp] = v;
-            __syncthreads();
-            if (threadIdx.x == 0 && p.mode == 0) {
-                double tsum = 0.0;
-                for (int i = 0; i < NW; ++i) tsum += wred[i];
-                p.norm_part[(size_t)kk * gridDim.x + blockIdx.x] = tsum;
-            }
+        __syncwarp();
+        if (p.mode == 0) {
+            const double vs = warp_sum(sq);
+            if (lane == 0) p.norm_part[(size_t)kk * NWG + blockIdx.x * NW + warp] = vs;
         }
-        // probes (all layers written by now)
+        // probes: all layers of this warp's subdomains are written
         const bool rec = (p.mode == 1) || (k % p.record_every == 0);
         if (rec && p.rows) {
             const long long row = (p.mode == 1) ? 0 : (k / p.record_every - 1);
-            for (int s = s0 + warp; s < s1; s += NW) {
-                if (p.prb_ptr[s] == p.prb_ptr[s + 1]) continue;
+            for (int t = 0; t < n_my; ++t) {
+                const int s = s0 + warp + t * NW;
                 const float* U = ((p.mode == 1) ? Wc : Wn) + (size_t)s * K;
                 for (int pq = p.prb_ptr[s]; pq < p.prb_ptr[s + 1]; ++pq) {
                     const int pid = p.prb_ids[pq];
-                    double val = 0.0;
+                    const int lo = p.prb_rng[2 * pid], cnt = p.prb_rng[2 * pid + 1];
                     const float* wv = p.prb_w + p.prb_woff[pid];
-                    for (long long i = lane; i < K; i += 32) val = fma((double)wv[i], (double)U[i], val);
+                    double val = 0.0;
+                    for (int b0 = 0; b0 < cnt; b0 += 32) {
+                        const int i = lo + b0 + lane;
+                        if (b0 + lane < cnt) val = fma((double)wv[i], (double)U[i], val);
+                    }
                     val = warp_sum(val);
                     if (lane == 0) p.rows[row * p.n_probe + pid] = val;
                 }
             }
         }
-        __syncthreads();
+        __syncwarp();
     }
-    (void)EPL;
 }
 
 // ---------------------------------------------------------------------------
@@ -555,10 +569,14 @@ namespace {
 struct WState {
     int BS = 0, nw = 0, ns = 0, smem = 0;
     const void* fn = nullptr;
-    float *coef = nullptr, *W[2] = {nullptr, nullptr}, *V0 = nullptr, *P = nullptr, *Cc = nullptr;
+    float *coef = nullptr, *W[2] = {nullptr, nullptr}, *V0 = nullptr;
     float *src = nullptr, *prb = nullptr, *ftab = nullptr;
     long long ftab_cap = 0;
-    double *sqs = nullptr, *d_tmp = nullptr, *d_tmp2 = nullptr;
+    unsigned long long* mbox = nullptr;  // [2][n_sub][w] tagged layer-0 partials
+    unsigned int tag = 0;                // last mailbox tag used
+    int* prb_rng = nullptr;              // [n_probe][2]
+    double* norm = nullptr;              // [n_steps][grid * nw] per-warp |W|^2 partials
+    long long norm_cap = 0;
     long long* first_blk = nullptr;
     int cur = 0;
 };
@@ -632,11 +650,10 @@ extern "C" int sfw_wform_setup(sfw_stepper* h, char* errbuf, int errlen) {
     if ((rc = dalloc(&ws->coef, (size_t)nb * ws->BS, errbuf, errlen)) || (rc = upload(&ws->first_blk, fb, errbuf, errlen)) ||
         (rc = upload(&d_ls, ls, errbuf, errlen)) || (rc = upload(&d_lj, lj, errbuf, errlen)) ||
         (rc = dalloc(&ws->W[0], (size_t)n * K, errbuf, errlen)) || (rc = dalloc(&ws->W[1], (size_t)n * K, errbuf, errlen)) ||
-        (rc = dalloc(&ws->P, (size_t)2 * n * K, errbuf, errlen)) || (rc = dalloc(&ws->Cc, (size_t)n * K, errbuf, errlen)) ||
-        (rc = dalloc(&ws->sqs, (size_t)n * L, errbuf, errlen)))
+        (rc = dalloc(&ws->mbox, (size_t)2 * n * w, errbuf, errlen)))
         return rc;
     cudaMemsetAsync(ws->coef, 0, (size_t)nb * ws->BS * 4, h->stream);
-    cudaMemsetAsync(ws->P, 0, (size_t)2 * n * K * 4, h->stream);
+    cudaMemsetAsync(ws->mbox, 0, (size_t)2 * n * w * 8, h->stream);
     const size_t sm = (size_t)3 * w * w * 8;
     SFW_CUDA_TRY(cudaFuncSetAttribute(k_wform_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     k_wform_blocks<<<(unsigned)ls.size(), 256, sm, h->stream>>>(h->scales, h->gam_dense, d_ls, d_lj, ws->first_blk,
@@ -645,32 +662,21 @@ extern "C" int sfw_wform_setup(sfw_stepper* h, char* errbuf, int errlen) {
     SFW_CUDA_TRY(cudaGetLastError());
     cudaFree(d_ls);
     cudaFree(d_lj);
-    // kernel variant
-    const char* env_nw = getenv("SFW_WSTEP_NW");
-    const int want = env_nw ? atoi(env_nw) : 12;
-    if (m == 9 && want == 16) {
-        ws->nw = 16;
-        ws->ns = 2;
-        ws->fn = (const void*)k_wstep<9, 16, 2>;
-    } else if (m == 9 && want == 12) {
-        ws->nw = 12;
-        ws->ns = 2;
-        ws->fn = (const void*)k_wstep<9, 12, 2>;
-    } else if (m == 9) {
-        ws->nw = 8;
-        ws->ns = 4;
-        ws->fn = (const void*)k_wstep<9, 8, 4>;
-    } else if (m == 4) {
-        ws->nw = 16;
-        ws->ns = 4;
-        ws->fn = (const void*)k_wstep<4, 16, 4>;
-    } else {
-        ws->nw = 8;
-        ws->ns = 4;
-        ws->fn = (const void*)k_wstep<1, 8, 4>;
-    }
-    const int WK = 4 * w + 42 * m;
-    ws->smem = ws->nw * ws->ns * ws->BS * 4 + ws->nw * ws->ns * 8 + ws->nw * WK * 4;
+    // launch shape: one CTA per SM (h->grid), NW warps, each owning whole subdomains.
+    // NW = ceil(spc / rounds) with rounds = ceil(spc / 8) balances the per-warp subdomain count.
+    int spc = 1;
+    for (int b = 0; b < h->grid; ++b) spc = std::max(spc, h->cta_ptr_h[b + 1] - h->cta_ptr_h[b]);
+    const int rounds = (spc + 7) / 8;
+    ws->nw = std::max(1, std::min(8, (spc + rounds - 1) / rounds));
+    if (const char* e = getenv("SFW_WSTEP_NW")) ws->nw = std::max(1, std::min(8, atoi(e)));  // test hook
+    ws->ns = 2;
+    if (m == 9)
+        ws->fn = (const void*)k_wstep<9, 2>;
+    else if (m == 4)
+        ws->fn = (const void*)k_wstep<4, 2>;
+    else
+        ws->fn = (const void*)k_wstep<1, 2>;
+    ws->smem = ws->nw * (ws->ns * 2 * ws->BS * 4 + ws->ns * 8 + (2 * w + m * PS) * 4);
     SFW_CUDA_TRY(cudaFuncSetAttribute(ws->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ws->smem));
     g_wf[h] = ws;
     return 0;
@@ -734,6 +740,19 @@ extern "C" int sfw_wform_vectors(sfw_stepper* h, const double* src_vec, const do
         if (ws->prb) cudaFree(ws->prb);
         ws->prb = nullptr;
         if ((rc = upload(&ws->prb, f, errbuf, errlen))) return rc;
+        // nonzero element range of each W-form probe (face-coefficient probes live in layer 0)
+        std::vector<int> rng(2 * h->n_probe, 0);
+        for (int i = 0; i < h->n_probe; ++i) {
+            const long long len = h->soff[vs[i] + 1] - h->soff[vs[i]];
+            long long lo = 0, hi = len;
+            while (lo < len && f[vo[i] + lo] == 0.f) ++lo;
+            while (hi > lo && f[vo[i] + hi - 1] == 0.f) --hi;
+            rng[2 * i] = (int)lo;
+            rng[2 * i + 1] = (int)(hi - lo);
+        }
+        if (ws->prb_rng) cudaFree(ws->prb_rng);
+        ws->prb_rng = nullptr;
+        if ((rc = upload(&ws->prb_rng, rng, errbuf, errlen))) return rc;
     }
     return 0;
 }
@@ -749,6 +768,7 @@ static int wf_launch(sfw_stepper* h, WState* ws, int mode, int n_steps, int reco
     p.n_probe = h->n_probe;
     p.ftab_stride = ftab_stride;
     p.mode = mode;
+    p.tag0 = ws->tag;
     p.dt = h->dt;
     p.dt2 = (float)(h->dt * h->dt);
     p.half = (float)((0.5 * h->dt) * h->dt);
@@ -756,8 +776,7 @@ static int wf_launch(sfw_stepper* h, WState* ws, int mode, int n_steps, int reco
     p.W0 = ws->W[ws->cur];
     p.W1 = ws->W[ws->cur ^ 1];
     p.V0 = ws->V0;
-    p.P = ws->P;
-    p.Cc = ws->Cc;
+    p.mbox = ws->mbox;
     p.cta_sub_ptr = h->cta_sub_ptr;
     p.nbr = h->nbr;
     p.src_ptr = h->src_ptr;
@@ -767,19 +786,14 @@ static int wf_launch(sfw_stepper* h, WState* ws, int mode, int n_steps, int reco
     p.ftab = ws->ftab;
     p.prb_ptr = h->prb_ptr;
     p.prb_ids = h->prb_ids;
-    p.prb_tap = h->prb_tap;
     p.prb_w = ws->prb;
     p.prb_woff = h->prb_woff;
+    p.prb_rng = ws->prb_rng;
     p.rows = h->rows;
-    p.sub_norm = h->sub_norm;
-    p.sqs = ws->sqs;
-    p.norm_part = h->norm_part;
-    p.flags = h->bar;
-    p.ncta_ptr = h->ncta_ptr;
-    p.ncta = h->ncta;
-    SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int) * h->grid, h->stream));
+    p.norm_part = ws->norm;
     void* args[] = {&p};
     SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ws->fn, dim3(h->grid), dim3(ws->nw * 32), args, ws->smem, h->stream));
+    ws->tag += (unsigned int)(mode == 0 ? n_steps : 1);
     return 0;
 }
 
@@ -843,12 +857,6 @@ extern "C" int sfw_wform_init(sfw_stepper* h, const double* u0, const double* v0
         if ((rc = dalloc(&h->rows, std::max(1, h->n_probe), errbuf, errlen))) return rc;
         h->rows_cap = std::max(1, h->n_probe);
     }
-    if (!h->norm_part || h->norm_cap < h->grid) {
-        if (h->norm_part) cudaFree(h->norm_part);
-        h->norm_part = nullptr;
-        if ((rc = dalloc(&h->norm_part, h->grid, errbuf, errlen))) return rc;
-        h->norm_cap = h->grid;
-    }
     if ((rc = wf_launch(h, ws, 1, 1, 1, 1, errbuf, errlen))) return rc;
     if (row0_out && h->n_probe)
         SFW_CUDA_TRY(cudaMemcpyAsync(row0_out, h->rows, h->n_probe * 8, cudaMemcpyDeviceToHost, h->stream));
@@ -877,28 +885,29 @@ extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, cons
         if ((rc = dalloc(&h->rows, std::max(1LL, nrec * h->n_probe), errbuf, errlen))) return rc;
         h->rows_cap = std::max(1LL, nrec * h->n_probe);
     }
-    if (h->norm_cap < (long long)n_steps * h->grid) {
-        if (h->norm_part) cudaFree(h->norm_part);
-        h->norm_part = nullptr;
-        if ((rc = dalloc(&h->norm_part, (size_t)n_steps * h->grid, errbuf, errlen))) return rc;
-        h->norm_cap = (long long)n_steps * h->grid;
+    const long long nwg = (long long)h->grid * ws->nw;
+    if (ws->norm_cap < (long long)n_steps * nwg) {
+        if (ws->norm) cudaFree(ws->norm);
+        ws->norm = nullptr;
+        if ((rc = dalloc(&ws->norm, (size_t)n_steps * nwg, errbuf, errlen))) return rc;
+        ws->norm_cap = (long long)n_steps * nwg;
     }
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
     if ((rc = wf_launch(h, ws, 0, n_steps, record_every, n_steps, errbuf, errlen))) return rc;
     SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
     ws->cur ^= (n_steps & 1);
-    std::vector<double> part((size_t)n_steps * h->grid);
+    std::vector<double> part((size_t)n_steps * nwg);
     if (rows_out && nrec * h->n_probe > 0)
         SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost, h->stream));
     if (norms_out)
-        SFW_CUDA_TRY(cudaMemcpyAsync(part.data(), h->norm_part, part.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+        SFW_CUDA_TRY(cudaMemcpyAsync(part.data(), ws->norm, part.size() * 8, cudaMemcpyDeviceToHost, h->stream));
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
     SFW_CUDA_TRY(cudaGetLastError());
     if (kernel_ms) cudaEventElapsedTime(kernel_ms, h->ev0, h->ev1);
     if (norms_out)
         for (int k = 0; k < n_steps; ++k) {
             double t = 0.0;
-            for (int c = 0; c < h->grid; ++c) t += part[(size_t)k * h->grid + c];
+            for (long long c = 0; c < nwg; ++c) t += part[(size_t)k * nwg + c];
             norms_out[k] = std::sqrt(t);
         }
     return 0;
@@ -945,8 +954,8 @@ extern "C" int sfw_wform_traffic(sfw_stepper* h, double* alg_bytes, double* stre
 extern "C" int sfw_wform_destroy(sfw_stepper* h) {
     if (!g_wf.count(h)) return 0;
     WState* ws = g_wf[h];
-    void* ptrs[] = {ws->coef, ws->W[0], ws->W[1], ws->V0, ws->P, ws->Cc, ws->src, ws->prb, ws->ftab, ws->sqs,
-                    ws->first_blk};
+    void* ptrs[] = {ws->coef, ws->W[0], ws->W[1], ws->V0, ws->mbox, ws->src, ws->prb, ws->ftab, ws->prb_rng,
+                    ws->norm, ws->first_blk};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     delete ws;
