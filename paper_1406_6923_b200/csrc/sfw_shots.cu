@@ -104,6 +104,8 @@ struct MsParams {
     int evict_first;
     unsigned long long* dbg;  // debug cycle counters (SFW_MS_CLK builds) or null
     const double* mblk;       // [n_sub][6][M*M] interface mass per face (0 for outer faces)
+    unsigned int* sflags;     // k_step_ms3: [n_sub][4] step tag of the published F_0 per shot group
+    unsigned int tag0;        // k_step_ms3: tag of this launch's step 0 (monotone across launches)
 };
 
 constexpr int MS_NW = 16;  // warp = (row tile I = warp/2, column half = warp%2)
@@ -1071,6 +1073,412 @@ static size_t ms2_smem_bytes(int RT, int TB, int W, int nsmax) {
            4 * (32 + 6 * (size_t)nsmax) + 64;
 }
 
+// ---------------------------------------------------------------------------
+// k_step_ms3: shot-group-per-warp multi-shot stepping.  The 32 shots are 4
+// independent groups of 8; warp (g, c) sweeps the layers of its subdomain group g
+// (subdomains s0+g, s0+g+NG, ...) for shots 8c..8c+7 alone, so no warp ever waits
+// for another inside a sweep.  Each block product is computed transposed,
+//     (B X)^T = X^T B      (B symmetric: the stored lower tiles serve as the DMMA B operand),
+// with the 8 x 4 X^T fragments built from the lane's own rows by two quad shuffles,
+// and the result lands in the same row layout as the input (lane (q, a) holds rows
+// 8I + 2a + {0,1} of shot q): the state, the fluxes and the accumulations of a sweep
+// stay in registers.  The four warps of a group consume the same chain block from a
+// shared TMA ring (full/empty mbarriers, 4 consumer arrivals per stage) fed by one
+// producer warp; H_0 is streamed and applied only for subdomains with outer faces
+// (the only rows of H_0 F_0 the step reads).  Layer-0 coupling waits on a per
+// (subdomain, shot group) tagged flag of the neighbour's F_0 instead of a CTA flag.
+
+__device__ __forceinline__ void mbar_wait_all(uint64_t* bar, uint32_t parity) {
+    while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+    }
+}
+
+// C = (B X)^T for this lane's shot, X = P - Q (SUB) or P, given row-wise: lane (shot, a)
+// holds rows 8I + 2a + {0,1}.  Two quad shuffles build each 8 x 4 X^T fragment.
+template <int RT, bool SUB>
+__device__ __forceinline__ void ms3_gemm(const double* __restrict__ tiles, const double (&P)[RT][2],
+                                         const double (&Q)[RT][2], double (&C)[RT][2], int lane, int src_lo,
+                                         int src_hi, const int (&tr)[2]) {
+#pragma unroll
+    for (int I = 0; I < RT; ++I) C[I][0] = C[I][1] = 0.0;
+    const bool odd = (lane & 1) != 0;
+#pragma unroll
+    for (int kap = 0; kap < 2 * RT; ++kap) {
+        const int Ip = kap >> 1, h = kap & 1;
+        const double d0 = SUB ? P[Ip][0] - Q[Ip][0] : P[Ip][0];
+        const double d1 = SUB ? P[Ip][1] - Q[Ip][1] : P[Ip][1];
+        const int src = h ? src_hi : src_lo;
+        const double v0 = __shfl_sync(0xffffffffu, d0, src);
+        const double v1 = __shfl_sync(0xffffffffu, d1, src);
+        const double xa = odd ? v1 : v0;
+#pragma unroll
+        for (int I = 0; I < RT; ++I) {
+            const double b = (I >= Ip) ? tiles[(I * (I + 1) / 2 + Ip) * 64 + h * 32 + lane]
+                                       : tiles[(Ip * (Ip + 1) / 2 + I) * 64 + tr[h]];
+            dmma8x8x4(C[I], xa, b);
+        }
+    }
+}
+
+template <int M, int NG, int NSTG>
+__global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
+    constexpr int S = 32;
+    constexpr int W = 6 * M;
+    constexpr int RT = (W + 7) / 8;
+    constexpr int NK = 2 * RT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L = p.L, TB = p.TB;
+    const long long K = p.K;
+    const long long WS = (long long)W * S, KS = K * S;
+    double* cst = reinterpret_cast<double*>(smem_raw);              // [NG][NS][TB]
+    double* Tall = cst + (size_t)NG * NSTG * TB;                // [NCW][W][8] face sums (phase C)
+    double* Sall = Tall + (size_t)(4 * NG) * W * 8;                  // [NCW][2][2 RT][32] staged state rows
+    uint64_t* full = reinterpret_cast<uint64_t*>(Sall + (size_t)(4 * NG) * 2 * 2 * RT * 32);
+    uint64_t* empty = full + NG * NSTG;
+    int* s_out = reinterpret_cast<int*>(empty + NG * NSTG);     // [ns] subdomain has an outer face
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int ns = s1 - s0;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        int o = 0;
+        for (int f = 0; f < 6; ++f) o |= p.nbr[(s0 + i) * 6 + f] < 0;
+        s_out[i] = o;
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NG * NSTG; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 4);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // ======== compute warps ========
+    const int g = warp >> 2, c = warp & 3;
+    const int a = lane & 3;
+    const int q = 8 * c + (lane >> 2);   // this lane's shot
+    const int src_lo = (lane & ~3) | (a >> 1), src_hi = src_lo | 2;
+    int tr[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int r = 4 * h + a, cc = lane >> 2;
+        tr[h] = (cc >> 2) * 32 + r * 4 + (cc & 3);
+    }
+    double* T = Tall + (size_t)warp * W * 8;
+    // lane-private staging of the next layer's U_{j+2} and this layer's Uprev_j (cp.async, 8 B per row)
+    double* sU = Sall + (size_t)warp * 2 * 2 * RT * 32;
+    double* sP = sU + 2 * RT * 32;
+#pragma unroll
+    for (int i = 0; i < 2 * RT; ++i) sU[i * 32 + lane] = sP[i * 32 + lane] = 0.0;  // padding rows stay 0
+    auto stage_rows = [&](const double* blk, double* dst) {
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = 8 * I + 2 * (lane & 3) + e;
+                if (r < W)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + (2 * I + e) * 32 + lane)),
+                                 "l"(blk + (size_t)r * 32 + 8 * c + (lane >> 2))
+                                 : "memory");
+            }
+    };
+    auto read_rows = [&](const double* src, double (&v)[RT][2]) {
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) v[I][e] = src[(2 * I + e) * 32 + lane];
+    };
+    // chain-block ring of the group: warp c == 0 of the group refills it (lane 0 issues)
+    // whenever all four consumers have released a stage -- at its own releases and while
+    // it waits, so the ring never stalls on a refill nobody is in a position to make.
+    long long con = 0, iss = 0, tot = 0;
+    int pt = 0, pj = 0, ph = 0;
+    if (c == 0) {
+        long long per = 0;
+        for (int sl = g; sl < ns; sl += NG) per += 2 * L - (s_out[sl] ? 0 : 1);
+        tot = per * p.n_steps;
+    }
+    const uint64_t pol = l2_policy_evict_first();
+    auto try_issue = [&]() {
+        while (iss < tot) {
+            const int st = (int)(iss % NSTG);
+            uint64_t* e = &empty[g * NSTG + st];
+            const int fr0 = lane == 0 ? (int)mbar_test_wait(e, (uint32_t)(((iss / NSTG) & 1) ^ 1)) : 0;
+            if (!__shfl_sync(0xffffffffu, fr0, 0)) break;
+            const int sl = g + pt * NG;
+            if (lane == 0) {
+                const long long blk = (long long)(s0 + sl) * 2 * L + 2 * pj + ph;
+                uint64_t* fb = &full[g * NSTG + st];
+                mbar_arrive_expect_tx(fb, (uint32_t)TB * 8u);
+                bulk_g2s(cst + (size_t)(g * NSTG + st) * TB, p.tcoef + blk * TB, (uint32_t)TB * 8u, fb, pol);
+            }
+            ++iss;
+            if (ph == 0 && (pj > 0 || s_out[sl])) {  // G_j, H_j per layer; H_0 only with an outer face
+                ph = 1;
+            } else {
+                ph = 0;
+                if (++pj == L) {
+                    pj = 0;
+                    if (g + (++pt) * NG >= ns) pt = 0;
+                }
+            }
+        }
+    };
+    if (c == 0) try_issue();
+    auto acquire = [&]() -> const double* {
+        const int st = (int)(con % NSTG);
+        uint64_t* fb = &full[g * NSTG + st];
+        const uint32_t par = (uint32_t)((con / NSTG) & 1);
+        while (!__all_sync(0xffffffffu, mbar_try_wait(fb, par)))
+            if (c == 0) try_issue();
+        return cst + (size_t)(g * NSTG + st) * TB;
+    };
+    auto release = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[g * NSTG + (con % NSTG)]);
+        ++con;
+        if (c == 0) try_issue();
+    };
+    auto row_of = [&](int I, int e) { return 8 * I + 2 * a + e; };
+    auto load_rows = [&](const double* blk, double (&v)[RT][2]) {  // blk: [W][S] layer block
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = row_of(I, e);
+                v[I][e] = r < W ? blk[(size_t)r * S + q] : 0.0;
+            }
+    };
+    const double dt2 = p.dt2;
+    const int ssq = p.shot_sub[q];
+    const double* svec = p.shot_vec + p.shot_voff[q];
+    const int n_g = ns > g ? (ns - g + NG - 1) / NG : 0;
+    const int NWG = gridDim.x * NG;
+    auto buf = [&](int lvl) -> double* { return (lvl & 1) ? p.U1 : p.U0; };  // level n lives in buf(n)
+    auto ftab_of = [&](int kk) -> double { return ssq >= 0 ? p.ftab[(size_t)q * p.ftab_stride + kk] : 0.0; };
+
+    // Layer-0 coupling of step kc (level kc): shared faces mass (own + neighbour F_0), outer
+    // faces acc_0, leapfrog.  Result rows also returned in u0n (the next sweep's U_0).
+    auto coupling = [&](int kc, int t, double (&u0n)[RT][2], double& sqc) {
+        const int sl = g + t * NG, s = s0 + sl;
+        const unsigned int tag = p.tag0 + (unsigned int)kc;
+        const double* fx = p.flux + (size_t)(tag & 1u) * p.n_sub * WS;
+        const double* uc = buf(kc - 1) + (size_t)s * KS;   // level kc-1
+        double* un = buf(kc) + (size_t)s * KS;             // level kc-2 on entry (layer 0), kc on exit
+        const bool srcs = ssq == s;
+        const double fq = ftab_of(kc - 1);
+        double u0[RT][2];
+        load_rows(uc, u0);
+        load_rows(un, u0n);  // Uprev_0 (overwritten below)
+        {   // neighbours' F_0 of this shot group: tags are monotone, a neighbour may be a step ahead
+            const int nb = lane < 6 ? p.nbr[s * 6 + lane] : -1;
+            int spins = 0;
+            while (!__all_sync(0xffffffffu, nb < 0 || (int)(ld_acquire(p.sflags + (size_t)nb * 4 + c) - tag) >= 0))
+                if (++spins > 2) __nanosleep(64);
+            __syncwarp();  // the acquiring lanes' view of the neighbours' F_0 -> every lane
+        }
+        const double* fo = fx + (size_t)s * WS;
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = row_of(I, e);
+                if (r < W) {
+                    const int f = r / M, cm = r % M, nb = p.nbr[s * 6 + f];
+                    if (nb >= 0) {
+                        const double own = __ldcg(fo + (size_t)r * S + q);
+                        const double oth = __ldcg(fx + ((size_t)nb * W + (f ^ 1) * M + cm) * S + q);
+                        T[r * 8 + (lane >> 2)] = __dadd_rn(own, oth);
+                    }
+                }
+            }
+        __syncwarp();
+        const double* mb = p.mblk + (size_t)s * 6 * M * M;
+#pragma unroll
+        for (int I = 0; I < RT; ++I)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = row_of(I, e);
+                double v = 0.0;
+                if (r < W) {
+                    const int f = r / M, rr = r % M;
+                    double acc;
+                    if (p.nbr[s * 6 + f] >= 0) {
+                        acc = 0.0;
+                        const double* mx = mb + (f * M + rr) * M;
+                        const double* tx = T + (f * M) * 8 + (lane >> 2);
+#pragma unroll
+                        for (int cm = 0; cm < M; ++cm) acc = fma(__ldg(mx + cm), tx[cm * 8], acc);
+                    } else {
+                        acc = __ldcg(p.acc1 + ((size_t)s * W + r) * S + q);
+                    }
+                    if (srcs) acc = __dadd_rn(acc, __dmul_rn(svec[r], fq));
+                    v = __dadd_rn(__dsub_rn(__dmul_rn(2.0, u0[I][e]), u0n[I][e]), __dmul_rn(dt2, acc));
+                    un[(size_t)r * S + q] = v;
+                    sqc = fma(v, v, sqc);
+                }
+                u0n[I][e] = v;
+            }
+        __syncwarp();
+    };
+    // probe rows of level kc for subdomain slot t (all its layers are final)
+    auto probes = [&](int kc, int t) {
+        if (kc % p.record_every != 0 || !p.rows) return;
+        const int s = s0 + g + t * NG;
+        if (p.prb_ptr[s] == p.prb_ptr[s + 1]) return;
+        const long long row = kc / p.record_every - 1;
+        const int qp = 8 * c + (lane & 7), part = lane >> 3;
+        const double* us = buf(kc) + (size_t)s * KS;
+        for (int pq = p.prb_ptr[s]; pq < p.prb_ptr[s + 1]; ++pq) {
+            const int pid = p.prb_ids[pq];
+            const int tap = p.prb_tap[pid];
+            double val = 0.0;
+            if (tap >= 0) {
+                val = part == 0 ? us[(size_t)tap * S + qp] : 0.0;
+            } else {
+                const double* wv = p.prb_w + p.prb_woff[pid];
+                for (long long i0 = 0; i0 < K; i0 += 4) {
+                    const long long i = i0 + part;
+                    if (i < K) val = fma(wv[i], us[i * S + qp], val);
+                }
+            }
+            val += __shfl_xor_sync(0xffffffffu, val, 8);
+            val += __shfl_xor_sync(0xffffffffu, val, 16);
+            if (part == 0) p.rows[(row * p.n_probe + pid) * S + qp] = val;
+        }
+        __syncwarp();
+    };
+    auto put_norm = [&](int kc, double v) {  // per-shot |U|^2 of level kc (the quad's 4 lanes share a shot)
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (a == 0) p.norm_part[((size_t)(kc - 1) * NWG + blockIdx.x * NG + g) * S + q] = v;
+    };
+
+    // Iteration k: for every subdomain of the group, the layer-0 coupling of step k-1 (its
+    // neighbours published F_0 during the previous sweep, so the flags are normally set)
+    // immediately followed by the sweep of step k, which takes the new U_0 from registers.
+    double sq_prev = 0.0;  // |U|^2 of the previous step's layers >= 1
+    for (int k = 1; k <= p.n_steps + 1; ++k) {
+        const bool sweep = k <= p.n_steps;
+        const unsigned int tag = p.tag0 + (unsigned int)k;
+        double* fx = p.flux + (size_t)(tag & 1u) * p.n_sub * WS;
+        const double* Uc = buf(k - 1);   // level k-1
+        double* Un = buf(k);             // level k-2 -> k
+        const double fq = ftab_of(k - 1);
+        double sq = 0.0, sqc = 0.0;
+        for (int t = 0; t < n_g; ++t) {
+            const int sl = g + t * NG, s = s0 + sl;
+            const bool outer = s_out[sl] != 0;
+            const bool srcs = ssq == s;
+            const double* us = Uc + (size_t)s * KS;
+            double* un = Un + (size_t)s * KS;
+            double Uj[RT][2], Uj1[RT][2], Fp[RT][2], C[RT][2];
+            if (sweep) load_rows(us + WS, Uj1);  // U_1 of level k-1 (in flight during the coupling)
+            if (k > 1) {
+                coupling(k - 1, t, Uj, sqc);
+                probes(k - 1, t);
+            } else {
+                load_rows(us, Uj);
+            }
+            if (!sweep) continue;
+            for (int j = 0; j < L; ++j) {
+                // stage U_{j+2} (level k-1) and Uprev_j (level k-2) while the two products run
+                if (j + 2 < L) stage_rows(us + (size_t)(j + 2) * WS, sU);
+                if (j > 0) stage_rows(un + (size_t)j * WS, sP);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                // F_j = G_j (U_{j+1} - U_j)
+                ms3_gemm<RT, true>(acquire(), Uj1, Uj, C, lane, src_lo, src_hi, tr);
+                release();
+                if (j == 0) {
+                    // F_0 -> face mailbox (all W rows are face rows), then the per-warp flag
+                    double* fo = fx + (size_t)s * WS;
+#pragma unroll
+                    for (int I = 0; I < RT; ++I)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int r = row_of(I, e);
+                            if (r < W) fo[(size_t)r * S + q] = C[I][e];
+                        }
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) st_release(p.sflags + (size_t)s * 4 + c, tag);
+                    if (outer) {  // acc_0 = H_0 F_0 (read back only on outer-face rows)
+                        double A0[RT][2];
+                        ms3_gemm<RT, false>(acquire(), C, C, A0, lane, src_lo, src_hi, tr);
+                        release();
+                        double* ao = p.acc1 + (size_t)s * WS;
+#pragma unroll
+                        for (int I = 0; I < RT; ++I)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int r = row_of(I, e);
+                                if (r < W && p.nbr[s * 6 + r / M] < 0) ao[(size_t)r * S + q] = A0[I][e];
+                            }
+                    }
+#pragma unroll
+                    for (int I = 0; I < RT; ++I) {
+                        Fp[I][0] = C[I][0];
+                        Fp[I][1] = C[I][1];
+                    }
+                } else {
+                    // acc_j = H_j (F_j - F_{j-1}); leapfrog of layer j
+                    double A[RT][2];
+                    ms3_gemm<RT, true>(acquire(), C, Fp, A, lane, src_lo, src_hi, tr);
+                    release();
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+                    for (int I = 0; I < RT; ++I)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int r = row_of(I, e);
+                            double tot = A[I][e];
+                            if (srcs && r < W) tot = __dadd_rn(tot, __dmul_rn(svec[(size_t)j * W + r], fq));
+                            const double upr = sP[(2 * I + e) * 32 + lane];
+                            const double v =
+                                __dadd_rn(__dsub_rn(__dmul_rn(2.0, Uj[I][e]), upr), __dmul_rn(dt2, tot));
+                            if (r < W) {
+                                un[(size_t)j * WS + (size_t)r * S + q] = v;
+                                sq = fma(v, v, sq);
+                            }
+                            Fp[I][e] = C[I][e];
+                        }
+                }
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+                for (int I = 0; I < RT; ++I)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) Uj[I][e] = Uj1[I][e];
+                if (j + 2 < L) {
+                    read_rows(sU, Uj1);
+                } else {
+#pragma unroll
+                    for (int I = 0; I < RT; ++I) Uj1[I][0] = Uj1[I][1] = 0.0;
+                }
+            }
+        }
+        if (k > 1) put_norm(k - 1, sq_prev + sqc);
+        sq_prev = sq;
+        __syncwarp();
+    }
+}
+
+static size_t ms3_smem_bytes(int TB, int W, int nsmax, int ng, int nstg) {
+    const size_t RT = (W + 7) / 8;
+    return 8 * ((size_t)ng * nstg * TB + (size_t)4 * ng * W * 8 + (size_t)4 * ng * 4 * RT * 32 + 2 * ng * nstg) +
+           4 * (size_t)nsmax + 64;
+}
+
+// launch shapes of k_step_ms3: (subdomain groups per CTA, chain stages per group)
+static const void* ms3_kernel(int m, int ng, int nstg) {
+#define SFW_MS3_CASE(MM, G, NSV) \
+    if (m == MM && ng == G && nstg == NSV) return (const void*)k_step_ms3<MM, G, NSV>;
+    SFW_MS3_CASE(9, 2, 3)
+    SFW_MS3_CASE(4, 2, 3)
+    SFW_MS3_CASE(1, 2, 3)
+#undef SFW_MS3_CASE
+    return nullptr;
+}
+
 // per-subdomain interface mass blocks [n_sub][6][m*m] (zeros on outer faces)
 __global__ void k_ms_massblocks(const double* __restrict__ mass, const int* __restrict__ mass_idx, int n_sub, int m,
                                 double* __restrict__ out) {
@@ -1196,6 +1604,31 @@ extern "C" int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub,
     } else {
         h->shot_smem2 = 0;
     }
+    h->shot_smem3 = 0;
+    // k_step_ms3 is opt-in (SFW_MS3="groups,stages", e.g. "2,3"): correct, but measured slower than
+    // k_step_ms2 on config 4 (0.93 vs 0.79 ms/step): with 2 warps per SMSP the in-sweep layer-0
+    // coupling (three dependent global round trips per subdomain) leaves the DMMA pipe idle.
+    int ng = 0, nstg = 0;
+    if (const char* e = getenv("SFW_MS3")) sscanf(e, "%d,%d", &ng, &nstg);
+    if (ng > 0 && ms3_kernel(h->m, ng, nstg) && !getenv("SFW_MS_V1")) {
+        int nsmax = 0;
+        for (int b = 0; b < h->grid; ++b) nsmax = std::max(nsmax, h->cta_ptr_h[b + 1] - h->cta_ptr_h[b]);
+        const size_t sm3 = ms3_smem_bytes(h->TB, W, nsmax, ng, nstg);
+        h->ms3_ng = ng;
+        h->ms3_ns = nstg;
+        if (!h->mmass && (rc = dalloc(&h->mmass, (size_t)h->n_sub * 6 * h->m * h->m, errbuf, errlen))) return rc;
+        k_ms_massblocks<<<592, 256, 0, h->stream>>>(h->mass, h->mass_idx, h->n_sub, h->m, h->mmass);
+        if (!h->sflags) {
+            if ((rc = dalloc(&h->sflags, (size_t)h->n_sub * 4, errbuf, errlen))) return rc;
+            SFW_CUDA_TRY(cudaMemsetAsync(h->sflags, 0, (size_t)h->n_sub * 4 * 4, h->stream));
+            h->stag = 0;
+        }
+        if (sm3 <= 220 * 1024) {
+            SFW_CUDA_TRY(cudaFuncSetAttribute(ms3_kernel(h->m, ng, nstg), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sm3));
+            h->shot_smem3 = (int)sm3;
+        }
+    }
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
     SFW_CUDA_TRY(cudaGetLastError());
     return 0;
@@ -1219,7 +1652,8 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
                                  h->stream));
     const long long nrec = n_steps / record_every;
     if ((rc = ms_ensure(&h->mrows, &h->mrows_cap, std::max(1LL, nrec * h->n_probe * S), errbuf, errlen))) return rc;
-    const int nparts = h->shot_smem2 ? M2_NQ * h->grid : h->grid;  // ms2: one partial per row-tile group
+    // norm partials per step: ms3 one per subdomain group, ms2 one per row-tile group, ms one per CTA
+    const int nparts = h->shot_smem3 ? h->ms3_ng * h->grid : h->shot_smem2 ? M2_NQ * h->grid : h->grid;
     if ((rc = ms_ensure(&h->mnorm, &h->mnorm_cap, (long long)n_steps * nparts * S + (long long)n_steps * S, errbuf,
                         errlen)))
         return rc;
@@ -1280,7 +1714,14 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
     }
     void* args[] = {&p};
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
-    if (h->shot_smem2)
+    p.sflags = h->sflags;
+    p.tag0 = h->stag;
+    if (h->shot_smem3) {
+        SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ms3_kernel(h->m, h->ms3_ng, h->ms3_ns), dim3(h->grid),
+                                                 dim3(128 * h->ms3_ng), args,
+                                                 h->shot_smem3, h->stream));
+        h->stag += (unsigned int)n_steps;
+    } else if (h->shot_smem2)
         SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ms2_kernel(h->m), dim3(h->grid), dim3((M2_NW + 1) * 32), args,
                                                  h->shot_smem2, h->stream));
     else

@@ -91,5 +91,9 @@ struct sfw_stepper {
     double* shot_ftab = nullptr;
     long long shot_ftab_cap = 0, mrows_cap = 0, mnorm_cap = 0;
     int mcur = 0;
+    int shot_smem3 = 0;               // k_step_ms3 dynamic smem (0: not used)
+    int ms3_ng = 2, ms3_ns = 4;       // k_step_ms3 launch shape (subdomain groups, chain stages)
+    unsigned int* sflags = nullptr;   // k_step_ms3: [n_sub][4] F_0 publication tags
+    unsigned int stag = 0;            // k_step_ms3: last tag used
 };
 
