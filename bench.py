@@ -48,6 +48,25 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _traffic(key, steps):
+    """ncu DRAM bytes per step of the stepping launch (profiles/traffic.json) x the launch's steps."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            ent = json.load(fh).get(key)
+        return ent["dram_bytes_per_step"] * steps if ent else None
+    except Exception:
+        return None
+
+
+def _fp64_peak():
+    """Measured FP64 DMMA peak (TFLOP/s) of this pool's B200 (profiles/r01_fp64_peak.json, tools/fp64_peak.cu)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as fh:
+            return float(json.load(fh)["dmma_f64_tflops"]), "measured (tools/fp64_peak.cu)"
+    except Exception:
+        return 37.0, "fallback"
+
+
 def _workload(cfg):
     from paper_1406_6923_b200 import grid as pg
     from paper_1406_6923_b200.configs import locate, make_workload
@@ -325,16 +344,7 @@ def run_ours(args):
         return
     peak, peak_kind = _peaks()
     achieved = alg_bytes * K / kernel_s / 1e9
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tfile):
-        try:
-            tj = json.load(open(tfile))
-            ent = tj.get(f"config{args.config}")
-            if ent:  # per launch, like achieved: ncu DRAM bytes per step x the K steps of this launch
-                traffic = ent.get("dram_bytes_per_step") * K
-        except Exception:
-            traffic = None
+    traffic = _traffic(f"config{args.config}", K)  # per launch, like achieved
     # CPU baseline: the oracle (reference algorithm) stepping the same models, bounded sample
     cpu = None
     if not args.no_cpu:
@@ -469,7 +479,8 @@ def _run_fp32(args, wl, models, ptrs, dt, lam, conv, src, probes, ws, rank, buil
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16, "d2h_bytes_per_step": 8 * (len(probes) + 1),
                 "api": "CoupledStepper(precision='fp32').run(K, probes)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_step": b.value,
+                     "traffic": _traffic(f"config{args.config}_fp32", K), "peak_kind": peak_kind,
+                     "alg_bytes_per_step": b.value,
                      "streamed_bytes_per_step": st_b.value,
                      "formula": "4[(2L-1)w(w+1)/2 + 3Lw] bytes per subdomain-step (SURVEY 8d fp32)"},
         "cpu_baseline": None, "clocks": clk.summary(), "gpu_launches": 2, "kernel_ms": kernel_s * 1e3,
@@ -513,6 +524,9 @@ def _run_shots(args, wl, models, ptrs, dt, lam, conv, probes, ws, rank, build_s,
         return
     peak, peak_kind = _peaks()
     achieved = alg_bytes * K / kernel_s / 1e9
+    fpk, fpk_kind = _fp64_peak()
+    t_hbm = alg_bytes / (peak * 1e9)
+    t_fp = alg_flops / (fpk * 1e12)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
         "ms_per_step": 1e3 * t_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -527,10 +541,13 @@ def _run_shots(args, wl, models, ptrs, dt, lam, conv, probes, ws, rank, build_s,
                 "d2h_bytes_per_step": 8 * len(shots) * (len(probes) + 1),
                 "api": "CoupledStepper.run_shots(K, 32 shots, probes): profile upload, init, kernel, "
                        "per-shot traces + norms download"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_kind": peak_kind, "alg_bytes_per_step": alg_bytes,
+        "roofline": {"bound": "hbm" if t_hbm >= t_fp else "fp64", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": max(t_hbm, t_fp) * K / kernel_s,
+                     "traffic": _traffic("config4", K), "peak_kind": peak_kind, "alg_bytes_per_step": alg_bytes,
                      "streamed_bytes_per_step": streamed, "alg_flops_per_step": alg_flops,
-                     "achieved_tflops": alg_flops * K / kernel_s / 1e12,
+                     "achieved_tflops": alg_flops * K / kernel_s / 1e12, "fp64_peak_tflops": fpk,
+                     "fp64_peak_kind": fpk_kind, "roofline_us_per_step": {"hbm": 1e6 * t_hbm, "fp64": 1e6 * t_fp},
+                     "frac_note": "slower of HBM bytes and FP64 flops at their measured peaks (north_star)",
                      "formula": "8[(2L-1)w(w+1)/2 + 3LwS] bytes, S(2(2L-1)w^2+5Lw) flops per subdomain-step"},
         "cpu_baseline": None,
         "clocks": clk.summary(),

@@ -4,21 +4,15 @@
 set -x
 O=gpurun_out
 python bench.py > $O/p_bench_default.json 2> $O/p_bench_default.err && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv --log-file $O/launches_default.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file $O/launches_default.csv \
     python bench.py > $O/ncu_launch.log 2>&1
-python bench.py --extra 0 --no-cpu > $O/p_c2.json 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:k_step_res -s 1 -c 1 -o $O/prof_c2_res \
-    python bench.py --extra 0 --no-cpu > $O/ncu_c2.log 2>&1
-python bench.py --config 3 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/p_c3.json 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:k_step2 -s 2858 -c 1 -o $O/prof_c3_step \
-    python bench.py --config 3 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/ncu_c3.log 2>&1
-python bench.py --config 4 --steps 20 --warmup 3 --no-cpu --extra 0 > $O/p_c4.json 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:k_step_ms -s 1 -c 1 -o $O/prof_c4_shots \
-    python bench.py --config 4 --steps 20 --warmup 3 --no-cpu --extra 0 > $O/ncu_c4.log 2>&1
+python bench.py --extra 0 --no-cpu --steps 2000 --warmup 50 > $O/p_c2.json 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:k_step_sw -s 1 -c 1 -o $O/prof_c2_sw \
+    python bench.py --extra 0 --no-cpu --steps 2000 --warmup 50 > $O/ncu_c2.log 2>&1
 python bench.py --config 3 --precision fp32 --steps 100 --warmup 3 --no-cpu --extra 0 > $O/p_c3f.json 2>&1 && \
 ncu --set full --import-source on --clock-control none -k regex:k_wstep -s 3 -c 1 -o $O/prof_c3_fp32 \
     python bench.py --config 3 --precision fp32 --steps 100 --warmup 3 --no-cpu --extra 0 > $O/ncu_c3f.log 2>&1
-python bench.py --config 3 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/p_c3b.json 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:k_pcg -s 0 -c 1 -o $O/prof_rom_pcg \
-    python bench.py --config 3 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/ncu_pcg.log 2>&1
+python bench.py --config 5 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/b_c5.json 2>&1
+python bench.py --config 5 --precision fp32 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/b_c5f.json 2>&1
+python bench.py --config 3 --precision fp32 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/b_c3f.json 2>&1
 ls -la $O

@@ -190,7 +190,64 @@ def golden_m9k8():
     print("golden_m9k8.npz")
 
 
+def golden_io():
+    """Files written by the reference io.py (.rom, coefficient arrays, .trc, .meta.txt) + cache keys."""
+    from sfwave.io import TraceRecord, save_model, write_meta, write_traces
+    from sfwave.sim import _model_cache_key
+    spec = DomainSpec((2.0, 1.0, 1.0), (2, 1, 1), (5, 5, 5))
+    part = build_partition(spec)
+    c = sample_medium(MediumModel(1.0), part)
+    keys = {}
+    for sub in part.subdomains:
+        op = assemble_subdomain_operator(part, sub.alpha, c)
+        md = build_subdomain_model(op, 1, 2, 4.0)
+        tag = "".join(map(str, sub.alpha))
+        save_model(os.path.join(HERE, f"io_pair{tag}.rom"), md)
+        keys["key_" + tag] = _model_cache_key(op, 1, md.layers, 4.0)
+    rng = np.random.default_rng(5)
+    rec = TraceRecord(coords=rng.standard_normal((3, 3)), dt=0.00125, samples=rng.standard_normal((7, 3)))
+    write_traces(os.path.join(HERE, "io.trc"), rec)
+    write_meta(os.path.join(HERE, "io.meta.txt"), {"run": "golden", "dt": 0.1 + 0.2, "steps": 7,
+                                                    "lambda_hat": np.float64(1.0) / 3.0, "tag": "a: b"})
+    np.savez_compressed(os.path.join(HERE, "golden_io.npz"), c_field=c, **{k: np.array(v) for k, v in keys.items()})
+    print("golden_io.npz", keys)
+
+
+def golden_fdtd():
+    """Fine-grid leapfrog (reference.py:86-157) on the config-1 grid, driven as sim.run_reference does."""
+    from sfwave.grid import assemble_global_operator
+    from sfwave.reference import estimate_lambda_max, run_leapfrog
+    wl = make_workload(1)
+    spec = DomainSpec(tuple((g - 1) * h for g, h in zip(wl.global_shape, wl.spacing)), wl.counts, wl.p)
+    part = build_partition(spec)
+    a = assemble_global_operator(part, wl.c_field)
+    lam = estimate_lambda_max(a)
+    dt = 0.9 * 2.0 / math.sqrt(lam)
+    shape = part.global_shape
+    src = int(np.ravel_multi_index(tuple(wl.sources[0]), shape))
+    vec = np.zeros(a.shape[0])
+    c_flat = wl.c_field.ravel()
+    vec[src] = 1.0 / c_flat[src]
+    sx, sy, sz = (int(v) for v in wl.sources[0])
+    rec = [int(np.ravel_multi_index((x, sy, sz), shape)) for x in range(0, shape[0], 4)] + [src]
+    pulse = make_pulse("ricker", wl.f0, 1.2 / wl.f0)
+    run = run_leapfrog(a, dt, 200, source_vec=vec, source_fn=pulse, record_idx=rec, record_every=1)
+    av = a @ np.random.default_rng(3).standard_normal(a.shape[0])
+    np.savez_compressed(os.path.join(HERE, "golden_fdtd.npz"), c_field=wl.c_field, lam=lam, dt=dt, src=src,
+                        rec=np.array(rec), samples=run.samples, times=run.times, u_curr=run.u_curr,
+                        u_prev=run.u_prev, av=av)
+    print("golden_fdtd.npz", lam, dt, run.samples.shape)
+
+
 if __name__ == "__main__":
-    golden_toy()
-    golden_config(1, None, 200, "golden_c1.npz")
-    golden_m9k8()
+    which = sys.argv[1:] or ["toy", "c1", "m9k8", "io", "fdtd"]
+    if "toy" in which:
+        golden_toy()
+    if "c1" in which:
+        golden_config(1, None, 200, "golden_c1.npz")
+    if "m9k8" in which:
+        golden_m9k8()
+    if "io" in which:
+        golden_io()
+    if "fdtd" in which:
+        golden_fdtd()
