@@ -198,6 +198,39 @@ int sfw_source_vector(int L, int w, const double* scales, const double* basis_ro
 int sfw_probe_weights(int L, int w, const double* scales, const double* basis_row, double scale,
                       double* out, char* errbuf, int errlen);
 
+/* ------------------------------------------------------------------------- */
+/* Fine-grid leapfrog reference solver (reference.py:26-157 on the operator of  */
+/* grid.py:461-467, the undivided C Lap_h C with mirror closure).  The matrix   */
+/* is never stored: rows are rebuilt from c and the per-axis scales in the      */
+/* reference's arithmetic, so trajectories match scipy/numpy bit for bit.       */
+/* ------------------------------------------------------------------------- */
+
+typedef struct sfw_fdtd sfw_fdtd;
+
+/* grid nx x ny x nz (C order, z fastest); scales[d] = 1 / (1.0 * h_d**2) as
+ * grid.py:366 forms it; c: HOST nx*ny*nz sound speed.  Replaces building
+ * assemble_global_operator's CSR (grid.py:461-467). */
+int sfw_fdtd_create(int nx, int ny, int nz, const double* scales, const double* c, sfw_fdtd** out,
+                    char* errbuf, int errlen);
+/* y = A x, HOST vectors (the `a @ u` of reference.py:117). */
+int sfw_fdtd_apply(sfw_fdtd* h, const double* x, double* y, char* errbuf, int errlen);
+/* estimate_lambda_max (reference.py:26-63) from the HOST normalised start
+ * vector v0 (numpy default_rng(seed)); *iters < 0: not converged. */
+int sfw_fdtd_power(sfw_fdtd* h, const double* v0, double tol, int max_iter, double* lam, int* iters,
+                   char* errbuf, int errlen);
+/* source_vec nonzeros (node, value), receiver rows, optional damping (HOST n). */
+int sfw_fdtd_setup(sfw_fdtd* h, int n_src, const long long* src_idx, const double* src_val, int n_rec,
+                   const long long* rec_idx, const double* damping, char* errbuf, int errlen);
+/* second-order start (reference.py:123-124); v0 may be NULL; f0 = source_fn(0). */
+int sfw_fdtd_init(sfw_fdtd* h, double dt, const double* u0, const double* v0, double f0, char* errbuf,
+                  int errlen);
+/* n_steps steps (reference.py:129-150): ftab[k-1] = source_fn((k-1) dt);
+ * norms_out[k-1] = |u_k|^2; rows_out[r][n_rec] every record_every steps. */
+int sfw_fdtd_run(sfw_fdtd* h, double dt, int n_steps, const double* ftab, int record_every,
+                 double* norms_out, double* rows_out, float* kernel_ms, char* errbuf, int errlen);
+int sfw_fdtd_state(sfw_fdtd* h, double* u_curr, double* u_prev, char* errbuf, int errlen);
+int sfw_fdtd_destroy(sfw_fdtd* h);
+
 #ifdef __cplusplus
 }
 #endif

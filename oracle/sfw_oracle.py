@@ -25,6 +25,7 @@ Algorithm map (reference file:line it restates):
 * energy ..................... stepper.py:419-449
 * coupled CFL power iteration  stepper.py:452-495, reference.py:20-23
 * Ricker pulse ............... sim.py:80-85
+* fine-grid operator / FDTD .. grid.py:461-467, reference.py:26-157
 """
 
 from __future__ import annotations
@@ -659,3 +660,67 @@ def cfl_power(models: dict, tol=POWER_TOL, max_iter=POWER_MAX_ITER, seed=0):
         lam = lam_new
         x = y
     return lam, False
+
+
+# ---------------------------------------------------------------------------
+# fine-grid reference solver (grid.py:461-467, reference.py:26-157)
+
+def global_matrix(shape, spacing, c_field):
+    """Undivided C Lap_h C on the full grid (grid.py:461-467): subdomain_matrix with no sharing."""
+    a, _ = subdomain_matrix(tuple(shape), tuple(spacing), np.asarray(c_field, float).ravel(), {})
+    return a
+
+
+def power_lambda(a, tol=POWER_TOL, max_iter=POWER_MAX_ITER, seed=0):
+    """(lambda_max(-A), iterations) by power iteration (reference.py:26-63)."""
+    n = a.shape[0]
+    v = np.random.default_rng(seed).standard_normal(n)
+    v /= np.linalg.norm(v)
+    lam = 0.0
+    for it in range(max_iter):
+        w = -(a @ v)
+        nw = np.linalg.norm(w)
+        if nw == 0.0:
+            return 0.0, it + 1
+        lam_new = float(v @ w)
+        v = w / nw
+        if it > 0 and abs(lam_new - lam) <= tol * abs(lam_new):
+            return lam_new, it + 1
+        lam = lam_new
+    return lam, -max_iter
+
+
+def leapfrog(a, dt, n_steps, u0=None, v0=None, source_vec=None, source_fn=None, record_idx=None,
+             record_every=1, damping=None, growth_limit=GROWTH_LIMIT):
+    """Central-difference integration of w_tt = A w + f(t) s (reference.py:86-157).
+
+    Returns (samples, times, u_prev, u_curr); raises OracleError on growth.
+    """
+    n = a.shape[0]
+    u = np.zeros(n) if u0 is None else np.array(u0, dtype=float)
+    vel = np.zeros(n) if v0 is None else np.asarray(v0, dtype=float)
+    forced = source_vec is not None and source_fn is not None
+    snorm = float(np.linalg.norm(source_vec)) if forced else 0.0
+
+    def acc_of(x, t):
+        y = a @ x
+        return y + source_fn(t) * source_vec if forced else y
+
+    up = u - dt * vel + 0.5 * dt * dt * acc_of(u, 0.0)
+    rec = None if record_idx is None else np.asarray(record_idx, dtype=np.int64)
+    samples, times = ([u[rec].copy()], [0.0]) if rec is not None else ([], [])
+    base = float(np.linalg.norm(u)) + dt * float(np.linalg.norm(vel))
+    for step in range(1, n_steps + 1):
+        t = (step - 1) * dt
+        un = 2.0 * u - up + dt * dt * acc_of(u, t)
+        if damping is not None:
+            un = un * damping
+        up, u = u, un
+        if forced:
+            base += dt * dt * abs(float(source_fn(t))) * snorm
+        if float(np.linalg.norm(u)) > growth_limit * max(base, 1e-300):
+            raise OracleError(f"leapfrog diverged at step {step}")
+        if rec is not None and step % record_every == 0:
+            samples.append(u[rec].copy())
+            times.append(step * dt)
+    return np.array(samples), np.array(times), up, u

@@ -24,6 +24,7 @@ _ERRMAP = {SFW_ECONFIG: ConfigError, SFW_ENUMERICAL: NumericalError,
 PD = C.POINTER(C.c_double)
 PI = C.POINTER(C.c_int)
 PF = C.POINTER(C.c_float)
+PL = C.POINTER(C.c_longlong)
 
 
 class StepDesc(C.Structure):
@@ -64,6 +65,14 @@ SIGNATURES = {
     "sfw_wform_destroy": (C.c_int, [C.c_void_p]),
     "sfw_source_vector": (C.c_int, [C.c_int, C.c_int, PD, PD, C.c_double, PD, PD, C.c_char_p, C.c_int]),
     "sfw_probe_weights": (C.c_int, [C.c_int, C.c_int, PD, PD, C.c_double, PD, C.c_char_p, C.c_int]),
+    "sfw_fdtd_create": (C.c_int, [C.c_int, C.c_int, C.c_int, PD, PD, C.POINTER(C.c_void_p), C.c_char_p, C.c_int]),
+    "sfw_fdtd_apply": (C.c_int, [C.c_void_p, PD, PD, C.c_char_p, C.c_int]),
+    "sfw_fdtd_power": (C.c_int, [C.c_void_p, PD, C.c_double, C.c_int, PD, PI, C.c_char_p, C.c_int]),
+    "sfw_fdtd_setup": (C.c_int, [C.c_void_p, C.c_int, PL, PD, C.c_int, PL, PD, C.c_char_p, C.c_int]),
+    "sfw_fdtd_init": (C.c_int, [C.c_void_p, C.c_double, PD, PD, C.c_double, C.c_char_p, C.c_int]),
+    "sfw_fdtd_run": (C.c_int, [C.c_void_p, C.c_double, C.c_int, PD, C.c_int, PD, PD, PF, C.c_char_p, C.c_int]),
+    "sfw_fdtd_state": (C.c_int, [C.c_void_p, PD, PD, C.c_char_p, C.c_int]),
+    "sfw_fdtd_destroy": (C.c_int, [C.c_void_p]),
 }
 
 _lib = None
@@ -117,6 +126,13 @@ def dptr(a: np.ndarray | None):
         return None
     assert a.dtype == np.float64 and a.flags.c_contiguous
     return a.ctypes.data_as(PD)
+
+
+def lptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.dtype == np.int64 and a.flags.c_contiguous
+    return a.ctypes.data_as(PL)
 
 
 def iptr(a: np.ndarray | None):

@@ -1,0 +1,439 @@
+// Fine-grid leapfrog reference solver on the GPU (reference reference.py:26-157,
+// operator grid.py:326-382 + 461-467).
+//
+// The reference integrates w_tt = A w + f(t) s on the undecomposed grid, with A = -C Lap_h C the
+// link-weighted graph stiffness (mirror closure) as a scipy CSR matrix.  Here A is never stored:
+// every thread rebuilds its row from c and the per-axis scales 1/h_d^2 in the reference's exact
+// arithmetic --
+//   off-diagonal (i, j):  (c_lo * c_hi) * s_d                      (grid.py:365-372)
+//   diagonal:             0 + sum over links in the order d = x, y, z, lower end then upper end
+//                         of (-c_i * c_i) * s_d                      (np.add.at, grid.py:373-374)
+//   row product:          0 + sum of a_ij * w_j over the sorted columns x-, y-, z-, i, z+, y+, x+
+//                         (scipy csr_matvec, no FMA)
+// and the leapfrog / start / forcing in numpy's evaluation order (reference.py:117-135), so the GPU
+// trajectory is the reference's bit for bit (tests/test_fdtd_gpu.py).
+//
+// Layout: C-order (x, y, z), z fastest; fp64 c, and two time levels ping-ponged in place (level
+// k+1 overwrites level k-1 element-wise).  One thread per node, 32 (z) x 8 (y) blocks, one
+// x-plane per grid z-index: the y/z neighbours of a warp hit L1, the x neighbours (a plane
+// apart) hit L2, so HBM sees u, c, u_prev read once and u_next written once -- 32 B per
+// node-step, the kernel's roofline (HBM-bound: 13 flop per 32 B).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "sfw_common.cuh"
+
+namespace sfw {
+
+struct FdParams {
+    int nx, ny, nz;
+    double s0, s1, s2;     // 1/h_d^2 exactly as the reference forms them
+    const double* c;
+    const double* u;       // current level (or the vector A is applied to)
+    double* out;           // mode 0: previous level in, next level out; 1: start level; 2: -A u
+    const double* vel;     // mode 1: initial velocity or null
+    double dt, dt2, half;  // dt, dt*dt, (0.5*dt)*dt
+    const double* damping; // mode 0: per-node factor or null
+    int n_src;
+    const long long* src_idx;
+    const double* src_val;
+    double f;              // source profile value of this step
+    double* part;          // per-block partial sums: mode 0/1 |out|^2, mode 2 unused
+};
+
+__device__ __forceinline__ double fd_row(const FdParams& p, long long i, int x, int y, int z, double ui) {
+    const long long sx = (long long)p.ny * p.nz, sy = p.nz;
+    const double ci = __ldg(p.c + i);
+    const double cc = __dmul_rn(-ci, ci);
+    double diag = 0.0;
+    if (p.nx > 1) {
+        if (x + 1 < p.nx) diag = __dadd_rn(diag, __dmul_rn(cc, p.s0));
+        if (x > 0) diag = __dadd_rn(diag, __dmul_rn(cc, p.s0));
+    }
+    if (p.ny > 1) {
+        if (y + 1 < p.ny) diag = __dadd_rn(diag, __dmul_rn(cc, p.s1));
+        if (y > 0) diag = __dadd_rn(diag, __dmul_rn(cc, p.s1));
+    }
+    if (p.nz > 1) {
+        if (z + 1 < p.nz) diag = __dadd_rn(diag, __dmul_rn(cc, p.s2));
+        if (z > 0) diag = __dadd_rn(diag, __dmul_rn(cc, p.s2));
+    }
+    double sum = 0.0;
+    auto term = [&](long long j, double s) {
+        const double a = __dmul_rn(__dmul_rn(__ldg(p.c + j), ci), s);
+        sum = __dadd_rn(sum, __dmul_rn(a, __ldg(p.u + j)));
+    };
+    if (x > 0) term(i - sx, p.s0);
+    if (y > 0) term(i - sy, p.s1);
+    if (z > 0) term(i - 1, p.s2);
+    sum = __dadd_rn(sum, __dmul_rn(diag, ui));
+    if (z + 1 < p.nz) term(i + 1, p.s2);
+    if (y + 1 < p.ny) term(i + sy, p.s1);
+    if (x + 1 < p.nx) term(i + sx, p.s0);
+    return sum;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
+    const int z = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, x = blockIdx.z;
+    const bool in = z < p.nz && y < p.ny;
+    double sq = 0.0;
+    if (in) {
+        const long long i = ((long long)x * p.ny + y) * p.nz + z;
+        const double ui = __ldg(p.u + i);
+        double acc = fd_row(p, i, x, y, z, ui);
+        if (MODE == 2) {
+            p.out[i] = -acc;
+        } else {
+            for (int q = 0; q < p.n_src; ++q)  // acc + f(t) * source_vec (reference.py:117-121)
+                if (p.src_idx[q] == i) acc = __dadd_rn(acc, __dmul_rn(p.f, p.src_val[q]));
+            double v;
+            if (MODE == 0) {  // 2 u - u_prev + (dt*dt) acc   (reference.py:131)
+                v = __dadd_rn(__dsub_rn(__dmul_rn(2.0, ui), p.out[i]), __dmul_rn(p.dt2, acc));
+                if (p.damping) v = __dmul_rn(v, p.damping[i]);
+            } else {          // u - dt v + (0.5 dt dt) acc   (reference.py:124)
+                const double vv = p.vel ? __dmul_rn(p.dt, p.vel[i]) : 0.0;
+                v = __dadd_rn(__dsub_rn(ui, vv), __dmul_rn(p.half, acc));
+            }
+            p.out[i] = v;
+            sq = v * v;
+        }
+    }
+    if (MODE != 2) {  // fixed-order block partial of |out|^2 (deterministic)
+        __shared__ double red[8];
+        const double w = warp_sum(sq);
+        const int wid = threadIdx.y, lane = threadIdx.x;
+        if (lane == 0) red[wid] = w;
+        __syncthreads();
+        if (wid == 0 && lane == 0) {
+            double t = 0.0;
+            for (int k = 0; k < 8; ++k) t += red[k];
+            p.part[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+        }
+    }
+}
+
+// one block: fixed-order sum of the block partials -> out[slot]; gather of the receiver rows
+__global__ void k_fd_finish(const double* __restrict__ part, long long nparts, double* __restrict__ out, int slot,
+                            const double* __restrict__ u, const long long* __restrict__ rec, int n_rec,
+                            double* __restrict__ rows) {
+    __shared__ double red[32];
+    double t = 0.0;
+    for (long long k = threadIdx.x; k < nparts; k += blockDim.x) t += part[k];
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        out[slot] = s;
+    }
+    if (rows)
+        for (int r = threadIdx.x; r < n_rec; r += blockDim.x) rows[r] = u[rec[r]];
+}
+
+// power iteration pieces: partials of v.w and w.w, then v <- w / |w|
+__global__ void k_fd_dots(const double* __restrict__ v, const double* __restrict__ w, long long n,
+                          double* __restrict__ part) {
+    double a = 0.0, b = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        a = fma(v[i], w[i], a);
+        b = fma(w[i], w[i], b);
+    }
+    __shared__ double ra[32], rb[32];
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if ((threadIdx.x & 31) == 0) {
+        ra[threadIdx.x >> 5] = a;
+        rb[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sa = 0.0, sb = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            sa += ra[k];
+            sb += rb[k];
+        }
+        part[2 * blockIdx.x] = sa;
+        part[2 * blockIdx.x + 1] = sb;
+    }
+}
+
+__global__ void k_fd_dots_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < nb; ++k) {
+            a += part[2 * k];
+            b += part[2 * k + 1];
+        }
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+__global__ void k_fd_scale(const double* __restrict__ w, double inv, long long n, double* __restrict__ v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        v[i] = w[i] / inv;
+}
+
+}  // namespace sfw
+
+using namespace sfw;
+
+struct sfw_fdtd {
+    int nx = 0, ny = 0, nz = 0;
+    long long n = 0;
+    double s[3] = {0, 0, 0};
+    double* c = nullptr;
+    double* U[2] = {nullptr, nullptr};
+    double* W = nullptr;      // scratch (apply / power iteration / velocity)
+    double* part = nullptr;   // block partials
+    double* acc = nullptr;    // device reduction results [>= 2]
+    double* norms = nullptr;  // [cap] per-step |u|^2
+    double* rows = nullptr;   // [cap_rows]
+    long long norms_cap = 0, rows_cap = 0;
+    long long* src = nullptr;
+    double* srcv = nullptr;
+    long long* rec = nullptr;
+    double* damp = nullptr;
+    int n_src = 0, n_rec = 0, cur = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    dim3 grid, block;
+    long long nparts = 0;
+};
+
+namespace {
+template <typename T>
+int fd_alloc(T** p, size_t n, char* errbuf, int errlen) {
+    *p = nullptr;
+    cudaError_t e = cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+    if (e != cudaSuccess) return fail(SFW_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e), errbuf, errlen);
+    return 0;
+}
+
+FdParams fd_params(sfw_fdtd* h) {
+    FdParams p{};
+    p.nx = h->nx;
+    p.ny = h->ny;
+    p.nz = h->nz;
+    p.s0 = h->s[0];
+    p.s1 = h->s[1];
+    p.s2 = h->s[2];
+    p.c = h->c;
+    p.part = h->part;
+    return p;
+}
+}  // namespace
+
+extern "C" int sfw_fdtd_create(int nx, int ny, int nz, const double* scales, const double* c, sfw_fdtd** out,
+                               char* errbuf, int errlen) {
+    *out = nullptr;
+    if (nx < 1 || ny < 1 || nz < 1) return fail(SFW_ECONFIG, "grid dimensions must be positive", errbuf, errlen);
+    auto* h = new sfw_fdtd();
+    h->nx = nx;
+    h->ny = ny;
+    h->nz = nz;
+    h->n = (long long)nx * ny * nz;
+    for (int d = 0; d < 3; ++d) h->s[d] = scales[d];
+    h->block = dim3(32, 8, 1);
+    h->grid = dim3((nz + 31) / 32, (ny + 7) / 8, nx);
+    h->nparts = (long long)h->grid.x * h->grid.y * h->grid.z;
+    int rc = 0;
+    if ((rc = fd_alloc(&h->c, h->n, errbuf, errlen)) || (rc = fd_alloc(&h->U[0], h->n, errbuf, errlen)) ||
+        (rc = fd_alloc(&h->U[1], h->n, errbuf, errlen)) || (rc = fd_alloc(&h->W, h->n, errbuf, errlen)) ||
+        (rc = fd_alloc(&h->part, std::max<long long>(h->nparts, 2 * 1184), errbuf, errlen)) ||
+        (rc = fd_alloc(&h->acc, 4, errbuf, errlen))) {
+        delete h;
+        return rc;
+    }
+    cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    cudaEventCreate(&h->ev0);
+    cudaEventCreate(&h->ev1);
+    SFW_CUDA_TRY(cudaMemcpy(h->c, c, h->n * 8, cudaMemcpyHostToDevice));
+    *out = h;
+    return 0;
+}
+
+// y = A x  (x, y HOST, length n) -- the row arithmetic of the solver, exposed for tests
+extern "C" int sfw_fdtd_apply(sfw_fdtd* h, const double* x, double* y, char* errbuf, int errlen) {
+    SFW_CUDA_TRY(cudaMemcpyAsync(h->W, x, h->n * 8, cudaMemcpyHostToDevice, h->stream));
+    FdParams p = fd_params(h);
+    p.u = h->W;
+    p.out = h->U[0];
+    k_fdtd<2><<<h->grid, h->block, 0, h->stream>>>(p);
+    SFW_CUDA_TRY(cudaMemcpyAsync(y, h->U[0], h->n * 8, cudaMemcpyDeviceToHost, h->stream));
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SFW_CUDA_TRY(cudaGetLastError());
+    for (long long i = 0; i < h->n; ++i) y[i] = -y[i];  // kernel mode 2 writes -A x
+    return 0;
+}
+
+// Largest eigenvalue of -A by power iteration from the HOST start vector v0 (already normalised,
+// reference.py:26-63): w = -A v, lam = v.w, v = w/|w|, stop when |lam - lam_prev| <= tol |lam|.
+extern "C" int sfw_fdtd_power(sfw_fdtd* h, const double* v0, double tol, int max_iter, double* lam_out,
+                              int* iters_out, char* errbuf, int errlen) {
+    double* v = h->U[0];
+    double* w = h->W;
+    SFW_CUDA_TRY(cudaMemcpyAsync(v, v0, h->n * 8, cudaMemcpyHostToDevice, h->stream));
+    FdParams p = fd_params(h);
+    const int nb = 1184;
+    double lam = 0.0, res[2];
+    int it = 0;
+    for (; it < max_iter; ++it) {
+        p.u = v;
+        p.out = w;
+        k_fdtd<2><<<h->grid, h->block, 0, h->stream>>>(p);
+        k_fd_dots<<<nb, 256, 0, h->stream>>>(v, w, h->n, h->part);
+        k_fd_dots_final<<<1, 32, 0, h->stream>>>(h->part, nb, h->acc);
+        SFW_CUDA_TRY(cudaMemcpyAsync(res, h->acc, 16, cudaMemcpyDeviceToHost, h->stream));
+        SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        const double nw = std::sqrt(res[1]);
+        if (nw == 0.0) {
+            *lam_out = 0.0;
+            *iters_out = it + 1;
+            return 0;
+        }
+        const double lam_new = res[0];
+        k_fd_scale<<<nb, 256, 0, h->stream>>>(w, nw, h->n, v);
+        if (it > 0 && std::fabs(lam_new - lam) <= tol * std::fabs(lam_new)) {
+            lam = lam_new;
+            ++it;
+            *lam_out = lam;
+            *iters_out = it;
+            SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+            return 0;
+        }
+        lam = lam_new;
+    }
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SFW_CUDA_TRY(cudaGetLastError());
+    *lam_out = lam;
+    *iters_out = -max_iter;  // not converged (the caller logs, as reference.py:62 does)
+    return 0;
+}
+
+// Sources (node index, value of source_vec there) and receiver rows; damping (HOST n) or null.
+extern "C" int sfw_fdtd_setup(sfw_fdtd* h, int n_src, const long long* src_idx, const double* src_val, int n_rec,
+                              const long long* rec_idx, const double* damping, char* errbuf, int errlen) {
+    cudaFree(h->src);
+    cudaFree(h->srcv);
+    cudaFree(h->rec);
+    cudaFree(h->damp);
+    h->src = nullptr;
+    h->srcv = nullptr;
+    h->rec = nullptr;
+    h->damp = nullptr;
+    for (int i = 0; i < n_src; ++i)
+        if (src_idx[i] < 0 || src_idx[i] >= h->n) return fail(SFW_ECONFIG, "source node outside the grid", errbuf, errlen);
+    for (int i = 0; i < n_rec; ++i)
+        if (rec_idx[i] < 0 || rec_idx[i] >= h->n) return fail(SFW_ECONFIG, "receiver node outside the grid", errbuf, errlen);
+    int rc = 0;
+    if ((rc = fd_alloc(&h->src, n_src, errbuf, errlen)) || (rc = fd_alloc(&h->srcv, n_src, errbuf, errlen)) ||
+        (rc = fd_alloc(&h->rec, n_rec, errbuf, errlen)))
+        return rc;
+    if (n_src) {
+        SFW_CUDA_TRY(cudaMemcpy(h->src, src_idx, n_src * 8, cudaMemcpyHostToDevice));
+        SFW_CUDA_TRY(cudaMemcpy(h->srcv, src_val, n_src * 8, cudaMemcpyHostToDevice));
+    }
+    if (n_rec) SFW_CUDA_TRY(cudaMemcpy(h->rec, rec_idx, n_rec * 8, cudaMemcpyHostToDevice));
+    if (damping) {
+        if ((rc = fd_alloc(&h->damp, h->n, errbuf, errlen))) return rc;
+        SFW_CUDA_TRY(cudaMemcpy(h->damp, damping, h->n * 8, cudaMemcpyHostToDevice));
+    }
+    h->n_src = n_src;
+    h->n_rec = n_rec;
+    return 0;
+}
+
+// Second-order start (reference.py:123-124): level 0 = u0, level -1 = u0 - dt v0 + (0.5 dt dt) a(u0, 0).
+// u0 / v0 HOST (v0 may be null); f0 = source_fn(0).
+extern "C" int sfw_fdtd_init(sfw_fdtd* h, double dt, const double* u0, const double* v0, double f0, char* errbuf,
+                             int errlen) {
+    h->cur = 0;
+    SFW_CUDA_TRY(cudaMemcpyAsync(h->U[0], u0, h->n * 8, cudaMemcpyHostToDevice, h->stream));
+    if (v0) SFW_CUDA_TRY(cudaMemcpyAsync(h->W, v0, h->n * 8, cudaMemcpyHostToDevice, h->stream));
+    FdParams p = fd_params(h);
+    p.u = h->U[0];
+    p.out = h->U[1];
+    p.vel = v0 ? h->W : nullptr;
+    p.dt = dt;
+    p.half = (0.5 * dt) * dt;
+    p.n_src = h->n_src;
+    p.src_idx = h->src;
+    p.src_val = h->srcv;
+    p.f = f0;
+    k_fdtd<1><<<h->grid, h->block, 0, h->stream>>>(p);
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SFW_CUDA_TRY(cudaGetLastError());
+    return 0;
+}
+
+// n_steps leapfrog steps.  ftab: HOST [n_steps] source_fn((k-1) dt) for step k = 1..n_steps.
+// norms_out: HOST [n_steps] |u_k|^2 (fixed-order); rows_out: HOST [n_steps / record_every][n_rec]
+// (u at the receivers after every record_every-th step).  *kernel_ms: CUDA-event time.
+extern "C" int sfw_fdtd_run(sfw_fdtd* h, double dt, int n_steps, const double* ftab, int record_every,
+                            double* norms_out, double* rows_out, float* kernel_ms, char* errbuf, int errlen) {
+    if (n_steps <= 0) return 0;
+    if (record_every < 1) return fail(SFW_ECONFIG, "record_every must be >= 1", errbuf, errlen);
+    const long long nrec = n_steps / record_every;
+    int rc = 0;
+    if (h->norms_cap < n_steps) {
+        cudaFree(h->norms);
+        if ((rc = fd_alloc(&h->norms, n_steps, errbuf, errlen))) return rc;
+        h->norms_cap = n_steps;
+    }
+    if (h->rows_cap < std::max(1LL, nrec * h->n_rec)) {
+        cudaFree(h->rows);
+        if ((rc = fd_alloc(&h->rows, std::max(1LL, nrec * h->n_rec), errbuf, errlen))) return rc;
+        h->rows_cap = std::max(1LL, nrec * h->n_rec);
+    }
+    FdParams p = fd_params(h);
+    p.dt = dt;
+    p.dt2 = dt * dt;
+    p.damping = h->damp;
+    p.n_src = h->n_src;
+    p.src_idx = h->src;
+    p.src_val = h->srcv;
+    SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
+    for (int k = 1; k <= n_steps; ++k) {
+        p.u = h->U[h->cur];
+        p.out = h->U[h->cur ^ 1];  // holds level k-2, receives level k
+        p.f = h->n_src ? ftab[k - 1] : 0.0;
+        k_fdtd<0><<<h->grid, h->block, 0, h->stream>>>(p);
+        h->cur ^= 1;
+        const bool rec = (k % record_every) == 0 && h->n_rec > 0;
+        k_fd_finish<<<1, 1024, 0, h->stream>>>(h->part, h->nparts, h->norms, k - 1, h->U[h->cur], h->rec, h->n_rec,
+                                               rec ? h->rows + (k / record_every - 1) * h->n_rec : nullptr);
+    }
+    SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
+    if (norms_out) SFW_CUDA_TRY(cudaMemcpyAsync(norms_out, h->norms, n_steps * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (rows_out && nrec * h->n_rec)
+        SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, nrec * h->n_rec * 8, cudaMemcpyDeviceToHost, h->stream));
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SFW_CUDA_TRY(cudaGetLastError());
+    if (kernel_ms) cudaEventElapsedTime(kernel_ms, h->ev0, h->ev1);
+    return 0;
+}
+
+// current and previous level (HOST n each, either may be null)
+extern "C" int sfw_fdtd_state(sfw_fdtd* h, double* u_curr, double* u_prev, char* errbuf, int errlen) {
+    if (u_curr) SFW_CUDA_TRY(cudaMemcpy(u_curr, h->U[h->cur], h->n * 8, cudaMemcpyDeviceToHost));
+    if (u_prev) SFW_CUDA_TRY(cudaMemcpy(u_prev, h->U[h->cur ^ 1], h->n * 8, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+extern "C" int sfw_fdtd_destroy(sfw_fdtd* h) {
+    if (!h) return 0;
+    void* ptrs[] = {h->c, h->U[0], h->U[1], h->W, h->part, h->acc, h->norms, h->rows, h->src, h->srcv, h->rec, h->damp};
+    for (void* q : ptrs)
+        if (q) cudaFree(q);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return 0;
+}

@@ -224,3 +224,13 @@ def _stiffness_csr(shape, spacing, c_loc, am):
     mat = (dm @ k.tocsr() @ dm).tocsr()
     mat.sum_duplicates()
     return mat
+
+
+def assemble_global_operator(partition: DomainPartition, c_field: np.ndarray):
+    """Undivided operator ``C Lap_h C`` on the full grid, mirror closure (grid.py:461-467).
+
+    Returns a matrix-free :class:`~paper_1406_6923_b200.fdtd.FineGridOperator`
+    (``a @ x`` and the fine-grid solver run on the GPU) instead of a host CSR.
+    """
+    from .fdtd import FineGridOperator
+    return FineGridOperator(partition.global_shape, partition.spacing, c_field)

@@ -103,3 +103,20 @@ def test_m9k8_subdomain_build():
         assert rel(md.gammas, g["gammas"][i]) < 1e-9
         assert rel(md.gamma_hats, g["hats"][i]) < 1e-9
         assert rel(md.scales, g["scales"][i]) < 1e-9
+
+
+def test_oracle_fine_grid_solver_pinned():
+    """Oracle restatement of grid.py:461-467 + reference.py:26-157 vs the reference's own outputs."""
+    g = np.load(os.path.join(GOLD, "golden_fdtd.npz"))
+    wl = make_workload(1)
+    a = so.global_matrix(wl.global_shape, wl.spacing, wl.c_field)
+    x = np.random.default_rng(3).standard_normal(a.shape[0])
+    assert np.array_equal(a @ x, g["av"])
+    lam, _ = so.power_lambda(a)
+    assert lam == float(g["lam"])
+    src = int(g["src"])
+    vec = np.zeros(a.shape[0])
+    vec[src] = 1.0 / wl.c_field.ravel()[src]
+    s, t, up, u = so.leapfrog(a, float(g["dt"]), 200, source_vec=vec, source_fn=so.ricker(wl.f0, wl.delay),
+                              record_idx=g["rec"])
+    assert np.array_equal(s, g["samples"]) and np.array_equal(u, g["u_curr"]) and np.array_equal(up, g["u_prev"])
