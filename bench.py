@@ -559,6 +559,62 @@ def _run_shots(args, wl, models, ptrs, dt, lam, conv, probes, ws, rank, build_s,
     print(json.dumps(line), flush=True)
 
 
+def _run_fdtd(args):
+    """Fine-grid leapfrog reference solver on the config's full grid: node-steps/s."""
+    import torch
+    from paper_1406_6923_b200 import assemble_global_operator, run_leapfrog, stability_limit
+    from paper_1406_6923_b200 import grid as pg
+    from paper_1406_6923_b200.configs import make_workload
+    from paper_1406_6923_b200.pulses import ricker
+    wl = make_workload(args.config)
+    ext = tuple((g - 1) * h for g, h in zip(wl.global_shape, wl.spacing))
+    part = pg.build_partition(pg.DomainSpec(ext, wl.counts, wl.p))
+    a = assemble_global_operator(part, wl.c_field)
+    t0 = time.perf_counter()
+    dt = 0.9 * stability_limit(a)
+    cfl_s = time.perf_counter() - t0
+    src = int(np.ravel_multi_index(tuple(wl.sources[0]), part.global_shape))
+    vec = np.zeros(a.n)
+    vec[src] = 1.0 / wl.c_field.ravel()[src]
+    kw = dict(source_vec=vec, source_fn=ricker(wl.f0, wl.delay), record_idx=[src], chunk=max(args.steps, 1))
+    run_leapfrog(a, dt, max(args.warmup, 1), **kw)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    flush.fill_(1.0)
+    torch.cuda.synchronize()
+    K = args.steps
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        t0 = time.perf_counter()
+        run = run_leapfrog(a, dt, K, **kw)
+        wall = time.perf_counter() - t0
+    sec = run.kernel_ms * 1e-3
+    peak, peak_kind = _peaks()
+    alg = 32.0 * a.n  # u, c, u_prev read + u_next written once per node-step (fp64)
+    cpu = None
+    if not args.no_cpu:  # the reference algorithm (scipy CSR product + numpy leapfrog), bounded sample
+        from oracle import sfw_oracle as so
+        am = so.global_matrix(part.global_shape, part.spacing, wl.c_field)
+        n_cpu = 3
+        t0 = time.perf_counter()
+        so.leapfrog(am, dt, n_cpu, source_vec=vec, source_fn=so.ricker(wl.f0, wl.delay))
+        el = time.perf_counter() - t0
+        cpu = {"value": a.n * n_cpu / el, "unit": "node-steps/s", "cores": 1, "kind": "port",
+               "sample": f"{n_cpu} fine-grid leapfrog steps of {a.n} nodes incl. the start, {el:.1f} s "
+                         "(oracle restatement of reference.py run_leapfrog, scipy CSR)"}
+    line = {"metric": "fine-grid leapfrog node-steps/s (reference solver, fp64)", "value": a.n * K / sec,
+            "unit": "node-steps/s", "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * sec / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded medium, SURVEY 8d)",
+            "config": {"workload": f"fine grid of {_describe(wl)}", "nodes": a.n, "grid": list(part.global_shape),
+                       "dt": dt, "cfl_seconds": cfl_s, "l2": "flushed before the timed run; 2 x 136 MB state > L2"},
+            "e2e": {"value": a.n * K / wall, "unit": "node-steps/s", "h2d_bytes_per_step": 8,
+                    "d2h_bytes_per_step": 16, "api": "run_leapfrog(a, dt, K, source, receiver)"},
+            "roofline": {"bound": "hbm", "achieved": alg * K / sec / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg * K / sec / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
+                         "formula": "32 B per node-step (u, c, u_prev read once, u_next written once)"},
+            "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": 2 * K}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -570,7 +626,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extra", type=int, default=1, help="also measure config 3 kernel-only stepping (default on)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--fdtd", action="store_true", help="fine-grid reference solver on the config's full grid")
     args = ap.parse_args()
+    if args.fdtd:
+        return _run_fdtd(args)
     if args.impl == "reference":
         run_reference(args)
     else:

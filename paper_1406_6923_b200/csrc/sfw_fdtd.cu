@@ -14,10 +14,9 @@
 // trajectory is the reference's bit for bit (tests/test_fdtd_gpu.py).
 //
 // Layout: C-order (x, y, z), z fastest; fp64 c, and two time levels ping-ponged in place (level
-// k+1 overwrites level k-1 element-wise).  One thread per node, 32 (z) x 8 (y) blocks, one
-// x-plane per grid z-index: the y/z neighbours of a warp hit L1, the x neighbours (a plane
-// apart) hit L2, so HBM sees u, c, u_prev read once and u_next written once -- 32 B per
-// node-step, the kernel's roofline (HBM-bound: 13 flop per 32 B).
+// k+1 overwrites level k-1 element-wise).  HBM sees u, c, u_prev read once and u_next written
+// once -- 32 B per node-step, the kernel's roofline (HBM-bound: 13 flop per 32 B); see k_fdtd
+// for the 2.5-D blocking that gets there.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -44,71 +43,151 @@ struct FdParams {
     double* part;          // per-block partial sums: mode 0/1 |out|^2, mode 2 unused
 };
 
-__device__ __forceinline__ double fd_row(const FdParams& p, long long i, int x, int y, int z, double ui) {
-    const long long sx = (long long)p.ny * p.nz, sy = p.nz;
-    const double ci = __ldg(p.c + i);
-    const double cc = __dmul_rn(-ci, ci);
-    double diag = 0.0;
-    if (p.nx > 1) {
-        if (x + 1 < p.nx) diag = __dadd_rn(diag, __dmul_rn(cc, p.s0));
-        if (x > 0) diag = __dadd_rn(diag, __dmul_rn(cc, p.s0));
-    }
-    if (p.ny > 1) {
-        if (y + 1 < p.ny) diag = __dadd_rn(diag, __dmul_rn(cc, p.s1));
-        if (y > 0) diag = __dadd_rn(diag, __dmul_rn(cc, p.s1));
-    }
-    if (p.nz > 1) {
-        if (z + 1 < p.nz) diag = __dadd_rn(diag, __dmul_rn(cc, p.s2));
-        if (z > 0) diag = __dadd_rn(diag, __dmul_rn(cc, p.s2));
-    }
-    double sum = 0.0;
-    auto term = [&](long long j, double s) {
-        const double a = __dmul_rn(__dmul_rn(__ldg(p.c + j), ci), s);
-        sum = __dadd_rn(sum, __dmul_rn(a, __ldg(p.u + j)));
-    };
-    if (x > 0) term(i - sx, p.s0);
-    if (y > 0) term(i - sy, p.s1);
-    if (z > 0) term(i - 1, p.s2);
-    sum = __dadd_rn(sum, __dmul_rn(diag, ui));
-    if (z + 1 < p.nz) term(i + 1, p.s2);
-    if (y + 1 < p.ny) term(i + sy, p.s1);
-    if (x + 1 < p.nx) term(i + sx, p.s0);
-    return sum;
-}
+// 2.5-D blocking: a CTA owns a 32 (z) x 8 (y) column of XC consecutive x-planes.  The thread's
+// own node of planes x-1, x, x+1 lives in registers (u and c), the current plane's y/z halo in
+// shared memory, so HBM sees each u, c, u_prev once and L2 only the tile halos.  The row sum is
+// formed in the reference's order (x-, y-, z-, diag, z+, y+, x+) whatever the operands' source.
+constexpr int FD_XC = 16;
 
 template <int MODE>
 __global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
-    const int z = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y, x = blockIdx.z;
+    __shared__ double su[10][34], sc[10][34];
+    __shared__ double red[8];
+    const int tz = threadIdx.x, ty = threadIdx.y;
+    const int z = blockIdx.x * 32 + tz, y = blockIdx.y * 8 + ty;
+    const int x0 = blockIdx.z * FD_XC, x1 = min(p.nx, x0 + FD_XC);
+    const int sx = p.ny * p.nz, sy = p.nz;  // 32-bit offsets: grids up to 2^31 nodes (checked at create)
     const bool in = z < p.nz && y < p.ny;
-    double sq = 0.0;
+    const int col = y * p.nz + z;
+    // does this CTA's column hold a source node?  (block-uniform; the per-node test runs only there)
+    bool src_here = false;
+    for (int q = 0; q < p.n_src; ++q) {
+        const long long s = p.src_idx[q];
+        const int sxq = (int)(s / sx), rem = (int)(s % sx), syq = rem / p.nz, szq = rem % p.nz;
+        src_here |= sxq >= x0 && sxq < x1 && syq / 8 == (int)blockIdx.y && szq / 32 == (int)blockIdx.x;
+    }
+    // halo duty of this thread: row y-1 (ty == 0), row y+1 (ty == 7), column z-1 (tz == 0), z+1 (tz == 31)
+    const int hy = (ty == 0 && y > 0) ? -1 : (ty == 7 && y + 1 < p.ny) ? 1 : 0;
+    const int hz = (tz == 0 && z > 0) ? -1 : (tz == 31 && z + 1 < p.nz) ? 1 : 0;
+    // software pipeline, two planes deep: centre (u, c) of x+1 and x+2, halos and u_prev of x+1
+    auto ld = [&](const double* a, int i) { return __ldg(a + i); };
+    double um = 0.0, uc = 0.0, up = 0.0, u2 = 0.0, cm = 0.0, cc = 0.0, cp = 0.0, c2 = 0.0;
+    double hyu = 0.0, hyc = 0.0, hzu = 0.0, hzc = 0.0, prv = 0.0, vel = 0.0;
     if (in) {
-        const long long i = ((long long)x * p.ny + y) * p.nz + z;
-        const double ui = __ldg(p.u + i);
-        double acc = fd_row(p, i, x, y, z, ui);
-        if (MODE == 2) {
-            p.out[i] = -acc;
-        } else {
-            for (int q = 0; q < p.n_src; ++q)  // acc + f(t) * source_vec (reference.py:117-121)
-                if (p.src_idx[q] == i) acc = __dadd_rn(acc, __dmul_rn(p.f, p.src_val[q]));
-            double v;
-            if (MODE == 0) {  // 2 u - u_prev + (dt*dt) acc   (reference.py:131)
-                v = __dadd_rn(__dsub_rn(__dmul_rn(2.0, ui), p.out[i]), __dmul_rn(p.dt2, acc));
-                if (p.damping) v = __dmul_rn(v, p.damping[i]);
-            } else {          // u - dt v + (0.5 dt dt) acc   (reference.py:124)
-                const double vv = p.vel ? __dmul_rn(p.dt, p.vel[i]) : 0.0;
-                v = __dadd_rn(__dsub_rn(ui, vv), __dmul_rn(p.half, acc));
-            }
-            p.out[i] = v;
-            sq = v * v;
+        const int i0 = x0 * sx + col;
+        if (x0 > 0) {
+            um = ld(p.u, i0 - sx);
+            cm = ld(p.c, i0 - sx);
         }
+        uc = ld(p.u, i0);
+        cc = ld(p.c, i0);
+        if (x0 + 1 < p.nx) {
+            up = ld(p.u, i0 + sx);
+            cp = ld(p.c, i0 + sx);
+        }
+        if (hy) {
+            hyu = ld(p.u, i0 + hy * sy);
+            hyc = ld(p.c, i0 + hy * sy);
+        }
+        if (hz) {
+            hzu = ld(p.u, i0 + hz);
+            hzc = ld(p.c, i0 + hz);
+        }
+        if (MODE == 0) prv = p.out[i0];
+        if (MODE == 1 && p.vel) vel = p.vel[i0];
+    }
+    double sq = 0.0;
+    for (int x = x0; x < x1; ++x) {
+        const int i = x * sx + col;
+        // current plane into shared memory (centre + halo)
+        su[ty + 1][tz + 1] = uc;
+        sc[ty + 1][tz + 1] = cc;
+        if (hy) {
+            su[ty + 1 + hy][tz + 1] = hyu;
+            sc[ty + 1 + hy][tz + 1] = hyc;
+        }
+        if (hz) {
+            su[ty + 1][tz + 1 + hz] = hzu;
+            sc[ty + 1][tz + 1 + hz] = hzc;
+        }
+        const double prev = prv, v0 = vel;
+        // next loads: plane x+2 centre, plane x+1 halos and u_prev
+        if (in) {
+            if (x + 2 < p.nx) {
+                u2 = ld(p.u, i + 2 * sx);
+                c2 = ld(p.c, i + 2 * sx);
+            }
+            if (x + 1 < x1) {
+                if (hy) {
+                    hyu = ld(p.u, i + sx + hy * sy);
+                    hyc = ld(p.c, i + sx + hy * sy);
+                }
+                if (hz) {
+                    hzu = ld(p.u, i + sx + hz);
+                    hzc = ld(p.c, i + sx + hz);
+                }
+                if (MODE == 0) prv = p.out[i + sx];
+                if (MODE == 1 && p.vel) vel = p.vel[i + sx];
+            }
+        }
+        __syncthreads();
+        if (in) {
+            const double ci = cc, ui = uc;
+            const double cn = __dmul_rn(-ci, ci);
+            double diag = 0.0;  // np.add.at order: x lower/upper end, y, z
+            if (p.nx > 1) {
+                if (x + 1 < p.nx) diag = __dadd_rn(diag, __dmul_rn(cn, p.s0));
+                if (x > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s0));
+            }
+            if (p.ny > 1) {
+                if (y + 1 < p.ny) diag = __dadd_rn(diag, __dmul_rn(cn, p.s1));
+                if (y > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s1));
+            }
+            if (p.nz > 1) {
+                if (z + 1 < p.nz) diag = __dadd_rn(diag, __dmul_rn(cn, p.s2));
+                if (z > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s2));
+            }
+            double acc = 0.0;
+            auto term = [&](double cj, double uj, double s) {
+                acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(cj, ci), s), uj));
+            };
+            if (x > 0) term(cm, um, p.s0);
+            if (y > 0) term(sc[ty][tz + 1], su[ty][tz + 1], p.s1);
+            if (z > 0) term(sc[ty + 1][tz], su[ty + 1][tz], p.s2);
+            acc = __dadd_rn(acc, __dmul_rn(diag, ui));
+            if (z + 1 < p.nz) term(sc[ty + 1][tz + 2], su[ty + 1][tz + 2], p.s2);
+            if (y + 1 < p.ny) term(sc[ty + 2][tz + 1], su[ty + 2][tz + 1], p.s1);
+            if (x + 1 < p.nx) term(cp, up, p.s0);
+            if (MODE == 2) {
+                p.out[i] = -acc;
+            } else {
+                if (src_here)  // acc + f(t) * source_vec (reference.py:117-121)
+                    for (int q = 0; q < p.n_src; ++q)
+                        if (p.src_idx[q] == i) acc = __dadd_rn(acc, __dmul_rn(p.f, p.src_val[q]));
+                double v;
+                if (MODE == 0) {  // 2 u - u_prev + (dt*dt) acc   (reference.py:131)
+                    v = __dadd_rn(__dsub_rn(__dmul_rn(2.0, ui), prev), __dmul_rn(p.dt2, acc));
+                    if (p.damping) v = __dmul_rn(v, p.damping[i]);
+                } else {          // u - dt v + (0.5 dt dt) acc   (reference.py:124)
+                    v = __dadd_rn(__dsub_rn(ui, __dmul_rn(p.dt, v0)), __dmul_rn(p.half, acc));
+                }
+                p.out[i] = v;
+                sq = fma(v, v, sq);
+            }
+        }
+        __syncthreads();
+        um = uc;
+        cm = cc;
+        uc = up;
+        cc = cp;
+        up = u2;
+        cp = c2;
     }
     if (MODE != 2) {  // fixed-order block partial of |out|^2 (deterministic)
-        __shared__ double red[8];
         const double w = warp_sum(sq);
-        const int wid = threadIdx.y, lane = threadIdx.x;
-        if (lane == 0) red[wid] = w;
+        if (tz == 0) red[ty] = w;
         __syncthreads();
-        if (wid == 0 && lane == 0) {
+        if (ty == 0 && tz == 0) {
             double t = 0.0;
             for (int k = 0; k < 8; ++k) t += red[k];
             p.part[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
@@ -163,14 +242,27 @@ __global__ void k_fd_dots(const double* __restrict__ v, const double* __restrict
 }
 
 __global__ void k_fd_dots_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int k = 0; k < nb; ++k) {
-            a += part[2 * k];
-            b += part[2 * k + 1];
+    __shared__ double ra[32], rb[32];
+    double a = 0.0, b = 0.0;
+    for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+        a += part[2 * k];
+        b += part[2 * k + 1];
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if ((threadIdx.x & 31) == 0) {
+        ra[threadIdx.x >> 5] = a;
+        rb[threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sa = 0.0, sb = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            sa += ra[w];
+            sb += rb[w];
         }
-        out[0] = a;
-        out[1] = b;
+        out[0] = sa;
+        out[1] = sb;
     }
 }
 
@@ -233,6 +325,8 @@ extern "C" int sfw_fdtd_create(int nx, int ny, int nz, const double* scales, con
                                char* errbuf, int errlen) {
     *out = nullptr;
     if (nx < 1 || ny < 1 || nz < 1) return fail(SFW_ECONFIG, "grid dimensions must be positive", errbuf, errlen);
+    if ((long long)nx * ny * nz >= (1LL << 31))
+        return fail(SFW_ECONFIG, "fine grids are limited to 2^31 nodes (32-bit stencil offsets)", errbuf, errlen);
     auto* h = new sfw_fdtd();
     h->nx = nx;
     h->ny = ny;
@@ -240,7 +334,7 @@ extern "C" int sfw_fdtd_create(int nx, int ny, int nz, const double* scales, con
     h->n = (long long)nx * ny * nz;
     for (int d = 0; d < 3; ++d) h->s[d] = scales[d];
     h->block = dim3(32, 8, 1);
-    h->grid = dim3((nz + 31) / 32, (ny + 7) / 8, nx);
+    h->grid = dim3((nz + 31) / 32, (ny + 7) / 8, (nx + FD_XC - 1) / FD_XC);
     h->nparts = (long long)h->grid.x * h->grid.y * h->grid.z;
     int rc = 0;
     if ((rc = fd_alloc(&h->c, h->n, errbuf, errlen)) || (rc = fd_alloc(&h->U[0], h->n, errbuf, errlen)) ||
@@ -288,7 +382,7 @@ extern "C" int sfw_fdtd_power(sfw_fdtd* h, const double* v0, double tol, int max
         p.out = w;
         k_fdtd<2><<<h->grid, h->block, 0, h->stream>>>(p);
         k_fd_dots<<<nb, 256, 0, h->stream>>>(v, w, h->n, h->part);
-        k_fd_dots_final<<<1, 32, 0, h->stream>>>(h->part, nb, h->acc);
+        k_fd_dots_final<<<1, 1024, 0, h->stream>>>(h->part, nb, h->acc);
         SFW_CUDA_TRY(cudaMemcpyAsync(res, h->acc, 16, cudaMemcpyDeviceToHost, h->stream));
         SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
         const double nw = std::sqrt(res[1]);
