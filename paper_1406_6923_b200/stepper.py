@@ -364,9 +364,24 @@ class CoupledStepper:
     def _profiles(self, t_values) -> np.ndarray:
         tab = np.empty((len(self.sources), len(t_values)))
         for i, s in enumerate(self.sources):
-            for k, t in enumerate(t_values):
-                tab[i, k] = float(s.profile(t))
+            tab[i] = [float(v) for v in map(s.profile, t_values)]
         return np.ascontiguousarray(tab)
+
+    def _limits(self, prof, norms_of_sources, n_steps):
+        """Growth-detector thresholds of the next n_steps and the final baseline (stepper.py:379-389).
+
+        The baseline gains dt*dt*|f_i(t_k)|*|src_i| per source and step, added in the
+        reference's order (step-major, source-minor); np.add.accumulate is a sequential
+        left-to-right sum, so the thresholds equal the reference's scalar loop bit for bit.
+        """
+        dt = self.dt
+        if prof is None or not len(self.sources):
+            base = np.full(n_steps, self._baseline)
+        else:
+            inc = (dt * dt * np.abs(prof.T)) * np.asarray(norms_of_sources, dtype=float)[None, :]  # (k, i)
+            seq = np.concatenate([[self._baseline], inc.reshape(-1)])
+            base = np.add.accumulate(seq)[len(self.sources)::len(self.sources)]
+        return GROWTH_LIMIT * np.maximum(base, 1e-300), float(base[-1]) if n_steps else self._baseline
 
     # -- integration -------------------------------------------------------------
 
@@ -400,12 +415,7 @@ class CoupledStepper:
         dt = self.dt
         t_vals = [(self.steps_done + k) * dt for k in range(n_steps)]
         prof = self._profiles(t_vals) if self.sources else None
-        limits = np.empty(n_steps)
-        base = self._baseline
-        for k, t in enumerate(t_vals):
-            for i, s in enumerate(self.sources):
-                base += dt * dt * abs(float(prof[i, k])) * self._src_norms[i]
-            limits[k] = GROWTH_LIMIT * max(base, 1e-300)
+        limits, base = self._limits(prof, self._src_norms, n_steps)
         n_rec = n_steps // record_every
         rows = np.empty((max(1, n_rec), max(1, len(self._probes))))
         norms = np.empty(n_steps)
@@ -413,11 +423,7 @@ class CoupledStepper:
         eb = _lib.errbuf()
         if self.precision == "fp32":
             # W-form: |W| against the same detector rule with W-form source norms
-            base = self._baseline
-            for k in range(n_steps):
-                for i in range(len(self.sources)):
-                    base += dt * dt * abs(float(prof[i, k])) * self._src_norms_w[i]
-                limits[k] = GROWTH_LIMIT * max(base, 1e-300)
+            limits, base = self._limits(prof, self._src_norms_w, n_steps)
             ms = C.c_float(0.0)
             rc = self._lib.sfw_wform_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(rows),
                                          _lib.dptr(norms), C.byref(ms), eb, 1024)

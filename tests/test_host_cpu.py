@@ -119,3 +119,23 @@ def test_product_path_fails_loudly_without_gpu():
         CoupledStepper(models, 0.01)
     with pytest.raises(DeviceError):
         project_source(models[sorted(models)[0]], 31)
+
+
+def test_growth_limits_match_the_scalar_loop():
+    """CoupledStepper._limits (vectorised) == the reference's per-step baseline loop (stepper.py:379-389)."""
+    import types
+
+    from paper_1406_6923_b200.stepper import GROWTH_LIMIT, CoupledStepper
+    rng = np.random.default_rng(4)
+    for n_src, n in ((1, 500), (3, 77), (0, 5)):
+        fake = types.SimpleNamespace(dt=0.0013, sources=[object()] * n_src, _baseline=float(rng.random()))
+        prof = rng.standard_normal((n_src, n)) if n_src else None
+        norms = rng.random(n_src) * 3
+        lim, base = CoupledStepper._limits(fake, prof, norms, n)
+        b = fake._baseline
+        ref = []
+        for k in range(n):
+            for i in range(n_src):
+                b += fake.dt * fake.dt * abs(float(prof[i, k])) * norms[i]
+            ref.append(GROWTH_LIMIT * max(b, 1e-300))
+        assert np.array_equal(lim, np.array(ref)) and base == b
