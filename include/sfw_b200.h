@@ -231,6 +231,19 @@ int sfw_fdtd_run(sfw_fdtd* h, double dt, int n_steps, const double* ftab, int re
 int sfw_fdtd_state(sfw_fdtd* h, double* u_curr, double* u_prev, char* errbuf, int errlen);
 int sfw_fdtd_destroy(sfw_fdtd* h);
 
+/* ------------------------------------------------------------------------- */
+/* Batched reduced transfer maps (ntd.py:101-185, sim.py:703-768 cross-check). */
+/* ------------------------------------------------------------------------- */
+
+/* form 0 = ntd_tridiag(diag A, off B, entry E, omega); form 1 = ntd_chain(gammas A,
+ * gamma_hats B, omega).  A: [n_models][L][w][w]; B: [n_models][L-1][w][w] (form 0)
+ * or [n_models][L][w][w] (form 1); E: [n_models][w][w] (form 0).  One item per
+ * (item_model[i], item_omega[i]); out [n_items][w][w] symmetrised maps; status[i]
+ * 0 = ok, 2 = singular (the reference raises NumericalError).  HOST arrays. */
+int sfw_ntd_batch(int form, int n_models, int L, int w, const double* A, const double* B, const double* E,
+                  int n_items, const int* item_model, const double* item_omega, double* out, int* status,
+                  char* errbuf, int errlen);
+
 #ifdef __cplusplus
 }
 #endif

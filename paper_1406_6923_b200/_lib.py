@@ -73,6 +73,8 @@ SIGNATURES = {
     "sfw_fdtd_run": (C.c_int, [C.c_void_p, C.c_double, C.c_int, PD, C.c_int, PD, PD, PF, C.c_char_p, C.c_int]),
     "sfw_fdtd_state": (C.c_int, [C.c_void_p, PD, PD, C.c_char_p, C.c_int]),
     "sfw_fdtd_destroy": (C.c_int, [C.c_void_p]),
+    "sfw_ntd_batch": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, PD, PD, PD, C.c_int, PI, PD, PD, PI, C.c_char_p,
+                                C.c_int]),
 }
 
 _lib = None

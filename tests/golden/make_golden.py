@@ -239,8 +239,25 @@ def golden_fdtd():
     print("golden_fdtd.npz", lam, dt, run.samples.shape)
 
 
+def golden_ntd():
+    """Reference ntd_tridiag / ntd_chain of the config-1 and m9k8 golden models over a frequency band."""
+    from sfwave.ntd import ntd_chain, ntd_tridiag
+    out = {}
+    for tag, name in (("c1", "golden_c1.npz"), ("m9", "golden_m9k8.npz")):
+        g = np.load(os.path.join(HERE, name))
+        omegas = np.geomspace(20.0, 400.0, 5)
+        tri = np.stack([[ntd_tridiag(list(g["tdiag"][i]), list(g["toff"][i]), g["entry"][i], w) for w in omegas]
+                        for i in range(len(g["tdiag"]))])
+        chn = np.stack([[ntd_chain(g["gammas"][i], g["hats"][i], w) for w in omegas] for i in range(len(g["gammas"]))])
+        out[tag + "_omegas"] = omegas
+        out[tag + "_tridiag"] = tri
+        out[tag + "_chain"] = chn
+        print(tag, "tridiag vs chain", float(np.max(np.abs(tri - chn)) / np.max(np.abs(tri))))
+    np.savez_compressed(os.path.join(HERE, "golden_ntd.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["toy", "c1", "m9k8", "io", "fdtd"]
+    which = sys.argv[1:] or ["toy", "c1", "m9k8", "io", "fdtd", "ntd"]
     if "toy" in which:
         golden_toy()
     if "c1" in which:
@@ -251,3 +268,5 @@ if __name__ == "__main__":
         golden_io()
     if "fdtd" in which:
         golden_fdtd()
+    if "ntd" in which:
+        golden_ntd()
