@@ -1,0 +1,148 @@
+"""Full-size BASELINE workloads (configs 2, 3, 4) checked through size-independent properties.
+
+At these sizes a reference run of the whole workload takes minutes to hours on the host, so the
+checks are the ones whose truth does not depend on size (task tier 3): bitwise run-to-run
+determinism and bitwise shared-face replicas (reference test_stepper.py:185-194, 308-322),
+short trace windows against the CPU oracle on the same GPU-built coefficients (tolerance as in
+SURVEY 8c: 1e-9, or 10x the oracle's own summation-order floor at m9k8), fp32 W-form vs fp64
+(<= 1e-4, north_star), discrete-energy conservation of a source-free run (reference criterion
+4), and every one of 32 shots equal to its own single-source run (config 4).
+"""
+
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+
+from helpers import face_probes, rel
+from oracle import sfw_oracle as so
+from paper_1406_6923_b200 import (CoupledStepper, Probe, SourceTerm, build_models, cfl_estimate_coupled,
+                                  project_source)
+from paper_1406_6923_b200 import grid as pg
+from paper_1406_6923_b200.configs import locate, make_workload
+from paper_1406_6923_b200.pulses import ricker
+
+pytestmark = pytest.mark.gpu
+
+
+def _build(cfg, extra_sources=()):
+    wl = make_workload(cfg)
+    ext = tuple((g - 1) * h for g, h in zip(wl.global_shape, wl.spacing))
+    part = pg.build_partition(pg.DomainSpec(ext, wl.counts, wl.p))
+    ops = [pg.assemble_subdomain_operator(part, a, wl.c_field) for a in sorted(s.alpha for s in part.subdomains)]
+    sa, sr = locate(wl.sources[0], wl.counts, wl.p)
+    rows = {sa: [sr]}
+    for ijk in list(wl.sources[1:]) + list(extra_sources):
+        a, r = locate(ijk, wl.counts, wl.p)
+        rows.setdefault(a, []).append(r)
+    models = build_models(ops, wl.modes_per_face, wl.n, wl.shift, rows=rows)
+    lam, conv = cfl_estimate_coupled(models)
+    assert conv
+    dt = 0.9 * 2.0 / math.sqrt(lam)
+    src = SourceTerm(sa, project_source(models[sa], sr), ricker(wl.f0, wl.delay))
+    probes = [Probe(a, w) for a, w in face_probes(models, wl)]
+    return wl, models, dt, src, probes
+
+
+def _oracle_models(models):
+    return {a: so.Model(alpha=a, lo=None, shape=None, spacing=None, modes_per_face=m.modes_per_face,
+                        layers=m.layers, shift=m.shift, neighbors=m.neighbors, face_indices=(), gammas=m.gammas,
+                        gamma_hats=m.gamma_hats, scales=m.scales, basis=None, c=m.c, mu=m.mu)
+            for a, m in models.items()}
+
+
+def _replicas_equal(st, models):
+    u = st.u_curr
+    for a, md in models.items():
+        for f, b in md.neighbors.items():
+            if not np.array_equal(u[a][md.face_slice(f)], u[b][models[b].face_slice(f ^ 1)]):
+                return False
+    return True
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    return _build(2)
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    return _build(3, extra_sources=make_workload(4).sources)  # config 4 = config 3 models + 32 shots
+
+
+def _check(wl, models, dt, src, probes, n_det, n_oracle, n_fp32, oracle_floor):
+    with CoupledStepper(models, dt, sources=(src,)) as st:
+        _, r1 = st.run(n_det, probes=probes)
+        assert _replicas_equal(st, models)
+        _, r2 = st.run(n_det, probes=probes)
+    assert np.array_equal(r1, r2), "run-to-run determinism"
+    om = _oracle_models(models)
+    osrc = [(src.alpha, src.vector, src.profile)]
+    oprobes = [(p.alpha, p.weights) for p in probes]
+    ref = so.Coupled(om, dt, sources=osrc).run(n_oracle, probes=oprobes)[1]
+    tol = 1e-9
+    if oracle_floor:
+        fm = {a: dataclasses.replace(m, gammas=[np.asfortranarray(b) for b in m.gammas],
+                                     gamma_hats=[np.asfortranarray(b) for b in m.gamma_hats]) for a, m in om.items()}
+        alt = so.Coupled(fm, dt, sources=osrc).run(n_oracle, probes=oprobes)[1]
+        tol = max(tol, 10 * rel(alt, ref))
+    err = rel(r1[:n_oracle + 1], ref)
+    print(f"{wl.name}: traces vs oracle ({n_oracle} steps) {err:.2e} (tol {tol:.1e})")
+    assert err <= tol
+    with CoupledStepper(models, dt, sources=(src,), precision="fp32") as st32:
+        _, r32 = st32.run(n_fp32, probes=probes)
+    e32 = rel(r32, r1[:n_fp32 + 1])
+    print(f"{wl.name}: fp32 W-form vs fp64 ({n_fp32} steps) {e32:.2e}")
+    assert e32 <= 1e-4
+
+
+def test_config2_full_size(cfg2):
+    wl, models, dt, src, probes = cfg2
+    assert len(models) == 512
+    _check(wl, models, dt, src, probes, n_det=400, n_oracle=60, n_fp32=400, oracle_floor=False)
+
+
+def test_config3_full_size(cfg3):
+    wl, models, dt, src, probes = cfg3
+    assert len(models) == 4096
+    _check(wl, models, dt, src, probes, n_det=200, n_oracle=6, n_fp32=200, oracle_floor=True)
+
+
+def test_config3_energy_conserved_without_source(cfg3):
+    wl, models, dt, _, _ = cfg3
+    rng = np.random.default_rng(9)
+    u0 = {a: rng.standard_normal(m.state_size) * 1e-3 for a, m in models.items()}
+    for a, m in models.items():  # shared-face replicas must agree initially
+        for f, b in m.neighbors.items():
+            if b > a:
+                u0[b][models[b].face_slice(f ^ 1)] = u0[a][m.face_slice(f)]
+    with CoupledStepper(models, dt) as st:
+        st.run(1, u0=u0)
+        e0 = st.energy()
+        st.run(400, u0=u0)
+        e1 = st.energy()
+    print(f"config3 energy drift over 400 steps {abs(e1 - e0) / abs(e0):.2e}")
+    assert abs(e1 - e0) <= 1e-6 * abs(e0)  # reference acceptance criterion 4 (test_acceptance.py:242-284)
+
+
+def test_config4_full_size_shots(cfg3):
+    _, models, dt, _, probes = cfg3
+    wl = make_workload(4)
+    shots = []
+    for ijk in wl.sources:
+        a, r = locate(ijk, wl.counts, wl.p)
+        shots.append(SourceTerm(a, project_source(models[a], r), ricker(wl.f0, wl.delay)))
+    assert len(shots) == 32
+    n = 30
+    with CoupledStepper(models, dt) as st:
+        times, rows = st.run_shots(n, shots, probes=probes)
+        _, rows2 = st.run_shots(n, shots, probes=probes)
+    assert np.array_equal(rows, rows2)
+    for q in (0, 13, 31):
+        with CoupledStepper(models, dt, sources=(shots[q],)) as st1:
+            t1, r1 = st1.run(n, probes=probes)
+        assert np.array_equal(times, t1)
+        e = rel(rows[:, q, :], r1)
+        print(f"config4 shot {q} vs single-source run {e:.2e}")
+        assert e <= 1e-10
