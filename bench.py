@@ -392,50 +392,110 @@ def run_ours(args):
     st.close()
     if args.extra and args.config == 2:
         try:
-            line["extra"] = _extra_config3(args)
+            line["extra"] = _extra_configs(args)
         except Exception as exc:  # the headline line must still print
-            line["extra"] = {"config3": {"error": str(exc)[:200]}}
+            line["extra"] = {"error": str(exc)[:300]}
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
 
 
-def _extra_config3(args):
-    """Kernel-only stepping of config 3 (4096 x m9k8, the HBM-bound case) for the roofline picture."""
+def _extra_configs(args):
+    """Kernel-only stepping of the other BASELINE configs (device-timed, L2 flushed), so the default
+    bench line carries every config: 3 (fp64 U-form and fp32 W-form), 4 (32 shots, DMMA) and 5
+    (fp64 and fp32).  Each entry: ms/step, subdomain-steps/s, roofline fraction, ROM build time."""
     import ctypes as C
 
     import torch
-    from paper_1406_6923_b200 import CoupledStepper, _lib, build_models, cfl_estimate_coupled
-    wl, ops, alphas, _, _ = _workload(3)
-    n_sub, w, L = len(ops), wl.width, wl.layers
-    dev = [torch.empty(n_sub * L * w * w, dtype=torch.float64, device="cuda") for _ in range(3)]
-    ptrs = tuple(t.data_ptr() for t in dev)
-    t0 = time.perf_counter()
-    models = build_models(ops, wl.modes_per_face, wl.n, wl.shift, device_out=ptrs)
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t0
-    lam, conv = cfl_estimate_coupled(models, device_coefficients=ptrs)
-    dt = 0.9 * 2.0 / math.sqrt(lam)
-    st = CoupledStepper(models, dt, device_coefficients=ptrs)
-    st.initialize()
-    ms = C.c_float(0.0)
-    eb = _lib.errbuf()
-    _lib.check(st._lib.sfw_step_run_resident(st._h, 5, 1, None, C.byref(ms), eb, 1024), eb)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    flush.fill_(1.0)
-    torch.cuda.synchronize()
-    K3 = 300
-    _lib.check(st._lib.sfw_step_run_resident(st._h, K3, 1, None, C.byref(ms), eb, 1024), eb)
-    b, f, sb = st.traffic()
-    st.close()
+    from paper_1406_6923_b200 import CoupledStepper, SourceTerm, _lib, build_models, cfl_estimate_coupled
+    from paper_1406_6923_b200 import project_source
+    from paper_1406_6923_b200.configs import locate, make_workload
+    from paper_1406_6923_b200.pulses import ricker
     peak, _ = _peaks()
-    sec = ms.value * 1e-3
-    return {"config3": {"workload": _describe(wl), "subdomains": n_sub, "steps": K3, "ms_per_step": ms.value / K3,
-                        "value": n_sub * K3 / sec, "unit": UNIT,
-                        "roofline": {"bound": "hbm", "achieved": b * K3 / sec / 1e9, "peak": peak, "unit": "GB/s",
-                                     "frac": b * K3 / sec / 1e9 / peak},
-                        "rom_build_seconds": build_s, "rom_build_subdomains_per_s": n_sub / build_s,
-                        "cfl_converged": conv}}
+    fpk, _ = _fp64_peak()
+    out = {}
+
+    def flush():
+        buf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+        buf.fill_(1.0)
+        torch.cuda.synchronize()
+
+    for cfg in (3, 5):
+        wl, ops, alphas, (sa, sr), _ = _workload(cfg)
+        n_sub, w, L = len(ops), wl.width, wl.layers
+        rows = {sa: [sr]}
+        if cfg == 3:  # config 4 = config 3 models + 32 shot sources
+            for ijk in make_workload(4).sources:
+                a, r = locate(ijk, wl.counts, wl.p)
+                rows.setdefault(a, []).append(r)
+        dev = [torch.empty(n_sub * L * w * w, dtype=torch.float64, device="cuda") for _ in range(3)]
+        ptrs = tuple(t.data_ptr() for t in dev)
+        t0 = time.perf_counter()
+        models = build_models(ops, wl.modes_per_face, wl.n, wl.shift, rows=rows, device_out=ptrs)
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
+        scl = dev[2].view(n_sub, L, w, w)
+        idx = {a: i for i, a in enumerate(alphas)}
+        for a in rows:
+            models[a].scales = scl[idx[a]].cpu().numpy()
+        lam, conv = cfl_estimate_coupled(models, device_coefficients=ptrs)
+        dt = 0.9 * 2.0 / math.sqrt(lam)
+        src = SourceTerm(sa, project_source(models[sa], sr), ricker(wl.f0, wl.delay))
+        K = 300 if cfg == 3 else 150
+        # fp64 U-form, one persistent launch
+        st = CoupledStepper(models, dt, sources=(src,), device_coefficients=ptrs)
+        st.initialize()
+        ms = C.c_float(0.0)
+        eb = _lib.errbuf()
+        _lib.check(st._lib.sfw_step_run_resident(st._h, 5, 1, None, C.byref(ms), eb, 1024), eb)
+        flush()
+        _lib.check(st._lib.sfw_step_run_resident(st._h, K, 1, None, C.byref(ms), eb, 1024), eb)
+        b, _f, _s = st.traffic()
+        st.close()
+        sec = ms.value * 1e-3
+        out[f"config{cfg}"] = {"workload": _describe(wl), "subdomains": n_sub, "steps": K, "ms_per_step": ms.value / K,
+                               "value": n_sub * K / sec, "unit": UNIT, "dtype": "f64",
+                               "roofline": {"bound": "hbm", "frac": b * K / sec / 1e9 / peak,
+                                            "achieved": b * K / sec / 1e9, "peak": peak, "unit": "GB/s"},
+                               "rom_build_seconds": build_s, "cfl_converged": conv}
+        # fp32 W-form
+        st = CoupledStepper(models, dt, sources=(src,), device_coefficients=ptrs, precision="fp32")
+        st.run(5)
+        flush()
+        st.run(K)
+        bb, sb = C.c_double(), C.c_double()
+        st._lib.sfw_wform_traffic(st._h, C.byref(bb), C.byref(sb))
+        sec = st.last_kernel_ms * 1e-3
+        st.close()
+        out[f"config{cfg}_fp32"] = {"workload": _describe(wl) + ", fp32 W-form", "steps": K,
+                                    "ms_per_step": 1e3 * sec / K, "value": n_sub * K / sec, "unit": UNIT,
+                                    "dtype": "f32", "roofline": {"bound": "hbm", "frac": bb.value * K / sec / 1e9 / peak,
+                                                                 "achieved": bb.value * K / sec / 1e9, "peak": peak,
+                                                                 "unit": "GB/s"}}
+        if cfg == 3:  # config 4: 32 independent shots on the DMMA path
+            wl4 = make_workload(4)
+            shots = []
+            for ijk in wl4.sources:
+                a, r = locate(ijk, wl4.counts, wl4.p)
+                shots.append(SourceTerm(a, project_source(models[a], r), ricker(wl4.f0, wl4.delay)))
+            K4 = 20
+            st = CoupledStepper(models, dt, device_coefficients=ptrs)
+            st.run_shots(3, shots)
+            flush()
+            st.run_shots(K4, shots)
+            ab, af, _ = st.shots_traffic()
+            sec = st.last_kernel_ms * 1e-3
+            st.close()
+            t_hbm, t_fp = ab / (peak * 1e9), af / (fpk * 1e12)
+            out["config4"] = {"workload": _describe(wl4) + ", S=32 shots", "steps": K4, "ms_per_step": 1e3 * sec / K4,
+                              "value": n_sub * K4 / sec, "unit": UNIT, "shot_steps_per_s": 32 * n_sub * K4 / sec,
+                              "dtype": "f64", "achieved_tflops": af * K4 / sec / 1e12,
+                              "roofline": {"bound": "hbm" if t_hbm >= t_fp else "fp64",
+                                           "frac": max(t_hbm, t_fp) * K4 / sec,
+                                           "roofline_us_per_step": {"hbm": 1e6 * t_hbm, "fp64": 1e6 * t_fp}}}
+        del models, dev
+        torch.cuda.empty_cache()
+    return out
 
 
 def _run_fp32(args, wl, models, ptrs, dt, lam, conv, src, probes, ws, rank, build_s, build_stats, cfl_s, cfl_iters):
@@ -624,7 +684,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--extra", type=int, default=1, help="also measure config 3 kernel-only stepping (default on)")
+    ap.add_argument("--extra", type=int, default=1,
+                    help="also measure configs 3, 4, 5 (fp64 and fp32) kernel-only stepping (default on)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--fdtd", action="store_true", help="fine-grid reference solver on the config's full grid")
     args = ap.parse_args()
