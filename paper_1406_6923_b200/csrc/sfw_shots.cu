@@ -1134,7 +1134,8 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
     double* cst = reinterpret_cast<double*>(smem_raw);              // [NG][NS][TB]
     double* Tall = cst + (size_t)NG * NSTG * TB;                // [NCW][W][8] face sums (phase C)
     double* Sall = Tall + (size_t)(4 * NG) * W * 8;                  // [NCW][2][2 RT][32] staged state rows
-    uint64_t* full = reinterpret_cast<uint64_t*>(Sall + (size_t)(4 * NG) * 2 * 2 * RT * 32);
+    double* Mall = Sall + (size_t)(4 * NG) * 2 * 2 * RT * 32;         // [NCW][6 M M] interface mass of the next coupling
+    uint64_t* full = reinterpret_cast<uint64_t*>(Mall + (size_t)(4 * NG) * 6 * M * M);
     uint64_t* empty = full + NG * NSTG;
     int* s_out = reinterpret_cast<int*>(empty + NG * NSTG);     // [ns] subdomain has an outer face
     const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
@@ -1182,6 +1183,15 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
                                  : "memory");
             }
     };
+    // interface mass blocks of a subdomain -> this warp's SMEM copy (cp.async, 16 B per lane-op)
+    double* Mw = Mall + (size_t)warp * 6 * M * M;
+    auto stage_mass = [&](int sl) {
+        const double* src = p.mblk + (size_t)(s0 + sl) * 6 * M * M;
+        for (int i = lane; i < 3 * M * M; i += 32)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(Mw + 2 * i)), "l"(src + 2 * i)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     auto read_rows = [&](const double* src, double (&v)[RT][2]) {
 #pragma unroll
         for (int I = 0; I < RT; ++I)
@@ -1225,12 +1235,18 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
         }
     };
     if (c == 0) try_issue();
+    // optional cycle accounting (p.dbg, SFW_STEP_PROF): [acquire wait, gemm, coupling, total]
+    const bool prof = p.dbg != nullptr;
+    long long clk_acq = 0, clk_gemm = 0, clk_coup = 0, clk_wait = 0, clk_f0 = 0;
+    const long long clk_start = prof ? clock64() : 0;
     auto acquire = [&]() -> const double* {
         const int st = (int)(con % NSTG);
         uint64_t* fb = &full[g * NSTG + st];
         const uint32_t par = (uint32_t)((con / NSTG) & 1);
+        const long long t0 = prof ? clock64() : 0;
         while (!__all_sync(0xffffffffu, mbar_try_wait(fb, par)))
             if (c == 0) try_issue();
+        if (prof) clk_acq += clock64() - t0;
         return cst + (size_t)(g * NSTG + st) * TB;
     };
     auto release = [&]() {
@@ -1293,7 +1309,8 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
                 }
             }
         __syncwarp();
-        const double* mb = p.mblk + (size_t)s * 6 * M * M;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();  // Mw (staged by every lane) visible to the warp
 #pragma unroll
         for (int I = 0; I < RT; ++I)
 #pragma unroll
@@ -1305,10 +1322,10 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
                     double acc;
                     if (p.nbr[s * 6 + f] >= 0) {
                         acc = 0.0;
-                        const double* mx = mb + (f * M + rr) * M;
+                        const double* mx = Mw + (f * M + rr) * M;
                         const double* tx = T + (f * M) * 8 + (lane >> 2);
 #pragma unroll
-                        for (int cm = 0; cm < M; ++cm) acc = fma(__ldg(mx + cm), tx[cm * 8], acc);
+                        for (int cm = 0; cm < M; ++cm) acc = fma(mx[cm], tx[cm * 8], acc);
                     } else {
                         acc = __ldcg(p.acc1 + ((size_t)s * W + r) * S + q);
                     }
@@ -1358,6 +1375,7 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
     // neighbours published F_0 during the previous sweep, so the flags are normally set)
     // immediately followed by the sweep of step k, which takes the new U_0 from registers.
     double sq_prev = 0.0;  // |U|^2 of the previous step's layers >= 1
+    if (n_g > 0) stage_mass(g);
     for (int k = 1; k <= p.n_steps + 1; ++k) {
         const bool sweep = k <= p.n_steps;
         const unsigned int tag = p.tag0 + (unsigned int)k;
@@ -1375,8 +1393,11 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
             double Uj[RT][2], Uj1[RT][2], Fp[RT][2], C[RT][2];
             if (sweep) load_rows(us + WS, Uj1);  // U_1 of level k-1 (in flight during the coupling)
             if (k > 1) {
+                const long long tc_ = prof ? clock64() : 0;
                 coupling(k - 1, t, Uj, sqc);
                 probes(k - 1, t);
+                if (prof) clk_coup += clock64() - tc_;
+                stage_mass(g + ((t + 1) % n_g) * NG);  // next coupling's mass, in flight during the sweep
             } else {
                 load_rows(us, Uj);
             }
@@ -1387,10 +1408,16 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
                 if (j > 0) stage_rows(un + (size_t)j * WS, sP);
                 asm volatile("cp.async.commit_group;" ::: "memory");
                 // F_j = G_j (U_{j+1} - U_j)
-                ms3_gemm<RT, true>(acquire(), Uj1, Uj, C, lane, src_lo, src_hi, tr);
+                {
+                    const double* tl_ = acquire();
+                    const long long tg_ = prof ? clock64() : 0;
+                    ms3_gemm<RT, true>(tl_, Uj1, Uj, C, lane, src_lo, src_hi, tr);
+                    if (prof) clk_gemm += clock64() - tg_;
+                }
                 release();
                 if (j == 0) {
                     // F_0 -> face mailbox (all W rows are face rows), then the per-warp flag
+                    const long long tf_ = prof ? clock64() : 0;
                     double* fo = fx + (size_t)s * WS;
 #pragma unroll
                     for (int I = 0; I < RT; ++I)
@@ -1402,9 +1429,15 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
                     __threadfence();
                     __syncwarp();
                     if (lane == 0) st_release(p.sflags + (size_t)s * 4 + c, tag);
+                    if (prof) clk_f0 += clock64() - tf_;
                     if (outer) {  // acc_0 = H_0 F_0 (read back only on outer-face rows)
                         double A0[RT][2];
-                        ms3_gemm<RT, false>(acquire(), C, C, A0, lane, src_lo, src_hi, tr);
+                        {
+                            const double* tl_ = acquire();
+                            const long long tg_ = prof ? clock64() : 0;
+                            ms3_gemm<RT, false>(tl_, C, C, A0, lane, src_lo, src_hi, tr);
+                            if (prof) clk_gemm += clock64() - tg_;
+                        }
                         release();
                         double* ao = p.acc1 + (size_t)s * WS;
 #pragma unroll
@@ -1423,9 +1456,18 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
                 } else {
                     // acc_j = H_j (F_j - F_{j-1}); leapfrog of layer j
                     double A[RT][2];
-                    ms3_gemm<RT, true>(acquire(), C, Fp, A, lane, src_lo, src_hi, tr);
+                    {
+                        const double* tl_ = acquire();
+                        const long long tg_ = prof ? clock64() : 0;
+                        ms3_gemm<RT, true>(tl_, C, Fp, A, lane, src_lo, src_hi, tr);
+                        if (prof) clk_gemm += clock64() - tg_;
+                    }
                     release();
-                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                    {
+                        const long long tw_ = prof ? clock64() : 0;
+                        asm volatile("cp.async.wait_group 0;" ::: "memory");
+                        if (prof) clk_wait += clock64() - tw_;
+                    }
 #pragma unroll
                     for (int I = 0; I < RT; ++I)
 #pragma unroll
@@ -1443,7 +1485,11 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
                             Fp[I][e] = C[I][e];
                         }
                 }
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                {
+                    const long long tw_ = prof ? clock64() : 0;
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                    if (prof) clk_wait += clock64() - tw_;
+                }
 #pragma unroll
                 for (int I = 0; I < RT; ++I)
 #pragma unroll
@@ -1460,11 +1506,17 @@ __global__ void __launch_bounds__(NG * 128, 1) k_step_ms3(const MsParams p) {
         sq_prev = sq;
         __syncwarp();
     }
+    if (prof && lane < 6) {
+        const long long v = lane == 0 ? clk_acq : lane == 1 ? clk_gemm : lane == 2 ? clk_coup
+                          : lane == 3 ? clock64() - clk_start : lane == 4 ? clk_wait : clk_f0;
+        p.dbg[(blockIdx.x * (4 * NG) + warp) * 8 + lane] = (unsigned long long)v;
+    }
 }
 
 static size_t ms3_smem_bytes(int TB, int W, int nsmax, int ng, int nstg) {
-    const size_t RT = (W + 7) / 8;
-    return 8 * ((size_t)ng * nstg * TB + (size_t)4 * ng * W * 8 + (size_t)4 * ng * 4 * RT * 32 + 2 * ng * nstg) +
+    const size_t RT = (W + 7) / 8, M = W / 6;
+    return 8 * ((size_t)ng * nstg * TB + (size_t)4 * ng * W * 8 + (size_t)4 * ng * 4 * RT * 32 +
+                (size_t)4 * ng * 6 * M * M + 2 * ng * nstg) +
            4 * (size_t)nsmax + 64;
 }
 
