@@ -986,7 +986,10 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32, 1) k_step_ms2(const MsParams
 
     // ======== producer warp: chain blocks (ungated) and state blocks (gated per step) ====
     if (warp == M2_NW) {
-        if (lane == 0) {
+        // lane 0 feeds the chain-block ring, lane 1 the state-block ring: each polls only its
+        // own ring, so a refill is issued as soon as its stage is released
+        if (lane < 2) {
+            const bool chain_lane = lane == 0;
             const uint64_t pol = l2_policy_evict_first();
             const uint64_t pol_state = l2_policy_evict_last();
             const int cper = ns * 2 * L;
@@ -995,7 +998,7 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32, 1) k_step_ms2(const MsParams
             const uint32_t mbytes = (uint32_t)(6 * M * M * 8);
             const long long stotal = (long long)sper * p.n_steps;
             const uint32_t sbytes = (uint32_t)(WS * 8), cbytes = (uint32_t)TB * 8u;
-            long long c_iss = 0, s_iss = 0;
+            long long c_iss = chain_lane ? 0 : ctotal, s_iss = chain_lane ? stotal : 0;
             int cpos = 0, spos = 0, sstep = 0;
             while (c_iss < ctotal || s_iss < stotal) {
                 if (c_iss < ctotal) {
