@@ -1806,6 +1806,458 @@ __global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// k_ustep: fp64 U-form stepping, warp per subdomain (configs 3 and 5).
+//
+// Same physics and arithmetic order per element as k_step2 (stepper.py:243-373), organised as
+// the fp32 W-form kernel is: a warp owns whole subdomains and sweeps their layers in order, so
+// no CTA barrier separates the flux and acceleration products.  Item j (0..L) of a sweep is one
+// TMA bulk copy of the contiguous pair (Gamma-hat_{j-1}, Gamma_j) (block layout G0 H0 G1 H1 ..)
+// and one pass of the warp over both blocks:
+//   half-warp 0:  F_j       = Gamma_j (U_{j+1} - U_j)                 (j < L)
+//   half-warp 1:  acc_{j-1} = Gamma-hat_{j-1} (F_{j-1} - F_{j-2})     (j >= 1; F_{-1} = 0)
+// followed by the leapfrog of layer j-1 >= 1.  F_0 goes to a tagged face mailbox (value and step
+// tag in each 64-bit word, no flag round trip); acc_0 (outer-face rows) to acc1.  After the sweeps
+// of all its subdomains the warp updates their layer 0 from the neighbours' F_0, records norms
+// and probe rows.  Blocks are re-laid out for 16-B shared loads (u2_pos).
+__host__ __device__ constexpr int u2_nc1(int m) { return (m * m) / 2; }
+__host__ __device__ constexpr int u2_nc2(int m) { return tri_count(m) / 2; }
+__host__ __device__ constexpr int u2_tri_base(int m) { return 30 * u2_nc1(m); }
+__host__ __device__ constexpr int u2_tail1(int m) { return 30 * u2_nc1(m) + 12 * u2_nc2(m); }
+__host__ __device__ constexpr int u2_tail2(int m) { return u2_tail1(m) + 15 * ((m * m) % 2); }
+__host__ __device__ constexpr int u2_row0(int m, int dd) { return dd * m - dd * (dd - 1) / 2; }
+__host__ __device__ constexpr int u2_dd(int m, int q) {
+    int dd = 0;
+    while (q >= u2_row0(m, dd + 1)) ++dd;
+    return dd;
+}
+__host__ __device__ inline int u2_pos(int m, int row, int col) {
+    if (row < col) {
+        const int t = row;
+        row = col;
+        col = t;
+    }
+    const int I = row / m, K = col / m, r = row % m, c = col % m;
+    if (I != K) {
+        const int t = off_tile(I, K), e = ((c - r + m) % m) * m + r;
+        return e < 2 * u2_nc1(m) ? (e / 2) * 30 + t * 2 + (e % 2) : u2_tail1(m) + t;
+    }
+    const int dd = r - c, q = u2_row0(m, dd) + c;
+    return q < 2 * u2_nc2(m) ? u2_tri_base(m) + (q / 2) * 12 + I * 2 + (q % 2) : u2_tail2(m) + I;
+}
+
+__global__ void k_repack_u2(const double* __restrict__ in, int BS, int m, int BS2, double* __restrict__ out,
+                            long long n_blocks) {
+    const long long b = blockIdx.x;
+    if (b >= n_blocks) return;
+    const int w = 6 * m;
+    for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+        const int row = idx / w, col = idx % w;
+        if (row >= col) out[b * BS2 + u2_pos(m, row, col)] = in[b * BS + packed_pos(m, row, col)];
+    }
+    if (threadIdx.x == 0 && (packed_len(m) & 1)) out[b * BS2 + BS2 - 1] = 0.0;
+}
+
+constexpr int UPS = 74;  // partial slots: half 0 (F) 0..35, half 1 (acc) 36..71, junk 72, 73
+
+template <int M>
+struct URed {
+    static constexpr int W = 6 * M, EPL = (W + 31) / 32;
+    int o[EPL][6];  // slots of output row i within one half's set (add 36 for half 1)
+    __device__ __forceinline__ explicit URed(int lane) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            const int i = lane + 32 * e;
+            const int R = i < W ? i / M : 0, r = i < W ? i % M : 0;
+#pragma unroll
+            for (int q = 0; q < 6; ++q)  // tiles (R, K < R) rows, tiles (I > R, R) columns, triangle R
+                o[e][q] = q < R ? r * UPS + off_tile(R, q)
+                                : q < 5 ? r * UPS + 15 + off_tile(q + 1, R) : r * UPS + 30 + R;
+        }
+    }
+};
+
+// both halves: y = B x for a symmetric block B (lower-packed, u2 layout) -> partial slots
+template <int M>
+__device__ __forceinline__ void upair(const double* __restrict__ stage, int BS2, const double* x0, const double* x1,
+                                      double* part, int lane, bool act0, bool act1) {
+    constexpr int MM = M * M, NC = u2_nc1(M), TRI = tri_count(M), NC2 = u2_nc2(M);
+    const int h = lane >> 4, t = lane & 15;
+    const double* blk = stage + (h ? 0 : BS2);  // stage = [Gamma-hat_{j-1} | Gamma_j]
+    const double* x = h ? x1 : x0;
+    const bool act = h ? act1 : act0;
+    const int so = h ? 36 : 0;
+    {
+        const int tt = t < 15 ? t : 14;
+        const double xs = (t < 15 && act) ? 1.0 : 0.0;
+        const int I = off_I(tt), K = off_K(tt);
+        double P[M], Q[M], xk[M], xi[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            xk[i] = x[K * M + i] * xs;
+            xi[i] = x[I * M + i] * xs;
+            P[i] = Q[i] = 0.0;
+        }
+#pragma unroll
+        for (int ch = 0; ch < NC; ++ch) {
+            const double2 a2 = *reinterpret_cast<const double2*>(blk + ch * 30 + tt * 2);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int e = ch * 2 + u, r = e % M, c = (e / M + r) % M;
+                const double a = u ? a2.y : a2.x;
+                P[r] = fma(a, xk[c], P[r]);
+                Q[c] = fma(a, xi[r], Q[c]);
+            }
+        }
+#pragma unroll
+        for (int e = 2 * NC; e < MM; ++e) {
+            const int r = e % M, c = (e / M + r) % M;
+            const double a = blk[u2_tail1(M) + tt];
+            P[r] = fma(a, xk[c], P[r]);
+            Q[c] = fma(a, xi[r], Q[c]);
+        }
+        const int sa = t == 15 ? 72 : so + t, sb = t == 15 ? 73 : so + 15 + t;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            part[i * UPS + sa] = P[i];
+            part[i * UPS + sb] = Q[i];
+        }
+    }
+    {
+        const int d = t < 6 ? t : 5;
+        const double xs = (t < 6 && act) ? 1.0 : 0.0;
+        double P[M], xa[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            xa[i] = x[d * M + i] * xs;
+            P[i] = 0.0;
+        }
+        auto term = [&](int q, double a) {
+            const int dd = u2_dd(M, q), c = q - u2_row0(M, dd), r = c + dd;
+            P[r] = fma(a, xa[c], P[r]);
+            if (dd != 0) P[c] = fma(a, xa[r], P[c]);
+        };
+#pragma unroll
+        for (int ch = 0; ch < NC2; ++ch) {
+            const double2 a2 = *reinterpret_cast<const double2*>(blk + u2_tri_base(M) + ch * 12 + d * 2);
+            term(ch * 2, a2.x);
+            term(ch * 2 + 1, a2.y);
+        }
+#pragma unroll
+        for (int q = 2 * NC2; q < TRI; ++q) term(q, blk[u2_tail2(M) + d]);
+        const int sd = t >= 6 ? 72 : so + 30 + t;
+#pragma unroll
+        for (int i = 0; i < M; ++i) part[i * UPS + sd] = P[i];
+    }
+}
+
+__device__ __forceinline__ void uwait_all(uint64_t* bar, uint32_t parity) {
+    while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+    }
+}
+
+template <int M, int NS>
+__global__ void __launch_bounds__(256, 1) k_ustep(const StepParams p) {
+    constexpr int W = 6 * M;
+    constexpr int EPL = (W + 31) / 32;
+    const int NW = blockDim.x >> 5;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const URed<M> ro(lane);
+    const int BS2 = p.BS, L = p.L;
+    const long long K = (long long)L * W;
+    const int PAIR = 2 * BS2;
+    double* stages = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + (size_t)NW * NS * PAIR);
+    double* wk = reinterpret_cast<double*>(bars + NW * NS) + (size_t)warp * (2 * W + M * UPS);
+    double* x0 = wk;           // half 0 input: U_{j+1} - U_j
+    double* x1 = wk + W;       // half 1 input: F_{j-1} - F_{j-2}
+    double* part = wk + 2 * W; // [M][UPS]
+    double* my_stage = stages + (size_t)warp * NS * PAIR;
+    uint64_t* my_bar = bars + warp * NS;
+    for (int i = lane; i < NS * PAIR; i += 32) my_stage[i] = 0.0;  // finite data for idle lanes
+    if (lane == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&my_bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int n_my = (s1 - s0) > warp ? (s1 - s0 - warp + NW - 1) / NW : 0;
+    const int per = L + 1;  // items per subdomain
+    const long long total = (long long)n_my * per * p.n_steps;
+    const uint64_t pol = l2_policy_evict_first();
+    long long issued = 0, consumed = 0;
+    int pr_t = 0, pr_j = 0;
+    // interior flags (all six faces shared) of this warp's first 128 subdomain slots, one bit each
+    unsigned int im0, im1, im2, im3;
+    {
+        unsigned int mk[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int t = c * 32 + lane;
+            bool in = false;
+            if (t < n_my) {
+                const int* nb6 = p.nbr + (s0 + warp + t * NW) * 6;
+                in = (nb6[0] | nb6[1] | nb6[2] | nb6[3] | nb6[4] | nb6[5]) >= 0;
+            }
+            mk[c] = __ballot_sync(0xffffffffu, in);
+        }
+        im0 = mk[0], im1 = mk[1], im2 = mk[2], im3 = mk[3];
+    }
+    auto issue = [&]() {  // warp-uniform bookkeeping, lane 0 issues
+        while (issued < total && issued < consumed + NS) {
+            const int s = s0 + warp + pr_t * NW;
+            const int st = (int)(issued % NS);
+            // item j: blocks [2j-1, 2j] of the subdomain, clipped to [0, 2L).  Gamma-hat_0
+            // (block 1) only feeds the outer-face rows of acc_0: an interior subdomain skips it
+            // (its half-1 product at item 1 then runs on stale, finite stage data and is dropped)
+            bool lo = pr_j == 0;
+            if (pr_j == 1) {
+                if (pr_t < 128) {
+                    const unsigned int mw = pr_t < 32 ? im0 : pr_t < 64 ? im1 : pr_t < 96 ? im2 : im3;
+                    lo = (mw >> (pr_t & 31)) & 1u;
+                } else {
+                    const int* nb6 = p.nbr + s * 6;
+                    lo = (nb6[0] | nb6[1] | nb6[2] | nb6[3] | nb6[4] | nb6[5]) >= 0;
+                }
+            }
+            const int b0 = lo ? 2 * pr_j : 2 * pr_j - 1, nb = (lo || pr_j == L) ? 1 : 2;
+            const uint32_t bytes = (uint32_t)(nb * BS2) * 8u;
+            double* dst = my_stage + (size_t)st * PAIR + (lo ? BS2 : 0);
+            if (lane == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&my_bar[st], bytes);
+                bulk_g2s(dst, p.coef + ((long long)s * 2 * L + b0) * BS2, bytes, &my_bar[st], pol);
+            }
+            ++issued;
+            if (++pr_j == per) {
+                pr_j = 0;
+                if (++pr_t == n_my) pr_t = 0;
+            }
+        }
+    };
+    issue();
+    const double dt = p.dt, dt2 = p.dt2, half = p.half_dt2;
+    const int G = p.groups;
+    bool ok_e[EPL];
+    int ic[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+        ok_e[e] = lane + 32 * e < W;
+        ic[e] = ok_e[e] ? lane + 32 * e : W - 1;
+    }
+    if (n_my == 0 && lane == 0)  // idle warp: zero its norm partials
+        for (int k = 0; k < p.n_steps; ++k) p.norm_part[((size_t)k * gridDim.x + blockIdx.x) * G + warp] = 0.0;
+
+    auto buf = [&](int lvl) -> double* { return (p.cur ^ (lvl & 1)) ? p.U1 : p.U0; };  // level lvl
+    // Layer-0 update of step kc for subdomain slot t (level kc, layer 0): shared faces
+    // mass (own + neighbour F_0), outer faces acc_0, leapfrog; then its probe rows.  Runs
+    // right before the subdomain's next sweep, long after the neighbours published F_0(kc),
+    // while the TMA ring keeps streaming the sweep's blocks.  Every global load (state,
+    // mass rows, acc_0, source flag, layer 1 for the next sweep) is issued before the one
+    // mailbox poll, so the update pays one memory round trip.  Returns layers 0 and 1 of
+    // level kc in u0 / u1 (the next sweep's first inputs).
+    auto layer0 = [&](int kc, int t, double& sql, double (&u0)[EPL], double (&u1)[EPL]) {
+        const int s = s0 + warp + t * NW;
+        const unsigned int tg = p.tag_base + (unsigned int)kc;
+        const unsigned long long* mbk = p.mbox + (size_t)(tg & 1u) * p.n_sub * W * 2;
+        const double* Uc = buf(kc - 1);
+        double* Un = buf(kc);
+        const size_t o = (size_t)s * K;
+        const bool hs = p.src_ptr[s] != p.src_ptr[s + 1];
+        double own[EPL], oth[EPL], ucur[EPL], uprv[EPL], mrow[EPL][M];
+        const unsigned long long* po[EPL];
+        const unsigned long long* pn[EPL];
+        bool sh[EPL];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            const int i = ic[e], f = i / M, r = i % M;
+            const int nb = p.nbr[s * 6 + f];
+            sh[e] = nb >= 0;
+            po[e] = mbk + ((size_t)s * W + i) * 2;
+            pn[e] = mbk + ((size_t)(nb >= 0 ? nb : s) * W + (nb >= 0 ? (f ^ 1) * M + r : i)) * 2;
+            ucur[e] = Uc[o + i];
+            uprv[e] = Un[o + i];
+            u1[e] = Un[o + W + i];
+            if (nb >= 0) {
+                const double* mx = p.mass + (size_t)p.mass_idx[s * 6 + f] * M * M + r * M;
+#pragma unroll
+                for (int c = 0; c < M; ++c) mrow[e][c] = mx[c];
+            } else {
+                mrow[e][0] = p.acc1[(size_t)s * W + i];
+#pragma unroll
+                for (int c = 1; c < M; ++c) mrow[e][c] = 0.0;
+            }
+        }
+        {
+            bool okw;
+            do {
+                okw = true;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    unsigned long long a0, b0, a1, b1;
+                    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a0), "=l"(b0) : "l"(po[e]) : "memory");
+                    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a1), "=l"(b1) : "l"(pn[e]) : "memory");
+                    okw = okw && (unsigned int)(a0 >> 32) == tg && (unsigned int)(b0 >> 32) == tg &&
+                          (unsigned int)(a1 >> 32) == tg && (unsigned int)(b1 >> 32) == tg;
+                    own[e] = __hiloint2double((int)(unsigned int)b0, (int)(unsigned int)a0);
+                    oth[e] = __hiloint2double((int)(unsigned int)b1, (int)(unsigned int)a1);
+                }
+            } while (!__all_sync(0xffffffffu, okw));
+        }
+        // seg = mass (own + nbr) needs the whole face: stage own and nbr rows in x0 / x1
+#pragma unroll
+        for (int e = 0; e < EPL; ++e)
+            if (ok_e[e]) {
+                x0[ic[e]] = own[e];
+                x1[ic[e]] = oth[e];
+            }
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+            const int i = ic[e], f = i / M;
+            double a;
+            if (sh[e]) {
+                a = 0.0;
+#pragma unroll
+                for (int c = 0; c < M; ++c) a = fma(mrow[e][c], __dadd_rn(x0[f * M + c], x1[f * M + c]), a);
+            } else {
+                a = mrow[e][0];
+            }
+            const double tot = hs ? add_force(p, s, i, kc - 1, a) : a;
+            const double v = __dadd_rn(__dsub_rn(__dmul_rn(2.0, ucur[e]), uprv[e]), __dmul_rn(dt2, tot));
+            u0[e] = v;  // idle lanes duplicate row W-1: same value
+            if (ok_e[e]) {
+                Un[o + i] = v;
+                sql = fma(v, v, sql);
+            }
+        }
+        __syncwarp();
+        if (kc % p.record_every == 0 && p.rows) {  // probe rows of level kc (all layers final)
+            const long long row = kc / p.record_every - 1;
+            const long long base = (long long)s * K;
+            const int pa = p.prb_ptr[s], pb = p.prb_ptr[s + 1];
+            for (int q0 = pa; q0 < pb; q0 += 32) {  // single-entry probes: one lane each
+                const int q = q0 + lane;
+                if (q < pb) {
+                    const int pid = p.prb_ids[q];
+                    const int tap = p.prb_tap[pid];
+                    if (tap >= 0) p.rows[row * p.n_probe + pid] = Un[base + tap];
+                }
+            }
+            for (int pq = pa; pq < pb; ++pq) {  // dense probes: warp-cooperative dot products
+                const int pid = p.prb_ids[pq];
+                if (p.prb_tap[pid] >= 0) continue;
+                const double* wv = p.prb_w + p.prb_woff[pid];
+                double acc = 0.0;
+                for (long long b0 = 0; b0 < K; b0 += 32) {
+                    const long long i = b0 + lane;
+                    if (i < K) acc = fma(wv[i], Un[base + i], acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) p.rows[row * p.n_probe + pid] = acc;
+            }
+            __syncwarp();
+        }
+    };
+
+    double sq_prev = 0.0;  // |U|^2 of the previous step's layers >= 1
+    for (int k = 1; k <= p.n_steps + 1; ++k) {
+        const bool sweep = k <= p.n_steps;
+        const unsigned int tag = p.tag_base + (unsigned int)k;
+        unsigned long long* mb = p.mbox + (size_t)(tag & 1u) * p.n_sub * W * 2;
+        const double* Uc = buf(k - 1);
+        double* Un = buf(k);
+        const int kk = k - 1;
+        double sq = 0.0, sql = 0.0;
+        for (int t = 0; t < n_my; ++t) {
+            const int s = s0 + warp + t * NW;
+            const double* us = Uc + (size_t)s * K;
+            double* un = Un + (size_t)s * K;
+            // registers: U_j, U_{j+1} of the half-0 input, U_{j-1}, Uprev_{j-1} for the leapfrog,
+            // F_{j-1}, F_{j-2} for the half-1 input (lane rows ic[e])
+            double uj[EPL], uj1[EPL], ujm[EPL], upm[EPL], f1[EPL], f2[EPL];
+            if (k > 1) {
+                layer0(k - 1, t, sql, uj, uj1);
+            } else {
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    uj[e] = us[ic[e]];
+                    uj1[e] = us[W + ic[e]];
+                }
+            }
+            if (!sweep) continue;
+            const bool hs = p.src_ptr[s] != p.src_ptr[s + 1];
+            bool outer[EPL];
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+                outer[e] = ok_e[e] && p.nbr[s * 6 + ic[e] / M] < 0;
+                ujm[e] = upm[e] = f1[e] = f2[e] = 0.0;
+            }
+            for (int j = 0; j <= L; ++j) {
+#pragma unroll
+                for (int e = 0; e < EPL; ++e)
+                    if (ok_e[e]) {
+                        x0[ic[e]] = uj1[e] - uj[e];
+                        x1[ic[e]] = j >= 2 ? f1[e] - f2[e] : f1[e];
+                    }
+                // prefetch: U_{j+2} (next half-0 input) and Uprev_j (leapfrog of layer j at item j+1)
+                double un2[EPL], upj[EPL];
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    un2[e] = (j + 2 < L) ? us[(size_t)(j + 2) * W + ic[e]] : 0.0;
+                    upj[e] = (j >= 1 && j < L) ? un[(size_t)j * W + ic[e]] : 0.0;
+                }
+                __syncwarp();
+                const int st = (int)(consumed % NS);
+                uwait_all(&my_bar[st], (uint32_t)((consumed / NS) & 1));
+                upair<M>(my_stage + (size_t)st * PAIR, BS2, x0, x1, part, lane, j < L, j >= 1);
+                __syncwarp();
+                ++consumed;
+                issue();
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) {
+                    double fj = part[ro.o[e][0]];
+#pragma unroll
+                    for (int q = 1; q < 6; ++q) fj += part[ro.o[e][q]];
+                    double ac = part[ro.o[e][0] + 36];
+#pragma unroll
+                    for (int q = 1; q < 6; ++q) ac += part[ro.o[e][q] + 36];
+                    if (j == 0) {
+                        if (ok_e[e]) mbox_put(mb + ((size_t)s * W + ic[e]) * 2, fj, tag);  // F_0 -> faces
+                    }
+                    if (j == 1) {  // acc_0: only its outer-face rows are read (layer-0 update)
+                        if (outer[e]) p.acc1[(size_t)s * W + ic[e]] = ac;
+                    } else if (j >= 2) {  // leapfrog of layer j-1
+                        const long long g = (long long)(j - 1) * W + ic[e];
+                        const double tot = hs ? add_force(p, s, g, kk, ac) : ac;
+                        const double v = __dadd_rn(__dsub_rn(__dmul_rn(2.0, ujm[e]), upm[e]), __dmul_rn(dt2, tot));
+                        if (ok_e[e]) {
+                            un[g] = v;
+                            sq = fma(v, v, sq);
+                        }
+                    }
+                    f2[e] = f1[e];
+                    f1[e] = fj;
+                    ujm[e] = uj[e];
+                    upm[e] = upj[e];
+                    uj[e] = uj1[e];
+                    uj1[e] = un2[e];
+                }
+                __syncwarp();
+            }
+        }
+        if (k > 1) {
+            const double vs = warp_sum(sq_prev + sql);
+            if (lane == 0) p.norm_part[((size_t)(k - 2) * gridDim.x + blockIdx.x) * G + warp] = vs;
+        }
+        sq_prev = sq;
+        __syncwarp();
+    }
+    (void)dt;
+    (void)half;
+}
+
+// ---------------------------------------------------------------------------
 // setup kernels
 
 // dense (L*w*w per subdomain) -> packed blocks [Gamma_j, Gamma-hat_j] per layer
@@ -2059,7 +2511,7 @@ static void free_all(sfw_stepper* h) {
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
                     h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta, h->tcoef, h->UM[0], h->UM[1],
                     h->mfb, h->macc1, h->mnorm, h->mrows, h->shot_vec, h->shot_sub, h->shot_voff,
-                    h->shot_ftab, h->mbox, h->mmass, h->sflags};
+                    h->shot_ftab, h->mbox, h->mmass, h->sflags, h->ucoef};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -2211,6 +2663,10 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
         k_hat1_dev<<<(n + 127) / 128, 128, 0, h->stream>>>(h_dev, d_first, n, W, d_dev);
 
         std::vector<int> nbr(d->neighbors, d->neighbors + 6 * n), mass_idx(6 * n, -1), iface;
+        h->n_interior = 0;
+        for (int s = 0; s < n; ++s)
+            h->n_interior += (nbr[6 * s] | nbr[6 * s + 1] | nbr[6 * s + 2] | nbr[6 * s + 3] | nbr[6 * s + 4] |
+                              nbr[6 * s + 5]) >= 0;
         for (int s = 0; s < n; ++s)
             for (int f = 0; f < 6; ++f) {
                 const int t = nbr[6 * s + f];
@@ -2452,6 +2908,30 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
                 h->tag_base = 0;
             }
         }
+        // fp64 U-form warp-per-subdomain streaming kernel (m = 9: configs 3 and 5); opt-in for now
+        if (!h->klw && !h->kres && h->uniform && m == 9 && h->L >= 2 && !getenv("SFW_NO_USTEP")) {
+            const int NWU = 4, NSU = 2;
+            const int BS2 = (packed_len(m) + 1) & ~1;
+            const size_t need = (size_t)NWU * ((size_t)NSU * 2 * BS2 * 8 + NSU * 8 + (size_t)(2 * W + m * UPS) * 8);
+            if (need <= 227 * 1024) {
+                TRY(dalloc(&h->ucoef, (size_t)h->n_blocks * BS2, errbuf, errlen));
+                k_repack_u2<<<(unsigned)h->n_blocks, 128, 0, h->stream>>>(h->coef, h->BS, m, BS2, h->ucoef,
+                                                                        h->n_blocks);
+                if (!h->mbox) {
+                    SFW_CUDA_TRY(cudaMalloc(&h->mbox, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
+                    SFW_CUDA_TRY(cudaMemset(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
+                    h->tag_base = 0;
+                }
+                h->BS2 = BS2;
+                h->klw = (const void*)k_ustep<9, 2>;
+                h->lw_smem = (int)need;
+                h->lw_threads = 32 * NWU;
+                h->lw_groups = NWU;
+                h->ustep = true;
+                SFW_CUDA_TRY(cudaFuncSetAttribute(h->klw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+                if (getenv("SFW_STEP_VERBOSE")) fprintf(stderr, "[sfw] k_ustep: smem=%zu\n", need);
+            }
+        }
         // layer-warp resident variant: one warp per (subdomain, layer), w <= 32
         if (!h->klw && h->uniform && !getenv("SFW_NO_RESIDENT") && !getenv("SFW_NO_LW") && (m == 1 || m == 4)) {
             int maxns = 0;
@@ -2581,6 +3061,10 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
         p.mbox = h->mbox;
         p.tag_base = h->tag_base;
         p.groups = h->lw_groups;
+        if (h->ustep) {  // k_ustep streams the 16-B-pair re-layout of the chain blocks
+            p.coef = h->ucoef;
+            p.BS = h->BS2;
+        }
         p.tprof = nullptr;
         if (getenv("SFW_STEP_PROF")) {
             static unsigned long long* tp = nullptr;
@@ -2772,8 +3256,9 @@ extern "C" int sfw_step_traffic(sfw_stepper* h, double* alg_bytes, double* alg_f
         const double L = h->layers[i];
         b += 8.0 * ((2 * L - 1) * w * (w + 1) / 2 + 3 * L * w);
         f += 2.0 * (2 * L - 1) * w * w + 5 * L * w;
-        s += 8.0 * (2 * L * h->BS + 3 * L * w);
+        s += 8.0 * ((h->ustep ? 2 * L * h->BS2 : 2 * L * h->BS) + 3 * L * w);
     }
+    if (h->ustep) s -= 8.0 * h->BS2 * h->n_interior;  // k_ustep skips Gamma-hat_0 of interior subdomains
     if (alg_bytes) *alg_bytes = b;
     if (alg_flops) *alg_flops = f;
     if (streamed) *streamed = s;

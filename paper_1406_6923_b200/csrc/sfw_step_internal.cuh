@@ -70,6 +70,10 @@ struct sfw_stepper {
     // k_step_lw (layer-warp resident kernel): launch shape + tagged face mailbox
     const void* klw = nullptr;
     int lw_smem = 0, lw_threads = 0, lw_groups = 1;
+    double* ucoef = nullptr;  // k_ustep: chain blocks in the 16-B-pair layout
+    int BS2 = 0;
+    bool ustep = false;
+    int n_interior = 0;  // subdomains with all six faces shared
     unsigned long long* mbox = nullptr;
     unsigned int tag_base = 0;
     int max_src_sub = 0;  // most sources injected into one subdomain

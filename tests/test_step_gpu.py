@@ -139,8 +139,15 @@ def test_acceleration_matches_oracle():
         assert rel(got[a], want[a]) < 1e-12
 
 
-def test_m9k8_stepping_parity_on_shared_coefficients():
-    wl = make_workload(3, counts=(2, 2, 2), n_steps=60)
+@pytest.mark.parametrize("counts,env", [
+    ((2, 2, 2), {}),                                                  # SMEM-resident kernel
+    ((3, 3, 3), {"SFW_NO_RESIDENT": "1"}),                            # k_ustep (one interior subdomain)
+    ((2, 2, 2), {"SFW_NO_RESIDENT": "1", "SFW_NO_USTEP": "1"}),       # streamed k_step2
+], ids=["resident", "ustep", "step2"])
+def test_m9k8_stepping_parity_on_shared_coefficients(counts, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    wl = make_workload(3, counts=counts, n_steps=60)
     models = oracle_models(wl)
     lam, _ = so.cfl_power(models)
     dt = 0.9 * 2.0 / math.sqrt(lam)
