@@ -2517,6 +2517,7 @@ static void free_all(sfw_stepper* h) {
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->dstream) cudaStreamDestroy(h->dstream);
 }
 
 
@@ -2980,7 +2981,7 @@ error:
 }
 
 static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, int ftab_stride,
-                       char* errbuf, int errlen, double* Ucur = nullptr, double* Uoth = nullptr) {
+                       char* errbuf, int errlen, double* Ucur = nullptr, double* Uoth = nullptr, int step0 = 0) {
     StepParams p{};
     p.n_sub = h->n_sub;
     p.BS = h->BS;
@@ -3019,15 +3020,17 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
     p.src_ids = h->src_ids;
     p.src_vec = h->src_vec;
     p.src_voff = h->src_voff;
-    p.ftab = h->ftab;
+    // step0 > 0: a later chunk of one run (step0 a multiple of record_every): profile column,
+    // probe-row and norm-partial offsets of its first step
+    p.ftab = h->ftab + step0;
     p.prb_ptr = h->prb_ptr;
     p.prb_ids = h->prb_ids;
     p.prb_tap = h->prb_tap;
     p.prb_w = h->prb_w;
     p.prb_woff = h->prb_woff;
-    p.rows = h->rows;
+    p.rows = h->rows + (size_t)(step0 / record_every) * h->n_probe;
     p.sub_norm = h->sub_norm;
-    p.norm_part = h->norm_part;
+    p.norm_part = h->norm_part + (size_t)step0 * h->grid * (h->klw ? h->lw_groups : 1);
     p.bar = h->bar;
     SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int) * h->grid, h->stream));
     p.ncta_ptr = h->ncta_ptr;
@@ -3191,9 +3194,36 @@ extern "C" int sfw_step_run(sfw_stepper* h, int n_steps, int record_every, const
     if (bad_step) *bad_step = 0;
     int rc = run_common(h, n_steps, record_every, profile, errbuf, errlen);
     if (rc || n_steps <= 0) return rc;
-    rc = launch_step(h, 0, n_steps, record_every, n_steps, errbuf, errlen);
-    if (rc) return rc;
-    h->cur ^= (n_steps & 1);
+    const long long nrec = n_steps / record_every;
+    // Large probe-row downloads are split: the run is launched as up to 16 chunks of whole
+    // record intervals, and chunk c's rows are copied (on a second stream, into the caller's
+    // pageable buffer) while chunks c+1.. compute.  Same kernels, same arithmetic: a chunk
+    // boundary only re-enters the persistent kernel with the state, tags and parity it left.
+    const long long row_bytes = nrec * h->n_probe * 8;
+    int n_chunks = 1;
+    long long chunk_min = 8LL << 20;
+    if (const char* e = getenv("SFW_CHUNK_BYTES")) chunk_min = atoll(e);  // test hook
+    if (rows_out && row_bytes >= chunk_min && nrec >= 16 && !getenv("SFW_NO_CHUNK")) n_chunks = 16;
+    const long long rec_per = (nrec + n_chunks - 1) / n_chunks;
+    std::vector<cudaEvent_t> evs;
+    if (n_chunks > 1 && !h->dstream) SFW_CUDA_TRY(cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking));
+    std::vector<std::pair<long long, long long>> rec_range;
+    for (long long r0 = 0; r0 < nrec || (r0 == 0 && n_chunks == 1); r0 += rec_per) {
+        const int s0 = (int)(r0 * record_every);
+        const long long r1 = std::min(nrec, r0 + rec_per);
+        const int s1 = (n_chunks == 1 || r1 == nrec) ? n_steps : (int)(r1 * record_every);
+        rc = launch_step(h, 0, s1 - s0, record_every, n_steps, errbuf, errlen, nullptr, nullptr, s0);
+        if (rc) return rc;
+        h->cur ^= ((s1 - s0) & 1);
+        if (n_chunks > 1) {
+            cudaEvent_t e;
+            SFW_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            SFW_CUDA_TRY(cudaEventRecord(e, h->stream));
+            evs.push_back(e);
+            rec_range.push_back({r0, r1});
+        }
+        if (n_chunks == 1) break;
+    }
     cudaFree(h->norms);
     h->norms = nullptr;
     rc = dalloc(&h->norms, n_steps, errbuf, errlen);
@@ -3202,10 +3232,20 @@ extern "C" int sfw_step_run(sfw_stepper* h, int n_steps, int record_every, const
                                                           h->klw ? h->lw_groups : 1, h->norms);
     std::vector<double> nrm(n_steps);
     SFW_CUDA_TRY(cudaMemcpyAsync(nrm.data(), h->norms, (size_t)n_steps * 8, cudaMemcpyDeviceToHost, h->stream));
-    const long long nrec = n_steps / record_every;
-    if (rows_out && nrec * h->n_probe > 0)
+    if (n_chunks > 1) {
+        for (size_t c = 0; c < evs.size(); ++c) {  // each pageable copy returns when done; later chunks keep running
+            const long long a = rec_range[c].first, b = rec_range[c].second;
+            SFW_CUDA_TRY(cudaStreamWaitEvent(h->dstream, evs[c], 0));
+            if (b > a)
+                SFW_CUDA_TRY(cudaMemcpyAsync(rows_out + a * h->n_probe, h->rows + a * h->n_probe,
+                                             (size_t)(b - a) * h->n_probe * 8, cudaMemcpyDeviceToHost, h->dstream));
+        }
+        SFW_CUDA_TRY(cudaStreamSynchronize(h->dstream));
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    } else if (rows_out && nrec * h->n_probe > 0) {
         SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost,
                                      h->stream));
+    }
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
     SFW_CUDA_TRY(cudaGetLastError());
     if (norms_out) std::memcpy(norms_out, nrm.data(), (size_t)n_steps * 8);

@@ -38,6 +38,7 @@ struct sfw_stepper {
     std::vector<int> layers;
     std::vector<long long> soff, src_len, prb_len;
     cudaStream_t stream = nullptr;
+    cudaStream_t dstream = nullptr;  // probe-row downloads overlapped with later step chunks
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double* coef = nullptr;
     long long* seq = nullptr;

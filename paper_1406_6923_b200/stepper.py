@@ -402,22 +402,24 @@ class CoupledStepper:
         self.message_count = 0
         dt = self.dt
         base = 0.0
-        for i, a in enumerate(self.order):
-            uu = u[self._offs[i]:self._offs[i + 1]] if u is not None else np.zeros(int(self._sizes[i]))
-            vv = v[self._offs[i]:self._offs[i + 1]] if v is not None else np.zeros(int(self._sizes[i]))
-            base += float(np.linalg.norm(uu)) + dt * float(np.linalg.norm(vv))
+        if u is not None or v is not None:  # from rest every term is 0.0
+            for i, a in enumerate(self.order):
+                uu = u[self._offs[i]:self._offs[i + 1]] if u is not None else np.zeros(int(self._sizes[i]))
+                vv = v[self._offs[i]:self._offs[i + 1]] if v is not None else np.zeros(int(self._sizes[i]))
+                base += float(np.linalg.norm(uu)) + dt * float(np.linalg.norm(vv))
         self._baseline = base
         self._initialized = True
 
-    def _steps(self, n_steps: int, record_every: int):
+    def _steps(self, n_steps: int, record_every: int, out: np.ndarray | None = None):
         if not self._initialized:
             raise ProtocolError("stepper not initialized")
         dt = self.dt
-        t_vals = [(self.steps_done + k) * dt for k in range(n_steps)]
-        prof = self._profiles(t_vals) if self.sources else None
+        # (steps_done + k) * dt: integer-valued doubles times dt, as the reference's int * float
+        t_vals = (np.arange(n_steps, dtype=np.float64) + float(self.steps_done)) * dt
+        prof = self._profiles(t_vals.tolist()) if self.sources else None
         limits, base = self._limits(prof, self._src_norms, n_steps)
         n_rec = n_steps // record_every
-        rows = np.empty((max(1, n_rec), max(1, len(self._probes))))
+        rows = out if out is not None else np.empty((max(1, n_rec), max(1, len(self._probes))))
         norms = np.empty(n_steps)
         bad = C.c_int(0)
         eb = _lib.errbuf()
@@ -467,13 +469,17 @@ class CoupledStepper:
         if record_every < 1:
             raise ConfigError("record_every must be at least 1")
         self.initialize(u0, v0, _probes=probes)
-        times = [0.0]
-        rows = [self._row0]
+        n_rec = n_steps // record_every if n_steps > 0 else 0
+        n_p = len(self._probes)
+        # one output array: the library writes the probe rows straight into rows 1..n_rec
+        out = np.empty((1 + n_rec, n_p)) if n_p else np.empty((1 + n_rec, 0))
+        out[0] = self._row0
+        start = self.steps_done
         if n_steps > 0:
-            steps, recs = self._steps(n_steps, record_every)
-            times += [s * self.dt for s in steps]
-            rows += list(recs)
-        return np.asarray(times), np.asarray(rows).reshape(len(times), len(self._probes))
+            self._steps(n_steps, record_every, out=out[1:] if (n_p and n_rec) else None)
+        times = np.concatenate([[0.0], (np.arange(record_every, n_steps + 1, record_every, dtype=np.float64)
+                                        + float(start)) * self.dt]) if n_steps > 0 else np.zeros(1)
+        return times, out
 
     # -- independent shots (BASELINE config 4) ------------------------------------
 

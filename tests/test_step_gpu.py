@@ -221,3 +221,32 @@ def test_advance_equals_run():
         b_state = st.u_curr
     for a in order:
         assert np.array_equal(a_state[a], b_state[a])
+
+
+@pytest.mark.parametrize("record_every,env", [(1, {}), (3, {}), (1, {"SFW_NO_RESIDENT": "1", "SFW_NO_SW": "1"})],
+                         ids=["resident", "record3", "streamed"])
+def test_chunked_run_equals_single_launch(record_every, env, monkeypatch):
+    """Large probe-row downloads split the run into chunks whose rows download while later
+    chunks compute (sfw_step_run); the traces, times and final state equal one launch bit for bit."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g, pre, models = _toy("quad")
+    order = sorted(models)
+    u0 = {a: g[pre + "u0"][i] for i, a in enumerate(order)}
+    dt = float(g[pre + "dt"])
+    probes = [Probe(a, np.eye(models[a].state_size)[j]) for a in order for j in (0, 3, models[a].state_size - 1)]
+    n = 203
+    out = {}
+    for mode in ("single", "chunked"):
+        monkeypatch.setenv("SFW_NO_CHUNK" if mode == "single" else "SFW_CHUNK_BYTES", "1")
+        if mode == "chunked":
+            monkeypatch.delenv("SFW_NO_CHUNK")
+        with CoupledStepper(models, dt) as st:
+            t, r = st.run(n, probes=probes, record_every=record_every, u0=u0)
+            out[mode] = (t, r, st.u_curr)
+    ts, rs, us = out["single"]
+    tc, rc, uc = out["chunked"]
+    assert rs.shape == (1 + n // record_every, len(probes))
+    assert np.array_equal(ts, tc) and np.array_equal(rs, rc)
+    for a in order:
+        assert np.array_equal(us[a], uc[a])
