@@ -181,6 +181,11 @@ int sfw_step_energy(sfw_stepper* h, double* energy, char* errbuf, int errlen);
  * SURVEY.md 8d), and the bytes actually streamed per step by this build. */
 int sfw_step_traffic(sfw_stepper* h, double* alg_bytes, double* alg_flops, double* streamed_bytes);
 
+/* Host table of a reference source pulse (sim.py:80-94; 0 = Ricker, 1 = Gaussian derivative)
+ * at t_k = (k0 + k) * dt, bit-identical to the Python callables in pulses.py.  Replaces
+ * the per-step SourceTerm.profile calls of stepper.py:313-321 on long runs. */
+int sfw_pulse_table(int kind, double f_peak, double delay, long long k0, double dt, int n, double* out);
+
 int sfw_step_destroy(sfw_stepper* h);
 
 /* ------------------------------------------------------------------------- */

@@ -51,6 +51,7 @@ SIGNATURES = {
     "sfw_step_get_state": (C.c_int, [C.c_void_p, PD, PD]),
     "sfw_step_energy": (C.c_int, [C.c_void_p, PD, C.c_char_p, C.c_int]),
     "sfw_step_traffic": (C.c_int, [C.c_void_p, PD, PD, PD]),
+    "sfw_pulse_table": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_longlong, C.c_double, C.c_int, PD]),
     "sfw_step_destroy": (C.c_int, [C.c_void_p]),
     "sfw_shots_setup": (C.c_int, [C.c_void_p, C.c_int, PI, PD, C.c_char_p, C.c_int]),
     "sfw_shots_run": (C.c_int, [C.c_void_p, C.c_int, C.c_int, PD, PD, PD, PD, PF, C.c_char_p, C.c_int]),

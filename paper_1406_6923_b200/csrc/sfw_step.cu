@@ -3288,6 +3288,29 @@ extern "C" int sfw_step_get_state(sfw_stepper* h, double* u_curr, double* u_prev
     return 0;
 }
 
+// Host table of the reference's source pulses (sim.py:80-94) at t_k = (k0 + k) dt, k < n:
+// kind 0 Ricker (1 - 2a) exp(-a), a = (pi f (t - delay))^2; kind 1 Gaussian derivative
+// -x sqrt(2e) exp(-x^2), x = pi f (t - delay).  Same libm calls and evaluation order as
+// the Python callables in pulses.py, so the values are bit-identical (tests/test_host_cpu.py);
+// it only saves the per-step Python call on long runs.
+extern "C" int sfw_pulse_table(int kind, double f_peak, double delay, long long k0, double dt, int n, double* out) {
+    if (!out || n < 0 || kind < 0 || kind > 1) return SFW_ECONFIG;
+    const double pf = M_PI * f_peak;
+    const double s2e = std::sqrt(2.0 * M_E);
+    for (int k = 0; k < n; ++k) {
+        volatile double t = (double)(k0 + k) * dt;  // int * float, rounded like Python's
+        const double x = pf * (t - delay);
+        if (kind == 0) {
+            volatile double two = 2.0;  // keep pow(): the Python ** operator calls libm pow
+            const double a = std::pow(x, (double)two);
+            out[k] = (1.0 - 2.0 * a) * std::exp(-a);
+        } else {
+            out[k] = -x * s2e * std::exp(-x * x);
+        }
+    }
+    return 0;
+}
+
 extern "C" int sfw_step_traffic(sfw_stepper* h, double* alg_bytes, double* alg_flops, double* streamed) {
     // bytes = 8[(2L-1) w(w+1)/2 + 3 L w], flops = 2(2L-1) w^2 + 5 L w per subdomain-step
     double b = 0, f = 0, s = 0;

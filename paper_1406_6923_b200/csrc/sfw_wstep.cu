@@ -758,7 +758,7 @@ extern "C" int sfw_wform_vectors(sfw_stepper* h, const double* src_vec, const do
 }
 
 static int wf_launch(sfw_stepper* h, WState* ws, int mode, int n_steps, int record_every, int ftab_stride, char* errbuf,
-                     int errlen) {
+                     int errlen, int step0 = 0) {  // step0: first step of a later chunk (see sfw_step_run)
     WParams p{};
     p.n_sub = h->n_sub;
     p.L = h->L;
@@ -783,14 +783,14 @@ static int wf_launch(sfw_stepper* h, WState* ws, int mode, int n_steps, int reco
     p.src_ids = h->src_ids;
     p.src_vec = ws->src;
     p.src_voff = h->src_voff;
-    p.ftab = ws->ftab;
+    p.ftab = ws->ftab + step0;
     p.prb_ptr = h->prb_ptr;
     p.prb_ids = h->prb_ids;
     p.prb_w = ws->prb;
     p.prb_woff = h->prb_woff;
     p.prb_rng = ws->prb_rng;
-    p.rows = h->rows;
-    p.norm_part = ws->norm;
+    p.rows = h->rows + (size_t)(step0 / record_every) * h->n_probe;
+    p.norm_part = ws->norm + (size_t)step0 * h->grid * ws->nw;
     void* args[] = {&p};
     SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ws->fn, dim3(h->grid), dim3(ws->nw * 32), args, ws->smem, h->stream));
     ws->tag += (unsigned int)(mode == 0 ? n_steps : 1);
@@ -892,15 +892,47 @@ extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, cons
         if ((rc = dalloc(&ws->norm, (size_t)n_steps * nwg, errbuf, errlen))) return rc;
         ws->norm_cap = (long long)n_steps * nwg;
     }
+    // large probe-row downloads overlap later chunks of the run (as sfw_step_run)
+    long long chunk_min = 8LL << 20;
+    if (const char* e = getenv("SFW_CHUNK_BYTES")) chunk_min = atoll(e);  // test hook
+    const int n_chunks = (rows_out && nrec * h->n_probe * 8 >= chunk_min && nrec >= 16 && !getenv("SFW_NO_CHUNK")) ? 16 : 1;
+    const long long rec_per = (nrec + n_chunks - 1) / n_chunks;
+    if (n_chunks > 1 && !h->dstream) SFW_CUDA_TRY(cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> evs;
+    std::vector<std::pair<long long, long long>> rr;
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
-    if ((rc = wf_launch(h, ws, 0, n_steps, record_every, n_steps, errbuf, errlen))) return rc;
+    for (long long r0 = 0;; r0 += rec_per) {
+        const int s0 = (int)(r0 * record_every);
+        const long long r1 = std::min(nrec, r0 + rec_per);
+        const int s1 = (n_chunks == 1 || r1 == nrec) ? n_steps : (int)(r1 * record_every);
+        if ((rc = wf_launch(h, ws, 0, s1 - s0, record_every, n_steps, errbuf, errlen, s0))) return rc;
+        ws->cur ^= ((s1 - s0) & 1);
+        if (n_chunks > 1) {
+            cudaEvent_t e;
+            SFW_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            SFW_CUDA_TRY(cudaEventRecord(e, h->stream));
+            evs.push_back(e);
+            rr.push_back({r0, r1});
+        }
+        if (s1 == n_steps) break;
+    }
     SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
-    ws->cur ^= (n_steps & 1);
     std::vector<double> part((size_t)n_steps * nwg);
-    if (rows_out && nrec * h->n_probe > 0)
-        SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost, h->stream));
     if (norms_out)
         SFW_CUDA_TRY(cudaMemcpyAsync(part.data(), ws->norm, part.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (n_chunks > 1) {
+        for (size_t c = 0; c < evs.size(); ++c) {
+            const long long a = rr[c].first, b = rr[c].second;
+            SFW_CUDA_TRY(cudaStreamWaitEvent(h->dstream, evs[c], 0));
+            if (b > a)
+                SFW_CUDA_TRY(cudaMemcpyAsync(rows_out + a * h->n_probe, h->rows + a * h->n_probe,
+                                             (size_t)(b - a) * h->n_probe * 8, cudaMemcpyDeviceToHost, h->dstream));
+        }
+        SFW_CUDA_TRY(cudaStreamSynchronize(h->dstream));
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    } else if (rows_out && nrec * h->n_probe > 0) {
+        SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost, h->stream));
+    }
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
     SFW_CUDA_TRY(cudaGetLastError());
     if (kernel_ms) cudaEventElapsedTime(kernel_ms, h->ev0, h->ev1);

@@ -15,6 +15,9 @@ def ricker(f_peak: float, delay: float):
         a = (math.pi * f_peak * (t - delay)) ** 2
         return (1.0 - 2.0 * a) * math.exp(-a)
 
+    # (kind, f, delay): lets the stepper tabulate long runs in the library (sfw_pulse_table),
+    # bit-identical to calling pulse(t) per step
+    pulse.sfw_pulse = (0, float(f_peak), float(delay))
     return pulse
 
 
@@ -24,6 +27,7 @@ def gauss_deriv(f_peak: float, delay: float):
         x = math.pi * f_peak * (t - delay)
         return -x * math.sqrt(2.0 * math.e) * math.exp(-x * x)
 
+    pulse.sfw_pulse = (1, float(f_peak), float(delay))
     return pulse
 
 

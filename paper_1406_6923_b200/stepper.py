@@ -367,6 +367,10 @@ class CoupledStepper:
             tab[i] = [float(v) for v in map(s.profile, t_values)]
         return np.ascontiguousarray(tab)
 
+    def _profile_steps(self, k0: int, n: int) -> np.ndarray:
+        """f_i(t_k), t_k = (k0 + k) dt for k < n: one row per source (stepper.py:313-321, 367)."""
+        return profile_table([s.profile for s in self.sources], k0, n, self.dt, self._lib)
+
     def _limits(self, prof, norms_of_sources, n_steps):
         """Growth-detector thresholds of the next n_steps and the final baseline (stepper.py:379-389).
 
@@ -414,9 +418,7 @@ class CoupledStepper:
         if not self._initialized:
             raise ProtocolError("stepper not initialized")
         dt = self.dt
-        # (steps_done + k) * dt: integer-valued doubles times dt, as the reference's int * float
-        t_vals = (np.arange(n_steps, dtype=np.float64) + float(self.steps_done)) * dt
-        prof = self._profiles(t_vals.tolist()) if self.sources else None
+        prof = self._profile_steps(self.steps_done, n_steps) if self.sources else None
         limits, base = self._limits(prof, self._src_norms, n_steps)
         n_rec = n_steps // record_every
         rows = out if out is not None else np.empty((max(1, n_rec), max(1, len(self._probes))))
@@ -518,10 +520,9 @@ class CoupledStepper:
         dt = self.dt
         prof = np.zeros((S, n_steps))
         prof0 = np.zeros(S)
+        prof[:len(shots)] = profile_table([sh.profile for sh in shots], 0, n_steps, dt, self._lib)
         for q, sh in enumerate(shots):
             prof0[q] = float(sh.profile(0.0))
-            for k in range(n_steps):
-                prof[q, k] = float(sh.profile(k * dt))
         n_rec = n_steps // record_every
         rows = np.zeros((max(n_rec, 1), max(len(self._probes), 1), S))
         norms = np.zeros((n_steps, S))
@@ -579,6 +580,29 @@ class CoupledStepper:
         b, f, s = C.c_double(), C.c_double(), C.c_double()
         self._lib.sfw_step_traffic(self._h, C.byref(b), C.byref(f), C.byref(s))
         return b.value, f.value, s.value
+
+
+def profile_table(profiles, k0: int, n: int, dt: float, lib=None) -> np.ndarray:
+    """[len(profiles), n] table of f(t_k), t_k = (k0 + k) * dt (the reference's int * float).
+
+    Pulses from ``pulses.py`` carry ``sfw_pulse`` and are tabulated by the library with the
+    same libm calls (bit-identical, tests/test_host_cpu.py); any other callable is evaluated
+    per step in Python, as the reference does.
+    """
+    tab = np.empty((len(profiles), n))
+    t_vals = None
+    for i, f in enumerate(profiles):
+        spec = getattr(f, "sfw_pulse", None)
+        if spec is not None and n > 0:
+            lib = lib or _lib.load()
+            rc = lib.sfw_pulse_table(int(spec[0]), float(spec[1]), float(spec[2]), int(k0), float(dt), int(n),
+                                     _lib.dptr(tab[i]))
+            if rc == 0:
+                continue
+        if t_vals is None:
+            t_vals = ((np.arange(n, dtype=np.float64) + float(k0)) * dt).tolist()
+        tab[i] = [float(v) for v in map(f, t_vals)]
+    return tab
 
 
 def chain_operator(model: SubdomainModel) -> np.ndarray:

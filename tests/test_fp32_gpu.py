@@ -69,3 +69,30 @@ def test_fp32_m9k8_vs_fp64():
     e = rel(r32, r64)
     print("fp32 m9k8 traces vs fp64", e)
     assert e < 1e-4
+
+
+@pytest.mark.parametrize("record_every", [1, 4])
+def test_fp32_chunked_run_equals_single_launch(record_every, monkeypatch):
+    """Chunked W-form runs (rows downloaded while later chunks compute) equal one launch bit for bit."""
+    g = load_golden("golden_c1.npz")
+    wl = make_workload(1, n_steps=int(g["n_steps"]))
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    models = models_from_arrays(part, wl.c_field, 4, g["gammas"], g["hats"], g["scales"], shift=wl.shift)
+    src = SourceTerm(tuple(int(x) for x in g["src_alpha"]), g["src_vec"], so.ricker(wl.f0, wl.delay))
+    probes = [Probe(a, w) for a, w in face_probes(models, wl)]
+    n = 161
+    out = {}
+    for mode in ("single", "chunked"):
+        if mode == "single":
+            monkeypatch.setenv("SFW_NO_CHUNK", "1")
+        else:
+            monkeypatch.delenv("SFW_NO_CHUNK")
+            monkeypatch.setenv("SFW_CHUNK_BYTES", "1")
+        with CoupledStepper(models, float(g["dt"]), sources=(src,), precision="fp32") as st:
+            t, r = st.run(n, probes=probes, record_every=record_every)
+            out[mode] = (t, r, st.u_curr)
+    (ts, rs, us), (tc, rc, uc) = out["single"], out["chunked"]
+    assert rs.shape == (1 + n // record_every, len(probes))
+    assert np.array_equal(ts, tc) and np.array_equal(rs, rc)
+    for a in us:
+        assert np.array_equal(us[a], uc[a])

@@ -139,3 +139,25 @@ def test_growth_limits_match_the_scalar_loop():
                 b += fake.dt * fake.dt * abs(float(prof[i, k])) * norms[i]
             ref.append(GROWTH_LIMIT * max(b, 1e-300))
         assert np.array_equal(lim, np.array(ref)) and base == b
+
+
+@pytest.mark.parametrize("name", ["ricker", "gauss_deriv"])
+def test_library_pulse_table_is_bit_identical_to_the_callable(name):
+    """sfw_pulse_table (host code in the library) equals per-step Python evaluation of
+    pulses.py bit for bit, so long runs may tabulate f(t_k) in the library."""
+    from paper_1406_6923_b200.pulses import PULSES
+    from paper_1406_6923_b200.stepper import profile_table
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        f0 = float(rng.uniform(2.0, 40.0))
+        delay = 1.2 / f0
+        dt = float(rng.uniform(1e-4, 3e-3))
+        k0 = int(rng.integers(0, 5000))
+        n = 20000
+        p = PULSES[name](f0, delay)
+        tab = profile_table([p], k0, n, dt, _lib.load(require_device=False))[0]
+        ref = np.array([p((k0 + k) * dt) for k in range(n)])
+        assert np.array_equal(tab, ref)
+    # any other callable goes through the per-step path
+    g = lambda t: 2.0 * t  # noqa: E731
+    assert np.array_equal(profile_table([g], 3, 5, 0.5)[0], [2.0 * (3 + k) * 0.5 for k in range(5)])
