@@ -1816,9 +1816,10 @@ __global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
 //   half-warp 0:  F_j       = Gamma_j (U_{j+1} - U_j)                 (j < L)
 //   half-warp 1:  acc_{j-1} = Gamma-hat_{j-1} (F_{j-1} - F_{j-2})     (j >= 1; F_{-1} = 0)
 // followed by the leapfrog of layer j-1 >= 1.  F_0 goes to a tagged face mailbox (value and step
-// tag in each 64-bit word, no flag round trip); acc_0 (outer-face rows) to acc1.  After the sweeps
-// of all its subdomains the warp updates their layer 0 from the neighbours' F_0, records norms
-// and probe rows.  Blocks are re-laid out for 16-B shared loads (u2_pos).
+// tag in each 64-bit word, no flag round trip); acc_0 (outer-face rows) to acc1.  The layer-0
+// update of step k for a subdomain (neighbours' F_0, masses, probes) runs right before that
+// subdomain's sweep of step k+1, a whole sweep after the neighbours published.  Blocks are
+// re-laid out for 16-B shared loads (u2_pos).
 __host__ __device__ constexpr int u2_nc1(int m) { return (m * m) / 2; }
 __host__ __device__ constexpr int u2_nc2(int m) { return tri_count(m) / 2; }
 __host__ __device__ constexpr int u2_tri_base(int m) { return 30 * u2_nc1(m); }
