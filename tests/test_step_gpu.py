@@ -153,7 +153,11 @@ def test_m9k8_stepping_parity_on_shared_coefficients(counts, env, monkeypatch):
     dt = 0.9 * 2.0 / math.sqrt(lam)
     src_alpha, row = locate(wl.sources[0], wl.counts, wl.p)
     vec = so.source_vector(models[src_alpha], row)
-    probes = face_probes(models, wl)
+    rng = np.random.default_rng(11)
+    order = sorted(models)
+    # face taps plus dense probes (every state entry weighted) on three subdomains
+    probes = face_probes(models, wl) + [(a, rng.standard_normal(models[a].state_size))
+                                        for a in (order[0], src_alpha, order[-1])]
     prof = so.ricker(wl.f0, wl.delay)
     ref_rows = so.Coupled(models, dt, sources=[(src_alpha, vec, prof)]).run(wl.n_steps, probes=probes)[1]
     # oracle's own summation-order floor: Fortran-ordered chain blocks
@@ -166,7 +170,10 @@ def test_m9k8_stepping_parity_on_shared_coefficients(counts, env, monkeypatch):
     floor = rel(alt_rows, ref_rows)
     tol = max(1e-9, 10 * floor)
     with CoupledStepper(models, dt, sources=(SourceTerm(src_alpha, vec, prof),)) as st:
-        _, rows = st.run(wl.n_steps, probes=[Probe(a, w) for a, w in probes])
+        gp = [Probe(a, w) for a, w in probes]
+        _, rows = st.run(wl.n_steps, probes=gp)
+        _, rows3 = st.run(wl.n_steps, probes=gp, record_every=3)
+    assert np.array_equal(rows3, rows[::3])  # sparse recording is the same arithmetic
     err = rel(rows, ref_rows)
     print(f"m9k8 trace rel err {err:.3e}, oracle floor {floor:.3e}")
     assert err <= tol
