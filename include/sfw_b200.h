@@ -249,6 +249,15 @@ int sfw_ntd_batch(int form, int n_models, int L, int w, const double* A, const d
                   int n_items, const int* item_model, const double* item_omega, double* out, int* status,
                   char* errbuf, int errlen);
 
+/* Transfer maps of an explicit operator (reference ntd.py:62-115 ntd_full / ntd_reduced):
+ * out[k] = sym(F^T (A + omegas[k]^2 I)^-1 F), A given as host CSR (n x n, row_ptr[n] nonzeros),
+ * F host [n][w] row-major.  Band LU with partial pivoting (LAPACK dgbtf2/dgbtrs order) on the
+ * device, one CTA per frequency.  resid[k] = ||A X + w^2 X - F||_F / ||F||_F (the reference's
+ * resonance measure); status[k] = 0, or j+1 for an exactly zero pivot in column j. */
+int sfw_ntd_operator(int n, const int* row_ptr, const int* col_idx, const double* vals, int w, const double* F,
+                     int n_omega, const double* omegas, double* out, double* resid, int* status, char* errbuf,
+                     int errlen);
+
 #ifdef __cplusplus
 }
 #endif

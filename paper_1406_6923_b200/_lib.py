@@ -76,6 +76,8 @@ SIGNATURES = {
     "sfw_fdtd_destroy": (C.c_int, [C.c_void_p]),
     "sfw_ntd_batch": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, PD, PD, PD, C.c_int, PI, PD, PD, PI, C.c_char_p,
                                 C.c_int]),
+    "sfw_ntd_operator": (C.c_int, [C.c_int, PI, PI, PD, C.c_int, PD, C.c_int, PD, PD, PD, PI, C.c_char_p,
+                                   C.c_int]),
 }
 
 _lib = None

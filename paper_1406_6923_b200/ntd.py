@@ -10,9 +10,13 @@ form (``ntd_tridiag``, ntd.py:101-146) and the S-fraction chain
 (model, frequency) (``sfw_ntd_batch``, csrc/sfw_ntd.cu).  ``frequency_band`` /
 ``nudge_off_poles`` are the reference's host bookkeeping.
 
-Not here: ``ntd_full`` / ``band_error`` (a sparse indefinite direct solve of
-the N x N operator per frequency) and ``ntd_reduced`` (needs the projected
-pair, which the GPU build does not keep).
+The explicit-operator forms -- ``ntd_full`` (the sparse N x N subdomain
+operator, ntd.py:62-98), ``ntd_reduced`` (the dense projected pair,
+ntd.py:101-115) and ``band_error`` (ntd.py:188-202) -- run on the device too
+(``sfw_ntd_operator``, csrc/sfw_ntdfull.cu): band LU with partial pivoting of
+A + w^2 I, one CTA per frequency, with the reference's residual-based
+resonance test.  The reference factors with SuperLU, so these agree with it to
+the conditioning of the shifted operator rather than bit for bit.
 """
 
 from __future__ import annotations
@@ -115,3 +119,67 @@ def ntd_batch(models, omegas, form: str = "chain") -> np.ndarray:
     else:
         raise ConfigError("form must be 'chain' or 'tridiag'")
     return out.reshape(nm, nw, *out.shape[1:])
+
+
+def _csr(matrix):
+    """Host CSR (int32 indices) of a scipy sparse matrix or a dense array."""
+    from scipy import sparse
+    m = matrix.tocsr() if sparse.issparse(matrix) else sparse.csr_matrix(np.asarray(matrix, dtype=float))
+    m.sort_indices()
+    return (np.ascontiguousarray(m.indptr, dtype=np.int32), np.ascontiguousarray(m.indices, dtype=np.int32),
+            np.ascontiguousarray(m.data, dtype=np.float64), m.shape[0])
+
+
+def _operator_maps(matrix, f, omegas):
+    rp, ci, val, n = _csr(matrix)
+    f = np.ascontiguousarray(np.asarray(f, dtype=float).reshape(n, -1))
+    om = np.ascontiguousarray(np.asarray(omegas, dtype=float).ravel())
+    w = f.shape[1]
+    out = np.empty((om.size, w, w))
+    resid = np.empty(om.size)
+    status = np.zeros(om.size, dtype=np.int32)
+    lib = _lib.load()
+    eb = _lib.errbuf()
+    _lib.check(lib.sfw_ntd_operator(n, _lib.iptr(rp), _lib.iptr(ci), _lib.dptr(val), w, _lib.dptr(f), om.size,
+                                    _lib.dptr(om), _lib.dptr(out), _lib.dptr(resid), _lib.iptr(status), eb, 1024),
+               eb, "sfw_ntd_operator")
+    return out, resid, status, om
+
+
+def ntd_full_band(matrix, f: np.ndarray, omegas) -> np.ndarray:
+    """ntd_full at many frequencies in one device call: array [len(omegas), w, w]."""
+    out, resid, status, om = _operator_maps(matrix, f, omegas)
+    for k, w in enumerate(om):
+        if status[k]:
+            raise NumericalError(f"transfer map solve failed at omega = {w:.6e}: matrix is exactly singular")
+        if not resid[k] <= RESONANCE_RTOL:
+            raise NumericalError(f"omega = {w:.6e} is resonant (relative residual {resid[k]:.2e}); "
+                                 "move the frequency off the operator spectrum")
+    return out
+
+
+def ntd_full(matrix, f: np.ndarray, omega: float) -> np.ndarray:
+    """F* (A + w^2 I)^-1 F of the full operator (ntd.py:62-98)."""
+    return ntd_full_band(matrix, f, [float(omega)])[0]
+
+
+def ntd_reduced(a_tilde: np.ndarray, f_tilde: np.ndarray, omega: float) -> np.ndarray:
+    """Transfer map of the Galerkin-projected pair (ntd.py:101-115)."""
+    out, _, status, _ = _operator_maps(np.asarray(a_tilde, dtype=float), f_tilde, [float(omega)])
+    if status[0]:
+        raise NumericalError(f"reduced transfer map is singular at omega = {float(omega):.6e}")
+    return out[0]
+
+
+def band_error(matrix, f: np.ndarray, a_tilde: np.ndarray, f_tilde: np.ndarray, omegas) -> float:
+    """Max relative deviation of the projected map from the full map (ntd.py:188-202)."""
+    om = np.asarray(omegas, dtype=float).ravel()
+    exact = ntd_full_band(matrix, f, om)
+    approx, _, status, _ = _operator_maps(np.asarray(a_tilde, dtype=float), f_tilde, om)
+    worst = 0.0
+    for k, w in enumerate(om):
+        if status[k]:
+            raise NumericalError(f"reduced transfer map is singular at omega = {w:.6e}")
+        denom = max(np.linalg.norm(exact[k]), 1e-300)
+        worst = max(worst, float(np.linalg.norm(approx[k] - exact[k]) / denom))
+    return worst

@@ -256,6 +256,28 @@ def golden_ntd():
     np.savez_compressed(os.path.join(HERE, "golden_ntd.npz"), **out)
 
 
+def golden_ntd_full():
+    """Reference ntd_full / ntd_reduced / band_error (ntd.py:62-115, 188-202) on one config-1
+    subdomain (N = 4913, w = 24): the face inputs F, the projected pair, and the maps."""
+    from sfwave.ntd import band_error, ntd_full, ntd_reduced
+    from sfwave.rom import build_krylov_basis, project_reduced, subdomain_inputs
+    wl = make_workload(1)
+    spec = DomainSpec(tuple((g - 1) * h for g, h in zip(wl.global_shape, wl.spacing)), wl.counts, wl.p)
+    part = build_partition(spec)
+    alpha = (0, 0, 0)
+    op = assemble_subdomain_operator(part, alpha, wl.c_field)
+    f_in = subdomain_inputs(op, wl.modes_per_face)
+    basis, _ = build_krylov_basis(op.matrix, f_in, wl.n, wl.shift)
+    a_t, f_t = project_reduced(basis, op.matrix, f_in)
+    omegas = np.geomspace(20.0, 400.0, 5)
+    full = np.stack([ntd_full(op.matrix, f_in, w) for w in omegas])
+    red = np.stack([ntd_reduced(a_t, f_t, w) for w in omegas])
+    out = {"alpha": np.array(alpha), "f": f_in, "omegas": omegas, "full": full, "a_tilde": a_t, "f_tilde": f_t,
+           "reduced": red, "band_error": band_error(op.matrix, f_in, a_t, f_t, omegas)}
+    print("ntd_full golden: band_error", out["band_error"])
+    np.savez_compressed(os.path.join(HERE, "golden_ntd_full.npz"), **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["toy", "c1", "m9k8", "io", "fdtd", "ntd"]
     if "toy" in which:
@@ -270,3 +292,5 @@ if __name__ == "__main__":
         golden_fdtd()
     if "ntd" in which:
         golden_ntd()
+    if "ntd_full" in which:
+        golden_ntd_full()

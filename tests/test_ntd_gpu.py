@@ -59,3 +59,44 @@ def test_singular_chain_raises():
     g = np.zeros((2, 3, 3))
     with pytest.raises(NumericalError):
         ntd_chain(g, g, 0.0)
+
+
+def _c1_operator():
+    wl = make_workload(1)
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    g = load_golden("golden_ntd_full.npz")
+    op = pg.assemble_subdomain_operator(part, tuple(int(x) for x in g["alpha"]), wl.c_field, with_matrix=True)
+    return op, g
+
+
+def test_ntd_full_reduced_and_band_error_vs_reference():
+    """Explicit-operator maps (ntd.py:62-115, 188-202) on the 4913-node config-1 subdomain.
+
+    Fixture: the reference's own ntd_full (SuperLU), ntd_reduced and band_error
+    (make_golden.py::golden_ntd_full).  The device solves by band LU with partial pivoting,
+    so the maps agree to the conditioning of A + w^2 I (measured on B200 in the print)."""
+    from paper_1406_6923_b200.ntd import band_error, ntd_full, ntd_full_band, ntd_reduced
+    op, g = _c1_operator()
+    om = g["omegas"]
+    full = ntd_full_band(op.matrix, g["f"], om)
+    e_full = _maxrel(full, g["full"])
+    red = np.stack([ntd_reduced(g["a_tilde"], g["f_tilde"], w) for w in om])
+    e_red = _maxrel(red, g["reduced"])
+    be = band_error(op.matrix, g["f"], g["a_tilde"], g["f_tilde"], om)
+    print("ntd_full", e_full, "ntd_reduced", e_red, "band_error", be, float(g["band_error"]))
+    assert e_full < 1e-9
+    assert e_red < 1e-9
+    assert abs(be - float(g["band_error"])) <= 1e-8 * float(g["band_error"])
+    assert np.array_equal(ntd_full(op.matrix, g["f"], om[2]), full[2])  # batch = single calls
+    assert np.array_equal(full, np.swapaxes(full, -1, -2))
+
+
+def test_ntd_full_resonance_raises():
+    """A frequency on the operator spectrum trips the reference's residual test (ntd.py:77-83)."""
+    from paper_1406_6923_b200.ntd import ntd_full
+    g = load_golden("golden_ntd_full.npz")
+    a = np.asarray(g["a_tilde"])
+    lam = np.linalg.eigvalsh(-a)
+    w_res = float(np.sqrt(lam[lam > 0][0]))
+    with pytest.raises(NumericalError):
+        ntd_full(a, g["f_tilde"], w_res)
