@@ -258,6 +258,11 @@ int sfw_ntd_operator(int n, const int* row_ptr, const int* col_idx, const double
                      int n_omega, const double* omegas, double* out, double* resid, int* status, char* errbuf,
                      int errlen);
 
+/* Face inputs F of one subdomain (reference rom.py:55-86 subdomain_inputs): out[c * N + node],
+ * N = px*py*pz, c < 6m, built by the ROM pipeline's own face-basis kernel.  nbr_mask bit f is
+ * set when face f is shared. */
+int sfw_face_inputs(int px, int py, int pz, int m, int nbr_mask, double* out, char* errbuf, int errlen);
+
 #ifdef __cplusplus
 }
 #endif

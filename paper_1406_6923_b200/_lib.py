@@ -78,6 +78,7 @@ SIGNATURES = {
                                 C.c_int]),
     "sfw_ntd_operator": (C.c_int, [C.c_int, PI, PI, PD, C.c_int, PD, C.c_int, PD, PD, PD, PI, C.c_char_p,
                                    C.c_int]),
+    "sfw_face_inputs": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, PD, C.c_char_p, C.c_int]),
 }
 
 _lib = None

@@ -713,6 +713,26 @@ struct DevBuf {
 };
 }  // namespace
 
+// Face inputs F of one subdomain (reference rom.py:55-86 subdomain_inputs), the same k_face_basis
+// the batched build uses: out[c * N + node] = column c of the N x 6m input matrix.
+extern "C" int sfw_face_inputs(int px, int py, int pz, int m, int nbr_mask, double* out, char* errbuf, int errlen) {
+    const int kk = (int)std::lround(std::sqrt((double)m));
+    if (m < 1 || kk * kk != m) return fail(SFW_ECONFIG, "modes per face must be a perfect square", errbuf, errlen);
+    const long long N = (long long)px * py * pz, w = 6LL * m;
+    double* V = nullptr;
+    int* dm = nullptr;
+    SFW_CUDA_TRY(cudaMalloc(&V, (size_t)N * w * 8));
+    SFW_CUDA_TRY(cudaMalloc(&dm, 4));
+    cudaMemset(V, 0, (size_t)N * w * 8);
+    cudaMemcpy(dm, &nbr_mask, 4, cudaMemcpyHostToDevice);
+    k_face_basis<<<dim3(6, 1), 128>>>(px, py, pz, m, kk, dm, V, N, N * w);
+    cudaError_t e = cudaMemcpy(out, V, (size_t)N * w * 8, cudaMemcpyDeviceToHost);
+    cudaFree(V);
+    cudaFree(dm);
+    if (e != cudaSuccess) return fail(SFW_ECUDA, cudaGetErrorString(e), errbuf, errlen);
+    return 0;
+}
+
 extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf, int errlen) {
     using clk = std::chrono::steady_clock;
     const int nsub = d->n_sub, m = d->m, n = d->n;

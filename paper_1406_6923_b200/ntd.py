@@ -183,3 +183,84 @@ def band_error(matrix, f: np.ndarray, a_tilde: np.ndarray, f_tilde: np.ndarray, 
         denom = max(np.linalg.norm(exact[k]), 1e-300)
         worst = max(worst, float(np.linalg.norm(approx[k] - exact[k]) / denom))
     return worst
+
+
+def subdomain_inputs(op, modes: int) -> np.ndarray:
+    """(N, 6 modes) face-input matrix F of a subdomain (rom.py:74-86), built on the device by the
+    ROM pipeline's face-basis kernel: orthonormal tensor cosine modes on each owned face window."""
+    px, py, pz = (int(s) for s in op.shape)
+    n = px * py * pz
+    out = np.empty((6 * modes, n))
+    mask = sum(1 << f for f in op.neighbors)
+    lib = _lib.load()
+    eb = _lib.errbuf()
+    _lib.check(lib.sfw_face_inputs(px, py, pz, int(modes), int(mask), _lib.dptr(out), eb, 1024), eb,
+               "sfw_face_inputs")
+    return np.ascontiguousarray(out.T)
+
+
+def _tridiag_pair(model):
+    """(T, [E; 0]): the block-Lanczos pair of a GPU-built model, assembled as ntd.py:130-139 does.
+    Its transfer map is the projected pair's (V^T A V, V^T F) up to the orthogonal Q."""
+    d = np.asarray(model.tdiag, dtype=float)
+    b = np.asarray(model.toff, dtype=float)
+    L, w = d.shape[0], d.shape[1]
+    t = np.zeros((L * w, L * w))
+    for j in range(L):
+        blk = slice(j * w, (j + 1) * w)
+        t[blk, blk] = d[j]
+        if j + 1 < L:
+            nxt = slice((j + 1) * w, (j + 2) * w)
+            t[nxt, blk] = b[j]
+            t[blk, nxt] = b[j].T
+    e = getattr(model, "entry", None)
+    ft = np.zeros((L * w, w))
+    ft[:w] = np.eye(w) if e is None else e
+    return t, ft
+
+
+def verify_subdomain(op, modes_per_face: int, shift: float, omegas, n_max: int = 5) -> dict:
+    """Transfer-map accuracy of one subdomain's reduction, depth by depth (sim.py:703-768).
+
+    ``op``: a subdomain operator with its host matrix (``grid.assemble_subdomain_operator(...,
+    with_matrix=True)``); ``omegas``: the verification band (the reference's ``source_band``).
+    For n = 1..n_max the GPU-built model's block-Lanczos pair is compared with the full
+    operator over the band (``band_error``); at n_max its reduced, tridiagonal and chain maps
+    are cross-checked at the quarter of the band farthest from the reduced spectrum.  Every
+    solve runs on the device; the pole ranking of the probe frequencies is host bookkeeping.
+    """
+    from .rom import build_models
+    if getattr(op, "matrix", None) is None:
+        raise ConfigError("verify_subdomain needs the operator matrix (assemble_subdomain_operator(..., "
+                          "with_matrix=True))")
+    om = np.asarray(omegas, dtype=float).ravel()
+    f = subdomain_inputs(op, modes_per_face)
+    exact = ntd_full_band(op.matrix, f, om)
+    rows = []
+    model = None
+    for n in range(1, n_max + 1):
+        model = build_models([op], modes_per_face, n, shift)[op.alpha]
+        t, ft = _tridiag_pair(model)
+        approx, _, status, _ = _operator_maps(t, ft, om)
+        worst = 0.0
+        for k, w in enumerate(om):
+            if status[k]:
+                raise NumericalError(f"reduced transfer map is singular at omega = {w:.6e}")
+            denom = max(np.linalg.norm(exact[k]), 1e-300)
+            worst = max(worst, float(np.linalg.norm(approx[k] - exact[k]) / denom))
+        rows.append((n, worst))
+    t, ft = _tridiag_pair(model)
+    poles = np.sqrt(np.maximum(-np.linalg.eigvalsh(t), 0.0))
+    probe = np.array(sorted(om, key=lambda w: -float(np.min(np.abs(poles - w)) / w))[:max(1, om.size // 4)])
+    base, _, status, _ = _operator_maps(t, ft, probe)
+    if status.any():
+        raise NumericalError(f"reduced transfer map is singular at omega = {probe[np.nonzero(status)[0][0]]:.6e}")
+    tri = ntd_batch([model], probe, "tridiag")[0]
+    chn = ntd_batch([model], probe, "chain")[0]
+    agreement = 0.0
+    for k in range(probe.size):
+        scale = max(float(np.linalg.norm(base[k])), 1e-300)
+        agreement = max(agreement, float(np.linalg.norm(tri[k] - base[k])) / scale,
+                        float(np.linalg.norm(chn[k] - base[k])) / scale)
+    return {"alpha": op.alpha, "omegas": om, "rows": rows, "agreement": agreement,
+            "truncated": bool(getattr(model, "truncated", False))}

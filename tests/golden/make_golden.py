@@ -275,6 +275,35 @@ def golden_ntd_full():
     out = {"alpha": np.array(alpha), "f": f_in, "omegas": omegas, "full": full, "a_tilde": a_t, "f_tilde": f_t,
            "reduced": red, "band_error": band_error(op.matrix, f_in, a_t, f_t, omegas)}
     print("ntd_full golden: band_error", out["band_error"])
+    # the verification sweep of sim.verify_subdomain (sim.py:703-768) on the same subdomain,
+    # band = source_band (SOURCE_BAND x 2 pi f0, 12 frequencies), depths 1..3
+    from sfwave.ntd import frequency_band, ntd_chain, ntd_tridiag
+    from sfwave.rom import block_lanczos
+    w_peak = 2.0 * math.pi * wl.f0
+    band = frequency_band(0.4 * w_peak, 1.6 * w_peak, 12)
+    rows = []
+    for n in range(1, 4):
+        bas, sizes = build_krylov_basis(op.matrix, f_in, n, wl.shift)
+        keep = 0
+        for size in sizes:
+            if size != f_in.shape[1]:
+                break
+            keep += 1
+        at, ft = project_reduced(bas[:, :keep * f_in.shape[1]], op.matrix, f_in)
+        rows.append(band_error(op.matrix, f_in, at, ft, band))
+    model = build_subdomain_model(op, wl.modes_per_face, 3, wl.shift)
+    chain = block_lanczos(at, ft)
+    poles = np.sqrt(np.maximum(-np.linalg.eigvalsh(at), 0.0))
+    probe = sorted(band, key=lambda w: -float(np.min(np.abs(poles - w)) / w))
+    agreement = 0.0
+    for w in probe[:max(1, len(band) // 4)]:
+        base = ntd_reduced(at, ft, w)
+        scale = max(float(np.linalg.norm(base)), 1e-300)
+        tri = ntd_tridiag(chain.diag_blocks, chain.off_blocks, chain.entry_block, w)
+        chn = ntd_chain(model.gammas, model.gamma_hats, w)
+        agreement = max(agreement, float(np.linalg.norm(tri - base)) / scale, float(np.linalg.norm(chn - base)) / scale)
+    out.update({"verify_band": band, "verify_rows": np.array(rows), "verify_agreement": agreement})
+    print("verify rows", rows, "agreement", agreement)
     np.savez_compressed(os.path.join(HERE, "golden_ntd_full.npz"), **out)
 
 

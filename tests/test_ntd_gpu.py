@@ -100,3 +100,20 @@ def test_ntd_full_resonance_raises():
     w_res = float(np.sqrt(lam[lam > 0][0]))
     with pytest.raises(NumericalError):
         ntd_full(a, g["f_tilde"], w_res)
+
+
+def test_face_inputs_and_verification_sweep_vs_reference():
+    """subdomain_inputs (rom.py:74-86) and the verify_subdomain sweep (sim.py:703-768) on the
+    config-1 subdomain: depth-by-depth band errors of the GPU-built reductions against the
+    reference's own sweep, and the reduced / tridiagonal / chain cross-check."""
+    from paper_1406_6923_b200.ntd import subdomain_inputs, verify_subdomain
+    op, g = _c1_operator()
+    wl = make_workload(1)
+    f = subdomain_inputs(op, wl.modes_per_face)
+    assert np.allclose(f, g["f"], rtol=0, atol=1e-15)
+    res = verify_subdomain(op, wl.modes_per_face, wl.shift, g["verify_band"], n_max=3)
+    rows = np.array([e for _, e in res["rows"]])
+    print("verify rows", rows, g["verify_rows"], "agreement", res["agreement"], float(g["verify_agreement"]))
+    assert [n for n, _ in res["rows"]] == [1, 2, 3]
+    assert np.allclose(rows, g["verify_rows"], rtol=1e-6, atol=0)
+    assert res["agreement"] < 1e-9 and not res["truncated"]
