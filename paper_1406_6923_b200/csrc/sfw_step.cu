@@ -2519,6 +2519,7 @@ static void free_all(sfw_stepper* h) {
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->dstream) cudaStreamDestroy(h->dstream);
+    if (h->pin) cudaFreeHost(h->pin);
 }
 
 
@@ -2574,7 +2575,14 @@ static int set_probes(sfw_stepper* h, int n_probe, const int* probe_sub, const d
 
 extern "C" int sfw_step_set_probes(sfw_stepper* h, int n_probe, const int* probe_sub, const double* probe_w,
                                    char* errbuf, int errlen) {
-    return set_probes(h, n_probe, probe_sub, probe_w, errbuf, errlen);
+    const int rc = set_probes(h, n_probe, probe_sub, probe_w, errbuf, errlen);
+    if (rc == 0 && n_probe > 0 && !h->pin) {  // staging ring for chunked row downloads (chunk_plan caps a
+        if (cudaMallocHost(reinterpret_cast<void**>(&h->pin), 2 * kChunkSlotBytes) == cudaSuccess)  // chunk at one slot)
+            h->pin_cap = 2 * kChunkSlotBytes;
+        else
+            h->pin = nullptr;
+    }
+    return rc;
 }
 
 extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* errbuf, int errlen) {
@@ -3183,10 +3191,9 @@ static int run_common(sfw_stepper* h, int n_steps, int record_every, const doubl
     rc = ensure(h, &h->norm_part, &h->norm_cap, (long long)n_steps * h->grid * (h->klw ? h->lw_groups : 1), errbuf,
                 errlen);
     if (rc) return rc;
-    if (!h->norms) {
-        rc = dalloc(&h->norms, 1, errbuf, errlen);
-    }
-    return rc;
+    // grown here, before any launch: a cudaFree after the launches would wait for the whole run
+    // and serialise the overlapped row downloads behind it
+    return ensure(h, &h->norms, &h->norms_cap, std::max(1, n_steps), errbuf, errlen);
 }
 
 extern "C" int sfw_step_run(sfw_stepper* h, int n_steps, int record_every, const double* profile,
@@ -3196,23 +3203,19 @@ extern "C" int sfw_step_run(sfw_stepper* h, int n_steps, int record_every, const
     int rc = run_common(h, n_steps, record_every, profile, errbuf, errlen);
     if (rc || n_steps <= 0) return rc;
     const long long nrec = n_steps / record_every;
-    // Large probe-row downloads are split: the run is launched as up to 16 chunks of whole
+    // Large probe-row downloads are split (chunk_plan): the run is launched as chunks of whole
     // record intervals, and chunk c's rows are copied (on a second stream, into the caller's
     // pageable buffer) while chunks c+1.. compute.  Same kernels, same arithmetic: a chunk
     // boundary only re-enters the persistent kernel with the state, tags and parity it left.
-    const long long row_bytes = nrec * h->n_probe * 8;
-    int n_chunks = 1;
-    long long chunk_min = 8LL << 20;
-    if (const char* e = getenv("SFW_CHUNK_BYTES")) chunk_min = atoll(e);  // test hook
-    if (rows_out && row_bytes >= chunk_min && nrec >= 16 && !getenv("SFW_NO_CHUNK")) n_chunks = 16;
-    const long long rec_per = (nrec + n_chunks - 1) / n_chunks;
+    const std::vector<long long> plan = chunk_plan(nrec, nrec * h->n_probe * 8, rows_out != nullptr);
+    const int n_chunks = (int)plan.size() - 1;
     std::vector<cudaEvent_t> evs;
     if (n_chunks > 1 && !h->dstream) SFW_CUDA_TRY(cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking));
-    std::vector<std::pair<long long, long long>> rec_range;
-    for (long long r0 = 0; r0 < nrec || (r0 == 0 && n_chunks == 1); r0 += rec_per) {
+    if (n_chunks > 1) SFW_CUDA_TRY(ensure_row_staging(h, plan, h->n_probe));
+    for (int c = 0; c < n_chunks; ++c) {
+        const long long r0 = plan[c], r1 = plan[c + 1];
         const int s0 = (int)(r0 * record_every);
-        const long long r1 = std::min(nrec, r0 + rec_per);
-        const int s1 = (n_chunks == 1 || r1 == nrec) ? n_steps : (int)(r1 * record_every);
+        const int s1 = (c == n_chunks - 1) ? n_steps : (int)(r1 * record_every);
         rc = launch_step(h, 0, s1 - s0, record_every, n_steps, errbuf, errlen, nullptr, nullptr, s0);
         if (rc) return rc;
         h->cur ^= ((s1 - s0) & 1);
@@ -3221,29 +3224,17 @@ extern "C" int sfw_step_run(sfw_stepper* h, int n_steps, int record_every, const
             SFW_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             SFW_CUDA_TRY(cudaEventRecord(e, h->stream));
             evs.push_back(e);
-            rec_range.push_back({r0, r1});
         }
-        if (n_chunks == 1) break;
     }
-    cudaFree(h->norms);
-    h->norms = nullptr;
-    rc = dalloc(&h->norms, n_steps, errbuf, errlen);
-    if (rc) return rc;
     k_norms<<<(n_steps + 127) / 128, 128, 0, h->stream>>>(h->norm_part, n_steps, h->grid,
                                                           h->klw ? h->lw_groups : 1, h->norms);
     std::vector<double> nrm(n_steps);
-    SFW_CUDA_TRY(cudaMemcpyAsync(nrm.data(), h->norms, (size_t)n_steps * 8, cudaMemcpyDeviceToHost, h->stream));
-    if (n_chunks > 1) {
-        for (size_t c = 0; c < evs.size(); ++c) {  // each pageable copy returns when done; later chunks keep running
-            const long long a = rec_range[c].first, b = rec_range[c].second;
-            SFW_CUDA_TRY(cudaStreamWaitEvent(h->dstream, evs[c], 0));
-            if (b > a)
-                SFW_CUDA_TRY(cudaMemcpyAsync(rows_out + a * h->n_probe, h->rows + a * h->n_probe,
-                                             (size_t)(b - a) * h->n_probe * 8, cudaMemcpyDeviceToHost, h->dstream));
-        }
-        SFW_CUDA_TRY(cudaStreamSynchronize(h->dstream));
+    if (n_chunks > 1) {  // rows first: the pageable norm copy below blocks until the run ends
+        SFW_CUDA_TRY(download_rows_overlapped(h, plan, evs, h->rows, rows_out, h->n_probe));
         for (cudaEvent_t e : evs) cudaEventDestroy(e);
-    } else if (rows_out && nrec * h->n_probe > 0) {
+    }
+    SFW_CUDA_TRY(cudaMemcpyAsync(nrm.data(), h->norms, (size_t)n_steps * 8, cudaMemcpyDeviceToHost, h->stream));
+    if (n_chunks == 1 && rows_out && nrec * h->n_probe > 0) {
         SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost,
                                      h->stream));
     }

@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -28,6 +31,34 @@ inline int upload(T** p, const std::vector<T>& v, char* errbuf, int errlen) {
     return 0;
 }
 
+
+constexpr long long kChunkSlotBytes = 8LL << 20;  // one slot of the pinned row-staging ring
+
+// Record boundaries 0 = b_0 < b_1 < ... < b_n = nrec of a run whose probe rows download while
+// later chunks compute (sfw_step_run, sfw_wform_run).  One chunk when the rows are small; else
+// n-1 equal chunks over the first 97% of the records and a short last chunk, whose download is
+// the only one not hidden behind compute.  SFW_NO_CHUNK / SFW_CHUNK_BYTES / SFW_NCHUNK: hooks.
+inline std::vector<long long> chunk_plan(long long nrec, long long row_bytes, bool have_rows) {
+    std::vector<long long> b{0};
+    long long chunk_min = 8LL << 20;
+    if (const char* e = std::getenv("SFW_CHUNK_BYTES")) chunk_min = std::atoll(e);
+    if (!have_rows || std::getenv("SFW_NO_CHUNK") || row_bytes < chunk_min || nrec < 16) {
+        b.push_back(nrec);
+        return b;
+    }
+    // >= 8 chunks, and enough that every chunk fits one staging slot (kChunkSlotBytes)
+    int n = (int)std::min<long long>(64, std::max<long long>(8, 2 + row_bytes / kChunkSlotBytes));
+    if (const char* e = std::getenv("SFW_NCHUNK")) n = std::max(2, std::min(64, std::atoi(e)));
+    const long long tail = std::max(1LL, nrec * 3 / 100), head = nrec - tail;
+    for (int c = 1; c < n; ++c) {
+        const long long v = head * c / (n - 1);
+        if (v > b.back()) b.push_back(v);
+    }
+    if (nrec > b.back()) b.push_back(nrec);
+    return b;
+}
+
+
 }  // namespace sfw
 
 struct sfw_stepper {
@@ -39,6 +70,8 @@ struct sfw_stepper {
     std::vector<long long> soff, src_len, prb_len;
     cudaStream_t stream = nullptr;
     cudaStream_t dstream = nullptr;  // probe-row downloads overlapped with later step chunks
+    double* pin = nullptr;            // 2-slot pinned staging ring for those downloads
+    size_t pin_cap = 0;               // bytes
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double* coef = nullptr;
     long long* seq = nullptr;
@@ -58,6 +91,7 @@ struct sfw_stepper {
     double* rows = nullptr;
     long long rows_cap = 0;
     double *sub_norm = nullptr, *norm_part = nullptr, *norms = nullptr;
+    long long norms_cap = 0;  // capacity of norms (grown, never freed per run: cudaFree would sync the device)
     long long norm_cap = 0;
     unsigned int* bar = nullptr;
     double* scales = nullptr;  // dense G_j (energy), may be null
@@ -101,4 +135,56 @@ struct sfw_stepper {
     unsigned int* sflags = nullptr;   // k_step_ms3: [n_sub][4] F_0 publication tags
     unsigned int stag = 0;            // k_step_ms3: last tag used
 };
+
+namespace sfw {
+// Pinned staging for download_rows_overlapped, grown before any launch of the run (a pinned
+// allocation must not wait behind the run it is meant to overlap).
+inline cudaError_t ensure_row_staging(sfw_stepper* h, const std::vector<long long>& plan, long long n_probe) {
+    size_t maxb = 0;
+    for (size_t c = 0; c + 1 < plan.size(); ++c) maxb = std::max<size_t>(maxb, (size_t)(plan[c + 1] - plan[c]) * n_probe * 8);
+    if (h->pin_cap >= 2 * maxb && h->pin) return cudaSuccess;
+    if (h->pin) cudaFreeHost(h->pin);
+    h->pin = nullptr;
+    h->pin_cap = 0;
+    cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&h->pin), 2 * maxb);
+    if (e == cudaSuccess) h->pin_cap = 2 * maxb;
+    return e;
+}
+
+// Rows [plan[c], plan[c+1]) of chunk c (n_probe doubles per record) go device -> pinned slot c&1
+// on dstream once chunk c's event fires, then pinned -> the caller's pageable array on the host
+// while the DMA of chunk c+1 and the compute of later chunks proceed.
+inline cudaError_t download_rows_overlapped(sfw_stepper* h, const std::vector<long long>& plan,
+                                            const std::vector<cudaEvent_t>& evs, const double* dev, double* host,
+                                            long long n_probe) {
+    const int n = (int)plan.size() - 1;
+    const size_t slot = h->pin_cap / 2 / 8;
+    std::vector<cudaEvent_t> done(n, nullptr);
+    cudaError_t err = cudaSuccess;
+    auto issue = [&](int c) {
+        const size_t bytes = (size_t)(plan[c + 1] - plan[c]) * n_probe * 8;
+        cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming);
+        cudaStreamWaitEvent(h->dstream, evs[c], 0);
+        if (bytes) {
+            cudaError_t e = cudaMemcpyAsync(h->pin + (c & 1) * slot, dev + plan[c] * n_probe, bytes,
+                                            cudaMemcpyDeviceToHost, h->dstream);
+            if (e != cudaSuccess) err = e;
+        }
+        cudaEventRecord(done[c], h->dstream);
+    };
+    issue(0);
+    for (int c = 1; c <= n; ++c) {
+        if (c < n) issue(c);
+        const int p = c - 1;
+        cudaError_t e = cudaEventSynchronize(done[p]);
+        if (e != cudaSuccess) err = e;
+        const size_t bytes = (size_t)(plan[p + 1] - plan[p]) * n_probe * 8;
+        if (bytes && err == cudaSuccess) std::memcpy(host + plan[p] * n_probe, h->pin + (p & 1) * slot, bytes);
+    }
+    for (cudaEvent_t e : done) cudaEventDestroy(e);
+    return err;
+}
+
+}  // namespace sfw
+
 

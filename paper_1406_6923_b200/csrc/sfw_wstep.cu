@@ -892,19 +892,17 @@ extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, cons
         if ((rc = dalloc(&ws->norm, (size_t)n_steps * nwg, errbuf, errlen))) return rc;
         ws->norm_cap = (long long)n_steps * nwg;
     }
-    // large probe-row downloads overlap later chunks of the run (as sfw_step_run)
-    long long chunk_min = 8LL << 20;
-    if (const char* e = getenv("SFW_CHUNK_BYTES")) chunk_min = atoll(e);  // test hook
-    const int n_chunks = (rows_out && nrec * h->n_probe * 8 >= chunk_min && nrec >= 16 && !getenv("SFW_NO_CHUNK")) ? 16 : 1;
-    const long long rec_per = (nrec + n_chunks - 1) / n_chunks;
+    // large probe-row downloads overlap later chunks of the run (chunk_plan, as sfw_step_run)
+    const std::vector<long long> plan = chunk_plan(nrec, nrec * h->n_probe * 8, rows_out != nullptr);
+    const int n_chunks = (int)plan.size() - 1;
     if (n_chunks > 1 && !h->dstream) SFW_CUDA_TRY(cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking));
+    if (n_chunks > 1) SFW_CUDA_TRY(ensure_row_staging(h, plan, h->n_probe));
     std::vector<cudaEvent_t> evs;
-    std::vector<std::pair<long long, long long>> rr;
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
-    for (long long r0 = 0;; r0 += rec_per) {
+    for (int c = 0; c < n_chunks; ++c) {
+        const long long r0 = plan[c], r1 = plan[c + 1];
         const int s0 = (int)(r0 * record_every);
-        const long long r1 = std::min(nrec, r0 + rec_per);
-        const int s1 = (n_chunks == 1 || r1 == nrec) ? n_steps : (int)(r1 * record_every);
+        const int s1 = (c == n_chunks - 1) ? n_steps : (int)(r1 * record_every);
         if ((rc = wf_launch(h, ws, 0, s1 - s0, record_every, n_steps, errbuf, errlen, s0))) return rc;
         ws->cur ^= ((s1 - s0) & 1);
         if (n_chunks > 1) {
@@ -912,25 +910,17 @@ extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, cons
             SFW_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             SFW_CUDA_TRY(cudaEventRecord(e, h->stream));
             evs.push_back(e);
-            rr.push_back({r0, r1});
         }
-        if (s1 == n_steps) break;
     }
     SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
     std::vector<double> part((size_t)n_steps * nwg);
+    if (n_chunks > 1) {  // rows first: the pageable norm copy below blocks until the run ends
+        SFW_CUDA_TRY(download_rows_overlapped(h, plan, evs, h->rows, rows_out, h->n_probe));
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    }
     if (norms_out)
         SFW_CUDA_TRY(cudaMemcpyAsync(part.data(), ws->norm, part.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-    if (n_chunks > 1) {
-        for (size_t c = 0; c < evs.size(); ++c) {
-            const long long a = rr[c].first, b = rr[c].second;
-            SFW_CUDA_TRY(cudaStreamWaitEvent(h->dstream, evs[c], 0));
-            if (b > a)
-                SFW_CUDA_TRY(cudaMemcpyAsync(rows_out + a * h->n_probe, h->rows + a * h->n_probe,
-                                             (size_t)(b - a) * h->n_probe * 8, cudaMemcpyDeviceToHost, h->dstream));
-        }
-        SFW_CUDA_TRY(cudaStreamSynchronize(h->dstream));
-        for (cudaEvent_t e : evs) cudaEventDestroy(e);
-    } else if (rows_out && nrec * h->n_probe > 0) {
+    if (n_chunks == 1 && rows_out && nrec * h->n_probe > 0) {
         SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost, h->stream));
     }
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
