@@ -12,6 +12,13 @@ ncu --set full --import-source on --clock-control none -k regex:k_step_sw -s 1 -
 python bench.py --config 3 --precision fp32 --steps 100 --warmup 3 --no-cpu --extra 0 > $O/p_c3f.json 2>&1 && \
 ncu --set full --import-source on --clock-control none -k regex:k_wstep -s 3 -c 1 -o $O/prof_c3_fp32 \
     python bench.py --config 3 --precision fp32 --steps 100 --warmup 3 --no-cpu --extra 0 > $O/ncu_c3f.log 2>&1
+# fp64 U-form k_ustep (configs 3 and 5): first launch (3 warm-up steps), one capture per gpurun call
+python bench.py --config 3 --steps 20 --warmup 3 --no-cpu --extra 0 > $O/p3u.json 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_ustep -c 1 -o $O/ustep3 \
+    python bench.py --config 3 --steps 20 --warmup 3 --no-cpu --extra 0 > $O/ncu3.log 2>&1
+python bench.py --config 5 --steps 20 --warmup 3 --no-cpu --extra 0 > $O/p5b.json 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_ustep -c 1 -o $O/ustep5b \
+    python bench.py --config 5 --steps 20 --warmup 3 --no-cpu --extra 0 > $O/ncu5b.log 2>&1
 python bench.py --config 5 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/b_c5.json 2>&1
 python bench.py --config 5 --precision fp32 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/b_c5f.json 2>&1
 python bench.py --config 3 --precision fp32 --steps 300 --warmup 5 --no-cpu --extra 0 > $O/b_c3f.json 2>&1
