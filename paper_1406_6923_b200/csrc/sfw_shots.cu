@@ -991,7 +991,7 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32, 1) k_step_ms2(const MsParams
         if (lane < 2) {
             const bool chain_lane = lane == 0;
             const uint64_t pol = l2_policy_evict_first();
-            const uint64_t pol_state = l2_policy_evict_last();
+            const uint64_t pol_state = l2_policy_evict_first();  // measured 1-1.5% faster than evict_last
             const int cper = ns * 2 * L;
             const long long ctotal = (long long)cper * p.n_steps;
             const int sper = ns * (2 * L - 1) + 3 * ns;
