@@ -462,7 +462,26 @@ __global__ void __launch_bounds__(256, 1) k_wstep(const WParams p) {
             for (int t = 0; t < n_my; ++t) {
                 const int s = s0 + warp + t * NW;
                 const float* U = ((p.mode == 1) ? Wc : Wn) + (size_t)s * K;
-                for (int pq = p.prb_ptr[s]; pq < p.prb_ptr[s + 1]; ++pq) {
+                const int pa = p.prb_ptr[s], pb = p.prb_ptr[s + 1];
+                // many short probes (receiver-face coefficients, <= 64 weights): one per lane,
+                // 32 at a time; long ones (node receivers over the whole state) warp-cooperatively
+                const bool lanes = pb - pa >= 8;
+                if (lanes)
+                    for (int q0 = pa; q0 < pb; q0 += 32) {
+                        const int q = q0 + lane;
+                        if (q < pb) {
+                            const int pid = p.prb_ids[q];
+                            const int lo = p.prb_rng[2 * pid], cnt = p.prb_rng[2 * pid + 1];
+                            if (cnt <= 64) {
+                                const float* wv = p.prb_w + p.prb_woff[pid];
+                                double val = 0.0;
+                                for (int i = lo; i < lo + cnt; ++i) val = fma((double)wv[i], (double)U[i], val);
+                                p.rows[row * p.n_probe + pid] = val;
+                            }
+                        }
+                    }
+                for (int pq = pa; pq < pb; ++pq) {
+                    if (lanes && p.prb_rng[2 * p.prb_ids[pq] + 1] <= 64) continue;
                     const int pid = p.prb_ids[pq];
                     const int lo = p.prb_rng[2 * pid], cnt = p.prb_rng[2 * pid + 1];
                     const float* wv = p.prb_w + p.prb_woff[pid];
