@@ -846,15 +846,15 @@ extern "C" int sfw_wform_init(sfw_stepper* h, const double* u0, const double* v0
         if (which == 0) {
             dst = ws->W[0];
         } else {
-            if (!src) {
-                if (ws->V0) cudaMemset(ws->V0, 0, n * 4);
+            if (!src) {  // stream-ordered: the legacy-stream cudaMemset would not order with h->stream
+                if (ws->V0) cudaMemsetAsync(ws->V0, 0, n * 4, h->stream);
                 continue;
             }
             if (!ws->V0 && (rc = dalloc(&ws->V0, n, errbuf, errlen))) return rc;
             dst = ws->V0;
         }
         if (!src) {
-            cudaMemset(dst, 0, n * 4);
+            cudaMemsetAsync(dst, 0, n * 4, h->stream);
             continue;
         }
         std::vector<double> out(n);
