@@ -15,6 +15,15 @@ namespace sfw {
 void set_error(int code, const std::string& msg);
 int fail(int code, const std::string& msg, char* errbuf, int errlen);
 
+// Pageable host -> device copy that has landed when it returns.  cudaMemcpy from pageable memory
+// may return with the DMA still in flight on the legacy stream, and kernels on the library's
+// non-blocking streams do not order with that stream.
+inline cudaError_t sfw_h2d(void* dst, const void* src, size_t bytes) {
+    cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(0);
+}
+
 #define SFW_CUDA_TRY(expr)                                                            \
     do {                                                                              \
         cudaError_t _e = (expr);                                                      \

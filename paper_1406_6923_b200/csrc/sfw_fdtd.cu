@@ -347,7 +347,7 @@ extern "C" int sfw_fdtd_create(int nx, int ny, int nz, const double* scales, con
     cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     cudaEventCreate(&h->ev0);
     cudaEventCreate(&h->ev1);
-    SFW_CUDA_TRY(cudaMemcpy(h->c, c, h->n * 8, cudaMemcpyHostToDevice));
+    SFW_CUDA_TRY(sfw_h2d(h->c, c, h->n * 8));
     *out = h;
     return 0;
 }
@@ -430,13 +430,13 @@ extern "C" int sfw_fdtd_setup(sfw_fdtd* h, int n_src, const long long* src_idx, 
         (rc = fd_alloc(&h->rec, n_rec, errbuf, errlen)))
         return rc;
     if (n_src) {
-        SFW_CUDA_TRY(cudaMemcpy(h->src, src_idx, n_src * 8, cudaMemcpyHostToDevice));
-        SFW_CUDA_TRY(cudaMemcpy(h->srcv, src_val, n_src * 8, cudaMemcpyHostToDevice));
+        SFW_CUDA_TRY(sfw_h2d(h->src, src_idx, n_src * 8));
+        SFW_CUDA_TRY(sfw_h2d(h->srcv, src_val, n_src * 8));
     }
-    if (n_rec) SFW_CUDA_TRY(cudaMemcpy(h->rec, rec_idx, n_rec * 8, cudaMemcpyHostToDevice));
+    if (n_rec) SFW_CUDA_TRY(sfw_h2d(h->rec, rec_idx, n_rec * 8));
     if (damping) {
         if ((rc = fd_alloc(&h->damp, h->n, errbuf, errlen))) return rc;
-        SFW_CUDA_TRY(cudaMemcpy(h->damp, damping, h->n * 8, cudaMemcpyHostToDevice));
+        SFW_CUDA_TRY(sfw_h2d(h->damp, damping, h->n * 8));
     }
     h->n_src = n_src;
     h->n_rec = n_rec;

@@ -127,8 +127,8 @@ static int maps_common(int L, int w, const double* G, const double* row, double 
         cleanup();
         return fail(SFW_ECUDA, "cudaMalloc failed in chain maps", errbuf, errlen);
     }
-    cudaMemcpy(dG, G, K * w * 8, cudaMemcpyHostToDevice);
-    cudaMemcpy(dv, row, K * 8, cudaMemcpyHostToDevice);
+    sfw_h2d(dG, G, K * w * 8);
+    sfw_h2d(dv, row, K * 8);
     cudaMemset(dst, 0, L * sizeof(int));
     if (kind == 0) {
         // coeff = row * (amp / c); leak check on the first block; zero it; apply G_j

@@ -241,11 +241,11 @@ extern "C" int sfw_ntd_batch(int form, int n_models, int L, int w, const double*
     SFW_CUDA_TRY(cudaMalloc(&dout, (size_t)n_items * ww * 8));
     SFW_CUDA_TRY(cudaMalloc(&dmod, n_items * 4));
     SFW_CUDA_TRY(cudaMalloc(&dst, n_items * 4));
-    SFW_CUDA_TRY(cudaMemcpy(dA, A, na * 8, cudaMemcpyHostToDevice));
-    if (form == 1 || L > 1) SFW_CUDA_TRY(cudaMemcpy(dB, B, nb * 8, cudaMemcpyHostToDevice));
-    if (form == 0) SFW_CUDA_TRY(cudaMemcpy(dE, E, (size_t)n_models * ww * 8, cudaMemcpyHostToDevice));
-    SFW_CUDA_TRY(cudaMemcpy(dom, item_omega, n_items * 8, cudaMemcpyHostToDevice));
-    SFW_CUDA_TRY(cudaMemcpy(dmod, item_model, n_items * 4, cudaMemcpyHostToDevice));
+    SFW_CUDA_TRY(sfw_h2d(dA, A, na * 8));
+    if (form == 1 || L > 1) SFW_CUDA_TRY(sfw_h2d(dB, B, nb * 8));
+    if (form == 0) SFW_CUDA_TRY(sfw_h2d(dE, E, (size_t)n_models * ww * 8));
+    SFW_CUDA_TRY(sfw_h2d(dom, item_omega, n_items * 8));
+    SFW_CUDA_TRY(sfw_h2d(dmod, item_model, n_items * 4));
     NtdArgs a{form, L, w, dA, dB, dE, dmod, dom, dout, dst};
     const size_t smem = 6 * ww * 8 + (size_t)w * 4 + 16;
     SFW_CUDA_TRY(cudaFuncSetAttribute(k_ntd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -263,7 +263,7 @@ extern "C" int sfw_ntd_batch(int form, int n_models, int L, int w, const double*
         int* ditems = nullptr;
         SFW_CUDA_TRY(cudaMalloc(&work, fb.size() * per * 8));
         SFW_CUDA_TRY(cudaMalloc(&ditems, fb.size() * 4));
-        SFW_CUDA_TRY(cudaMemcpy(ditems, fb.data(), fb.size() * 4, cudaMemcpyHostToDevice));
+        SFW_CUDA_TRY(sfw_h2d(ditems, fb.data(), fb.size() * 4));
         k_ntd_assembled<<<(unsigned)fb.size(), 256>>>(a, ditems, work);
         cudaError_t e = cudaDeviceSynchronize();
         cudaFree(work);

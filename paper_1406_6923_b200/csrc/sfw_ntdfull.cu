@@ -252,13 +252,13 @@ extern "C" int sfw_ntd_operator(int n, const int* row_ptr, const int* col_idx, c
     GB_TRY(cudaMalloc(&dout, (size_t)n_omega * w * w * 8));
     GB_TRY(cudaMalloc(&dres, n_omega * 8));
     GB_TRY(cudaMalloc(&dst, n_omega * 4));
-    GB_TRY(cudaMemcpy(drp, row_ptr, (n + 1) * 4, cudaMemcpyHostToDevice));
+    GB_TRY(sfw_h2d(drp, row_ptr, (n + 1) * 4));
     if (nnz) {
-        GB_TRY(cudaMemcpy(dci, col_idx, nnz * 4, cudaMemcpyHostToDevice));
-        GB_TRY(cudaMemcpy(dval, vals, (size_t)nnz * 8, cudaMemcpyHostToDevice));
+        GB_TRY(sfw_h2d(dci, col_idx, nnz * 4));
+        GB_TRY(sfw_h2d(dval, vals, (size_t)nnz * 8));
     }
-    GB_TRY(cudaMemcpy(dF, F, (size_t)n * w * 8, cudaMemcpyHostToDevice));
-    GB_TRY(cudaMemcpy(dom, omegas, n_omega * 8, cudaMemcpyHostToDevice));
+    GB_TRY(sfw_h2d(dF, F, (size_t)n * w * 8));
+    GB_TRY(sfw_h2d(dom, omegas, n_omega * 8));
     for (int s0 = 0; s0 < n_omega; s0 += batch) {
         const int nb = std::min(batch, n_omega - s0);
         GbArgs ga{n, kl, ku, ldab, w, drp, dci, dval, dF, dom + s0, dab, dpiv, dX,

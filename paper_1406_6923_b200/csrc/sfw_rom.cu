@@ -724,7 +724,7 @@ extern "C" int sfw_face_inputs(int px, int py, int pz, int m, int nbr_mask, doub
     SFW_CUDA_TRY(cudaMalloc(&V, (size_t)N * w * 8));
     SFW_CUDA_TRY(cudaMalloc(&dm, 4));
     cudaMemset(V, 0, (size_t)N * w * 8);
-    cudaMemcpy(dm, &nbr_mask, 4, cudaMemcpyHostToDevice);
+    sfw_h2d(dm, &nbr_mask, 4);
     k_face_basis<<<dim3(6, 1), 128>>>(px, py, pz, m, kk, dm, V, N, N * w);
     cudaError_t e = cudaMemcpy(out, V, (size_t)N * w * 8, cudaMemcpyDeviceToHost);
     cudaFree(V);

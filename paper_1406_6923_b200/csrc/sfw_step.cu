@@ -2581,6 +2581,14 @@ extern "C" int sfw_step_set_probes(sfw_stepper* h, int n_probe, const int* probe
             h->pin_cap = 2 * kChunkSlotBytes;
         else
             h->pin = nullptr;
+        // first use of everything a recorded run touches besides the stepping kernel (download
+        // stream, pinned DMA, k_norms module load): paid here, not inside the first run
+        if (!h->dstream) cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking);
+        if (h->pin && h->dstream && h->U[0]) {  // n_steps = 0: k_norms touches nothing
+            k_norms<<<1, 32, 0, h->dstream>>>(h->U[0], 0, 1, 1, h->U[0]);
+            cudaMemcpyAsync(h->pin, h->U[0], 8, cudaMemcpyDeviceToHost, h->dstream);
+            cudaStreamSynchronize(h->dstream);
+        }
     }
     return rc;
 }
@@ -2655,8 +2663,8 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
             own_dense = true;
             TRY(dalloc(&g_dev, dense_n, errbuf, errlen));
             TRY(dalloc(&h_dev, dense_n, errbuf, errlen));
-            SFW_CUDA_TRY(cudaMemcpy(g_dev, d->gammas, dense_n * 8, cudaMemcpyHostToDevice));
-            SFW_CUDA_TRY(cudaMemcpy(h_dev, d->gamma_hats, dense_n * 8, cudaMemcpyHostToDevice));
+            SFW_CUDA_TRY(sfw_h2d(g_dev, d->gammas, dense_n * 8));
+            SFW_CUDA_TRY(sfw_h2d(h_dev, d->gamma_hats, dense_n * 8));
         }
         TRY(dalloc(&h->coef, (size_t)h->n_blocks * h->BS, errbuf, errlen));
         long long* d_dense_off = nullptr;

@@ -13,6 +13,8 @@
 
 namespace sfw {
 
+inline int g_wform_scope = 0;  // debug poisoning: > 0 while a W-form entry point allocates
+
 template <typename T>
 inline int dalloc(T** p, size_t n, char* errbuf, int errlen) {
     *p = nullptr;
@@ -20,6 +22,13 @@ inline int dalloc(T** p, size_t n, char* errbuf, int errlen) {
     cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
     if (e != cudaSuccess)
         return fail(SFW_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e), errbuf, errlen);
+    if (const char* pz = std::getenv("SFW_POISON")) {  // debug: fresh buffers read as NaN until written
+        const bool w = g_wform_scope > 0;
+        if (pz[0] == 'a' || (pz[0] == 'w' && w) || (pz[0] == 's' && !w)) {
+            cudaMemset(*p, 0xFF, n * sizeof(T));
+            cudaDeviceSynchronize();
+        }
+    }
     return 0;
 }
 
@@ -27,7 +36,7 @@ template <typename T>
 inline int upload(T** p, const std::vector<T>& v, char* errbuf, int errlen) {
     int rc = dalloc(p, v.size(), errbuf, errlen);
     if (rc) return rc;
-    if (!v.empty()) SFW_CUDA_TRY(cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!v.empty()) SFW_CUDA_TRY(sfw_h2d(*p, v.data(), v.size() * sizeof(T)));
     return 0;
 }
 

@@ -624,7 +624,7 @@ static int wf_vectors(sfw_stepper* h, WState* ws, int nvec, const int* vsub_h, c
         (rc = upload(&d_lv, lv, errbuf, errlen)) || (rc = dalloc(&d_in, n, errbuf, errlen)) ||
         (rc = dalloc(&d_out, n, errbuf, errlen)))
         return rc;
-    cudaMemcpy(d_in, in_host, n * 8, cudaMemcpyHostToDevice);
+    sfw_h2d(d_in, in_host, n * 8);
     const int w = h->W;
     const size_t sm = (size_t)(w * w + w) * 8 + w * 4 + 16;
     cudaFuncSetAttribute(k_layer_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -646,6 +646,7 @@ static int wf_vectors(sfw_stepper* h, WState* ws, int nvec, const int* vsub_h, c
 // Switch a stepper to fp32 W-form (requires the scales G_j at creation).
 // src_vec / probe weights of the handle are converted from U-form on the device.
 extern "C" int sfw_wform_setup(sfw_stepper* h, char* errbuf, int errlen) {
+    struct WScope { WScope() { ++sfw::g_wform_scope; } ~WScope() { --sfw::g_wform_scope; } } wscope_;
     if (!h->scales) return fail(SFW_ECONFIG, "fp32 W-form stepping needs the models' scales (G_j)", errbuf, errlen);
     if (!h->uniform) return fail(SFW_ECONFIG, "fp32 W-form stepping needs one layer count", errbuf, errlen);
     if (h->m != 4 && h->m != 9 && h->m != 1)
@@ -705,6 +706,7 @@ extern "C" int sfw_wform_setup(sfw_stepper* h, char* errbuf, int errlen) {
 // sources/probes in fp32.  src_vec/probe_w: HOST U-form arrays as given at create/set_probes.
 extern "C" int sfw_wform_vectors(sfw_stepper* h, const double* src_vec, const double* probe_w, double* src_norms,
                                  char* errbuf, int errlen) {
+    struct WScope { WScope() { ++sfw::g_wform_scope; } ~WScope() { --sfw::g_wform_scope; } } wscope_;
     WState* ws = g_wf.count(h) ? g_wf[h] : nullptr;
     if (!ws) return fail(SFW_ECONFIG, "call sfw_wform_setup first", errbuf, errlen);
     int rc = 0;
@@ -829,6 +831,7 @@ static int wf_ensure(float** p, long long* cap, long long need, char* errbuf, in
 // Two-level start in W-form.  u0/v0: HOST U-form (or NULL); converted with G^-1.
 extern "C" int sfw_wform_init(sfw_stepper* h, const double* u0, const double* v0, const double* profile0,
                               double* row0_out, char* errbuf, int errlen) {
+    struct WScope { WScope() { ++sfw::g_wform_scope; } ~WScope() { --sfw::g_wform_scope; } } wscope_;
     WState* ws = g_wf.count(h) ? g_wf[h] : nullptr;
     if (!ws) return fail(SFW_ECONFIG, "call sfw_wform_setup first", errbuf, errlen);
     const long long n = h->state_len;
@@ -860,12 +863,12 @@ extern "C" int sfw_wform_init(sfw_stepper* h, const double* u0, const double* v0
         std::vector<double> out(n);
         if ((rc = wf_vectors(h, ws, h->n_sub, vs.data(), vo.data(), n, 0, src, out.data(), errbuf, errlen))) return rc;
         std::vector<float> f(out.begin(), out.end());
-        cudaMemcpy(dst, f.data(), n * 4, cudaMemcpyHostToDevice);
+        sfw_h2d(dst, f.data(), n * 4);
     }
     if ((rc = wf_ensure(&ws->ftab, &ws->ftab_cap, std::max(1, h->n_src), errbuf, errlen))) return rc;
     if (h->n_src) {
         std::vector<float> f(profile0, profile0 + h->n_src);
-        cudaMemcpy(ws->ftab, f.data(), h->n_src * 4, cudaMemcpyHostToDevice);
+        sfw_h2d(ws->ftab, f.data(), h->n_src * 4);
     }
     // row buffer / norm partials owned by the fp64 handle
     double* tmp = nullptr;
@@ -888,6 +891,7 @@ extern "C" int sfw_wform_init(sfw_stepper* h, const double* u0, const double* v0
 // norms are |W| (the W-form invariant scale), rows are the physical probe values.
 extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, const double* profile,
                              double* rows_out, double* norms_out, float* kernel_ms, char* errbuf, int errlen) {
+    struct WScope { WScope() { ++sfw::g_wform_scope; } ~WScope() { --sfw::g_wform_scope; } } wscope_;
     WState* ws = g_wf.count(h) ? g_wf[h] : nullptr;
     if (!ws) return fail(SFW_ECONFIG, "call sfw_wform_setup first", errbuf, errlen);
     if (n_steps <= 0) return 0;
@@ -895,7 +899,7 @@ extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, cons
     if (rc) return rc;
     if (h->n_src && profile) {
         std::vector<float> f(profile, profile + (size_t)h->n_src * n_steps);
-        cudaMemcpy(ws->ftab, f.data(), f.size() * 4, cudaMemcpyHostToDevice);
+        sfw_h2d(ws->ftab, f.data(), f.size() * 4);
     }
     const long long nrec = n_steps / record_every;
     if (h->rows_cap < std::max(1LL, nrec * h->n_probe)) {
@@ -956,6 +960,7 @@ extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, cons
 
 // W-form state as U-form (U_j = G_j W_j), fp64, HOST concat.
 extern "C" int sfw_wform_state(sfw_stepper* h, double* u_curr, double* u_prev, char* errbuf, int errlen) {
+    struct WScope { WScope() { ++sfw::g_wform_scope; } ~WScope() { --sfw::g_wform_scope; } } wscope_;
     WState* ws = g_wf.count(h) ? g_wf[h] : nullptr;
     if (!ws) return fail(SFW_ECONFIG, "call sfw_wform_setup first", errbuf, errlen);
     const long long n = h->state_len;
@@ -979,6 +984,7 @@ extern "C" int sfw_wform_state(sfw_stepper* h, double* u_curr, double* u_prev, c
 
 // bytes per step of the fp32 W-form launch (4[(2L-1)w(w+1)/2 + 3Lw] per subdomain)
 extern "C" int sfw_wform_traffic(sfw_stepper* h, double* alg_bytes, double* streamed) {
+    struct WScope { WScope() { ++sfw::g_wform_scope; } ~WScope() { --sfw::g_wform_scope; } } wscope_;
     const double w = h->W;
     double b = 0, s = 0;
     const int BS = wf::packed_stride32(h->m);
@@ -993,6 +999,7 @@ extern "C" int sfw_wform_traffic(sfw_stepper* h, double* alg_bytes, double* stre
 }
 
 extern "C" int sfw_wform_destroy(sfw_stepper* h) {
+    struct WScope { WScope() { ++sfw::g_wform_scope; } ~WScope() { --sfw::g_wform_scope; } } wscope_;
     if (!g_wf.count(h)) return 0;
     WState* ws = g_wf[h];
     void* ptrs[] = {ws->coef, ws->W[0], ws->W[1], ws->V0, ws->mbox, ws->src, ws->prb, ws->ftab, ws->prb_rng,
