@@ -96,3 +96,26 @@ def test_fp32_chunked_run_equals_single_launch(record_every, monkeypatch):
     assert np.array_equal(ts, tc) and np.array_equal(rs, rc)
     for a in us:
         assert np.array_equal(us[a], uc[a])
+
+
+def test_no_reads_of_unwritten_device_memory(monkeypatch):
+    """With SFW_POISON=a every fresh library allocation is filled with NaN (debug hook in dalloc):
+    a kernel that read memory nothing wrote first (e.g. an upload whose DMA had not landed, the
+    race fixed by sfw_h2d) would turn the traces into NaN.  fp64 and fp32 config-1 runs stay
+    finite and equal to the unpoisoned runs."""
+    g = load_golden("golden_c1.npz")
+    wl = make_workload(1, n_steps=int(g["n_steps"]))
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    models = models_from_arrays(part, wl.c_field, 4, g["gammas"], g["hats"], g["scales"], shift=wl.shift)
+    src = SourceTerm(tuple(int(x) for x in g["src_alpha"]), g["src_vec"], so.ricker(wl.f0, wl.delay))
+    probes = [Probe(a, w) for a, w in face_probes(models, wl)]
+    out = {}
+    for poison in ("", "a"):
+        if poison:
+            monkeypatch.setenv("SFW_POISON", poison)
+        for prec in ("fp64", "fp32"):
+            with CoupledStepper(models, float(g["dt"]), sources=(src,), precision=prec) as st:
+                out[(poison, prec)] = st.run(120, probes=probes)[1]
+    for prec in ("fp64", "fp32"):
+        assert np.isfinite(out[("a", prec)]).all()
+        assert np.array_equal(out[("a", prec)], out[("", prec)])
