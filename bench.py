@@ -2,18 +2,25 @@
 """Benchmark of the S-fraction ROM hot path on B200 (driver contract: one JSON line).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+                    [--precision fp64|fp32] [--no-cpu] [--extra 0|1] [--fdtd]
 
-Workload (BASELINE.json configs[1]): config 2 = 8 x 8 x 8 subdomains
-of 17^3 nodes, seeded 5-layer medium + 24^3 inclusion, m=4, k=6 (K = 168 ROM
-DOF per subdomain), 15 Hz Ricker source, fp64.  A bench "step" is one coupled
-leapfrog step of every subdomain; the K timed steps run as ONE persistent
-kernel launch.  Models are built on the GPU first (reported as ``rom_build``).
+Headline workload (BASELINE.json metric, quoted on the largest config): config 5 =
+32 x 32 x 16 = 16384 subdomains of 17^3 nodes, seeded 4^3-cell blocky medium + 10
+inclusions of 5500 m/s, m=9, k=8 (K = 486 ROM DOF per subdomain), 10 Hz Ricker
+source, fp64 U-form, 9224 receivers (z-midplane face coefficients + 8 node
+receivers) recorded every step.  A bench "step" is one coupled leapfrog step of
+every subdomain; the K timed steps run as ONE persistent kernel launch.  Models
+are built on the GPU first (``rom_build``), dt = 0.9 * 2 / sqrt(lambda) from the GPU
+CFL power iteration.  ``e2e`` is the same K steps through ``CoupledStepper.run``.
+``extra`` carries configs 5 fp32, 3 (fp64/fp32), 4 (32 shots, DMMA) and 2 with the
+same work (source, receivers, host profile table).
 
-``--impl reference`` times the reference algorithm on the host cores instead:
-the CPU oracle port (oracle/sfw_oracle.py, restating reference rom.py and
-stepper.py; pinned bitwise to reference golden vectors), which is the
-reference's own CPU implementation of the path.  Under torchrun only rank 0
-runs it.
+``--impl reference`` times the reference algorithm on the host cores instead: the
+CPU oracle port (oracle/sfw_oracle.py, restating reference rom.py and stepper.py;
+pinned bitwise to reference golden vectors) on a stated 4x4x4-subdomain window of
+the same medium (a full config-5 CPU build takes about an hour): oracle build,
+oracle CFL, then W + K coupled steps with the window's receivers.  Under torchrun
+only rank 0 runs it.  ``cpu_baseline`` in the GPU arm's line is the same sample.
 
 Multi-GPU: the north star scopes the path to one GPU, so --gpus N
 runs N independent replicas (weak scaling), timed on the device, max over ranks.
@@ -164,107 +171,138 @@ def _dist():
     return ws, rank, lrank
 
 
-def cpu_oracle_models(ops, cfg, workers):
-    """Models built by the CPU oracle (reference algorithm) with a process pool."""
-    from concurrent.futures import ProcessPoolExecutor
-    with ProcessPoolExecutor(max_workers=workers) as ex:
-        res = list(ex.map(_oracle_build_one, [(cfg, op.alpha) for op in ops], chunksize=4))
-    return dict(res)
+# ---------------------------------------------------------------------------
+# CPU leg: the reference algorithm (oracle port) on a stated subset of the workload
+
+SUBSET = 4  # subdomains per axis of the CPU sample window
 
 
-def _oracle_build_one(args):
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+def subset_window(wl, n=SUBSET):
+    """Low corner (subdomain index) of the n^3-subdomain window centred on the source subdomain."""
+    from paper_1406_6923_b200.configs import locate
+    sa, _ = locate(wl.sources[0], wl.counts, wl.p)
+    return tuple(max(0, min(a - n // 2 + 1, c - n)) for a, c in zip(sa, wl.counts))
+
+
+_SUB_CTX: dict = {}
+
+
+def _subset_build_one(alpha):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
     from oracle import sfw_oracle as so
-    from paper_1406_6923_b200.configs import make_workload
-    cfg, alpha = args
-    wl = _WL_CACHE.get(cfg)
-    if wl is None:
-        wl = _WL_CACHE[cfg] = make_workload(int(cfg))
-    op = so.make_subops(wl.counts, wl.p, wl.spacing, wl.c_field, alphas=[alpha])[alpha]
-    md = so.build_model(op, wl.modes_per_face, wl.n, wl.shift)
-    md.basis = None
+    ctx = _SUB_CTX
+    op = so.make_subops(ctx["counts"], ctx["p"], ctx["spacing"], ctx["c"], alphas=[alpha])[alpha]
+    md = so.build_model(op, ctx["m"], ctx["n"], ctx["shift"])
+    if alpha not in ctx["need_basis"]:
+        md.basis = None
     return alpha, md
 
 
-_WL_CACHE: dict = {}
+def cpu_subset_run(cfg, steps, warmup, cores=None, n=SUBSET):
+    """The reference's CPU path on an n^3-subdomain window of config ``cfg``'s medium.
 
+    The window (centred on the source subdomain) is a domain of its own: the oracle port of
+    reference rom.py builds its n^3 models (one process per core, one BLAS thread each), the
+    oracle port of cfl_estimate_coupled (stepper.py:452-487, tol 1e-8) gives dt = 0.9 * 2 / sqrt(lam)
+    as for the GPU arm, and the oracle port of CoupledStepper (stepper.py:325-415, one thread:
+    the reference's workers > 1 is slower) steps it from rest with the 15/10 Hz
+    Ricker source and the configuration's receivers that fall inside the window (z-midplane
+    face coefficients + node receivers), recording every step.  ``warmup`` untimed steps, then
+    ``steps`` timed ones.  Returns a dict (rate in subdomain-steps/s of the window)."""
+    import multiprocessing as mp
 
-def oracle_step_rate(models, dt, src, budget_s=15.0, max_steps=400, warmup=1):
-    """Time the oracle's coupled leapfrog (reference stepper.py:362-389 loop shape)."""
-    from oracle import sfw_oracle as so
-    st = so.Coupled(models, dt, sources=[src])
-    st.initialize()
-    for _ in range(warmup):
-        st.advance()
-    t0 = time.perf_counter()
-    n = 0
-    while n < max_steps and (time.perf_counter() - t0) < budget_s:
-        st.advance()
-        n += 1
-    el = time.perf_counter() - t0
-    return len(models) * n / el, n, el
-
-
-def run_reference(args):
-    ws, rank, _ = _dist()
-    if rank != 0:
-        return
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import sfw_oracle as so
-    wl, ops, alphas, (src_alpha, src_row), _ = _workload(args.config)
-    cores = os.cpu_count() or 1
+    from paper_1406_6923_b200.configs import locate, make_workload
+    wl = make_workload(3 if cfg == 4 else cfg)
+    lo = subset_window(wl, n)
+    counts = (n, n, n)
+    sl = tuple(slice(16 * a, 16 * (a + n) + 1) for a in lo)
+    c_sub = np.ascontiguousarray(wl.c_field[sl])
+    inside = lambda ijk: all(16 * a < x < 16 * (a + n) for x, a in zip(ijk, lo))  # noqa: E731
+    local = lambda ijk: tuple(x - 16 * a for x, a in zip(ijk, lo))  # noqa: E731
+    src_alpha, src_row = locate(local(wl.sources[0]), counts, wl.p)
+    node_rx = [locate(local(ijk), counts, wl.p) for ijk in wl.node_receivers if inside(ijk)]
+    kz = wl.counts[2] // 2 - 1 - lo[2]
+    face_rx = [((i, j, kz), 5) for i in range(n) for j in range(n)] if 0 <= kz < n else []
+    need = {src_alpha} | {a for a, _ in node_rx}
+    alphas = [(i, j, k) for i in range(n) for j in range(n) for k in range(n)]
+    cores = cores or os.cpu_count() or 1
+    _SUB_CTX.update(counts=counts, p=wl.p, spacing=wl.spacing, c=c_sub, m=wl.modes_per_face, n=wl.n,
+                    shift=wl.shift, need_basis=need)
     t0 = time.perf_counter()
-    models = cpu_oracle_models(ops, args.config, cores)
+    with mp.get_context("fork").Pool(min(cores, len(alphas))) as pool:
+        models = dict(pool.map(_subset_build_one, alphas, chunksize=1))
     build_s = time.perf_counter() - t0
-    # dt: short power iteration (timing does not depend on dt; 0.5 x the estimate keeps the sample stable)
-    lam, _ = so.cfl_power(models, max_iter=40)
-    dt = 0.5 * 2.0 / math.sqrt(lam)
-    # source needs the basis row: rebuild the source subdomain with its basis
-    sop = so.make_subops(wl.counts, wl.p, wl.spacing, wl.c_field, alphas=[src_alpha])[src_alpha]
-    smd = so.build_model(sop, wl.modes_per_face, wl.n, wl.shift)
-    vec = so.source_vector(smd, src_row)
-    steps = max(1, min(args.steps, 60))
-    rate, n, el = oracle_step_rate(models, dt, (src_alpha, vec, so.ricker(wl.f0, wl.delay)),
-                                   budget_s=60.0, max_steps=steps, warmup=max(1, min(args.warmup, 3)))
-    line = {
-        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws, "steps": n,
-        "warmup": max(1, min(args.warmup, 3)), "ms_per_step": 1e3 * el / n, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8d)",
-        "config": {"workload": _describe(wl), "subdomains": len(models)},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{n} coupled leapfrog steps of all {len(models)} subdomains "
-                                   f"(oracle restatement of reference stepper.py, single thread)"},
-        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "rom_build": {"subdomains_per_s": len(models) / build_s, "seconds": build_s, "cores": cores,
-                      "kind": "port (scipy SuperLU + LAPACK, one process per core)"},
-    }
-    print(json.dumps(line), flush=True)
+    t0 = time.perf_counter()
+    lam, conv = so.cfl_power(models)
+    cfl_s = time.perf_counter() - t0
+    dt = 0.9 * 2.0 / math.sqrt(lam)
+    vec = so.source_vector(models[src_alpha], src_row)
+    probes = []
+    for a, f in face_rx:
+        for q in range(wl.modes_per_face):
+            wts = np.zeros(models[a].state_size)
+            wts[f * wl.modes_per_face + q] = 1.0
+            probes.append((a, wts))
+    probes += [(a, so.probe_weights(models[a], r)) for a, r in node_rx]
+    st = so.Coupled(models, dt, sources=[(src_alpha, vec, so.ricker(wl.f0, wl.delay))])
+    st.initialize()
+    rows = [st._row(probes)]
+    for _ in range(warmup):
+        st.advance()
+        rows.append(st._row(probes))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st.advance()
+        rows.append(st._row(probes))
+    el = time.perf_counter() - t0
+    nsub = len(models)
+    return {"rate": nsub * steps / el, "seconds": el, "steps": steps, "warmup": warmup, "subdomains": nsub,
+            "window": {"counts": list(counts), "low_subdomain": list(lo)}, "probes": len(probes),
+            "dt": dt, "lambda_hat": lam, "cfl_converged": bool(conv), "cfl_seconds": cfl_s,
+            "build_seconds": build_s, "build_cores": min(cores, len(alphas)),
+            "build_subdomains_per_s": nsub / build_s,
+            "sample": (f"{n}x{n}x{n}-subdomain window (low corner {lo}) of the {wl.name} medium, m={wl.modes_per_face} "
+                       f"k={wl.n}: oracle-port build ({min(cores, len(alphas))} processes, {build_s:.1f} s) + "
+                       f"CPU CFL ({cfl_s:.1f} s) + {steps} timed coupled leapfrog steps ({warmup} warm-up) with the "
+                       f"Ricker source and {len(probes)} receivers in the window recorded every step, "
+                       f"{el:.2f} s on 1 thread (oracle restatement of reference stepper.py)")}
 
 
-def run_ours(args):
-    import ctypes as C
+# ---------------------------------------------------------------------------
+# GPU arm
 
+def config_key(wl, n_probes, shots=1):
+    """The ``config`` object of both arms (identical for the same workload)."""
+    return {"workload": _describe(wl) + (f", S={shots} independent shots" if shots > 1 else ""),
+            "subdomains": wl.n_sub, "rom_dof_per_subdomain": wl.layers * wl.width, "sources": shots,
+            "probes": n_probes, "record_every": 1,
+            "l2": "flushed (512 MB write) before the timed launch; the K steps run in one persistent launch"}
+
+
+def flush_l2():
     import torch
+    buf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    buf.fill_(1.0)
+    torch.cuda.synchronize()
+    del buf
 
-    ws, rank, lrank = _dist()
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(lrank)
-    from paper_1406_6923_b200 import (CoupledStepper, Probe, SourceTerm, _lib, build_models,
-                                      cfl_estimate_coupled, make_probe, project_source)
-    from paper_1406_6923_b200.rom import LAST_BUILD_STATS
-    from paper_1406_6923_b200.pulses import ricker
 
-    wl, ops, alphas, (src_alpha, src_row), node_rx = _workload(args.config)
-    n_sub = len(ops)
-    w, L = wl.width, wl.layers
-    rows = {src_alpha: [src_row]}
-    for a, r in node_rx:
-        rows.setdefault(a, []).append(r)
+def prepare(cfg, extra_rows=()):
+    """GPU ROM build of a config's workload (chain stacks left in HBM), GPU CFL, source and probes."""
+    import torch
+    from paper_1406_6923_b200 import Probe, SourceTerm, build_models, cfl_estimate_coupled, make_probe
+    from paper_1406_6923_b200 import project_source
     from paper_1406_6923_b200.configs import locate
-    for ijk in wl.sources[1:]:
-        a, r = locate(ijk, wl.counts, wl.p)
+    from paper_1406_6923_b200.pulses import ricker
+    from paper_1406_6923_b200.rom import LAST_BUILD_STATS
+    from paper_1406_6923_b200.stepper import LAST_CFL
+    wl, ops, alphas, (sa, sr), node_rx = _workload(cfg)
+    n_sub, w, L = len(ops), wl.width, wl.layers
+    rows = {sa: [sr]}
+    for a, r in list(node_rx) + [locate(ijk, wl.counts, wl.p) for ijk in list(wl.sources[1:]) + list(extra_rows)]:
         rows.setdefault(a, []).append(r)
     dev = [torch.empty(n_sub * L * w * w, dtype=torch.float64, device="cuda") for _ in range(3)]
     ptrs = tuple(t.data_ptr() for t in dev)
@@ -273,7 +311,7 @@ def run_ours(args):
     models = build_models(ops, wl.modes_per_face, wl.n, wl.shift, rows=rows, device_out=ptrs)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
-    build_stats = dict(LAST_BUILD_STATS)
+    stats = dict(LAST_BUILD_STATS)
     scl = dev[2].view(n_sub, L, w, w)
     idx = {a: i for i, a in enumerate(alphas)}
     for a in rows:
@@ -281,352 +319,331 @@ def run_ours(args):
     t0 = time.perf_counter()
     lam, conv = cfl_estimate_coupled(models, device_coefficients=ptrs)
     cfl_s = time.perf_counter() - t0
-    from paper_1406_6923_b200.stepper import LAST_CFL
-    cfl_iters = LAST_CFL.get("iterations")
     dt = 0.9 * 2.0 / math.sqrt(lam)
-    vec = project_source(models[src_alpha], src_row)
+    src = SourceTerm(sa, project_source(models[sa], sr), ricker(wl.f0, wl.delay))
     probes = []
     for alpha, face in wl.face_receivers:
         for q in range(wl.modes_per_face):
             wts = np.zeros(models[alpha].state_size)
             wts[face * wl.modes_per_face + q] = 1.0
             probes.append(Probe(alpha, wts))
-    for a, r in node_rx:
-        probes.append(make_probe(models[a], r))
-    src = SourceTerm(src_alpha, vec, ricker(wl.f0, wl.delay))
-    if len(wl.sources) > 1:
-        return _run_shots(args, wl, models, ptrs, dt, lam, conv, probes, ws, rank, build_s, build_stats, cfl_s,
-                          cfl_iters)
-    if args.precision == "fp32":
-        return _run_fp32(args, wl, models, ptrs, dt, lam, conv, src, probes, ws, rank, build_s, build_stats, cfl_s,
-                         cfl_iters)
-    st = CoupledStepper(models, dt, sources=(src,), device_coefficients=ptrs)
-    st.initialize(_probes=probes)
-    lib = st._lib
-    K = args.steps
-    prof_w = np.ascontiguousarray(np.array([[src.profile(k * dt) for k in range(max(args.warmup, 1))]]))
-    prof_k = np.ascontiguousarray(np.array([[src.profile(k * dt) for k in range(K)]]))
-    ms = C.c_float(0.0)
-    eb = _lib.errbuf()
-    _lib.check(lib.sfw_step_run_resident(st._h, max(args.warmup, 1), 1, _lib.dptr(prof_w), C.byref(ms), eb, 1024), eb)
-    # flush L2 (126 MB) before the timed launch
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    flush.fill_(1.0)
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(lrank) as clk:
-        t0 = time.perf_counter()
-        _lib.check(lib.sfw_step_run_resident(st._h, K, 1, _lib.dptr(prof_k), C.byref(ms), eb, 1024), eb)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-    if ws > 1:
-        dist.barrier()
-    kernel_s = ms.value * 1e-3
-    t_max = reduce_max(kernel_s)
-    value = replica_value(n_sub, K, ws, t_max)
-    alg_bytes, alg_flops, streamed = st.traffic()
-    # e2e through the public API: host profile/limit tables in, probe rows + norms out, every step
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    times, trace = st.run(K, probes=probes)
-    torch.cuda.synchronize()
-    e2e_wall = time.perf_counter() - t0
-    e2e_t = reduce_max(e2e_wall)
-    e2e_value = replica_value(n_sub, K, ws, e2e_t)
-    h2d = 8 * (1 + len(st.sources))  # growth limit + profile value per source
-    d2h = 8 * (len(probes) + 1)      # probe row + |U|
-    if rank != 0:
-        st.close()
-        if ws > 1:
-            dist.destroy_process_group()
-        return
-    peak, peak_kind = _peaks()
-    achieved = alg_bytes * K / kernel_s / 1e9
-    traffic = _traffic(f"config{args.config}", K)  # per launch, like achieved
-    # CPU baseline: the oracle (reference algorithm) stepping the same models, bounded sample
-    cpu = None
-    if not args.no_cpu:
-        from oracle import sfw_oracle as so
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-        G = dev[0].view(n_sub, L, w, w).cpu().numpy()
-        H = dev[1].view(n_sub, L, w, w).cpu().numpy()
-        S = scl.cpu().numpy()
-        omodels = {a: so.Model(alpha=a, lo=None, shape=None, spacing=None, modes_per_face=wl.modes_per_face,
-                               layers=L, shift=wl.shift, neighbors=dict(ops[i].neighbors), face_indices=(),
-                               gammas=G[i], gamma_hats=H[i], scales=S[i], basis=None, c=None, mu=None)
-                   for i, a in enumerate(alphas)}
-        rate, n, el = oracle_step_rate(omodels, dt, (src_alpha, vec, so.ricker(wl.f0, wl.delay)),
-                                       budget_s=args.cpu_seconds, max_steps=2000)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{n} coupled leapfrog steps of all {n_sub} subdomains on GPU-built models, "
-                         f"{el:.1f} s (oracle restatement of reference stepper.py, single thread)"}
-    clocks = clk.summary()
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded medium, SURVEY 8d); models built on the GPU from it",
-        "config": {"workload": _describe(wl), "subdomains": n_sub, "rom_dof_per_subdomain": L * w,
-                   "sources": 1, "probes": len(probes), "dt": dt, "lambda_hat": lam, "cfl_converged": conv,
-                   "l2": ("flushed (512 MB write) before the timed launch; the K steps run in one persistent "
-                          "launch that loads the 16 MB of chain coefficients into SMEM once and keeps them there "
-                          "(ncu DRAM traffic ~9.5 KB/step)") if args.config == 2 else
-                         ("flushed (512 MB write) before the timed launch; the K steps run in one persistent "
-                          "launch, so chain coefficients stream HBM->SMEM per step (L2-resident when they fit)"),
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
-        "dof_updates_per_s": value * L * w,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "CoupledStepper.run(K, probes) incl. init, profile/limit upload, trace/norm download"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "alg_bytes_per_launch": alg_bytes * K,
-                     "alg_bytes_per_step": alg_bytes, "streamed_bytes_per_step": streamed,
-                     "alg_flops_per_step": alg_flops,
-                     "formula": "8[(2L-1)w(w+1)/2 + 3Lw] bytes per subdomain-step (SURVEY 8d)"},
-        "cpu_baseline": cpu,
-        "clocks": clocks,
-        "gpu_launches": 1,
-        "kernel_ms": ms.value, "wall_ms": wall * 1e3,
-        "rom_build": {"seconds": build_s, "subdomains_per_s": n_sub / build_s, "stages_s": build_stats,
-                      "cfl_seconds": cfl_s, "cfl_iterations": cfl_iters,
-                      "k_step2_launches_before_timed": (cfl_iters or 0) + 2},
-    }
-    st.close()
-    if args.extra and args.config == 2:
-        try:
-            line["extra"] = _extra_configs(args)
-        except Exception as exc:  # the headline line must still print
-            line["extra"] = {"error": str(exc)[:300]}
-    print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
+    probes += [make_probe(models[a], r) for a, r in node_rx]
+    return {"wl": wl, "ops": ops, "alphas": alphas, "models": models, "dev": dev, "ptrs": ptrs, "dt": dt,
+            "lam": lam, "conv": conv, "src": src, "probes": probes,
+            "build": {"seconds": build_s, "subdomains_per_s": n_sub / build_s, "stages_s": stats,
+                      "cfl_seconds": cfl_s, "cfl_iterations": LAST_CFL.get("iterations")}}
 
 
-def _extra_configs(args):
-    """Kernel-only stepping of the other BASELINE configs (device-timed, L2 flushed), so the default
-    bench line carries every config: 3 (fp64 U-form and fp32 W-form), 4 (32 shots, DMMA) and 5
-    (fp64 and fp32).  Each entry: ms/step, subdomain-steps/s, roofline fraction, ROM build time."""
-    import ctypes as C
-
-    import torch
-    from paper_1406_6923_b200 import CoupledStepper, SourceTerm, _lib, build_models, cfl_estimate_coupled
-    from paper_1406_6923_b200 import project_source
-    from paper_1406_6923_b200.configs import locate, make_workload
-    from paper_1406_6923_b200.pulses import ricker
-    peak, _ = _peaks()
-    fpk, _ = _fp64_peak()
-    out = {}
-
-    def flush():
-        buf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-        buf.fill_(1.0)
-        torch.cuda.synchronize()
-
-    for cfg in (3, 5):
-        wl, ops, alphas, (sa, sr), _ = _workload(cfg)
-        n_sub, w, L = len(ops), wl.width, wl.layers
-        rows = {sa: [sr]}
-        if cfg == 3:  # config 4 = config 3 models + 32 shot sources
-            for ijk in make_workload(4).sources:
-                a, r = locate(ijk, wl.counts, wl.p)
-                rows.setdefault(a, []).append(r)
-        dev = [torch.empty(n_sub * L * w * w, dtype=torch.float64, device="cuda") for _ in range(3)]
-        ptrs = tuple(t.data_ptr() for t in dev)
-        t0 = time.perf_counter()
-        models = build_models(ops, wl.modes_per_face, wl.n, wl.shift, rows=rows, device_out=ptrs)
-        torch.cuda.synchronize()
-        build_s = time.perf_counter() - t0
-        scl = dev[2].view(n_sub, L, w, w)
-        idx = {a: i for i, a in enumerate(alphas)}
-        for a in rows:
-            models[a].scales = scl[idx[a]].cpu().numpy()
-        lam, conv = cfl_estimate_coupled(models, device_coefficients=ptrs)
-        dt = 0.9 * 2.0 / math.sqrt(lam)
-        src = SourceTerm(sa, project_source(models[sa], sr), ricker(wl.f0, wl.delay))
-        K = 300 if cfg == 3 else 150
-        # fp64 U-form, one persistent launch
-        st = CoupledStepper(models, dt, sources=(src,), device_coefficients=ptrs)
-        st.initialize()
-        ms = C.c_float(0.0)
-        eb = _lib.errbuf()
-        _lib.check(st._lib.sfw_step_run_resident(st._h, 5, 1, None, C.byref(ms), eb, 1024), eb)
-        flush()
-        _lib.check(st._lib.sfw_step_run_resident(st._h, K, 1, None, C.byref(ms), eb, 1024), eb)
-        b, _f, _s = st.traffic()
-        st.close()
-        sec = ms.value * 1e-3
-        out[f"config{cfg}"] = {"workload": _describe(wl), "subdomains": n_sub, "steps": K, "ms_per_step": ms.value / K,
-                               "value": n_sub * K / sec, "unit": UNIT, "dtype": "f64",
-                               "roofline": {"bound": "hbm", "frac": b * K / sec / 1e9 / peak,
-                                            "achieved": b * K / sec / 1e9, "peak": peak, "unit": "GB/s"},
-                               "rom_build_seconds": build_s, "cfl_converged": conv}
-        # fp32 W-form
-        st = CoupledStepper(models, dt, sources=(src,), device_coefficients=ptrs, precision="fp32")
-        st.run(5)
-        flush()
-        st.run(K)
-        bb, sb = C.c_double(), C.c_double()
-        st._lib.sfw_wform_traffic(st._h, C.byref(bb), C.byref(sb))
-        sec = st.last_kernel_ms * 1e-3
-        st.close()
-        out[f"config{cfg}_fp32"] = {"workload": _describe(wl) + ", fp32 W-form", "steps": K,
-                                    "ms_per_step": 1e3 * sec / K, "value": n_sub * K / sec, "unit": UNIT,
-                                    "dtype": "f32", "roofline": {"bound": "hbm", "frac": bb.value * K / sec / 1e9 / peak,
-                                                                 "achieved": bb.value * K / sec / 1e9, "peak": peak,
-                                                                 "unit": "GB/s"}}
-        if cfg == 3:  # config 4: 32 independent shots on the DMMA path
-            wl4 = make_workload(4)
-            shots = []
-            for ijk in wl4.sources:
-                a, r = locate(ijk, wl4.counts, wl4.p)
-                shots.append(SourceTerm(a, project_source(models[a], r), ricker(wl4.f0, wl4.delay)))
-            K4 = 20
-            st = CoupledStepper(models, dt, device_coefficients=ptrs)
-            st.run_shots(3, shots)
-            flush()
-            st.run_shots(K4, shots)
-            ab, af, _ = st.shots_traffic()
-            sec = st.last_kernel_ms * 1e-3
-            st.close()
-            t_hbm, t_fp = ab / (peak * 1e9), af / (fpk * 1e12)
-            out["config4"] = {"workload": _describe(wl4) + ", S=32 shots", "steps": K4, "ms_per_step": 1e3 * sec / K4,
-                              "value": n_sub * K4 / sec, "unit": UNIT, "shot_steps_per_s": 32 * n_sub * K4 / sec,
-                              "dtype": "f64", "achieved_tflops": af * K4 / sec / 1e12,
-                              "roofline": {"bound": "hbm" if t_hbm >= t_fp else "fp64",
-                                           "frac": max(t_hbm, t_fp) * K4 / sec,
-                                           "roofline_us_per_step": {"hbm": 1e6 * t_hbm, "fp64": 1e6 * t_fp}}}
-        del models, dev
-        torch.cuda.empty_cache()
-    return out
-
-
-def _run_fp32(args, wl, models, ptrs, dt, lam, conv, src, probes, ws, rank, build_s, build_stats, cfl_s, cfl_iters):
-    """Config 5 fp32 variant: W-form stepping (U_j = G_j W_j), fp32 blocks."""
+def measure_fp64(pp, K, W, lrank=0):
+    """Kernel-only (one persistent launch of K steps, CUDA events on the library's stream, probes
+    recorded on the device) and e2e (CoupledStepper.run(K, probes): host profile table in, rows +
+    norms out) of the fp64 U-form stepper."""
     import ctypes as C
 
     import torch
     from paper_1406_6923_b200 import CoupledStepper, _lib
+    wl, models, dt, src, probes = pp["wl"], pp["models"], pp["dt"], pp["src"], pp["probes"]
     n_sub = len(models)
-    w, L = wl.width, wl.layers
-    st = CoupledStepper(models, dt, sources=(src,), device_coefficients=ptrs, precision="fp32")
-    st.run(max(args.warmup, 1), probes=probes)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    flush.fill_(1.0)
-    torch.cuda.synchronize()
-    K = args.steps
-    # kernel-only: one launch (rows downloaded after it), CUDA-event time of the launch
-    os.environ["SFW_NO_CHUNK"] = "1"
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        st.run(K, probes=probes)
+    st = CoupledStepper(models, dt, sources=(src,), device_coefficients=pp["ptrs"])
+    try:
+        st.initialize(_probes=probes)
+        lib = st._lib
+        ms = C.c_float(0.0)
+        eb = _lib.errbuf()
+        prof_w = st._profile_steps(0, max(W, 1))
+        _lib.check(lib.sfw_step_run_resident(st._h, max(W, 1), 1, _lib.dptr(prof_w), C.byref(ms), eb, 1024), eb)
+        prof_k = st._profile_steps(max(W, 1), K)
+        flush_l2()
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.barrier()
         torch.cuda.synchronize()
-    del os.environ["SFW_NO_CHUNK"]
-    kernel_s = st.last_kernel_ms * 1e-3
-    # e2e: the public call as a user makes it (row downloads overlap later chunks)
-    flush.fill_(2.0)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    times, rows = st.run(K, probes=probes)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
-    t_max = reduce_max(kernel_s)
-    value = replica_value(n_sub, K, ws, t_max)
-    e2e_value = replica_value(n_sub, K, ws, reduce_max(wall))
-    b, st_b = C.c_double(), C.c_double()
-    st._lib.sfw_wform_traffic(st._h, C.byref(b), C.byref(st_b))
-    st.close()
-    if rank != 0:
-        return
-    peak, peak_kind = _peaks()
-    achieved = b.value * K / kernel_s / 1e9
-    line = {
-        "metric": METRIC.replace("fp64", "fp32 W-form"), "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t_max / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded medium, SURVEY 8d); models built on the GPU",
-        "config": {"workload": _describe(wl) + ", fp32 W-form variant", "subdomains": n_sub,
-                   "rom_dof_per_subdomain": L * w, "dt": dt, "lambda_hat": lam, "cfl_converged": conv,
-                   "probes": len(probes), "l2": "flushed before the timed launch", "parallelism": "1 GPU"},
-        "dof_updates_per_s": value * L * w,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16, "d2h_bytes_per_step": 8 * (len(probes) + 1),
-                "api": "CoupledStepper(precision='fp32').run(K, probes)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": _traffic(f"config{args.config}_fp32", K), "peak_kind": peak_kind,
-                     "alg_bytes_per_step": b.value,
-                     "streamed_bytes_per_step": st_b.value,
-                     "formula": "4[(2L-1)w(w+1)/2 + 3Lw] bytes per subdomain-step (SURVEY 8d fp32)"},
-        "cpu_baseline": None, "clocks": clk.summary(), "gpu_launches": 2, "kernel_ms": kernel_s * 1e3,
-        "rom_build": {"seconds": build_s, "subdomains_per_s": n_sub / build_s, "stages_s": build_stats,
-                      "cfl_seconds": cfl_s, "cfl_iterations": cfl_iters},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def _run_shots(args, wl, models, ptrs, dt, lam, conv, probes, ws, rank, build_s, build_stats, cfl_s, cfl_iters):
-    """Config 4: 32 independent sources stepped together (DMMA path)."""
-    import torch
-    from paper_1406_6923_b200 import CoupledStepper, SourceTerm, project_source
-    from paper_1406_6923_b200.configs import locate
-    from paper_1406_6923_b200.pulses import ricker
-    shots = []
-    for ijk in wl.sources:
-        a, r = locate(ijk, wl.counts, wl.p)
-        shots.append(SourceTerm(a, project_source(models[a], r), ricker(wl.f0, wl.delay)))
-    n_sub = len(models)
-    w, L = wl.width, wl.layers
-    st = CoupledStepper(models, dt, device_coefficients=ptrs)
-    st.run_shots(max(args.warmup, 1), shots, probes=probes)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    flush.fill_(1.0)
-    torch.cuda.synchronize()
-    K = args.steps
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        with ClockSampler(lrank) as clk:
+            t0 = time.perf_counter()
+            _lib.check(lib.sfw_step_run_resident(st._h, K, 1, _lib.dptr(prof_k), C.byref(ms), eb, 1024), eb)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+        if dist.is_available() and dist.is_initialized():
+            dist.barrier()
+        kernel_s = ms.value * 1e-3
+        alg_bytes, alg_flops, streamed = st.traffic()
+        # e2e through the public API, from rest, as a user calls it (after one warm-up call of W steps)
         t0 = time.perf_counter()
-        times, rows = st.run_shots(K, shots, probes=probes)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-    kernel_s = st.last_kernel_ms * 1e-3
-    t_max = reduce_max(kernel_s)
-    value = replica_value(n_sub, K, ws, t_max)
-    e2e_t = reduce_max(wall)
-    e2e_value = replica_value(n_sub, K, ws, e2e_t)
-    alg_bytes, alg_flops, streamed = st.shots_traffic()
-    st.close()
-    if rank != 0:
-        return
+        st.run(max(W, 1), probes=probes)
+        cold_s = time.perf_counter() - t0
+        flush_l2()
+        t0 = time.perf_counter()
+        times, rows = st.run(K, probes=probes)
+        e2e_s = time.perf_counter() - t0
+        assert np.all(np.isfinite(rows))
+    finally:
+        st.close()
+    return {"kernel_s": kernel_s, "wall_s": wall, "e2e_s": e2e_s, "e2e_warmup_call_s": cold_s, "alg_bytes": alg_bytes,
+            "alg_flops": alg_flops,
+            "streamed": streamed, "clocks": clk.summary(), "n_sub": n_sub,
+            "h2d": 8 * (1 + len(st.sources)), "d2h": 8 * (len(probes) + 1)}
+
+
+def measure_fp32(pp, K, W):
+    """fp32 W-form: kernel-only single launch (rows downloaded after it) and the chunked e2e call."""
+    import ctypes as C
+
+    from paper_1406_6923_b200 import CoupledStepper
+    models, dt, src, probes = pp["models"], pp["dt"], pp["src"], pp["probes"]
+    st = CoupledStepper(models, dt, sources=(src,), device_coefficients=pp["ptrs"], precision="fp32")
+    try:
+        st.run(max(W, 1), probes=probes)
+        flush_l2()
+        os.environ["SFW_NO_CHUNK"] = "1"
+        try:
+            st.run(K, probes=probes)
+        finally:
+            del os.environ["SFW_NO_CHUNK"]
+        kernel_s = st.last_kernel_ms * 1e-3
+        st.run(max(W, 1), probes=probes)  # warm the chunked download path
+        flush_l2()
+        t0 = time.perf_counter()
+        _, rows = st.run(K, probes=probes)
+        e2e_s = time.perf_counter() - t0
+        assert np.all(np.isfinite(rows))
+        b, sb = C.c_double(), C.c_double()
+        st._lib.sfw_wform_traffic(st._h, C.byref(b), C.byref(sb))
+    finally:
+        st.close()
+    return {"kernel_s": kernel_s, "e2e_s": e2e_s, "alg_bytes": b.value, "streamed": sb.value, "n_sub": len(models),
+            "h2d": 16, "d2h": 8 * (len(probes) + 1)}
+
+
+def measure_shots(pp, K, W):
+    """Config 4: 32 independent single-source wavefields in one DMMA launch (run_shots)."""
+    from paper_1406_6923_b200 import CoupledStepper, SourceTerm, project_source
+    from paper_1406_6923_b200.configs import locate, make_workload
+    from paper_1406_6923_b200.pulses import ricker
+    wl4 = make_workload(4)
+    models, dt, probes = pp["models"], pp["dt"], pp["probes"]
+    shots = []
+    for ijk in wl4.sources:
+        a, r = locate(ijk, wl4.counts, wl4.p)
+        shots.append(SourceTerm(a, project_source(models[a], r), ricker(wl4.f0, wl4.delay)))
+    st = CoupledStepper(models, dt, device_coefficients=pp["ptrs"])
+    try:
+        st.run_shots(max(W, 1), shots, probes=probes)
+        flush_l2()
+        t0 = time.perf_counter()
+        _, rows = st.run_shots(K, shots, probes=probes)
+        e2e_s = time.perf_counter() - t0
+        assert np.all(np.isfinite(rows))
+        kernel_s = st.last_kernel_ms * 1e-3  # the same call's CUDA-event launch time
+        ab, af, sb = st.shots_traffic()
+    finally:
+        st.close()
+    return {"kernel_s": kernel_s, "e2e_s": e2e_s, "alg_bytes": ab, "alg_flops": af, "streamed": sb,
+            "n_sub": len(models), "shots": len(shots), "h2d": 8 * len(shots), "d2h": 8 * len(shots) * (len(probes) + 1)}
+
+
+def roofline(alg_bytes, alg_flops, K, kernel_s, traffic_key=None, fp64=True):
+    """HBM roofline of one launch; when flops matter (config 4) the slower of bytes at the measured
+    HBM peak and flops at the measured DMMA peak (north_star)."""
     peak, peak_kind = _peaks()
     achieved = alg_bytes * K / kernel_s / 1e9
-    fpk, fpk_kind = _fp64_peak()
-    t_hbm = alg_bytes / (peak * 1e9)
-    t_fp = alg_flops / (fpk * 1e12)
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded medium, SURVEY 8d); models built on the GPU from it",
-        "config": {"workload": _describe(wl) + ", S=32 independent shots (one SourceTerm each)",
-                   "subdomains": n_sub, "shots": len(shots), "rom_dof_per_subdomain": L * w, "dt": dt,
-                   "lambda_hat": lam, "cfl_converged": conv, "probes": len(probes),
-                   "l2": "flushed before the timed launch", "parallelism": "1 GPU"},
-        "shot_steps_per_s": value * len(shots),
-        "dof_updates_per_s": value * L * w * len(shots),
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * len(shots),
-                "d2h_bytes_per_step": 8 * len(shots) * (len(probes) + 1),
-                "api": "CoupledStepper.run_shots(K, 32 shots, probes): profile upload, init, kernel, "
-                       "per-shot traces + norms download"},
-        "roofline": {"bound": "hbm" if t_hbm >= t_fp else "fp64", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": max(t_hbm, t_fp) * K / kernel_s,
-                     "traffic": _traffic("config4", K), "peak_kind": peak_kind, "alg_bytes_per_step": alg_bytes,
-                     "streamed_bytes_per_step": streamed, "alg_flops_per_step": alg_flops,
-                     "achieved_tflops": alg_flops * K / kernel_s / 1e12, "fp64_peak_tflops": fpk,
-                     "fp64_peak_kind": fpk_kind, "roofline_us_per_step": {"hbm": 1e6 * t_hbm, "fp64": 1e6 * t_fp},
-                     "frac_note": "slower of HBM bytes and FP64 flops at their measured peaks (north_star)",
-                     "formula": "8[(2L-1)w(w+1)/2 + 3LwS] bytes, S(2(2L-1)w^2+5Lw) flops per subdomain-step"},
-        "cpu_baseline": None,
-        "clocks": clk.summary(),
-        "gpu_launches": 2,
-        "kernel_ms": st.last_kernel_ms,
-        "rom_build": {"seconds": build_s, "subdomains_per_s": n_sub / build_s, "stages_s": build_stats,
-                      "cfl_seconds": cfl_s, "cfl_iterations": cfl_iters},
-    }
+    out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "traffic": _traffic(traffic_key, K) if traffic_key else None, "peak_kind": peak_kind,
+           "alg_bytes_per_launch": alg_bytes * K, "alg_bytes_per_step": alg_bytes}
+    if alg_flops:
+        fpk, fpk_kind = _fp64_peak()
+        t_hbm, t_fp = alg_bytes / (peak * 1e9), alg_flops / (fpk * 1e12)
+        out.update({"alg_flops_per_step": alg_flops, "achieved_tflops": alg_flops * K / kernel_s / 1e12,
+                    "fp64_peak_tflops": fpk, "fp64_peak_kind": fpk_kind,
+                    "roofline_us_per_step": {"hbm": 1e6 * t_hbm, "fp64": 1e6 * t_fp}})
+        if t_fp > t_hbm:
+            out.update({"bound": "fp64", "frac": t_fp * K / kernel_s})
+    return out
+
+
+def _line(metric, value, K, W, ws, t_max, dtype, cfg_obj):
+    return {"metric": metric, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": 1e3 * t_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": dtype, "data": "synthetic (seeded medium, SURVEY 8d); models built on the GPU from it",
+            "config": cfg_obj}
+
+
+def run_ours(args):
+    import torch
+
+    ws, rank, lrank = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(lrank)
+    K, W = args.steps, args.warmup
+    cfg = args.config
+    if cfg == 4:  # config 4 = the config-3 models + 32 independent shot sources
+        from paper_1406_6923_b200.configs import make_workload
+        wl4 = make_workload(4)
+        pp = prepare(3, extra_rows=wl4.sources)
+        pp["wl"] = wl4
+    else:
+        pp = prepare(cfg)
+    wl = pp["wl"]
+    n_sub = len(pp["models"])
+    if cfg == 4:
+        r = measure_shots(pp, K, W)
+        kernel_s = reduce_max(r["kernel_s"])
+        value = replica_value(n_sub, K, ws, kernel_s)
+        line = _line(METRIC, value, K, W, ws, kernel_s, "f64", config_key(wl, len(pp["probes"]), shots=r["shots"]))
+        line["shot_steps_per_s"] = value * r["shots"]
+        line["dof_updates_per_s"] = value * wl.layers * wl.width * r["shots"]
+        line["roofline"] = roofline(r["alg_bytes"], r["alg_flops"], K, r["kernel_s"], "config4")
+        clocks = None
+    elif args.precision == "fp32":
+        r = measure_fp32(pp, K, W)
+        kernel_s = reduce_max(r["kernel_s"])
+        value = replica_value(n_sub, K, ws, kernel_s)
+        line = _line(METRIC.replace("fp64", "fp32 W-form"), value, K, W, ws, kernel_s, "f32",
+                     config_key(wl, len(pp["probes"])))
+        line["dof_updates_per_s"] = value * wl.layers * wl.width
+        line["roofline"] = roofline(r["alg_bytes"], None, K, r["kernel_s"], f"config{cfg}_fp32")
+        clocks = None
+    else:
+        r = measure_fp64(pp, K, W, lrank)
+        kernel_s = reduce_max(r["kernel_s"])
+        value = replica_value(n_sub, K, ws, kernel_s)
+        line = _line(METRIC, value, K, W, ws, kernel_s, "f64", config_key(wl, len(pp["probes"])))
+        line["dof_updates_per_s"] = value * wl.layers * wl.width
+        line["roofline"] = roofline(r["alg_bytes"], None, K, r["kernel_s"], f"config{cfg}")
+        clocks = r["clocks"]
+    e2e_t = reduce_max(r["e2e_s"])
+    line["e2e"] = {"value": replica_value(n_sub, K, ws, e2e_t), "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
+                   "d2h_bytes_per_step": r["d2h"],
+                   "api": ("CoupledStepper.run_shots(K, 32 shots, probes)" if cfg == 4 else
+                           "CoupledStepper(precision='fp32').run(K, probes)" if args.precision == "fp32" else
+                           "CoupledStepper.run(K, probes)") +
+                          ": initialize from rest, host Ricker table in, probe rows + |U| norms out (pinned staging); "
+                          "timed after one warm-up call of W steps", "warmup_call_s": r.get("e2e_warmup_call_s")}
+    line["roofline"]["streamed_bytes_per_step"] = r["streamed"]
+    line["roofline"]["formula"] = ("8[(2L-1)w(w+1)/2 + 3LwS] bytes, S(2(2L-1)w^2+5Lw) flops per subdomain-step"
+                                   if cfg == 4 else
+                                   f"{4 if args.precision == 'fp32' else 8}[(2L-1)w(w+1)/2 + 3Lw] bytes per "
+                                   "subdomain-step (SURVEY 8d)")
+    line["run"] = {"dt": pp["dt"], "lambda_hat": pp["lam"], "cfl_converged": pp["conv"],
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU", "kernel_ms": r["kernel_s"] * 1e3}
+    line["rom_build"] = pp["build"]
+    line["gpu_launches"] = 1
+    line["clocks"] = clocks
+    if rank != 0:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    if clocks is None:
+        line["clocks"] = {"note": "see the headline fp64 run"}
+    cpu = None
+    if not args.no_cpu and ws == 1:
+        try:
+            c = cpu_subset_run(cfg, min(K, args.cpu_steps), min(W, 3))
+            val = c["rate"] / (32 if cfg == 4 else 1)
+            cpu = {"value": val, "unit": UNIT, "cores": 1, "kind": "port", "sample": c["sample"] +
+                   ("; config 4 = 32 separate single-source runs (SURVEY 8d), so 1/32 of the single-source rate"
+                    if cfg == 4 else ""), "detail": c}
+        except Exception as exc:  # the GPU line must still print
+            cpu = {"value": None, "error": str(exc)[:300]}
+    line["cpu_baseline"] = cpu
+    del pp
+    torch.cuda.empty_cache()
+    if args.extra and cfg == 5 and args.precision == "fp64":
+        try:
+            line["extra"] = _extra_configs(args, line)
+        except Exception as exc:
+            line["extra"] = {"error": str(exc)[:300]}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _entry(wl, r, K, metric_dtype, traffic_key, flops=False, shots=1):
+    n_sub = r["n_sub"]
+    ent = {"workload": _describe(wl) + (f", S={shots} shots" if shots > 1 else ""), "subdomains": n_sub,
+           "steps": K, "ms_per_step": 1e3 * r["kernel_s"] / K, "value": n_sub * K / r["kernel_s"], "unit": UNIT,
+           "dtype": metric_dtype,
+           "roofline": roofline(r["alg_bytes"], r.get("alg_flops") if flops else None, K, r["kernel_s"], traffic_key),
+           "e2e": {"value": n_sub * K / r["e2e_s"], "unit": UNIT, "h2d_bytes_per_step": r["h2d"],
+                   "d2h_bytes_per_step": r["d2h"]}}
+    if shots > 1:
+        ent["shot_steps_per_s"] = shots * ent["value"]
+    return ent
+
+
+def _extra_configs(args, head):
+    """The other BASELINE configs with the same work as the headline (source, probes recorded every
+    step, host profile table) -- kernel-only launch + e2e through the public API, + CPU sample."""
+    import torch
+    K, W = args.steps, args.warmup
+    out = {}
+    # config 5 fp32 W-form (re-builds config 5: the headline's buffers were released)
+    for cfg in (5, 3, 2):
+        from paper_1406_6923_b200.configs import make_workload
+        extra = make_workload(4).sources if cfg == 3 else ()
+        pp = prepare(cfg, extra_rows=extra)
+        wl = pp["wl"]
+        if cfg != 5:
+            r = measure_fp64(pp, K, W)
+            e = _entry(wl, r, K, "f64", f"config{cfg}")
+            e["probes"] = len(pp["probes"])
+            e["rom_build"] = pp["build"]
+            if not args.no_cpu and cfg == 3:
+                try:
+                    c = cpu_subset_run(3, min(K, args.cpu_steps), min(W, 3))
+                    e["cpu_baseline"] = {"value": c["rate"], "unit": UNIT, "cores": 1, "kind": "port",
+                                         "sample": c["sample"]}
+                    out["_cpu3"] = c["rate"]
+                except Exception as exc:
+                    e["cpu_baseline"] = {"error": str(exc)[:200]}
+            out[f"config{cfg}"] = e
+        if cfg in (5, 3):
+            r = measure_fp32(pp, K, W)
+            e = _entry(wl, r, K, "f32", f"config{cfg}_fp32")
+            e["workload"] += ", fp32 W-form"
+            e["probes"] = len(pp["probes"])
+            out[f"config{cfg}_fp32"] = e
+        if cfg == 3:
+            r = measure_shots(pp, K, W)
+            wl4 = make_workload(4)
+            e = _entry(wl4, r, K, "f64", "config4", flops=True, shots=r["shots"])
+            e["probes"] = len(pp["probes"])
+            if "_cpu3" in out:
+                e["cpu_baseline"] = {"value": out["_cpu3"] / 32, "unit": UNIT, "cores": 1, "kind": "port",
+                                     "sample": "config-3 CPU sample rate / 32 (config 4 = 32 separate single-source "
+                                               "runs, SURVEY 8d)"}
+            out["config4"] = e
+        del pp
+        torch.cuda.empty_cache()
+    out.pop("_cpu3", None)
+    return out
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from paper_1406_6923_b200.configs import make_workload
+    cfg = args.config
+    wl = make_workload(cfg)
+    c = cpu_subset_run(cfg, args.steps, args.warmup)
+    n_probes = len(wl.face_receivers) * wl.modes_per_face + len(wl.node_receivers)
+    val = c["rate"] / (32 if cfg == 4 else 1)
+    line = _line(METRIC if args.precision == "fp64" else METRIC.replace("fp64", "fp32 W-form"), val, args.steps,
+                 args.warmup, ws, c["seconds"], "f64",
+                 config_key(wl, n_probes, shots=32 if cfg == 4 else 1))
+    line["ms_per_step"] = 1e3 * c["seconds"] / args.steps
+    line["data"] = "synthetic (seeded medium, SURVEY 8d); models built on the host by the oracle port of rom.py"
+    line["impl"] = "reference"
+    line["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": 1, "kind": "port", "sample": c["sample"]}
+    line["e2e"] = {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    line["run"] = {k: c[k] for k in ("dt", "lambda_hat", "cfl_converged", "cfl_seconds", "window", "subdomains",
+                                     "probes")}
+    line["rom_build"] = {"seconds": c["build_seconds"], "subdomains_per_s": c["build_subdomains_per_s"],
+                         "cores": c["build_cores"], "kind": "port (scipy SuperLU + LAPACK, one process per core)"}
     print(json.dumps(line), flush=True)
 
 
@@ -689,15 +706,15 @@ def _run_fdtd(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20000)
-    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extra", type=int, default=1,
-                    help="also measure configs 3, 4, 5 (fp64 and fp32) kernel-only stepping (default on)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+                    help="with config 5 fp64: also measure configs 5 fp32, 3 (fp64/fp32), 4 and 2 (default on)")
+    ap.add_argument("--cpu-steps", type=int, default=200, help="cap on the CPU sample's timed steps")
     ap.add_argument("--fdtd", action="store_true", help="fine-grid reference solver on the config's full grid")
     args = ap.parse_args()
     if args.fdtd:

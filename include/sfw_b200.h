@@ -41,6 +41,67 @@ const char* sfw_last_error(void);
 int sfw_device_info(int* n_sm, char* name, int name_len);
 
 /* ------------------------------------------------------------------------- */
+/* Stage 1: off-line ROM build, batched over subdomains.                      */
+/* Replaces sfwave.rom.build_subdomain_model (rom.py:359-434) called once per   */
+/* subdomain by sim.run_offline (sim.py:318-330):                              */
+/*   SubdomainOperator.matrix (grid.py:415-458)  -> a stencil from c, mu, h     */
+/*   subdomain_inputs (rom.py:45-86)             -> face basis kernel          */
+/*   _shifted_solver + build_krylov_basis (rom.py:89-174) -> PCG + CGS2/CholQR2 */
+/*   truncation (rom.py:375-403), project_reduced (rom.py:177-182)             */
+/*   block_lanczos (rom.py:185-262), sfraction_transform (rom.py:265-316)      */
+/* ------------------------------------------------------------------------- */
+
+typedef struct sfw_rom_desc {
+    int n_sub;             /* subdomains in this call                                          */
+    int p[3];              /* nodes per axis of every subdomain (the reference's op.shape)     */
+    double h[3];           /* grid spacing per axis (op.spacing)                               */
+    int m, n;              /* modes per face (a perfect square), Krylov depth (rom.n)          */
+    double shift;          /* shift s of the shifted-inverse Krylov space (rom.py:89-116)      */
+    const double* c;       /* HOST [n_sub][p0*p1*p2] sound speed on the subdomain's nodes      */
+    const int* nbr_mask;   /* HOST [n_sub] bit f set when face f is shared (op.neighbors)      */
+    int n_rows;            /* node rows of V Q to return (sources / receivers)                 */
+    const int* row_sub;    /* HOST [n_rows] subdomain index of each row                        */
+    const int* row_node;   /* HOST [n_rows] local node index                                   */
+    int full_basis;        /* 1: also return the full N x K basis V Q                          */
+    int out_on_device;     /* 1: gammas / gamma_hats / scales are DEVICE pointers              */
+    int batch;             /* subdomains per internal batch (0 = fit 45% of free HBM)         */
+} sfw_rom_desc;
+
+typedef struct sfw_rom_out {
+    int* layers;           /* HOST [n_sub] kept chain layers (complete w-blocks, rom.py:375-403) */
+    int* flags;            /* HOST [n_sub] bit0 deflated, bit1 truncated                      */
+    int* status;           /* HOST [n_sub] 0 ok, else the failing stage (NumericalError)     */
+    double* gammas;        /* [n_sub][n+1][w][w] Gamma_j (HOST, or DEVICE if out_on_device)   */
+    double* gamma_hats;    /* same layout, Gamma-hat_j                                        */
+    double* scales;        /* same layout, G_j                                                */
+    double* tdiag;         /* HOST [n_sub][n+1][w][w] Lanczos A_j, or NULL                    */
+    double* toff;          /* HOST [n_sub][n][w][w] Lanczos B_j (upper triangular), or NULL  */
+    double* basis_rows;    /* HOST [n_rows][K] rows of V Q, or NULL                           */
+    double* basis;         /* HOST [n_sub][K][N] (column-major N x K) V Q, or NULL            */
+    double* stats;         /* HOST [16]: seconds per stage, max PCG iterations, batch, wall  */
+} sfw_rom_out;
+
+/* Build the S-fraction chains of n_sub subdomains (SURVEY 8b sfw_rom_build_batch).
+ * Per-subdomain failures (dependent depth-1 block, rank loss, cond > 1e12 in the
+ * S-fraction recursion, Gamma-hat_1 != I) set status[i] and return SFW_ENUMERICAL
+ * after the whole batch ran, as sim.run_offline aggregates them (sim.py:342-350). */
+int sfw_rom_build(const sfw_rom_desc* desc, sfw_rom_out* out, char* errbuf, int errlen);
+
+/* Y = A X with the build's stencil form of the subdomain operator (A = -C S C, grid.py:415-458)
+ * for n_sub subdomains of one shape: c HOST [n_sub][N], X / Y HOST [n_sub][ncols][N].  Lets the
+ * caller check an explicit SubdomainOperator.matrix against what the GPU build factors. */
+int sfw_subdomain_apply(int n_sub, const int* p, const double* h, const double* c, const int* nbr_mask,
+                        int ncols, const double* X, double* Y, char* errbuf, int errlen);
+
+/* project_state (rom.py:437-447): out (K) = blockdiag(G_j) (V Q)^T x for a node-space
+ * field x (N).  state_to_nodes (rom.py:450-459): out (N) = V Q blockdiag(G_j^-1) u.
+ * basis: HOST N x K row-major (SubdomainModel.basis), scales: HOST L x w x w, K = L w. */
+int sfw_project_state(int N, int L, int w, const double* basis, const double* scales, const double* x,
+                      double* out, char* errbuf, int errlen);
+int sfw_state_to_nodes(int N, int L, int w, const double* basis, const double* scales, const double* u,
+                       double* out, char* errbuf, int errlen);
+
+/* ------------------------------------------------------------------------- */
 /* Stage 2: coupled leapfrog stepping.                                         */
 /* Replaces sfwave.stepper.CoupledStepper (stepper.py:144-449):               */
 /*   __init__ + _pair_interfaces (stepper.py:147-220)  -> sfw_step_create      */
@@ -170,6 +231,11 @@ int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, const double* p
 int sfw_wform_state(sfw_stepper* h, double* u_curr, double* u_prev, char* errbuf, int errlen);
 int sfw_wform_traffic(sfw_stepper* h, double* alg_bytes, double* streamed_bytes);
 int sfw_wform_destroy(sfw_stepper* h);
+
+/* Interface masses ha (ha + hb)^-1 hb, symmetrised (stepper.py:64-70, 204-210), as the device
+ * computed them at create: *n_iface interfaces in _pair_interfaces order (low subdomain
+ * ascending, then face), out HOST [n_iface][m][m] (may be NULL to query the count). */
+int sfw_step_masses(sfw_stepper* h, int* n_iface, double* out, char* errbuf, int errlen);
 
 /* Copy the current/previous state (HOST concat of L_s*w per subdomain). */
 int sfw_step_get_state(sfw_stepper* h, double* u_curr, double* u_prev);

@@ -636,6 +636,129 @@ class Coupled:
         return tot
 
 
+class CoupledBatched:
+    """``Coupled`` restated over stacked arrays, for full-size (4096 / 16384-subdomain) windows.
+
+    Same formulas and evaluation order per subdomain as ``Coupled`` (stepper.py:243-389):
+    flux_1 = Gamma_1 (U_2 - U_1); acc_1 = Gamma-hat_1 flux_1 with shared face slices replaced by
+    mass (own + msg); acc_j = Gamma-hat_j (Gamma_j (U_{j+1} - U_j) - Gamma_{j-1} (U_j - U_{j-1}));
+    U_next = 2 U - U_prev + dt^2 (acc + f).  The block products are numpy stacked matmuls instead
+    of per-subdomain gemv calls, so it agrees with ``Coupled`` to rounding (tests/test_oracle_golden.py
+    pins the two against each other), not bit for bit.  Uniform layer count only.
+
+    gammas / hats: (n, L, w, w) in sorted(alpha) order; nbr: (n, 6) neighbour index or -1;
+    sources: list of (index, vector, profile); probes: list of (index, weights).
+    """
+
+    def __init__(self, gammas, hats, nbr, m, dt, sources=(), alt=False):
+        self.alt = bool(alt)  # einsum products: another summation order (measures the oracle's floor)
+        self.G = np.asarray(gammas, dtype=float)
+        self.H = np.asarray(hats, dtype=float)
+        self.n, self.L, self.w = self.G.shape[0], self.G.shape[1], self.G.shape[2]
+        self.m = int(m)
+        self.nbr = np.asarray(nbr, dtype=np.int64)
+        self.dt = float(dt)
+        self.sources = tuple(sources)
+        lo, lf, hi, hf, mass = [], [], [], [], []
+        for a in range(self.n):  # stepper.py:178-220 pairing, low index owns the interface
+            for f in range(6):
+                b = int(self.nbr[a, f])
+                if b > a:
+                    sa = slice(f * m, (f + 1) * m)
+                    sb = slice((f ^ 1) * m, ((f ^ 1) + 1) * m)
+                    ha = self.H[a, 0][sa, sa]
+                    hb = self.H[b, 0][sb, sb]
+                    mm = ha @ np.linalg.solve(ha + hb, hb)
+                    lo.append(a)
+                    lf.append(f)
+                    hi.append(b)
+                    hf.append(f ^ 1)
+                    mass.append(0.5 * (mm + mm.T))
+        self.if_lo, self.if_lf = np.array(lo, dtype=np.int64), np.array(lf, dtype=np.int64)
+        self.if_hi, self.if_hf = np.array(hi, dtype=np.int64), np.array(hf, dtype=np.int64)
+        self.mass = np.stack(mass) if mass else np.zeros((0, m, m))
+        self._fidx = np.arange(m)
+        self.steps_done = 0
+        self.time = 0.0
+        self._base = 0.0
+
+    def _mv(self, A, x):
+        if self.alt:
+            return np.einsum("nij,nj->ni", A, x)
+        return np.matmul(A, x[..., None])[..., 0]
+
+    def acceleration(self, U):
+        """U: (n, L, w) -> acc (n, L, w)."""
+        m, L = self.m, self.L
+        u2 = U[:, 1] if L > 1 else np.zeros_like(U[:, 0])
+        flux = self._mv(self.G[:, 0], u2 - U[:, 0])
+        acc = np.empty_like(U)
+        acc[:, 0] = self._mv(self.H[:, 0], flux)
+        if len(self.if_lo):
+            cols_lo = self.if_lf[:, None] * m + self._fidx[None, :]
+            cols_hi = self.if_hf[:, None] * m + self._fidx[None, :]
+            own = flux[self.if_lo[:, None], cols_lo]
+            msg = flux[self.if_hi[:, None], cols_hi]
+            seg = self._mv(self.mass, own + msg)
+            acc[self.if_lo[:, None], 0, cols_lo] = seg
+            acc[self.if_hi[:, None], 0, cols_hi] = seg
+        for j in range(1, L):
+            cur, prv = U[:, j], U[:, j - 1]
+            nxt = U[:, j + 1] if j + 1 < L else 0.0
+            acc[:, j] = self._mv(self.H[:, j], self._mv(self.G[:, j], nxt - cur) - self._mv(self.G[:, j - 1], cur - prv))
+        return acc
+
+    def _force(self, t):
+        out = {}
+        for i, vec, prof in self.sources:
+            term = np.asarray(vec, dtype=float).reshape(self.L, self.w) * prof(t)
+            out[i] = out[i] + term if i in out else term
+        return out
+
+    def initialize(self, u0=None, v0=None):
+        self.u_curr = np.zeros((self.n, self.L, self.w)) if u0 is None else np.array(u0, dtype=float)
+        vel = np.zeros_like(self.u_curr) if v0 is None else np.asarray(v0, dtype=float)
+        acc = self.acceleration(self.u_curr)
+        for i, f in self._force(0.0).items():
+            acc[i] = acc[i] + f
+        dt = self.dt
+        self.u_prev = self.u_curr - dt * vel + 0.5 * dt * dt * acc
+        self.steps_done = 0
+        self.time = 0.0
+        self._base = float(np.sum(np.linalg.norm(self.u_curr.reshape(self.n, -1), axis=1))
+                           + dt * np.sum(np.linalg.norm(vel.reshape(self.n, -1), axis=1)))
+
+    def advance(self):
+        dt = self.dt
+        t = self.time
+        acc = self.acceleration(self.u_curr)
+        for i, f in self._force(t).items():
+            acc[i] = acc[i] + f
+        nxt = 2.0 * self.u_curr - self.u_prev + dt * dt * acc
+        self.u_prev, self.u_curr = self.u_curr, nxt
+        self.steps_done += 1
+        self.time = self.steps_done * dt
+        for _, vec, prof in self.sources:
+            self._base += dt * dt * abs(float(prof(t))) * float(np.linalg.norm(vec))
+        nrm = float(np.sqrt(np.sum(self.u_curr * self.u_curr)))
+        if nrm > GROWTH_LIMIT * max(self._base, 1e-300):
+            raise OracleError("InstabilityError", f"coupled stepping diverged at step {self.steps_done}")
+
+    def run(self, n_steps, probes=(), u0=None, v0=None):
+        self.initialize(u0, v0)
+        pi = np.array([i for i, _ in probes], dtype=np.int64)
+        pw = np.stack([np.asarray(wt, dtype=float) for _, wt in probes]) if probes else np.zeros((0, self.L * self.w))
+
+        def row():
+            return np.einsum("pk,pk->p", pw, self.u_curr.reshape(self.n, -1)[pi]) if len(pi) else np.zeros(0)
+
+        rows = [row()]
+        for _ in range(n_steps):
+            self.advance()
+            rows.append(row())
+        return np.arange(n_steps + 1) * self.dt, np.asarray(rows)
+
+
 def cfl_power(models: dict, tol=POWER_TOL, max_iter=POWER_MAX_ITER, seed=0):
     """(lambda_hat, converged) of the coupled map (stepper.py:452-487)."""
     st = Coupled(models, dt=1.0)

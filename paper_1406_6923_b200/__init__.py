@@ -16,9 +16,10 @@ from .grid import (DomainPartition, DomainSpec, SubdomainOperator, assemble_glob
 from .fdtd import (FineGridOperator, LeapfrogRun, estimate_lambda_max, leapfrog_energy, run_leapfrog,  # noqa: F401
                    stability_limit)
 from .io import TraceRecord, load_model, read_traces, save_model, write_traces  # noqa: F401
-from .rom import SubdomainModel, build_models, build_subdomain_model  # noqa: F401
+from .rom import (SubdomainModel, build_models, build_subdomain_model, project_state,  # noqa: F401
+                  state_to_nodes)
 from .stepper import (CoupledStepper, Probe, SourceTerm, cfl_estimate_coupled, make_probe,  # noqa: F401
-                      project_source, stable_step_coupled)
+                      project_source, resolve_dt, stable_step_coupled)
 
 __all__ = [
     "ConfigError", "CoupledStepper", "DataError", "DeviceError", "DomainPartition", "DomainSpec",
@@ -27,6 +28,7 @@ __all__ = [
     "write_traces",
     "InstabilityError", "NumericalError", "Probe", "ProtocolError", "SfwaveError", "SourceTerm",
     "SubdomainModel", "SubdomainOperator", "build_models", "build_subdomain_model", "assemble_subdomain_operator", "build_partition",
-    "cfl_estimate_coupled", "make_probe", "opposite_face", "project_source", "stable_step_coupled",
+    "cfl_estimate_coupled", "make_probe", "opposite_face", "project_source", "project_state", "resolve_dt",
+    "stable_step_coupled", "state_to_nodes",
     "__version__",
 ]

@@ -37,8 +37,27 @@ class StepDesc(C.Structure):
     ]
 
 
+class RomDesc(C.Structure):
+    """include/sfw_b200.h sfw_rom_desc."""
+    _fields_ = [("n_sub", C.c_int), ("p", C.c_int * 3), ("h", C.c_double * 3), ("m", C.c_int),
+                ("n", C.c_int), ("shift", C.c_double), ("c", PD), ("nbr_mask", PI),
+                ("n_rows", C.c_int), ("row_sub", PI), ("row_node", PI), ("full_basis", C.c_int),
+                ("out_on_device", C.c_int), ("batch", C.c_int)]
+
+
+class RomOut(C.Structure):
+    """include/sfw_b200.h sfw_rom_out."""
+    _fields_ = [("layers", PI), ("flags", PI), ("status", PI), ("gammas", PD),
+                ("gamma_hats", PD), ("scales", PD), ("tdiag", PD), ("toff", PD),
+                ("basis_rows", PD), ("basis", PD), ("stats", PD)]
+
+
 # name -> (restype, argtypes); every symbol include/sfw_b200.h declares
 SIGNATURES = {
+    "sfw_rom_build": (C.c_int, [C.POINTER(RomDesc), C.POINTER(RomOut), C.c_char_p, C.c_int]),
+    "sfw_subdomain_apply": (C.c_int, [C.c_int, PI, PD, PD, PI, C.c_int, PD, PD, C.c_char_p, C.c_int]),
+    "sfw_project_state": (C.c_int, [C.c_int, C.c_int, C.c_int, PD, PD, PD, PD, C.c_char_p, C.c_int]),
+    "sfw_state_to_nodes": (C.c_int, [C.c_int, C.c_int, C.c_int, PD, PD, PD, PD, C.c_char_p, C.c_int]),
     "sfw_last_error": (C.c_char_p, []),
     "sfw_device_info": (C.c_int, [PI, C.c_char_p, C.c_int]),
     "sfw_step_create": (C.c_int, [C.POINTER(StepDesc), C.POINTER(C.c_void_p), C.c_char_p, C.c_int]),
@@ -48,6 +67,7 @@ SIGNATURES = {
     "sfw_step_set_probes": (C.c_int, [C.c_void_p, C.c_int, PI, PD, C.c_char_p, C.c_int]),
     "sfw_step_accel": (C.c_int, [C.c_void_p, PD, PD, PD, C.c_char_p, C.c_int]),
     "sfw_step_power": (C.c_int, [C.c_void_p, PD, C.c_double, C.c_int, PD, PI, PI, C.c_char_p, C.c_int]),
+    "sfw_step_masses": (C.c_int, [C.c_void_p, PI, PD, C.c_char_p, C.c_int]),
     "sfw_step_get_state": (C.c_int, [C.c_void_p, PD, PD]),
     "sfw_step_energy": (C.c_int, [C.c_void_p, PD, C.c_char_p, C.c_int]),
     "sfw_step_traffic": (C.c_int, [C.c_void_p, PD, PD, PD]),

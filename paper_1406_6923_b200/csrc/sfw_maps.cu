@@ -6,6 +6,7 @@
 // pivoting (LAPACK gesv semantics) in shared memory.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -13,7 +14,7 @@
 
 namespace sfw {
 
-// out_j = G_j v_j   (kind 0)   or   out_j = G_j^-T v_j   (kind 1); v already scaled
+// out_j = G_j v_j (kind 0), out_j = G_j^-T v_j (kind 1) or out_j = G_j^-1 v_j (kind 2); v already scaled
 __global__ void k_layer_map(const double* __restrict__ G, const double* __restrict__ v, int w, int kind,
                             double* __restrict__ out, int* __restrict__ status) {
     extern __shared__ double sh[];
@@ -34,7 +35,7 @@ __global__ void k_layer_map(const double* __restrict__ G, const double* __restri
     __shared__ int piv;
     for (int i = threadIdx.x; i < w * w; i += blockDim.x) {
         const int r = i / w, c = i % w;
-        A[i] = Gj[c * w + r];
+        A[i] = (kind == 1) ? Gj[c * w + r] : Gj[i];
     }
     for (int i = threadIdx.x; i < w; i += blockDim.x) b[i] = vj[i];
     __syncthreads();
@@ -80,6 +81,28 @@ __global__ void k_layer_map(const double* __restrict__ G, const double* __restri
         }
         for (int i = 0; i < w; ++i) oj[i] = b[i];
     }
+}
+
+// out[k] = sum_n B[n][k] x[n] (B row-major N x K): one thread per column, n ascending
+__global__ void k_basis_t(const double* __restrict__ B, const double* __restrict__ x, int N, int K,
+                          double* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    double s = 0.0;
+    for (int n = 0; n < N; ++n) s = fma(B[(size_t)n * K + k], x[n], s);
+    out[k] = s;
+}
+
+// out[n] = sum_k B[n][k] c[k]: one warp per row, lane-strided partials, fixed-order butterfly
+__global__ void k_basis_n(const double* __restrict__ B, const double* __restrict__ c, int N, int K,
+                          double* __restrict__ out) {
+    const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (n >= N) return;
+    double s = 0.0;
+    for (int k = lane; k < K; k += 32) s = fma(B[(size_t)n * K + k], c[k], s);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[n] = s;
 }
 
 __global__ void k_scale_vec(const double* __restrict__ x, long long n, double s, double* __restrict__ y) {
@@ -163,4 +186,64 @@ extern "C" int sfw_source_vector(int L, int w, const double* scales, const doubl
 extern "C" int sfw_probe_weights(int L, int w, const double* scales, const double* basis_row, double scale,
                                  double* out, char* errbuf, int errlen) {
     return maps_common(L, w, scales, basis_row, scale, 1, out, nullptr, errbuf, errlen);
+}
+
+// project_state / state_to_nodes (reference rom.py:437-459): basis HOST N x K row-major (V Q as
+// SubdomainModel.basis stores it), scales HOST L x w x w; dir 0: x = node field (N) -> out (K),
+// out_j = G_j (B^T x)_j; dir 1: x = chain state (K) -> out (N) = B (G_j^-1 x_j)_j.
+static int state_map(int dir, int N, int L, int w, const double* basis, const double* scales, const double* x,
+                     double* out, char* errbuf, int errlen) {
+    if (N < 1 || L < 1 || w < 1 || !basis || !scales || !x || !out)
+        return fail(SFW_ECONFIG, "state map: bad sizes or NULL arrays", errbuf, errlen);
+    const int K = L * w;
+    double *dB = nullptr, *dG = nullptr, *dx = nullptr, *dc = nullptr, *dout = nullptr;
+    int* dst = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(dB);
+        cudaFree(dG);
+        cudaFree(dx);
+        cudaFree(dc);
+        cudaFree(dout);
+        cudaFree(dst);
+    };
+    if (cudaMalloc(&dB, (size_t)N * K * 8) != cudaSuccess || cudaMalloc(&dG, (size_t)K * w * 8) != cudaSuccess ||
+        cudaMalloc(&dx, (size_t)std::max(N, K) * 8) != cudaSuccess || cudaMalloc(&dc, (size_t)K * 8) != cudaSuccess ||
+        cudaMalloc(&dout, (size_t)std::max(N, K) * 8) != cudaSuccess || cudaMalloc(&dst, L * sizeof(int)) != cudaSuccess) {
+        cleanup();
+        return fail(SFW_ECUDA, "cudaMalloc failed in the state maps", errbuf, errlen);
+    }
+    sfw_h2d(dB, basis, (size_t)N * K * 8);
+    sfw_h2d(dG, scales, (size_t)K * w * 8);
+    sfw_h2d(dx, x, (size_t)(dir == 0 ? N : K) * 8);
+    cudaMemset(dst, 0, L * sizeof(int));
+    int rc = 0;
+    if (dir == 0) {
+        k_basis_t<<<(K + 127) / 128, 128>>>(dB, dx, N, K, dc);
+        k_layer_map<<<L, 128>>>(dG, dc, w, 0, dout, dst);
+        cudaMemcpy(out, dout, (size_t)K * 8, cudaMemcpyDeviceToHost);
+    } else {
+        const size_t sm = (size_t)(w * w + w) * 8;
+        cudaFuncSetAttribute(k_layer_map, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_layer_map<<<L, 128, sm>>>(dG, dx, w, 2, dc, dst);
+        k_basis_n<<<(N * 32 + 255) / 256, 256>>>(dB, dc, N, K, dout);
+        cudaMemcpy(out, dout, (size_t)N * 8, cudaMemcpyDeviceToHost);
+        std::vector<int> st(L);
+        cudaMemcpy(st.data(), dst, L * sizeof(int), cudaMemcpyDeviceToHost);
+        for (int j = 0; j < L; ++j)
+            if (st[j]) rc = fail(SFW_ENUMERICAL, "singular chain scale matrix in state_to_nodes", errbuf, errlen);
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = fail(SFW_ECUDA, cudaGetErrorString(e), errbuf, errlen);
+    cleanup();
+    return rc;
+}
+
+extern "C" int sfw_project_state(int N, int L, int w, const double* basis, const double* scales, const double* x,
+                                 double* out, char* errbuf, int errlen) {
+    return state_map(0, N, L, w, basis, scales, x, out, errbuf, errlen);
+}
+
+extern "C" int sfw_state_to_nodes(int N, int L, int w, const double* basis, const double* scales, const double* u,
+                                  double* out, char* errbuf, int errlen) {
+    return state_map(1, N, L, w, basis, scales, u, out, errbuf, errlen);
 }

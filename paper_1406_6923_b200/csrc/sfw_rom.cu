@@ -665,37 +665,7 @@ static void gemm(cudaStream_t st, bool ta, int M, int N, int K, double alpha, co
 
 using namespace sfw;
 
-extern "C" {
-typedef struct sfw_rom_desc {
-    int n_sub;
-    int p[3];
-    double h[3];
-    int m, n;
-    double shift;
-    const double* c;       // HOST [n_sub][p0*p1*p2]
-    const int* nbr_mask;   // HOST [n_sub]
-    int n_rows;
-    const int* row_sub;    // HOST [n_rows]
-    const int* row_node;   // HOST [n_rows]
-    int full_basis;
-    int out_on_device;
-    int batch;             // subdomains per batch (0 = automatic)
-} sfw_rom_desc;
-
-typedef struct sfw_rom_out {
-    int* layers;           // HOST [n_sub]
-    int* flags;            // HOST [n_sub] bit0 deflated, bit1 truncated
-    int* status;           // HOST [n_sub]
-    double* gammas;        // [n_sub][L][w][w]  (HOST, or DEVICE if out_on_device)
-    double* gamma_hats;
-    double* scales;
-    double* tdiag;         // HOST [n_sub][L][w][w] or NULL
-    double* toff;          // HOST [n_sub][L-1][w][w] or NULL
-    double* basis_rows;    // HOST [n_rows][K] or NULL
-    double* basis;         // HOST [n_sub][K][N] (column-major N x K) or NULL
-    double* stats;         // HOST [16]: seconds per stage, max PCG iterations, ...
-} sfw_rom_out;
-}
+// sfw_rom_desc / sfw_rom_out: include/sfw_b200.h
 
 namespace {
 struct DevBuf {
@@ -731,6 +701,49 @@ extern "C" int sfw_face_inputs(int px, int py, int pz, int m, int nbr_mask, doub
     cudaFree(dm);
     if (e != cudaSuccess) return fail(SFW_ECUDA, cudaGetErrorString(e), errbuf, errlen);
     return 0;
+}
+
+// Y = A X for n_sub subdomains with the build's own stencil (k_axis_eig tables + k_stencil):
+// the operator the GPU pipeline factors, so a caller can check it against an explicit
+// SubdomainOperator.matrix (reference grid.py:415-458) before trusting the build.
+extern "C" int sfw_subdomain_apply(int n_sub, const int* p, const double* h, const double* c, const int* nbr_mask,
+                                   int ncols, const double* X, double* Y, char* errbuf, int errlen) {
+    if (n_sub <= 0 || ncols <= 0) return 0;
+    const int px = p[0], py = p[1], pz = p[2];
+    if (px < 4 || py < 4 || pz < 4 || px > PMAX || py > PMAX || pz > PMAX)
+        return fail(SFW_ECONFIG, "nodes per subdomain axis must be in [4, 32]", errbuf, errlen);
+    const int N = px * py * pz;
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(SFW_ECUDA, "stream creation failed", errbuf, errlen);
+    int rc = 0;
+    {
+        DevBuf db;
+        double* dQt = db.get<double>(12 * PMAX * PMAX);
+        double* dlam = db.get<double>(12 * PMAX);
+        double* ddt = db.get<double>(12 * PMAX);
+        double* det = db.get<double>(12 * PMAX);
+        double* dc = db.get<double>((size_t)n_sub * N);
+        int* dm = db.get<int>(n_sub);
+        double* dX = db.get<double>((size_t)n_sub * ncols * N);
+        double* dY = db.get<double>((size_t)n_sub * ncols * N);
+        if (!dQt || !dc || !dm || !dX || !dY) {
+            rc = fail(SFW_ECUDA, "out of device memory in sfw_subdomain_apply", errbuf, errlen);
+        } else {
+            sfw_h2d(dc, c, (size_t)n_sub * N * 8);
+            sfw_h2d(dm, nbr_mask, (size_t)n_sub * sizeof(int));
+            sfw_h2d(dX, X, (size_t)n_sub * ncols * N * 8);
+            k_axis_eig<<<1, 32, 0, st>>>(px, py, pz, h[0], h[1], h[2], dQt, dlam, ddt, det);
+            k_stencil<<<dim3(ncols, n_sub, 8), 128, 0, st>>>(px, py, pz, N, ncols, dc, dm, ddt, det, dX, N,
+                                                              (long long)ncols * N, 0, dY, (long long)ncols * N);
+            cudaMemcpyAsync(Y, dY, (size_t)n_sub * ncols * N * 8, cudaMemcpyDeviceToHost, st);
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e == cudaSuccess) e = cudaGetLastError();
+            if (e != cudaSuccess) rc = fail(SFW_ECUDA, cudaGetErrorString(e), errbuf, errlen);
+        }
+    }
+    cudaStreamDestroy(st);
+    return rc;
 }
 
 extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf, int errlen) {

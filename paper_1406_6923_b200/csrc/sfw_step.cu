@@ -3188,9 +3188,11 @@ static int run_common(sfw_stepper* h, int n_steps, int record_every, const doubl
                       int errlen) {
     if (n_steps <= 0) return 0;
     if (record_every < 1) return fail(SFW_ECONFIG, "record_every must be >= 1", errbuf, errlen);
+    if (h->n_src && !profile)  // the kernel would read a stale or unwritten f(t_k) table
+        return fail(SFW_ECONFIG, "a stepper with sources needs the f(t_k) profile table", errbuf, errlen);
     int rc = ensure(h, &h->ftab, &h->ftab_cap, std::max(1LL, (long long)h->n_src * n_steps), errbuf, errlen);
     if (rc) return rc;
-    if (h->n_src && profile)
+    if (h->n_src)
         SFW_CUDA_TRY(cudaMemcpyAsync(h->ftab, profile, (size_t)h->n_src * n_steps * 8, cudaMemcpyHostToDevice,
                                      h->stream));
     const long long nrec = n_steps / record_every;
@@ -3273,6 +3275,18 @@ extern "C" int sfw_step_run_resident(sfw_stepper* h, int n_steps, int record_eve
     SFW_CUDA_TRY(cudaEventSynchronize(h->ev1));
     SFW_CUDA_TRY(cudaGetLastError());
     if (kernel_ms) cudaEventElapsedTime(kernel_ms, h->ev0, h->ev1);
+    return 0;
+}
+
+extern "C" int sfw_step_masses(sfw_stepper* h, int* n_iface, double* out, char* errbuf, int errlen) {
+    // interface masses ha (ha + hb)^-1 hb (stepper.py:204-210) as computed on the device at create, in
+    // the reference's _pair_interfaces order (low subdomain ascending, then face)
+    if (n_iface) *n_iface = h->n_iface;
+    if (out && h->n_iface > 0) {
+        SFW_CUDA_TRY(cudaMemcpyAsync(out, h->mass, (size_t)h->n_iface * h->m * h->m * 8, cudaMemcpyDeviceToHost,
+                                     h->stream));
+        SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
     return 0;
 }
 

@@ -1,7 +1,7 @@
-"""Off-line ROM data model (mirror of reference rom.py:319-356 SubdomainModel).
-
-The batched sm_100a build pipeline lives in ``romgpu.py`` / ``csrc/sfw_rom.cu``;
-``build_subdomain_model`` keeps the reference signature (rom.py:359-364).
+"""Off-line ROM stage: data model (reference rom.py:319-356 SubdomainModel), the batched
+sm_100a build (``build_models`` -> ``sfw_rom_build`` in csrc/sfw_rom.cu) behind the reference
+signature ``build_subdomain_model`` (rom.py:359-364), and the node/chain maps ``project_state``
+/ ``state_to_nodes`` (rom.py:437-459, ``sfw_project_state`` / ``sfw_state_to_nodes``).
 """
 
 from __future__ import annotations
@@ -86,26 +86,47 @@ from . import _lib  # noqa: E402
 from .errors import ConfigError  # noqa: E402
 
 
-class _RomDesc(_C.Structure):
-    _fields_ = [("n_sub", _C.c_int), ("p", _C.c_int * 3), ("h", _C.c_double * 3), ("m", _C.c_int),
-                ("n", _C.c_int), ("shift", _C.c_double), ("c", _lib.PD), ("nbr_mask", _lib.PI),
-                ("n_rows", _C.c_int), ("row_sub", _lib.PI), ("row_node", _lib.PI), ("full_basis", _C.c_int),
-                ("out_on_device", _C.c_int), ("batch", _C.c_int)]
-
-
-class _RomOut(_C.Structure):
-    _fields_ = [("layers", _lib.PI), ("flags", _lib.PI), ("status", _lib.PI), ("gammas", _lib.PD),
-                ("gamma_hats", _lib.PD), ("scales", _lib.PD), ("tdiag", _lib.PD), ("toff", _lib.PD),
-                ("basis_rows", _lib.PD), ("basis", _lib.PD), ("stats", _lib.PD)]
-
-
-_lib.SIGNATURES["sfw_rom_build"] = (_C.c_int, [_C.POINTER(_RomDesc), _C.POINTER(_RomOut), _C.c_char_p, _C.c_int])
-
 LAST_BUILD_STATS: dict = {}
 
 
 def _mask(neighbors) -> int:
     return sum(1 << f for f in neighbors)
+
+
+def check_operators(ops, shape, spacing, c, masks, tol: float = 1e-10):
+    """The GPU build never reads ``op.matrix``: it rebuilds the operator from (c, mu, h, neighbours)
+    as the stencil A = -C S C of grid.py:415-458.  When an operator carries an explicit matrix (a
+    reference ``SubdomainOperator`` always does), apply both to one seeded random vector -- the
+    stencil on the device (``sfw_subdomain_apply``) -- and refuse operators that differ, instead
+    of silently building a model of another operator."""
+    idx = [i for i, op in enumerate(ops) if getattr(op, "matrix", None) is not None]
+    if not idx:
+        return
+    lib = _lib.load()
+    N = int(np.prod(shape))
+    x = np.random.default_rng(1406).standard_normal(N)
+    p = np.array(shape, dtype=np.int32)
+    h = np.array(spacing, dtype=np.float64)
+    for s0 in range(0, len(idx), 512):
+        sel = idx[s0:s0 + 512]
+        X = np.ascontiguousarray(np.broadcast_to(x, (len(sel), N)))
+        Y = np.empty((len(sel), N))
+        eb = _lib.errbuf()
+        rc = lib.sfw_subdomain_apply(len(sel), _lib.iptr(p), _lib.dptr(h), _lib.dptr(np.ascontiguousarray(c[sel])),
+                                     _lib.iptr(np.ascontiguousarray(masks[sel])), 1, _lib.dptr(X), _lib.dptr(Y),
+                                     eb, 1024)
+        _lib.check(rc, eb, "operator check")
+        for k, i in enumerate(sel):
+            mat = ops[i].matrix
+            if getattr(mat, "shape", None) != (N, N):
+                raise ConfigError(f"subdomain {ops[i].alpha}: operator matrix has shape {getattr(mat, 'shape', None)}, "
+                                  f"expected {(N, N)}")
+            want = np.asarray(mat @ x, dtype=np.float64).reshape(-1)
+            err = float(np.linalg.norm(Y[k] - want)) / max(float(np.linalg.norm(want)), 1e-300)
+            if not err <= tol:
+                raise ConfigError(f"subdomain {ops[i].alpha}: op.matrix is not the finite-volume operator of its "
+                                  f"(c, mu, spacing, neighbours) (relative mismatch {err:.2e}); the GPU build "
+                                  "assembles that operator itself and cannot take an arbitrary matrix")
 
 
 def build_models(ops, modes_per_face: int, n: int, shift: float, basis=None, rows=None, batch: int = 0,
@@ -122,10 +143,6 @@ def build_models(ops, modes_per_face: int, n: int, shift: float, basis=None, row
     (int addresses) receiving the chain stacks directly in HBM.
     """
     lib = _lib.load()
-    if not hasattr(lib.sfw_rom_build, "_typed"):
-        fn = lib.sfw_rom_build
-        fn.restype, fn.argtypes = _lib.SIGNATURES["sfw_rom_build"]
-        fn._typed = True
     ops = list(ops)
     if not ops:
         return {}
@@ -150,6 +167,7 @@ def build_models(ops, modes_per_face: int, n: int, shift: float, basis=None, row
     ns = len(ops)
     c = np.ascontiguousarray(np.stack([np.asarray(op.c, dtype=np.float64).reshape(-1) for op in ops]))
     masks = np.array([_mask(op.neighbors) for op in ops], dtype=np.int32)
+    check_operators(ops, shape, spacing, c, masks)
     want_basis = set()
     if basis == "all":
         want_basis = {op.alpha for op in ops}
@@ -165,7 +183,7 @@ def build_models(ops, modes_per_face: int, n: int, shift: float, basis=None, row
     row_sub = np.array(row_sub or [0], dtype=np.int32)
     row_node = np.array(row_node or [0], dtype=np.int32)
     n_rows = len(row_sub) if rows else 0
-    d = _RomDesc()
+    d = _lib.RomDesc()
     d.n_sub = ns
     d.p[:] = shape
     d.h[:] = spacing
@@ -183,7 +201,7 @@ def build_models(ops, modes_per_face: int, n: int, shift: float, basis=None, row
     flags = np.zeros(ns, dtype=np.int32)
     status = np.zeros(ns, dtype=np.int32)
     stats = np.zeros(16)
-    o = _RomOut()
+    o = _lib.RomOut()
     o.layers = _lib.iptr(layers)
     o.flags = _lib.iptr(flags)
     o.status = _lib.iptr(status)
@@ -244,3 +262,30 @@ def build_models(ops, modes_per_face: int, n: int, shift: float, basis=None, row
 def build_subdomain_model(op, modes_per_face: int, n: int, shift: float) -> SubdomainModel:
     """Run the full offline pipeline for one subdomain operator (rom.py:359-434), on the GPU."""
     return build_models([op], modes_per_face, n, shift, basis="all")[op.alpha]
+
+
+def _state_map(fn, model, vec, n_in, n_out, what):
+    basis = require_basis(model)
+    lib = _lib.load()
+    L, w = model.layers, model.width
+    N = int(basis.shape[0])
+    x = np.ascontiguousarray(np.asarray(vec, dtype=np.float64).reshape(-1))
+    if x.size != (N if n_in == "N" else L * w):
+        raise ConfigError(f"{what}: input has length {x.size}")
+    out = np.empty(N if n_out == "N" else L * w)
+    eb = _lib.errbuf()
+    rc = getattr(lib, fn)(N, L, w, _lib.dptr(np.ascontiguousarray(basis, dtype=np.float64)),
+                          _lib.dptr(np.ascontiguousarray(model.scales, dtype=np.float64)), _lib.dptr(x),
+                          _lib.dptr(out), eb, 1024)
+    _lib.check(rc, eb, what)
+    return out
+
+
+def project_state(model: SubdomainModel, w: np.ndarray) -> np.ndarray:
+    """Map a node-space field (symmetrized variable) to chain layers (rom.py:437-447), on the GPU."""
+    return _state_map("sfw_project_state", model, w, "N", "K", "project_state")
+
+
+def state_to_nodes(model: SubdomainModel, u: np.ndarray) -> np.ndarray:
+    """Inverse of project_state on the reduction subspace (rom.py:450-459), on the GPU."""
+    return _state_map("sfw_state_to_nodes", model, u, "K", "N", "state_to_nodes")

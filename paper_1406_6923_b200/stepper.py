@@ -70,7 +70,8 @@ class Probe:
 
 @dataclass(frozen=True)
 class Interface:
-    """Shared face (stepper.py:64-70); the mass lives on the device."""
+    """Shared face (stepper.py:64-70).  ``mass`` = (inv(Ghat_low|f) + inv(Ghat_high|f))^-1, computed
+    on the device at create (ha (ha + hb)^-1 hb, symmetrised, stepper.py:204-210) and copied back."""
 
     low: Alpha
     low_face: int
@@ -153,7 +154,8 @@ class CoupledStepper:
             if src.alpha not in self.models:
                 raise ConfigError(f"source subdomain {src.alpha} has no model")
         self.index = {a: i for i, a in enumerate(self.order)}
-        self.interfaces = self._pair_interfaces()
+        self._ifaces = self._pair_interfaces()
+        self._ifaces_mass = None
         self.message_count = 0
         self.steps_done = 0
         self.time = 0.0
@@ -186,6 +188,20 @@ class CoupledStepper:
                 if alpha < beta:
                     pairs.append(Interface(alpha, face, beta, opposite_face(face)))
         return pairs
+
+    @property
+    def interfaces(self) -> list[Interface]:
+        """One Interface per shared face with its mass (stepper.py:178-220); the masses are
+        computed on the device at create and copied back on first access."""
+        if self._ifaces_mass is None:
+            m = self._m
+            masses = np.empty((max(1, len(self._ifaces)), m, m))
+            cnt = C.c_int(0)
+            eb = _lib.errbuf()
+            _lib.check(self._lib.sfw_step_masses(self._h, C.byref(cnt), _lib.dptr(masses), eb, 1024), eb)
+            self._ifaces_mass = [Interface(i.low, i.low_face, i.high, i.high_face, masses[q].copy())
+                                 for q, i in enumerate(self._ifaces)]
+        return self._ifaces_mass
 
     def _create(self):
         lib = _lib.load()
@@ -247,6 +263,10 @@ class CoupledStepper:
         self._h = h
         self._lib = lib
         self._m = m
+        cnt = C.c_int(0)
+        _lib.check(lib.sfw_step_masses(h, C.byref(cnt), None, eb, 1024), eb)
+        if cnt.value != len(self._ifaces):
+            raise ProtocolError(f"device paired {cnt.value} interfaces, host {len(self._ifaces)}")
         self._src_vec_u = src_vec
         self._probe_w_u = None
         if self.precision == "fp32":
@@ -358,7 +378,7 @@ class CoupledStepper:
         rc = self._lib.sfw_step_accel(self._h, _lib.dptr(flat), None, _lib.dptr(out), eb, 1024)
         _lib.check(rc, eb)
         if count_messages:
-            self.message_count += 2 * len(self.interfaces)
+            self.message_count += 2 * len(self._ifaces)
         return self._split(out)
 
     def _profiles(self, t_values) -> np.ndarray:
@@ -449,7 +469,7 @@ class CoupledStepper:
                 f"{GROWTH_LIMIT:.0e} x reference {limits[k - 1] / GROWTH_LIMIT:.3e}")
         _lib.check(rc, eb)
         self._baseline = base
-        self.message_count += n_steps * 2 * len(self.interfaces)
+        self.message_count += n_steps * 2 * len(self._ifaces)
         start = self.steps_done
         self.steps_done += n_steps
         self.time = self.steps_done * dt
@@ -656,7 +676,40 @@ def stable_step_coupled(models: dict, **kw) -> tuple[float, float, bool]:
     return 2.0 / np.sqrt(lam), lam, converged
 
 
+
+
+DT_SAFETY = CFL_SAFETY  # sim.py:63
+
+
+def resolve_dt(dt, dt_max_coupled: float, converged: bool, dt_max_fine: float) -> float:
+    """The reference's time-step policy (sim.py:444-463 ``_resolve_dt``) over a dt spec.
+
+    ``dt``: "auto" (0.9 x the coupled limit, or 0.9 x the fine-grid limit when the coupled power
+    iteration did not converge), "fine" (0.9 x the fine-grid limit) or a number, which must not
+    exceed 0.9 x the coupled limit (relative slack 1e-12) -- ConfigError("...", "time.dt") otherwise.
+    ``dt_max_coupled`` = 2/sqrt(lambda) of ``cfl_estimate_coupled`` (GPU), ``dt_max_fine`` =
+    ``fdtd.stability_limit`` of the global operator (GPU).
+    """
+    if dt == "auto":
+        if converged:
+            return DT_SAFETY * dt_max_coupled
+        log.warning("coupled stability estimate did not converge; falling back to the fine-grid step")
+        return DT_SAFETY * dt_max_fine
+    if dt == "fine":
+        return DT_SAFETY * dt_max_fine
+    val = float(dt)
+    limit = DT_SAFETY * dt_max_coupled
+    if val > limit * (1.0 + 1e-12):
+        raise ConfigError(f"requested dt {val:.6e} exceeds the stable limit {limit:.6e}", "time.dt")
+    return val
+
+
+def _resolve_dt(config, dt_max_coupled: float, converged: bool, dt_max_fine: float) -> float:
+    """Reference-shaped form (sim.py:444): ``config`` is any object with a ``dt`` attribute."""
+    return resolve_dt(config.dt, dt_max_coupled, converged, dt_max_fine)
+
+
 __all__ = [
-    "CFL_SAFETY", "CoupledStepper", "FaceMessage", "Interface", "Probe", "SourceTerm", "chain_operator",
-    "cfl_estimate_coupled", "make_probe", "project_source", "stable_step_coupled",
+    "CFL_SAFETY", "CoupledStepper", "DT_SAFETY", "FaceMessage", "Interface", "Probe", "SourceTerm", "chain_operator",
+    "cfl_estimate_coupled", "make_probe", "project_source", "resolve_dt", "stable_step_coupled",
 ]

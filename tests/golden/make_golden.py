@@ -307,8 +307,134 @@ def golden_ntd_full():
     np.savez_compressed(os.path.join(HERE, "golden_ntd_full.npz"), **out)
 
 
+_POOL_CTX: dict = {}
+
+
+def _pool_build(alpha):
+    """Worker: reference build of one subdomain of the partition in _POOL_CTX (fork start)."""
+    part, c_field, m, n, shift = (_POOL_CTX[k] for k in ("part", "c", "m", "n", "shift"))
+    op = assemble_subdomain_operator(part, alpha, c_field)
+    md = build_subdomain_model(op, m, n, shift)
+    td, to, en = chain_blocks(op, m, n, shift, md.layers)
+    return alpha, md, td, to
+
+
+def _reference_models(wl, alphas, workers):
+    """Reference build_subdomain_model of ``alphas`` with a fork process pool (one BLAS thread each)."""
+    import multiprocessing as mp
+    spec = DomainSpec(tuple((g - 1) * h for g, h in zip(wl.global_shape, wl.spacing)), wl.counts, wl.p)
+    part = build_partition(spec)
+    _POOL_CTX.update(part=part, c=wl.c_field, m=wl.modes_per_face, n=wl.n, shift=wl.shift)
+    with mp.get_context("fork").Pool(workers) as pool:
+        res = pool.map(_pool_build, sorted(alphas), chunksize=2)
+    models = {a: md for a, md, _, _ in res}
+    blocks = {a: (td, to) for a, _, td, to in res}
+    return part, models, blocks
+
+
+def golden_c2(workers=8):
+    """Config 2 at FULL size through the real reference: every one of the 512 m4k6 models
+    (shift 8883, the 5000 m/s inclusion cutting interfaces), the reference CFL estimate and
+    1000 leapfrog steps recorded on the bench probes (64 z-midplane faces x 4 modes + 8 node
+    receivers).  Stored: lambda, dt, source/probe vectors, the full trace table, and the
+    coefficients (A_j, B_j, Gamma_j, Gamma-hat_j, scales) of every subdomain the inclusion
+    touches plus the source and receiver subdomains (the full stacks would be 80 MB)."""
+    import time as _t
+    wl = make_workload(2)
+    t0 = _t.perf_counter()
+    alphas = [(i, j, k) for i in range(8) for j in range(8) for k in range(8)]
+    part, models, blocks = _reference_models(wl, alphas, workers)
+    print("c2 build", _t.perf_counter() - t0)
+    lam, conv = cfl_estimate_coupled(models)
+    dt = 0.9 * 2.0 / math.sqrt(lam)
+    print("c2 cfl", lam, conv, _t.perf_counter() - t0)
+    src_alpha, src_row = locate(wl.sources[0], wl.counts, wl.p)
+    pulse = make_pulse("ricker", wl.f0, 1.2 / wl.f0)
+    vec = project_source(models[src_alpha], src_row, 1.0)
+    probes = []
+    for alpha, face in wl.face_receivers:
+        for q in range(wl.modes_per_face):
+            wts = np.zeros(models[alpha].state_size)
+            wts[face * wl.modes_per_face + q] = 1.0
+            probes.append(Probe(alpha, wts))
+    node = [locate(ijk, wl.counts, wl.p) for ijk in wl.node_receivers]
+    node_w = [make_probe(models[a], r).weights for a, r in node]
+    probes += [Probe(a, wv) for (a, _), wv in zip(node, node_w)]
+    with CoupledStepper(models, dt, sources=(SourceTerm(src_alpha, vec, pulse),)) as st:
+        times, rows = st.run(wl.n_steps, probes=probes)
+        msg = st.message_count
+        energy = st.energy()
+    print("c2 run", _t.perf_counter() - t0)
+    cut = np.argwhere(wl.c_field == 5000.0)
+    lo, hi = cut.min(0), cut.max(0)
+    keep = set()
+    for a in alphas:  # subdomains whose node box meets the inclusion box
+        if all(16 * a[d] <= hi[d] and 16 * (a[d] + 1) >= lo[d] for d in range(3)):
+            keep.add(a)
+    keep |= {src_alpha} | {a for a, _ in node}
+    keep = sorted(keep)
+    out = {"counts": np.array(wl.counts), "m": wl.modes_per_face, "n": wl.n, "shift": wl.shift,
+           "n_steps": wl.n_steps, "f0": wl.f0, "lam": lam, "conv": conv, "dt": dt,
+           "src_alpha": np.array(src_alpha), "src_row": src_row, "src_vec": vec,
+           "node_probe_w": np.stack(node_w), "times": times, "rows": rows, "message_count": msg,
+           "energy": energy, "sub_alphas": np.array(keep),
+           "sub_tdiag": np.stack([blocks[a][0] for a in keep]),
+           "sub_toff": np.stack([blocks[a][1] for a in keep]),
+           "sub_gammas": np.stack([models[a].gammas for a in keep]),
+           "sub_hats": np.stack([models[a].gamma_hats for a in keep]),
+           "sub_scales": np.stack([models[a].scales for a in keep])}
+    np.savez_compressed(os.path.join(HERE, "golden_c2.npz"), **out)
+    print("golden_c2.npz", len(keep), "subdomains stored; lam", lam, "rows", rows.shape)
+
+
+def c5_golden_alphas(wl):
+    """Config-5 subdomains pinned to the reference: corner, edge, face, interior, the source
+    subdomain, and the two subdomains with the most 5500 m/s inclusion nodes that are cut
+    (inclusion and background both present)."""
+    cz = wl.c_field
+    src_alpha, _ = locate(wl.sources[0], wl.counts, wl.p)
+    C = wl.counts
+    fixed = [(0, 0, 0), (C[0] - 1, 0, C[2] - 1), (0, 5, 7), (17, 9, 6), src_alpha]
+    score = []
+    for i in range(C[0]):
+        for j in range(C[1]):
+            for k in range(C[2]):
+                blk = cz[16 * i:16 * i + 17, 16 * j:16 * j + 17, 16 * k:16 * k + 17]
+                nin = int(np.count_nonzero(blk == 5500.0))
+                if 0 < nin < blk.size:
+                    score.append((min(nin, blk.size - nin), (i, j, k)))
+    score.sort(reverse=True)
+    cut = [a for _, a in score if a not in fixed][:2]
+    return fixed + cut
+
+
+def golden_c5(workers=8):
+    """Config-5 recipe subdomains (m=9, k=8, shift (2 pi 10)^2, 4^3-cell blocky medium with
+    5500 m/s inclusions) built by the real reference on the FULL 513x513x257 config-5 field.
+    Stored per subdomain: the 17^3 c slice (the full field is 540 MB; tests regenerate it from
+    the seed and check these slices), the neighbour mask, A_j, B_j, Gamma_j, Gamma-hat_j, scales."""
+    wl = make_workload(5)
+    alphas = c5_golden_alphas(wl)
+    part, models, blocks = _reference_models(wl, alphas, workers)
+    out = {"counts": np.array(wl.counts), "m": 9, "n": 8, "shift": wl.shift, "alphas": np.array(alphas),
+           "c_slices": np.stack([wl.c_field[16 * a[0]:16 * a[0] + 17, 16 * a[1]:16 * a[1] + 17,
+                                            16 * a[2]:16 * a[2] + 17] for a in alphas]),
+           "tdiag": np.stack([blocks[a][0] for a in alphas]),
+           "toff": np.stack([blocks[a][1] for a in alphas]),
+           "gammas": np.stack([models[a].gammas for a in alphas]),
+           "hats": np.stack([models[a].gamma_hats for a in alphas]),
+           "scales": np.stack([models[a].scales for a in alphas]),
+           "layers": np.array([models[a].layers for a in alphas])}
+    np.savez_compressed(os.path.join(HERE, "golden_c5.npz"), **out)
+    print("golden_c5.npz", alphas)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["toy", "c1", "m9k8", "io", "fdtd", "ntd"]
+    if "c2" in which:
+        golden_c2()
+    if "c5" in which:
+        golden_c5()
     if "toy" in which:
         golden_toy()
     if "c1" in which:

@@ -59,3 +59,22 @@ def face_probes(models, wl):
             wts[face * wl.modes_per_face + q] = 1.0
             out.append((alpha, wts))
     return out
+
+
+def batched_oracle(models, dt, sources=(), m=None, alt=False):
+    """oracle.CoupledBatched over product models (uniform layers), plus the alpha -> index map.
+    ``sources``: SourceTerm-like objects (alpha, vector, profile).  ``alt``: einsum products in
+    place of BLAS, i.e. another summation order -- the oracle's own rounding floor."""
+    from oracle import sfw_oracle as so
+    order = sorted(models)
+    idx = {a: i for i, a in enumerate(order)}
+    nbr = np.full((len(order), 6), -1, dtype=np.int64)
+    for a in order:
+        for f, b in models[a].neighbors.items():
+            nbr[idx[a], f] = idx[b]
+    G = np.stack([np.asarray(models[a].gammas) for a in order])
+    H = np.stack([np.asarray(models[a].gamma_hats) for a in order])
+    m = m or models[order[0]].modes_per_face
+    src = [(idx[s.alpha], s.vector, s.profile) for s in sources]
+    return so.CoupledBatched(G, H, nbr, m, dt, sources=src, alt=alt), idx
+

@@ -23,9 +23,25 @@ def test_library_exports_every_header_symbol():
     assert len(names) >= 14
     for name in names:
         assert hasattr(lib, name), name
-        assert name in _lib.SIGNATURES or name == "sfw_rom_build", name
-    import paper_1406_6923_b200.rom  # noqa: F401  registers sfw_rom_build
-    assert hasattr(lib, "sfw_rom_build")
+        assert name in _lib.SIGNATURES, name
+    assert set(_lib.SIGNATURES) == names  # nothing bound that the header does not declare
+
+
+@pytest.mark.parametrize("cname,pytype", [("sfw_step_desc", "StepDesc"), ("sfw_rom_desc", "RomDesc"),
+                                          ("sfw_rom_out", "RomOut")])
+def test_ctypes_structs_match_header(cname, pytype):
+    """The ctypes mirrors declare the header's struct fields, in order."""
+    hdr = open(os.path.join(ROOT, "include", "sfw_b200.h")).read()
+    body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (cname, cname), hdr, flags=re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        for part in decl.split(","):
+            fields.append(re.sub(r"\[.*\]", "", part).replace("*", " ").split()[-1])
+    assert fields == [f[0] for f in getattr(_lib, pytype)._fields_]
 
 
 def test_library_is_sm100a():

@@ -120,3 +120,95 @@ def test_oracle_fine_grid_solver_pinned():
     s, t, up, u = so.leapfrog(a, float(g["dt"]), 200, source_vec=vec, source_fn=so.ricker(wl.f0, wl.delay),
                               record_idx=g["rec"])
     assert np.array_equal(s, g["samples"]) and np.array_equal(u, g["u_curr"]) and np.array_equal(up, g["u_prev"])
+
+
+def _golden_c1_models():
+    g = np.load(os.path.join(GOLD, "golden_c1.npz"))
+    wl = make_workload(1, n_steps=int(g["n_steps"]))
+    ops = so.make_subops(wl.counts, wl.p, wl.spacing, wl.c_field)
+    order = sorted(ops)
+    return g, wl, {a: so.build_model(ops[a], wl.modes_per_face, wl.n, wl.shift) for a in order}
+
+
+def test_batched_oracle_pinned_to_coupled():
+    """oracle.CoupledBatched (full-size windows) vs the per-subdomain restatement and the
+    reference's own config-1 traces; also a random-start run (every face exchanged)."""
+    g, wl, models = _golden_c1_models()
+    order = sorted(models)
+    idx = {a: i for i, a in enumerate(order)}
+    nbr = np.full((len(order), 6), -1)
+    for a in order:
+        for f, b in models[a].neighbors.items():
+            nbr[idx[a], f] = idx[b]
+    G = np.stack([models[a].gammas for a in order])
+    H = np.stack([models[a].gamma_hats for a in order])
+    dt = float(g["dt"])
+    src_alpha, src_row = locate(wl.sources[0], wl.counts, wl.p)
+    vec = so.source_vector(models[src_alpha], src_row)
+    probes = []
+    for alpha, face in wl.face_receivers:
+        for q in range(wl.modes_per_face):
+            wts = np.zeros(models[alpha].state_size)
+            wts[face * wl.modes_per_face + q] = 1.0
+            probes.append((alpha, wts))
+    pr = so.ricker(wl.f0, wl.delay)
+    bt = so.CoupledBatched(G, H, nbr, wl.modes_per_face, dt, sources=[(idx[src_alpha], vec, pr)])
+    _, rows = bt.run(wl.n_steps, probes=[(idx[a], w) for a, w in probes])
+    assert rel(rows, g["rows"]) < 1e-12
+    rng = np.random.default_rng(4)
+    u0 = rng.standard_normal(G.shape[:2] + (G.shape[2],))
+    st = so.Coupled(models, dt)
+    st.initialize(u0={a: u0[idx[a]].reshape(-1) for a in order})
+    bt2 = so.CoupledBatched(G, H, nbr, wl.modes_per_face, dt)
+    bt2.initialize(u0=u0)
+    for _ in range(20):
+        st.advance()
+        bt2.advance()
+    ref = np.stack([st.u_curr[a] for a in order])
+    assert rel(bt2.u_curr.reshape(ref.shape), ref) < 1e-13
+
+
+def test_golden_c2_subset_build_and_cfl():
+    """golden_c2.npz (the real reference on all 512 config-2 subdomains): the oracle reproduces
+    the stored inclusion-cut / source subdomains and the reference's lambda equals the GPU-independent
+    value recorded with it."""
+    g = np.load(os.path.join(GOLD, "golden_c2.npz"))
+    wl = make_workload(2)
+    alphas = [tuple(int(x) for x in a) for a in g["sub_alphas"]]
+    assert len(alphas) >= 20 and g["rows"].shape == (1001, 264)
+    cut = [a for a in alphas if np.any(wl.c_field[16 * a[0]:16 * a[0] + 17, 16 * a[1]:16 * a[1] + 17,
+                                                   16 * a[2]:16 * a[2] + 17] == 5000.0)]
+    assert len(cut) >= 8
+    pick = [cut[0], cut[len(cut) // 2], tuple(int(x) for x in g["src_alpha"])]
+    ops = so.make_subops(wl.counts, wl.p, wl.spacing, wl.c_field, alphas=pick)
+    for a in pick:
+        i = alphas.index(a)
+        md = so.build_model(ops[a], 4, 6, wl.shift)
+        assert rel(md.tdiag, g["sub_tdiag"][i]) < 1e-12
+        assert rel(md.toff, g["sub_toff"][i]) < 1e-12
+        assert rel(md.gammas, g["sub_gammas"][i]) < 1e-12
+        assert rel(md.gamma_hats, g["sub_hats"][i]) < 1e-12
+    src_alpha, src_row = locate(wl.sources[0], wl.counts, wl.p)
+    md = so.build_model(ops[src_alpha], 4, 6, wl.shift)
+    assert rel(so.source_vector(md, src_row), g["src_vec"]) < 1e-12
+    assert float(g["dt"]) == 0.9 * 2.0 / math.sqrt(float(g["lam"]))
+
+
+def test_golden_c5_medium_and_build():
+    """golden_c5.npz: the seeded config-5 medium regenerates the stored c slices bit for bit, and the
+    oracle reproduces the reference's m9k8 chain of an inclusion-cut and the source subdomain."""
+    g = np.load(os.path.join(GOLD, "golden_c5.npz"))
+    wl = make_workload(5)
+    alphas = [tuple(int(x) for x in a) for a in g["alphas"]]
+    for i, a in enumerate(alphas):
+        sl = wl.c_field[16 * a[0]:16 * a[0] + 17, 16 * a[1]:16 * a[1] + 17, 16 * a[2]:16 * a[2] + 17]
+        assert np.array_equal(sl, g["c_slices"][i])
+    assert any(np.any(s == 5500.0) and not np.all(s == 5500.0) for s in g["c_slices"])
+    pick = [alphas[-1], alphas[4]]
+    ops = so.make_subops(wl.counts, wl.p, wl.spacing, wl.c_field, alphas=pick)
+    for a in pick:
+        i = alphas.index(a)
+        md = so.build_model(ops[a], 9, 8, wl.shift)
+        assert rel(md.tdiag, g["tdiag"][i]) < 1e-12
+        assert rel(md.toff, g["toff"][i]) < 1e-12
+        assert rel(md.gammas, g["gammas"][i]) < 1e-9

@@ -4,7 +4,8 @@ Contract: Lanczos blocks (A_j, B_j) and Gamma_j within 1e-9
 relative per block; Gamma-hat_j and G_j within 1e-9 for j < L; the last layer's
 Gamma-hat_L / G_L are intrinsically ill-conditioned at m=9, k=8 (cond(Gamma_9)
 ~ 1e17), so they are compared at 10 x the oracle's own algorithm floor
-(SuperLU vs dense Cholesky: 6.4e-7 / 3.2e-7, SURVEY appendix probe2) = 1e-5.
+(SuperLU vs dense Cholesky: 6.4e-7 / 3.2e-7, SURVEY appendix probe2); the GPU build
+measures 5.6e-10 / 2.8e-10 there, so the assert is 1e-8 (a regression of 20x fails).
 """
 
 import numpy as np
@@ -78,7 +79,7 @@ def test_m9k8_build_matches_reference_golden():
     order = [op.alpha for op in ops]
     assert order == alphas
     models = build_models(ops, 9, 8, wl.shift)
-    print(_check_blocks(models, g, order, last_tol=1e-5))
+    print(_check_blocks(models, g, order, last_tol=1e-8))  # measured 5.6e-10
 
 
 def test_config1_end_to_end_traces():
@@ -90,7 +91,7 @@ def test_config1_end_to_end_traces():
     src_alpha, row = locate(wl.sources[0], wl.counts, wl.p)
     models = build_models(ops, wl.modes_per_face, wl.n, wl.shift, basis={src_alpha})
     lam, conv = cfl_estimate_coupled(models)
-    assert conv and abs(lam - float(g["lam"])) <= 1e-7 * lam
+    assert conv and abs(lam - float(g["lam"])) <= 1e-8 * lam
     vec = project_source(models[src_alpha], row)
     assert rel(vec, g["src_vec"]) < 1e-9
     probes = [Probe(a, w) for a, w in face_probes(models, wl)]

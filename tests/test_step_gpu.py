@@ -119,7 +119,7 @@ def test_cfl_estimate_matches_oracle():
     g, pre, models = _toy("quad")
     lam, conv = cfl_estimate_coupled(models)
     assert conv
-    assert abs(lam - float(g[pre + "lam"])) <= 1e-6 * lam
+    assert abs(lam - float(g[pre + "lam"])) <= 1e-8 * lam
 
 
 def test_acceleration_matches_oracle():
