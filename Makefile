@@ -22,9 +22,7 @@ build/%.o: $(PKG)/csrc/%.cu $(wildcard $(PKG)/csrc/*.cuh) include/sfw_b200.h
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
 
-oracle: oracle/_ref/.stamp
-
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean oracle tools
+.PHONY: all clean tools

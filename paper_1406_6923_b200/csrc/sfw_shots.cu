@@ -558,9 +558,32 @@ __global__ void __launch_bounds__((MS_NW + 1) * 32, 1) k_step_ms(const MsParams 
 //   per subdomain (A+B): F_0 = G_0 (U_1 - U_0) -> face buffer; acc_0 = H_0 F_0;
 //     j = 1..L-1: F_j = G_j (U_{j+1} - U_j); A_j = H_j (F_j - F_{j-1}); leapfrog.
 //   after all subdomains: step flag; neighbour flags; C: layer-1 coupling + leapfrog.
-constexpr int M2_NC = 4;    // chain-block stages
+#ifndef SFW_M2_NC
+#define SFW_M2_NC 4
+#endif
+#ifndef SFW_M2_SLEEP
+#define SFW_M2_SLEEP 0
+#endif
+constexpr int M2_NC = SFW_M2_NC;  // chain-block stages
+#if SFW_M2_SLEEP
+#define M2_PWAIT mbar_wait_sleep
+#else
+#define M2_PWAIT mbar_wait
+#endif
 constexpr int M2_NSS = 8;   // state-block stages
-constexpr int M2_LDX = 12;  // X row stride (conflict-free B-fragment reads)
+#ifndef SFW_M2_SWZ
+#define SFW_M2_SWZ 0
+#endif
+#if SFW_M2_SWZ
+constexpr int M2_LDX = 8;   // X row stride; columns XOR-swizzled by m2_xs (conflict-free fragment reads)
+
+// X / T tile element (row, col), col < 8: the column is XORed with 4 on row pairs 2,3 (mod 4), so
+// the B-fragment reads (rows 4k+q, q < 4) and the double2 row writes are both bank-conflict free
+__device__ __forceinline__ int m2_xs(int row, int col) { return row * M2_LDX + (col ^ (((row >> 1) & 1) << 2)); }
+#else
+constexpr int M2_LDX = 12;  // padded X row stride (conflict-free fragment reads)
+__device__ __forceinline__ int m2_xs(int row, int col) { return row * M2_LDX + col; }
+#endif
 constexpr int M2_NQ = 4;    // warps per shot column tile (row-tile groups)
 constexpr int M2_NW = 4 * M2_NQ;  // compute warps
 
@@ -644,28 +667,39 @@ __device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst
 #pragma unroll
         for (int i = 0; i < NI; ++i)
             if (I0 + i < RT)
-                *reinterpret_cast<double2*>(Xw + (8 * (I0 + i) + r0) * M2_LDX + 2 * (lane & 3)) =
+                *reinterpret_cast<double2*>(Xw + m2_xs(8 * (I0 + i) + r0, 2 * (lane & 3))) =
                     make_double2(v[i][0], v[i][1]);
         asm volatile("bar.sync %0, %1;" ::"r"(barP), "r"(M2_NQ * 32) : "memory");
         return Xw;
     };
     // acc = B X over this warp's row tiles, B symmetric (lower tiles, fragment order)
+    // two accumulator chains per row tile (even / odd k-steps, summed at the end): 2 NI independent
+    // DMMA chains per warp, so one warp alone keeps its SMSP's FP64 tensor pipe fed
     auto gemm = [&](const double* tiles, const double* Xw, double (&acc)[NI][2]) {
         MS_T0
+        double acc2[NI][2];
 #pragma unroll
-        for (int i = 0; i < NI; ++i) acc[i][0] = acc[i][1] = 0.0;
+        for (int i = 0; i < NI; ++i) acc[i][0] = acc[i][1] = acc2[i][0] = acc2[i][1] = 0.0;
 #pragma unroll
         for (int kap = 0; kap < 2 * RT; ++kap) {
             const int Kt = kap >> 1, h = kap & 1;
-            const double b = Xw[(4 * kap + (lane & 3)) * M2_LDX + r0];
+            const double b = Xw[m2_xs(4 * kap + (lane & 3), r0)];
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
                 const int I = I0 + i;
                 if (I >= RT) break;
                 const double a = (I >= Kt) ? tiles[(I * (I + 1) / 2 + Kt) * 64 + h * 32 + lane]
                                            : tiles[(Kt * (Kt + 1) / 2 + I) * 64 + tr[h]];
-                dmma8x8x4(acc[i], a, b);
+                if (h)
+                    dmma8x8x4(acc2[i], a, b);
+                else
+                    dmma8x8x4(acc[i], a, b);
             }
+        }
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            acc[i][0] += acc2[i][0];
+            acc[i][1] += acc2[i][1];
         }
 #ifdef SFW_MS_CLK
         for (int i = 0; i < NI; ++i) asm volatile("" ::"d"(acc[i][0]), "d"(acc[i][1]));
@@ -682,6 +716,14 @@ __device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst
     const double dt2 = p.dt2;
     const bool src0 = ssub[q0] >= 0, src1 = ssub[q0 + 1] >= 0;
 
+#ifndef SFW_M2_LAG
+#define SFW_M2_LAG 0
+#endif
+#ifdef SFW_M2_FAKE_STATE  // timing experiment: state reads all hit the CTA's first subdomain (L2)
+#define M2_FAKE_S 1
+#else
+#define M2_FAKE_S 0
+#endif
     for (int k = 1; k <= p.n_steps; ++k) {
         const int par = k & 1;
         const int cb = (k - 1) & 1;
@@ -691,6 +733,7 @@ __device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst
         const double f0 = src0 ? p.ftab[(size_t)q0 * p.ftab_stride + kk] : 0.0;
         const double f1 = src1 ? p.ftab[(size_t)(q0 + 1) * p.ftab_stride + kk] : 0.0;
         double sq0 = 0.0, sq1 = 0.0;
+        if (SFW_M2_LAG > 0 && cw >= 2) __nanosleep(SFW_M2_LAG);  // column groups 2,3 trail 0,1
         auto force = [&](int s, long long idx, int e) -> double {  // shot source term (ssub[q] == s)
             const int q = q0 + e;
             return __dmul_rn(p.shot_vec[p.shot_voff[q] + idx], e ? f1 : f0);
@@ -717,15 +760,19 @@ __device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst
             gemm(c_acquire(), Xw, fp);  // F_0
             c_release();
             store_global(fx + (size_t)s * WS, fp);
-            Xw = put_x(fp);
-            gemm(c_acquire(), Xw, acc);  // acc_0 = H_0 F_0 (boundary faces)
-            c_release();
+            const bool interior = s_nb[sl * 6] >= 0 && s_nb[sl * 6 + 1] >= 0 && s_nb[sl * 6 + 2] >= 0 &&
+                                  s_nb[sl * 6 + 3] >= 0 && s_nb[sl * 6 + 4] >= 0 && s_nb[sl * 6 + 5] >= 0;
+            if (!interior) {  // acc_0 = H_0 F_0: only outer-face rows are ever read back
+                Xw = put_x(fp);
+                gemm(c_acquire(), Xw, acc);
+                c_release();
 #pragma unroll
-            for (int i = 0; i < NI; ++i) {  // only rows of outer faces are ever read back
-                const int row = 8 * (I0 + i) + r0;
-                if (row < W && s_nb[sl * 6 + row / M] < 0)
-                    *reinterpret_cast<double2*>(p.acc1 + ((size_t)s * W + row) * S + q0) =
-                        make_double2(acc[i][0], acc[i][1]);
+                for (int i = 0; i < NI; ++i) {
+                    const int row = 8 * (I0 + i) + r0;
+                    if (row < W && s_nb[sl * 6 + row / M] < 0)
+                        *reinterpret_cast<double2*>(p.acc1 + ((size_t)s * W + row) * S + q0) =
+                            make_double2(acc[i][0], acc[i][1]);
+                }
             }
             for (int j = 1; j < L; ++j) {
                 if (j + 1 < L) {
@@ -830,7 +877,7 @@ __device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst
                 for (int t = 0; t < NIT; ++t) {
                     const int it = lane + 32 * t, row = HH * NROW + (it >> 2), pr = it & 3;
                     if ((it >> 2) < NROW && row < 6 * M)
-                        *reinterpret_cast<double2*>(T + row * M2_LDX + 2 * pr) =
+                        *reinterpret_cast<double2*>(T + m2_xs(row, 2 * pr)) =
                             make_double2(__dadd_rn(ow[t].x, ot[t].x), __dadd_rn(ow[t].y, ot[t].y));
                 }
             }
@@ -859,11 +906,10 @@ __device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst
                 if (s_nb[sl * 6 + f] >= 0) {
                     a[0] = a[1] = 0.0;
                     const double* mx = mb + (f * M + r) * M;
-                    const double* tx = T + (f * M) * M2_LDX + 2 * (lane & 3);
 #pragma unroll
                     for (int c = 0; c < M; ++c) {
                         const double mc = mx[c];
-                        const double2 t = *reinterpret_cast<const double2*>(tx + c * M2_LDX);
+                        const double2 t = *reinterpret_cast<const double2*>(T + m2_xs(f * M + c, 2 * (lane & 3)));
                         a[0] = fma(mc, t.x, a[0]);
                         a[1] = fma(mc, t.y, a[1]);
                     }
@@ -944,7 +990,7 @@ __device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst
 }
 
 template <int M>
-__global__ void __launch_bounds__((M2_NW + 1) * 32, 1) k_step_ms2(const MsParams p) {
+__global__ void __launch_bounds__((M2_NW + 2) * 32, 1) k_step_ms2(const MsParams p) {
     constexpr int S = 32;
     constexpr int RT = (6 * M + 7) / 8;
     constexpr int WP = 8 * RT;
@@ -984,75 +1030,77 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32, 1) k_step_ms2(const MsParams
     for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nb[i] = p.nbr[s0 * 6 + i];
     __syncthreads();
 
-    // ======== producer warp: chain blocks (ungated) and state blocks (gated per step) ====
-    if (warp == M2_NW) {
-        // lane 0 feeds the chain-block ring, lane 1 the state-block ring: each polls only its
-        // own ring, so a refill is issued as soon as its stage is released
-        if (lane < 2) {
-            const bool chain_lane = lane == 0;
+    // ======== producer warps: chain blocks (ungated) and state blocks (gated per step) ====
+    // one warp per ring (lane 0 issues); waits are blocking mbarrier try_waits, so the producers
+    // take no issue slots from the compute warps while their ring is full.  Interior subdomains
+    // never read acc_0 (only outer-face rows do), so their Gamma-hat_0 block is not streamed.
+    if (warp >= M2_NW) {
+        if (lane == 0 && warp == M2_NW) {  // chain-block ring
             const uint64_t pol = l2_policy_evict_first();
-            const uint64_t pol_state = l2_policy_evict_first();  // measured 1-1.5% faster than evict_last
-            const int cper = ns * 2 * L;
-            const long long ctotal = (long long)cper * p.n_steps;
-            const int sper = ns * (2 * L - 1) + 3 * ns;
-            const uint32_t mbytes = (uint32_t)(6 * M * M * 8);
-            const long long stotal = (long long)sper * p.n_steps;
-            const uint32_t sbytes = (uint32_t)(WS * 8), cbytes = (uint32_t)TB * 8u;
-            long long c_iss = chain_lane ? 0 : ctotal, s_iss = chain_lane ? stotal : 0;
-            int cpos = 0, spos = 0, sstep = 0;
-            while (c_iss < ctotal || s_iss < stotal) {
-                if (c_iss < ctotal) {
-                    const int st = (int)(c_iss % M2_NC);
-                    if (mbar_test_wait(&cempty[st], (uint32_t)(((c_iss / M2_NC) & 1) ^ 1))) {
+            const uint32_t cbytes = (uint32_t)TB * 8u;
+            long long c_iss = 0;
+            for (int k = 0; k < p.n_steps; ++k)
+                for (int sl = 0; sl < ns; ++sl) {
+                    const bool interior = s_nb[sl * 6] >= 0 && s_nb[sl * 6 + 1] >= 0 && s_nb[sl * 6 + 2] >= 0 &&
+                                          s_nb[sl * 6 + 3] >= 0 && s_nb[sl * 6 + 4] >= 0 && s_nb[sl * 6 + 5] >= 0;
+                    for (int b = 0; b < 2 * L; ++b) {
+                        if (b == 1 && interior) continue;
+                        const int st = (int)(c_iss % M2_NC);
+                        M2_PWAIT(&cempty[st], (uint32_t)(((c_iss / M2_NC) & 1) ^ 1));
                         mbar_arrive_expect_tx(&cfull[st], cbytes);
-                        bulk_g2s(cst + (size_t)st * TB, p.tcoef + ((long long)s0 * 2 * L + cpos) * TB, cbytes, &cfull[st],
-                                 pol);
+#ifdef SFW_M2_FAKE_CHAIN  // timing experiment: every CTA streams its first subdomain's blocks (L2 hits)
+                        bulk_g2s(cst + (size_t)st * TB, p.tcoef + ((long long)(s0) * 2 * L + b) * TB, cbytes,
+                                 &cfull[st], pol);
+#else
+                        bulk_g2s(cst + (size_t)st * TB, p.tcoef + ((long long)(s0 + sl) * 2 * L + b) * TB, cbytes,
+                                 &cfull[st], pol);
+#endif
                         ++c_iss;
-                        if (++cpos == cper) cpos = 0;
                     }
                 }
-                if (s_iss < stotal) {
-                    // step k >= 2 reads what step k-1 wrote: wait for all compute warps
-                    const bool ready = spos > 0 || sstep == 0 || mbar_test_wait(stepdone, (uint32_t)((sstep - 1) & 1));
-                    const int st = (int)(s_iss % M2_NSS);
-                    if (ready && mbar_test_wait(&sempty[st], (uint32_t)(((s_iss / M2_NSS) & 1) ^ 1))) {
-                        const int cb = sstep & 1;
-                        const double* cur = cb ? p.U1 : p.U0;
-                        const double* prv = cb ? p.U0 : p.U1;
-                        const double* src;
-                        uint32_t bytes = sbytes;
-                        const int nab = 2 * L - 1;
-                        if (spos < ns * nab) {
-                            const int sl = spos / nab, r = spos % nab;
-                            const long long base = (long long)(s0 + sl) * KS;
-                            if (r < 2) {
-                                src = cur + base + r * WS;  // U_0, U_1
-                            } else {
-                                const int rp = r - 2;   // j = 1..L-1: [U_{j+1}], Uprev_j
-                                if (rp < 2 * (L - 2)) {
-                                    const int j = 1 + rp / 2;
-                                    src = (rp & 1) ? prv + base + j * WS : cur + base + (j + 1) * WS;
-                                } else {
-                                    src = prv + base + (L - 1) * WS;
-                                }
-                            }
+        } else if (lane == 0 && warp == M2_NW + 1) {  // state-block ring, gated per step
+            const uint64_t pol_state = l2_policy_evict_first();  // measured 1-1.5% faster than evict_last
+            const uint32_t mbytes = (uint32_t)(6 * M * M * 8);
+            const uint32_t sbytes = (uint32_t)(WS * 8);
+            const int nab = 2 * L - 1;
+            long long s_iss = 0;
+            for (int k = 0; k < p.n_steps; ++k) {
+                // step k >= 1 reads what step k-1 wrote: wait for all compute warps
+                if (k > 0) M2_PWAIT(stepdone, (uint32_t)((k - 1) & 1));
+                const int cb = k & 1;
+                const double* cur = cb ? p.U1 : p.U0;
+                const double* prv = cb ? p.U0 : p.U1;
+                for (int spos = 0; spos < ns * (nab + 3); ++spos) {
+                    const double* src;
+                    uint32_t bytes = sbytes;
+                    if (spos < ns * nab) {
+                        const int sl = M2_FAKE_S ? 0 : spos / nab, r = spos % nab;
+                        const long long base = (long long)(s0 + sl) * KS;
+                        if (r < 2) {
+                            src = cur + base + r * WS;  // U_0, U_1
                         } else {
-                            const int r = spos - ns * nab, sl = r / 3, w3 = r % 3;
-                            if (w3 == 0) {  // interface mass of the 6 faces
-                                src = p.mblk + (size_t)(s0 + sl) * 6 * M * M;
-                                bytes = mbytes;
+                            const int rp = r - 2;  // j = 1..L-1: [U_{j+1}], Uprev_j
+                            if (rp < 2 * (L - 2)) {
+                                const int j = 1 + rp / 2;
+                                src = (rp & 1) ? prv + base + j * WS : cur + base + (j + 1) * WS;
                             } else {
-                                src = ((w3 == 2) ? prv : cur) + (long long)(s0 + sl) * KS;  // U_0, Uprev_0
+                                src = prv + base + (L - 1) * WS;
                             }
                         }
-                        mbar_arrive_expect_tx(&sfull[st], bytes);
-                        bulk_g2s(sst + (size_t)st * WS, src, bytes, &sfull[st], pol_state);
-                        ++s_iss;
-                        if (++spos == sper) {
-                            spos = 0;
-                            ++sstep;
+                    } else {
+                        const int r = spos - ns * nab, sl = M2_FAKE_S ? 0 : r / 3, w3 = r % 3;
+                        if (w3 == 0) {  // interface mass of the 6 faces
+                            src = p.mblk + (size_t)(s0 + sl) * 6 * M * M;
+                            bytes = mbytes;
+                        } else {
+                            src = ((w3 == 2) ? prv : cur) + (long long)(s0 + sl) * KS;  // U_0, Uprev_0
                         }
                     }
+                    const int st = (int)(s_iss % M2_NSS);
+                    M2_PWAIT(&sempty[st], (uint32_t)(((s_iss / M2_NSS) & 1) ^ 1));
+                    mbar_arrive_expect_tx(&sfull[st], bytes);
+                    bulk_g2s(sst + (size_t)st * WS, src, bytes, &sfull[st], pol_state);
+                    ++s_iss;
                 }
             }
         }
@@ -1073,6 +1121,527 @@ __global__ void __launch_bounds__((M2_NW + 1) * 32, 1) k_step_ms2(const MsParams
 static size_t ms2_smem_bytes(int RT, int TB, int W, int nsmax) {
     return 8 * ((size_t)M2_NC * TB + (size_t)M2_NSS * W * 32 + (size_t)4 * 2 * 8 * RT * M2_LDX + 2 * M2_NC +
                 2 * M2_NSS + 1) +
+           4 * (32 + 6 * (size_t)nsmax) + 64;
+}
+
+// ---------------------------------------------------------------------------
+// k_step_ms4: two-team multi-shot stepping (config 4 default).
+//
+// k_step_ms2 splits every GEMM's output rows over the 4 warps of a shot column, so each of the
+// 17-18 GEMMs of a subdomain sweep ends in a named barrier (X exchange) and every warp reaches its
+// ring waits and barriers at the same time as all others: measured, feeding every chain and state
+// block from L2 did not change its step time at all (0.760 ms both ways) -- the DMMA pipe idles in
+// the synchronised non-GEMM stretches, not for lack of bytes.
+//
+// Here a warp owns 8 shots and ALL row tiles of its GEMMs (Y = B X, 56 x 8 per warp, 7 row tiles x
+// 14 k-steps = 98 DMMA), so the layer sweep needs no cross-warp exchange: X goes through a per-warp
+// shared-memory tile (__syncwarp only).  The 8 compute warps form two teams of 4 (one warp per
+// 8-shot column); team t sweeps subdomains sl = t, t+2, ... of the CTA with its own chain-block
+// and state-block rings and its own producer warps, so the teams drift independently and one
+// team's non-GEMM work (ring waits, X transposes, leapfrog, stores) overlaps the other team's
+// DMMA on the same SMSP (each SMSP hosts one warp of each team and one producer warp).
+// Per subdomain the arithmetic is that of k_step_ms2 (stepper.py:243-389 per shot):
+//   F_0 = G_0 (U_1 - U_0) -> face buffer;  acc_0 = H_0 F_0 (outer faces only);
+//   j = 1..L-1: F_j = G_j (U_{j+1} - U_j); A_j = H_j (F_j - F_{j-1}); leapfrog of layer j;
+// then, after the CTA's step flag and its neighbours' (phase C): layer-0 face coupling
+// mass (own + neighbour F_0) and leapfrog, per-shot |U|^2 partials, probe rows.
+constexpr int M4_NC = 3;     // chain-block stages per team
+constexpr int M4_NSS = 3;    // state-block stages per team
+constexpr int M4_LDX = 12;   // X row stride (conflict-free fragment reads)
+constexpr int M4_NT = 2;     // teams
+constexpr int M4_NW = 4 * M4_NT;  // compute warps
+
+template <int M>
+__device__ __forceinline__ void ms4_compute(const MsParams& p, const double* cst, const double* sst, double* Xs,
+                                            uint64_t* cfull, uint64_t* cempty, uint64_t* sfull, uint64_t* sempty,
+                                            uint64_t* stepdone, const int* ssub, const int* s_nb, int s0, int ns,
+                                            int team, int cw, int lane) {
+    constexpr int S = 32;
+    constexpr int RT = (6 * M + 7) / 8;
+    constexpr int W = 6 * M;
+    const int TB = p.TB, L = p.L;
+    const long long K = p.K;
+    const long long WS = (long long)W * S, KS = K * S;
+    int tr[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int r = 4 * h + (lane & 3), c = lane >> 2;
+        tr[h] = (c >> 2) * 32 + r * 4 + (c & 3);
+    }
+    long long c_con = 0, s_con = 0;
+#ifdef SFW_MS_CLK
+    long long clk[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // c-wait, s-wait, gemm, total, flags, C, -, -
+    const long long clk_start = clock64();
+#define M4_T0 const long long t0_ = clock64();
+#define M4_T1(i) clk[i] += clock64() - t0_;
+#else
+#define M4_T0
+#define M4_T1(i)
+#endif
+    auto c_acquire = [&]() -> const double* {
+        const int st = (int)(c_con % M4_NC);
+        M4_T0
+        mbar_wait(&cfull[st], (uint32_t)((c_con / M4_NC) & 1));
+        M4_T1(0)
+        return cst + (size_t)st * TB;
+    };
+    auto c_release = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[c_con % M4_NC]);
+        ++c_con;
+    };
+    auto s_acquire = [&]() -> const double* {
+        const int st = (int)(s_con % M4_NSS);
+        M4_T0
+        mbar_wait(&sfull[st], (uint32_t)((s_con / M4_NSS) & 1));
+        M4_T1(1)
+        return sst + (size_t)st * WS;
+    };
+    auto s_release = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[s_con % M4_NSS]);
+        ++s_con;
+    };
+    const int r0 = lane >> 2;                 // fragment row within a row tile
+    const int q0 = 8 * cw + 2 * (lane & 3);   // first of the lane's two shots
+    // the lane's slice of a W x S block: rows 8I + r0 (I < RT), shots q0, q0 + 1
+    auto load_slice = [&](const double* blk, double (&v)[RT][2]) {
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+            const int row = 8 * i + r0;
+            if (row < W) {
+                const double2 t = *reinterpret_cast<const double2*>(blk + (size_t)row * S + q0);
+                v[i][0] = t.x;
+                v[i][1] = t.y;
+            } else {
+                v[i][0] = v[i][1] = 0.0;
+            }
+        }
+    };
+    auto store_global = [&](double* blk, const double (&v)[RT][2]) {
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+            const int row = 8 * i + r0;
+            if (row < W) *reinterpret_cast<double2*>(blk + (size_t)row * S + q0) = make_double2(v[i][0], v[i][1]);
+        }
+    };
+    // X (56 x 8, this warp's shots) into the warp's own tile; padding rows carry zeros
+    auto put_x = [&](const double (&v)[RT][2]) {
+        __syncwarp();  // previous GEMM's reads of Xs are done
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+            *reinterpret_cast<double2*>(Xs + (8 * i + r0) * M4_LDX + 2 * (lane & 3)) = make_double2(v[i][0], v[i][1]);
+        __syncwarp();
+    };
+    // acc = B X, B symmetric (lower 8x8 tiles in DMMA fragment order), all RT row tiles
+    auto gemm = [&](const double* tiles, double (&acc)[RT][2]) {
+        M4_T0
+#pragma unroll
+        for (int i = 0; i < RT; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+        for (int kap = 0; kap < 2 * RT; ++kap) {
+            const int Kt = kap >> 1, h = kap & 1;
+            const double b = Xs[(4 * kap + (lane & 3)) * M4_LDX + r0];
+#pragma unroll
+            for (int I = 0; I < RT; ++I) {
+                const double a = (I >= Kt) ? tiles[(I * (I + 1) / 2 + Kt) * 64 + h * 32 + lane]
+                                           : tiles[(Kt * (Kt + 1) / 2 + I) * 64 + tr[h]];
+                dmma8x8x4(acc[I], a, b);
+            }
+        }
+#ifdef SFW_MS_CLK
+        for (int i = 0; i < RT; ++i) asm volatile("" ::"d"(acc[i][0]), "d"(acc[i][1]));
+#endif
+        M4_T1(2)
+    };
+    const double dt2 = p.dt2;
+    const bool src0 = ssub[q0] >= 0, src1 = ssub[q0 + 1] >= 0;
+    auto interior_of = [&](int sl) {
+        return s_nb[sl * 6] >= 0 && s_nb[sl * 6 + 1] >= 0 && s_nb[sl * 6 + 2] >= 0 && s_nb[sl * 6 + 3] >= 0 &&
+               s_nb[sl * 6 + 4] >= 0 && s_nb[sl * 6 + 5] >= 0;
+    };
+
+    for (int k = 1; k <= p.n_steps; ++k) {
+        const int par = k & 1;
+        const int cb = (k - 1) & 1;
+        double* Un = cb ? p.U0 : p.U1;
+        double* fx = p.flux + (size_t)par * p.n_sub * WS;
+        const int kk = k - 1;
+        const double f0 = src0 ? p.ftab[(size_t)q0 * p.ftab_stride + kk] : 0.0;
+        const double f1 = src1 ? p.ftab[(size_t)(q0 + 1) * p.ftab_stride + kk] : 0.0;
+        double sq0 = 0.0, sq1 = 0.0;
+        auto force = [&](long long idx, int e) -> double {  // shot source term (ssub[q] == s)
+            return __dmul_rn(p.shot_vec[p.shot_voff[q0 + e] + idx], e ? f1 : f0);
+        };
+
+        // ---------------- A: layer-0 fluxes of this team's subdomains ----------------------
+        for (int sl = team; sl < ns; sl += M4_NT) {
+            const int s = s0 + sl;
+            double ua[RT][2], fp[RT][2], x[RT][2];
+            load_slice(s_acquire(), x);  // U_0
+            s_release();
+            load_slice(s_acquire(), ua);  // U_1
+            s_release();
+#pragma unroll
+            for (int i = 0; i < RT; ++i) {
+                x[i][0] = ua[i][0] - x[i][0];
+                x[i][1] = ua[i][1] - x[i][1];
+            }
+            put_x(x);
+            gemm(c_acquire(), fp);  // F_0
+            c_release();
+            store_global(fx + (size_t)s * WS, fp);
+            if (!interior_of(sl)) {  // acc_0 = H_0 F_0: only outer-face rows are ever read back
+                put_x(fp);
+                gemm(c_acquire(), x);
+                c_release();
+#pragma unroll
+                for (int i = 0; i < RT; ++i) {
+                    const int row = 8 * i + r0;
+                    if (row < W && s_nb[sl * 6 + row / M] < 0)
+                        *reinterpret_cast<double2*>(p.acc1 + ((size_t)s * W + row) * S + q0) =
+                            make_double2(x[i][0], x[i][1]);
+                }
+            }
+        }
+        // ---------------- step flag after phase A, neighbour flags (both teams) --------------
+#ifdef SFW_MS_CLK
+        long long tf0 = clock64();
+#endif
+        asm volatile("bar.sync 1, %0;" ::"r"(M4_NW * 32) : "memory");
+        if (team == 0 && cw == 0 && lane == 0) flag_publish(p.flags, (unsigned int)k);
+        if (team == 0 && cw == 0)
+            flags_wait(p.flags, p.ncta + p.ncta_ptr[blockIdx.x], p.ncta_ptr[blockIdx.x + 1] - p.ncta_ptr[blockIdx.x],
+                       (unsigned int)k, lane);
+        asm volatile("bar.sync 1, %0;" ::"r"(M4_NW * 32) : "memory");
+#ifdef SFW_MS_CLK
+        clk[4] += clock64() - tf0;
+#endif
+        // ---------------- per subdomain: C (layer-0 coupling + leapfrog), then B (layers >= 1)
+        for (int sl = team; sl < ns; sl += M4_NT) {
+            const int s = s0 + sl;
+#ifdef SFW_MS_CLK
+            long long tc0 = clock64();
+#endif
+            {
+                double u0[RT][2], uo[RT][2];
+                load_slice(s_acquire(), u0);  // U_0
+                s_release();
+                load_slice(s_acquire(), uo);  // Uprev_0
+                s_release();
+                const double* mb = s_acquire();  // [6][M][M] interface mass
+                // own + neighbour F_0 of every shared-face row, this warp's 8 shots, into its tile
+                __syncwarp();
+                constexpr int NIT = (W * 4 + 31) / 32;
+                double2 ow[NIT], ot[NIT];
+#pragma unroll
+                for (int t = 0; t < NIT; ++t) {  // all loads first (one L2 round trip)
+                    const int it = lane + 32 * t, row = it >> 2, pr = it & 3;
+                    ow[t] = ot[t] = make_double2(0.0, 0.0);
+                    if (row < W) {
+                        const int f = row / M, c = row % M, nb = s_nb[sl * 6 + f];
+                        if (nb >= 0) {
+                            ow[t] = __ldcg(reinterpret_cast<const double2*>(fx + ((size_t)s * W + row) * S + 8 * cw +
+                                                                            2 * pr));
+                            ot[t] = __ldcg(reinterpret_cast<const double2*>(
+                                fx + ((size_t)nb * W + (f ^ 1) * M + c) * S + 8 * cw + 2 * pr));
+                        }
+                    }
+                }
+                double a1[RT][2];
+#pragma unroll
+                for (int i = 0; i < RT; ++i) {  // outer-face accelerations
+                    const int row = 8 * i + r0;
+                    a1[i][0] = a1[i][1] = 0.0;
+                    if (row < W && s_nb[sl * 6 + row / M] < 0) {
+                        const double2 t = __ldcg(reinterpret_cast<const double2*>(p.acc1 + ((size_t)s * W + row) * S + q0));
+                        a1[i][0] = t.x;
+                        a1[i][1] = t.y;
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < NIT; ++t) {
+                    const int it = lane + 32 * t, row = it >> 2, pr = it & 3;
+                    if (row < W)
+                        *reinterpret_cast<double2*>(Xs + row * M4_LDX + 2 * pr) =
+                            make_double2(__dadd_rn(ow[t].x, ot[t].x), __dadd_rn(ow[t].y, ot[t].y));
+                }
+                __syncwarp();
+                double* un = Un + (size_t)s * KS;
+#pragma unroll
+                for (int i = 0; i < RT; ++i) {
+                    const int row = 8 * i + r0;
+                    if (row >= W) continue;
+                    const int f = row / M, r = row % M;
+                    double a[2] = {a1[i][0], a1[i][1]};
+                    if (s_nb[sl * 6 + f] >= 0) {
+                        a[0] = a[1] = 0.0;
+                        const double* mx = mb + (f * M + r) * M;
+#pragma unroll
+                        for (int c = 0; c < M; ++c) {
+                            const double mc = mx[c];
+                            const double2 t = *reinterpret_cast<const double2*>(Xs + (f * M + c) * M4_LDX + 2 * (lane & 3));
+                            a[0] = fma(mc, t.x, a[0]);
+                            a[1] = fma(mc, t.y, a[1]);
+                        }
+                    }
+                    double v[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        double tot = a[e];
+                        if ((e ? src1 : src0) && ssub[q0 + e] == s) tot = __dadd_rn(tot, force(row, e));
+                        v[e] = __dadd_rn(__dsub_rn(__dmul_rn(2.0, u0[i][e]), uo[i][e]), __dmul_rn(dt2, tot));
+                    }
+                    *reinterpret_cast<double2*>(un + (size_t)row * S + q0) = make_double2(v[0], v[1]);
+                    sq0 = fma(v[0], v[0], sq0);
+                    sq1 = fma(v[1], v[1], sq1);
+                }
+                s_release();  // mass
+            }
+#ifdef SFW_MS_CLK
+            clk[5] += clock64() - tc0;
+#endif
+            // B: layers 1..L-1 (F_0 of this warp's rows and shots re-read from the face buffer)
+            double ua[RT][2], fp[RT][2], acc[RT][2];
+            load_slice(s_acquire(), ua);  // U_1
+            s_release();
+#pragma unroll
+            for (int i = 0; i < RT; ++i) {
+                const int row = 8 * i + r0;
+                fp[i][0] = fp[i][1] = 0.0;
+                if (row < W) {
+                    const double2 t = *reinterpret_cast<const double2*>(fx + ((size_t)s * W + row) * S + q0);
+                    fp[i][0] = t.x;
+                    fp[i][1] = t.y;
+                }
+            }
+            for (int j = 1; j < L; ++j) {
+                double x[RT][2];
+                if (j + 1 < L) {
+                    load_slice(s_acquire(), x);  // U_{j+1}
+                    s_release();
+                } else {
+#pragma unroll
+                    for (int i = 0; i < RT; ++i) x[i][0] = x[i][1] = 0.0;
+                }
+                double d[RT][2];
+#pragma unroll
+                for (int i = 0; i < RT; ++i) {
+                    d[i][0] = x[i][0] - ua[i][0];
+                    d[i][1] = x[i][1] - ua[i][1];
+                }
+                put_x(d);
+                gemm(c_acquire(), acc);  // F_j
+                c_release();
+#pragma unroll
+                for (int i = 0; i < RT; ++i) {
+                    d[i][0] = acc[i][0] - fp[i][0];
+                    d[i][1] = acc[i][1] - fp[i][1];
+                    fp[i][0] = acc[i][0];
+                    fp[i][1] = acc[i][1];
+                }
+                put_x(d);
+                gemm(c_acquire(), acc);  // A_j
+                c_release();
+                double uo[RT][2];
+                load_slice(s_acquire(), uo);  // Uprev_j
+                s_release();
+                double* un = Un + (size_t)s * KS + (size_t)j * WS;
+#pragma unroll
+                for (int i = 0; i < RT; ++i) {
+                    const int row = 8 * i + r0;
+                    double v[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        double tot = acc[i][e];
+                        if ((e ? src1 : src0) && row < W && ssub[q0 + e] == s)
+                            tot = __dadd_rn(tot, force((long long)j * W + row, e));
+                        v[e] = __dadd_rn(__dsub_rn(__dmul_rn(2.0, ua[i][e]), uo[i][e]), __dmul_rn(dt2, tot));
+                    }
+                    if (row < W) {
+                        *reinterpret_cast<double2*>(un + (size_t)row * S + q0) = make_double2(v[0], v[1]);
+                        sq0 = fma(v[0], v[0], sq0);
+                        sq1 = fma(v[1], v[1], sq1);
+                    }
+                    ua[i][0] = x[i][0];
+                    ua[i][1] = x[i][1];
+                }
+            }
+        }
+        // per-shot |U|^2 of this warp's rows (lanes with equal lane & 3 hold the same shots); one
+        // partial slot per team (k_ms_norms sums them in a fixed order)
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            sq0 += __shfl_xor_sync(0xffffffffu, sq0, o);
+            sq1 += __shfl_xor_sync(0xffffffffu, sq1, o);
+        }
+        if (lane < 4) {
+            double* np = p.norm_part + (((size_t)kk * gridDim.x + blockIdx.x) * M4_NT + team) * S + q0;
+            np[0] = sq0;
+            np[1] = sq1;
+        }
+        // probes of this team's subdomains (this warp's 8 shots): rows of U after the step
+        if (k % p.record_every == 0 && p.rows) {
+            __syncwarp();
+            const long long row = k / p.record_every - 1;
+            const int q = 8 * cw + (lane & 7);
+            for (int sl = team; sl < ns; sl += M4_NT) {
+                const int s = s0 + sl;
+                const double* us = Un + (size_t)s * KS;
+                for (int pq = p.prb_ptr[s] + (lane >> 3); pq < p.prb_ptr[s + 1]; pq += 4) {
+                    const int pid = p.prb_ids[pq];
+                    const int tap = p.prb_tap[pid];
+                    double val;
+                    if (tap >= 0) {
+                        val = us[(size_t)tap * S + q];
+                    } else {
+                        const double* wv = p.prb_w + p.prb_woff[pid];
+                        val = 0.0;
+                        for (long long i = 0; i < K; ++i) val = fma(wv[i], us[i * S + q], val);
+                    }
+                    p.rows[(row * p.n_probe + pid) * S + q] = val;
+                }
+            }
+        }
+        // this step's state writes feed the next step's TMA reads (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(stepdone);
+    }
+#ifdef SFW_MS_CLK
+    clk[3] = clock64() - clk_start;
+    if (lane < 8 && p.dbg) {
+        long long v = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (lane == i) v = clk[i];
+        p.dbg[(blockIdx.x * M2_NW + 4 * team + cw) * 8 + lane] = v;
+    }
+#endif
+#undef M4_T0
+#undef M4_T1
+}
+
+template <int M>
+__global__ void __launch_bounds__((M4_NW + 2 * M4_NT) * 32, 1) k_step_ms4(const MsParams p) {
+    constexpr int S = 32;
+    constexpr int RT = (6 * M + 7) / 8;
+    constexpr int WP = 8 * RT;
+    constexpr int W = 6 * M;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L = p.L, TB = p.TB;
+    const long long K = p.K;
+    const long long WS = (long long)W * S, KS = K * S;
+    double* cst = reinterpret_cast<double*>(smem_raw);          // [NT][NC][TB]
+    double* sst = cst + (size_t)M4_NT * M4_NC * TB;             // [NT][NSS][W*S]
+    double* Xall = sst + (size_t)M4_NT * M4_NSS * WS;           // [NW][WP][LDX]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Xall + (size_t)M4_NW * WP * M4_LDX);
+    // per team: cfull[NC], cempty[NC], sfull[NSS], sempty[NSS], stepdone
+    constexpr int NB = 2 * M4_NC + 2 * M4_NSS + 1;
+    int* ssub = reinterpret_cast<int*>(bars + M4_NT * NB);
+    int* s_nb = ssub + S;  // [ns][6]
+
+    for (int q = threadIdx.x; q < S; q += blockDim.x) ssub[q] = p.shot_sub[q];
+    if (threadIdx.x == 0) {
+        for (int t = 0; t < M4_NT; ++t) {
+            uint64_t* b = bars + t * NB;
+            for (int i = 0; i < M4_NC; ++i) {
+                mbar_init(&b[i], 1);
+                mbar_init(&b[M4_NC + i], 4);
+            }
+            for (int i = 0; i < M4_NSS; ++i) {
+                mbar_init(&b[2 * M4_NC + i], 1);
+                mbar_init(&b[2 * M4_NC + M4_NSS + i], 4);
+            }
+            mbar_init(&b[NB - 1], 4);
+        }
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < M4_NW * WP * M4_LDX; i += blockDim.x) Xall[i] = 0.0;
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int ns = s1 - s0;
+    for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nb[i] = p.nbr[s0 * 6 + i];
+    __syncthreads();
+
+    if (warp >= M4_NW) {  // producer warps: (team, ring) = ((warp - NW) / 2, (warp - NW) % 2)
+        const int pw = warp - M4_NW, team = pw >> 1;
+        uint64_t* b = bars + team * NB;
+        uint64_t *cfull = b, *cempty = b + M4_NC, *sfull = b + 2 * M4_NC, *sempty = b + 2 * M4_NC + M4_NSS,
+                 *stepdone = b + NB - 1;
+        double* tc = cst + (size_t)team * M4_NC * TB;
+        double* ts = sst + (size_t)team * M4_NSS * WS;
+        if (lane != 0) return;
+        if ((pw & 1) == 0) {  // chain-block ring of this team (ungated)
+            const uint64_t pol = l2_policy_evict_first();
+            const uint32_t cbytes = (uint32_t)TB * 8u;
+            long long c_iss = 0;
+            auto issue = [&](int sl, int bk) {
+                const int st = (int)(c_iss % M4_NC);
+                mbar_wait_sleep(&cempty[st], (uint32_t)(((c_iss / M4_NC) & 1) ^ 1));
+                mbar_arrive_expect_tx(&cfull[st], cbytes);
+                bulk_g2s(tc + (size_t)st * TB, p.tcoef + ((long long)(s0 + sl) * 2 * L + bk) * TB, cbytes, &cfull[st],
+                         pol);
+                ++c_iss;
+            };
+            for (int k = 0; k < p.n_steps; ++k) {
+                for (int sl = team; sl < ns; sl += M4_NT) {  // A: G_0 [, H_0 on boundary subdomains]
+                    const bool interior = s_nb[sl * 6] >= 0 && s_nb[sl * 6 + 1] >= 0 && s_nb[sl * 6 + 2] >= 0 &&
+                                          s_nb[sl * 6 + 3] >= 0 && s_nb[sl * 6 + 4] >= 0 && s_nb[sl * 6 + 5] >= 0;
+                    issue(sl, 0);
+                    if (!interior) issue(sl, 1);
+                }
+                for (int sl = team; sl < ns; sl += M4_NT)  // B: G_j, H_j, j >= 1
+                    for (int bk = 2; bk < 2 * L; ++bk) issue(sl, bk);
+            }
+        } else {  // state-block ring of this team, gated per step on the team's stepdone
+            const uint64_t pol = l2_policy_evict_first();
+            const uint32_t mbytes = (uint32_t)(6 * M * M * 8);
+            const uint32_t sbytes = (uint32_t)(WS * 8);
+            long long s_iss = 0;
+            auto issue = [&](const double* src, uint32_t bytes) {
+                const int st = (int)(s_iss % M4_NSS);
+                mbar_wait_sleep(&sempty[st], (uint32_t)(((s_iss / M4_NSS) & 1) ^ 1));
+                mbar_arrive_expect_tx(&sfull[st], bytes);
+                bulk_g2s(ts + (size_t)st * WS, src, bytes, &sfull[st], pol);
+                ++s_iss;
+            };
+            for (int k = 0; k < p.n_steps; ++k) {
+                if (k > 0) mbar_wait_sleep(stepdone, (uint32_t)((k - 1) & 1));  // step k reads step k-1's output
+                const int cbuf = k & 1;
+                const double* cur = cbuf ? p.U1 : p.U0;
+                const double* prv = cbuf ? p.U0 : p.U1;
+                for (int sl = team; sl < ns; sl += M4_NT) {  // A: U_0, U_1
+                    const long long base = (long long)(s0 + sl) * KS;
+                    issue(cur + base, sbytes);
+                    issue(cur + base + WS, sbytes);
+                }
+                for (int sl = team; sl < ns; sl += M4_NT) {  // C: U_0, Uprev_0, mass; B: U_1, [U_{j+1}], Uprev_j
+                    const long long base = (long long)(s0 + sl) * KS;
+                    issue(cur + base, sbytes);
+                    issue(prv + base, sbytes);
+                    issue(p.mblk + (size_t)(s0 + sl) * 6 * M * M, mbytes);
+                    issue(cur + base + WS, sbytes);
+                    for (int j = 1; j < L; ++j) {
+                        if (j + 1 < L) issue(cur + base + (j + 1) * WS, sbytes);
+                        issue(prv + base + j * WS, sbytes);
+                    }
+                }
+            }
+        }
+        return;
+    }
+    const int team = warp / 4, cw = warp % 4;
+    uint64_t* b = bars + team * NB;
+    ms4_compute<M>(p, cst + (size_t)team * M4_NC * TB, sst + (size_t)team * M4_NSS * WS,
+                   Xall + (size_t)warp * WP * M4_LDX, b, b + M4_NC, b + 2 * M4_NC, b + 2 * M4_NC + M4_NSS, b + NB - 1,
+                   ssub, s_nb, s0, ns, team, cw, lane);
+    (void)K;
+}
+
+static size_t ms4_smem_bytes(int RT, int TB, int W, int nsmax) {
+    return 8 * ((size_t)M4_NT * M4_NC * TB + (size_t)M4_NT * M4_NSS * W * 32 + (size_t)M4_NW * 8 * RT * M4_LDX +
+                (size_t)M4_NT * (2 * M4_NC + 2 * M4_NSS + 1)) +
            4 * (32 + 6 * (size_t)nsmax) + 64;
 }
 
@@ -1561,6 +2130,20 @@ static const void* ms2_kernel(int m) {
     return (m >= 1 && m <= 9) ? tab[m] : nullptr;
 }
 
+static const void* ms4_kernel(int m) {
+    static const void* const tab[10] = {nullptr,
+                                        (const void*)k_step_ms4<1>,
+                                        (const void*)k_step_ms4<2>,
+                                        (const void*)k_step_ms4<3>,
+                                        (const void*)k_step_ms4<4>,
+                                        (const void*)k_step_ms4<5>,
+                                        (const void*)k_step_ms4<6>,
+                                        (const void*)k_step_ms4<7>,
+                                        (const void*)k_step_ms4<8>,
+                                        (const void*)k_step_ms4<9>};
+    return (m >= 1 && m <= 9) ? tab[m] : nullptr;
+}
+
 // shots start from rest (u0 = v0 = 0): U_curr = 0, U_prev = ((0.5 dt) dt) (vec_q f_q(0))  (stepper.py:347-353)
 __global__ void k_ms_init(double* U0, double* U1, long long total, int S, const int* shot_sub,
                           const double* shot_vec, const long long* shot_voff, const double* f0, double half,
@@ -1659,6 +2242,18 @@ extern "C" int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub,
     } else {
         h->shot_smem2 = 0;
     }
+    h->shot_smem4 = 0;
+    if (ms4_kernel(h->m) && getenv("SFW_MS4")) {  // opt-in two-team kernel (measured slower)
+        int nsmax = 0;
+        for (int b = 0; b < h->grid; ++b) nsmax = std::max(nsmax, h->cta_ptr_h[b + 1] - h->cta_ptr_h[b]);
+        const size_t sm4 = ms4_smem_bytes(RT, h->TB, W, nsmax);
+        if (!h->mmass && (rc = dalloc(&h->mmass, (size_t)h->n_sub * 6 * h->m * h->m, errbuf, errlen))) return rc;
+        k_ms_massblocks<<<592, 256, 0, h->stream>>>(h->mass, h->mass_idx, h->n_sub, h->m, h->mmass);
+        if (sm4 <= 227 * 1024) {
+            SFW_CUDA_TRY(cudaFuncSetAttribute(ms4_kernel(h->m), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4));
+            h->shot_smem4 = (int)sm4;
+        }
+    }
     h->shot_smem3 = 0;
     // k_step_ms3 is opt-in (SFW_MS3="groups,stages", e.g. "2,3"): correct, but measured slower than
     // k_step_ms2 on config 4 (0.93 vs 0.79 ms/step): with 2 warps per SMSP the in-sweep layer-0
@@ -1708,7 +2303,10 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
     const long long nrec = n_steps / record_every;
     if ((rc = ms_ensure(&h->mrows, &h->mrows_cap, std::max(1LL, nrec * h->n_probe * S), errbuf, errlen))) return rc;
     // norm partials per step: ms3 one per subdomain group, ms2 one per row-tile group, ms one per CTA
-    const int nparts = h->shot_smem3 ? h->ms3_ng * h->grid : h->shot_smem2 ? M2_NQ * h->grid : h->grid;
+    const int nparts = h->shot_smem4   ? M4_NT * h->grid
+                       : h->shot_smem3 ? h->ms3_ng * h->grid
+                       : h->shot_smem2 ? M2_NQ * h->grid
+                                       : h->grid;
     if ((rc = ms_ensure(&h->mnorm, &h->mnorm_cap, (long long)n_steps * nparts * S + (long long)n_steps * S, errbuf,
                         errlen)))
         return rc;
@@ -1771,13 +2369,16 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
     p.sflags = h->sflags;
     p.tag0 = h->stag;
-    if (h->shot_smem3) {
+    if (h->shot_smem4) {
+        SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ms4_kernel(h->m), dim3(h->grid), dim3((M4_NW + 2 * M4_NT) * 32), args,
+                                                 h->shot_smem4, h->stream));
+    } else if (h->shot_smem3) {
         SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ms3_kernel(h->m, h->ms3_ng, h->ms3_ns), dim3(h->grid),
                                                  dim3(128 * h->ms3_ng), args,
                                                  h->shot_smem3, h->stream));
         h->stag += (unsigned int)n_steps;
     } else if (h->shot_smem2)
-        SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ms2_kernel(h->m), dim3(h->grid), dim3((M2_NW + 1) * 32), args,
+        SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ms2_kernel(h->m), dim3(h->grid), dim3((M2_NW + 2) * 32), args,
                                                  h->shot_smem2, h->stream));
     else
         SFW_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_step_ms<32>, dim3(h->grid), dim3((MS_NW + 1) * 32),

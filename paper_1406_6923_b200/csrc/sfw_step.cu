@@ -357,9 +357,10 @@ struct StepParams {
     const int* ncta;
     unsigned long long* tprof;  // debug: [gridDim.x][n_steps][5] globaltimer stamps or null
     int res_pmax, res_pdense;   // k_step_res: probes / dense probe weight vectors staged per CTA
-    unsigned long long* mbox;   // k_step_lw: tagged face mailbox [2][n_sub][W] x {lo|tag, hi|tag}
-    unsigned int tag_base;      // k_step_lw: step tag of this launch's step 0
-    int groups;                 // k_step_lw: subdomain groups (norm partials) per CTA
+    unsigned long long* mbox;   // k_step_sw / k_ustep: tagged face mailbox [2][n_sub][W] x {lo|tag, hi|tag}
+    const double* swimg;        // k_step_sw: SMEM image of the chain blocks, [n_sub][2L][21 M^2]
+    unsigned int tag_base;      // k_step_sw / k_ustep: step tag of this launch's step 0
+    int groups;                 // k_step_sw / k_ustep: subdomain groups (norm partials) per CTA
 };
 
 __device__ __forceinline__ double leap(int mode, double uc, double uo, double v, double tot,
@@ -1091,15 +1092,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_step_res(const StepParams p) {
 
 
 // ---------------------------------------------------------------------------
-// k_step_lw: layer-warp SMEM-resident variant for small-m configurations
-// (config 2: 512 x m4k6, <= 4 subdomains per CTA, w = 24 <= 32).
-//
-// Warp (g, j) owns layer j of the CTA's g-th subdomain for the whole launch:
-// U_j (current, previous) live in its registers, its two chain blocks in SMEM.
-// Per step: phase 1 flux_j = Gamma_j (U_{j+1} - U_j); phase 2 acc_j =
-// Gamma-hat_j (flux_j - flux_{j-1}) and the leapfrog.  The two phases of one
-// subdomain meet on two named barriers (the layer-1 warp only arrives on the
-// first, the last-layer warp only on the second), so groups run independently.
+// Tagged face mailbox of the warp-per-subdomain kernels (k_step_sw, k_ustep).
 //
 // Face exchange goes through a tagged mailbox instead of a flag + data pair:
 // each fp64 face value is stored as two 64-bit words {32 data bits | step tag}
@@ -1137,259 +1130,6 @@ __device__ __forceinline__ double mbox_take(const unsigned long long* slot, unsi
     return __hiloint2double((int)(unsigned int)b, (int)(unsigned int)a);
 }
 
-template <int M, int NT>
-__global__ void __launch_bounds__(NT, 1) k_step_lw(const StepParams p) {
-    constexpr int W = 6 * M;
-    static_assert(W <= 32, "one lane per chain row");
-    constexpr int WK = W + 21 * 2 * M;
-    constexpr int FB = 21 * M * M;
-    constexpr unsigned FULL = 0xffffffffu;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
-    const RedOff7<M> ro(lane);
-    const int L = p.L;
-    const int K = L * W;
-    const int G = p.groups;
-    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
-    const int ns = s1 - s0;
-    const int BS = p.BS;
-    double* cf = reinterpret_cast<double*>(smem_raw);          // [G][2L][FB]
-    double* Us = cf + (size_t)G * 2 * L * FB;                  // [G][L][W] current U
-    double* Fl = Us + (size_t)G * K;                           // [G][L][W] layer fluxes
-    double* ms = Fl + (size_t)G * K;                           // [G][6][M*M]
-    double* sqv = ms + (size_t)G * 6 * M * M;                  // [G][L]
-    double* wk = sqv + (size_t)G * L + (size_t)warp * WK;      // per-warp matvec scratch
-    double* pwv = sqv + (size_t)G * L + (size_t)nwarps * WK;   // [npd][K] dense probe weights
-    int* pmeta = reinterpret_cast<int*>(pwv + (size_t)p.res_pdense * K);
-    __shared__ int s_nbr[8 * 6];
-    __shared__ int s_src[8 + 1];
-    __shared__ int s_prb[8 + 1];
-    double* xs = wk;
-    double* part = xs + W;
-    const int g = warp / L, j = warp % L;  // subdomain group, layer
-    const bool live = g < ns;
-    const bool act = lane < W;
-
-    // ---- one-time loads (whole CTA) ----------------------------------------
-    for (int bk = warp; bk < ns * 2 * L; bk += nwarps)
-        expand_block_full<M>(p.coef + ((size_t)s0 * 2 * L + bk) * BS, cf + (size_t)bk * FB, lane, 32);
-    {
-        const int pa = p.prb_ptr[s0], pb = p.prb_ptr[s1];
-        if (threadIdx.x == 0) {
-            int nd = 0;
-            for (int q = pa; q < pb && q - pa < p.res_pmax; ++q) {
-                const int pid = p.prb_ids[q];
-                const int tap = p.prb_tap[pid];
-                pmeta[2 * (q - pa)] = pid;
-                if (tap >= 0) {
-                    pmeta[2 * (q - pa) + 1] = tap;
-                } else if (nd < p.res_pdense) {
-                    pmeta[2 * (q - pa) + 1] = -1 - nd;
-                    ++nd;
-                } else {
-                    pmeta[2 * (q - pa) + 1] = -1000000;
-                }
-            }
-        }
-        __syncthreads();
-        for (int q = pa + warp; q < pb && q - pa < p.res_pmax; q += nwarps) {
-            const int slot = pmeta[2 * (q - pa) + 1];
-            if (slot < 0 && slot > -1000000) {
-                const double* wv = p.prb_w + p.prb_woff[pmeta[2 * (q - pa)]];
-                for (int i = lane; i < K; i += 32) pwv[(size_t)(-1 - slot) * K + i] = wv[i];
-            }
-        }
-    }
-    for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nbr[i] = p.nbr[s0 * 6 + i];
-    for (int i = threadIdx.x; i <= ns; i += blockDim.x) {
-        s_src[i] = p.src_ptr[s0 + i];
-        s_prb[i] = p.prb_ptr[s0 + i];
-    }
-    for (int i = threadIdx.x; i < ns * 6 * M * M; i += blockDim.x) {
-        const int sl = i / (6 * M * M), f = (i / (M * M)) % 6, e = i % (M * M);
-        const int mi = p.mass_idx[(s0 + sl) * 6 + f];
-        ms[i] = mi >= 0 ? p.mass[(size_t)mi * M * M + e] : 0.0;
-    }
-    double uc = 0.0, up = 0.0;
-    const double* Ug0 = p.cur ? p.U1 : p.U0;
-    const double* Ug1 = p.cur ? p.U0 : p.U1;
-    if (live && act) {
-        const size_t gi = (size_t)(s0 + g) * K + j * W + lane;
-        uc = Ug0[gi];
-        up = Ug1[gi];
-        Us[(g * L + j) * W + lane] = uc;
-    }
-    __syncthreads();
-    if (!live) {  // empty group slot: zero norm partials, then leave
-        if (j == 0 && lane == 0)
-            for (int k = 0; k < p.n_steps; ++k) p.norm_part[((size_t)k * gridDim.x + blockIdx.x) * G + g] = 0.0;
-        return;
-    }
-    const int s = s0 + g;
-    // sources of this subdomain (<= 2) staged in registers: a dependent chain of global
-    // loads per step would sit on the critical path of the whole coupled grid
-    const int src_a = s_src[g], nsrc = s_src[g + 1] - s_src[g];
-    double sv0 = 0.0, sv1 = 0.0;
-    const double *ft0 = p.ftab, *ft1 = p.ftab;
-    if (nsrc >= 1 && nsrc <= 2 && act) {
-        const int q0 = p.src_ids[src_a];
-        sv0 = p.src_vec[p.src_voff[q0] + (long long)j * W + lane];
-        ft0 = p.ftab + (long long)q0 * p.ftab_stride;
-        if (nsrc == 2) {
-            const int q1 = p.src_ids[src_a + 1];
-            sv1 = p.src_vec[p.src_voff[q1] + (long long)j * W + lane];
-            ft1 = p.ftab + (long long)q1 * p.ftab_stride;
-        }
-    }
-    const int pa0 = s_prb[0], pq0 = s_prb[g], pq1 = s_prb[g + 1];
-    const double dt2 = p.dt2;
-    const int barA = 1 + 2 * g, barB = 2 + 2 * g, nthr = L * 32;
-    const double* cfj = cf + (size_t)(g * L + j) * 2 * FB;
-    double* Usj = Us + (g * L + j) * W;
-    double* Flj = Fl + (g * L + j) * W;
-    // face of this lane (layer-1 warp only)
-    const int f = lane / M, r = lane % M;
-    const int nb = (j == 0 && act) ? s_nbr[g * 6 + f] : -1;
-    unsigned long long* mb_out = p.mbox + ((size_t)s * W + lane) * 2;
-    const unsigned long long* mb_in = p.mbox + ((size_t)(nb < 0 ? 0 : nb) * W + (f ^ 1) * M + r) * 2;
-    const size_t mb_par = (size_t)p.n_sub * W * 2;
-    const double* mrow = ms + (g * 6 + (f < 6 ? f : 0)) * M * M + r * M;
-
-#ifdef SFW_LW_CLK  // debug: per-warp cycle accounting of the step phases
-    long long clk_prev = clock64(), clk_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-#define LW_CLK(ph)                          \
-    {                                       \
-        const long long c_ = clock64();     \
-        clk_acc[ph] += c_ - clk_prev;       \
-        clk_prev = c_;                      \
-    }
-#else
-#define LW_CLK(ph)
-#endif
-    int rec_cnt = p.record_every;
-    long long row = -1;
-    for (int k = 1; k <= p.n_steps; ++k) {
-        const int par = k & 1;
-        const unsigned int tag = p.tag_base + (unsigned int)k;
-        const int kk = k - 1;
-        const bool rec = (--rec_cnt == 0) && p.rows;
-        if (rec_cnt == 0) {
-            rec_cnt = p.record_every;
-            ++row;
-        }
-        // this step's source amplitudes, loaded early (consumed after phase 2)
-        const double fa0 = (nsrc >= 1 && nsrc <= 2) ? ft0[kk] : 0.0;
-        const double fa1 = (nsrc == 2) ? ft1[kk] : 0.0;
-        // ---- phase 1: flux_j = Gamma_j (U_{j+1} - U_j) ----------------------
-        if (act) xs[lane] = (j + 1 < L ? Usj[W + lane] : 0.0) - uc;
-        __syncwarp();
-        LW_CLK(0);
-        const double fl = sym_matvec_lane<M>(cfj, xs, part, lane, ro);
-        if (act) Flj[lane] = fl;
-        if (nb >= 0) mbox_put(mb_out + par * mb_par, fl, tag);
-        LW_CLK(1);
-        if (j == 0)
-            asm volatile("bar.arrive %0, %1;" ::"r"(barA), "r"(nthr) : "memory");
-        else
-            asm volatile("bar.sync %0, %1;" ::"r"(barA), "r"(nthr) : "memory");
-        LW_CLK(2);
-        // ---- phase 2: acc_j = Gamma-hat_j (flux_j - flux_{j-1}), leapfrog -----
-        if (act) xs[lane] = j > 0 ? fl - Flj[lane - W] : fl;
-        __syncwarp();
-        double a = sym_matvec_lane<M>(cfj + FB, xs, part, lane, ro);
-        LW_CLK(3);
-        if (j == 0) {
-            // interface faces: seg = mass (own + nbr)  (stepper.py:283-300)
-            const double oth = mbox_take_warp(mb_in + par * mb_par, tag, nb >= 0);
-            // face values regrouped through SMEM, not shuffles: right after the divergent
-            // poll loop a shuffle takes the warp-divergent slow path (~1 us per step measured)
-            if (nb >= 0) xs[lane] = oth;
-            __syncwarp();
-            LW_CLK(4);
-            double acc_if = 0.0;
-#pragma unroll
-            for (int c = 0; c < M; ++c) acc_if = fma(mrow[c], __dadd_rn(Flj[f * M + c], xs[f * M + c]), acc_if);
-            if (nb >= 0) a = acc_if;
-        }
-        double un = 0.0;
-        if (act) {
-            double tot = a;
-            if (nsrc == 1) {  // add_force order: f = term_0 (+ term_1); tot = acc + f
-                tot = __dadd_rn(a, __dmul_rn(sv0, fa0));
-            } else if (nsrc == 2) {
-                tot = __dadd_rn(a, __dadd_rn(__dmul_rn(sv0, fa0), __dmul_rn(sv1, fa1)));
-            } else if (nsrc > 2) {
-                tot = add_force(p, s, (long long)j * W + lane, kk, a);
-            }
-            un = __dadd_rn(__dsub_rn(__dmul_rn(2.0, uc), up), __dmul_rn(dt2, tot));
-            up = uc;
-            uc = un;
-            Usj[lane] = un;
-        }
-        __syncwarp();
-        LW_CLK(5);
-        const double sq = warp_sum(act ? un * un : 0.0);
-        if (lane == 0) sqv[g * L + j] = sq;
-        if (rec) {  // tap probes on this layer, straight from registers
-            for (int q = pq0; q < pq1; ++q) {
-                const bool staged = q - pa0 < p.res_pmax;
-                const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
-                const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
-                if (tap >= j * W && tap < (j + 1) * W) {
-                    const double v = __shfl_sync(FULL, un, tap - j * W);
-                    if (lane == 0) p.rows[row * p.n_probe + pid] = v;
-                }
-            }
-        }
-        LW_CLK(6);
-        if (j == L - 1 && L > 1)
-            asm volatile("bar.arrive %0, %1;" ::"r"(barB), "r"(nthr) : "memory");
-        else
-            asm volatile("bar.sync %0, %1;" ::"r"(barB), "r"(nthr) : "memory");
-        LW_CLK(7);
-        if (j == 0) {
-            if (lane == 0) {
-                double t = sqv[g * L];
-                for (int jj = 1; jj < L; ++jj) t += sqv[g * L + jj];
-                p.norm_part[((size_t)kk * gridDim.x + blockIdx.x) * G + g] = t;
-            }
-            if (rec) {  // dense probes: whole subdomain state (all layers published by barrier B)
-                const double* Ug = Us + (size_t)g * K;
-                for (int q = pq0; q < pq1; ++q) {
-                    const bool staged = q - pa0 < p.res_pmax;
-                    const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
-                    const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
-                    if (tap >= 0) continue;
-                    const double* wv = (tap > -1000000) ? pwv + (size_t)(-1 - tap) * K : p.prb_w + p.prb_woff[pid];
-                    double acc = 0.0;
-                    for (int i = lane; i < K; i += 32) acc = fma(wv[i], Ug[i], acc);
-                    const double v = warp_sum(acc);
-                    if (lane == 0) p.rows[row * p.n_probe + pid] = v;
-                }
-            }
-        }
-        LW_CLK(8);
-    }
-#ifdef SFW_LW_CLK
-    if (p.tprof && lane < 10) {
-        long long v = 0;
-#pragma unroll
-        for (int q = 0; q < 10; ++q)
-            if (lane == q) v = clk_acc[q];
-        p.tprof[((size_t)blockIdx.x * nwarps + warp) * 16 + lane] = v;
-    }
-#endif
-#undef LW_CLK
-    // write both time levels back (global layout as k_step2: U[cur ^ (n & 1)] is current)
-    if (act) {
-        double* Gc = (p.cur ^ (p.n_steps & 1)) ? p.U1 : p.U0;
-        double* Go = (p.cur ^ (p.n_steps & 1)) ? p.U0 : p.U1;
-        const size_t gi = (size_t)s * K + j * W + lane;
-        Gc[gi] = uc;
-        Go[gi] = up;
-    }
-}
 
 
 // ---------------------------------------------------------------------------
@@ -1424,6 +1164,14 @@ __device__ __forceinline__ void expand_block_pairs(const double* __restrict__ pa
         }
         out[((e >> 1) * 21 + t) * 2 + (e & 1)] = v;
     }
+}
+
+// create-time expansion of every packed block into k_step_sw's SMEM image (one CTA per block), so a
+// launch's prologue is one contiguous bulk copy per CTA instead of a gather per element
+template <int M>
+__global__ void k_expand_sw(const double* __restrict__ coef, int BS, double* __restrict__ img) {
+    expand_block_pairs<M>(coef + (size_t)blockIdx.x * BS, img + (size_t)blockIdx.x * 21 * M * M, threadIdx.x,
+                          blockDim.x);
 }
 
 // NL independent symmetric block mat-vecs y_j = B_j x_j (tile lanes 0..20), results in
@@ -1512,8 +1260,20 @@ __global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
     const bool act = lane < W;
 
     // ---- one-time loads (whole CTA) ----------------------------------------
-    for (int bk = warp; bk < ns * 2 * L; bk += nwarps)
-        expand_block_pairs<M>(p.coef + ((size_t)s0 * 2 * L + bk) * BS, cf + (size_t)bk * FB, lane, 32);
+    // the CTA's chain blocks: one contiguous region of the create-time SMEM image, moved by the
+    // TMA engine in 32 KB pieces while the threads stage probes, neighbours and masses
+    __shared__ __align__(8) uint64_t s_bar;
+    const uint32_t img_bytes = (uint32_t)ns * 2 * L * FB * 8;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&s_bar, img_bytes);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(p.swimg + (size_t)s0 * 2 * L * FB);
+        for (uint32_t off = 0; off < img_bytes; off += 32768u)
+            bulk_g2s(reinterpret_cast<unsigned char*>(cf) + off, src + off, min(32768u, img_bytes - off), &s_bar,
+                     l2_policy_evict_last());
+    }
+    (void)BS;
     {
         const int pa = p.prb_ptr[s0], pb = p.prb_ptr[s1];
         if (threadIdx.x == 0) {
@@ -1552,6 +1312,7 @@ __global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
         ms[i] = mi >= 0 ? p.mass[(size_t)mi * M * M + e] : 0.0;
     }
     __syncthreads();
+    mbar_wait(&s_bar, 0);
     if (!live) {  // no subdomain for this warp: zero its norm partials
         if (lane == 0)
             for (int k = 0; k < p.n_steps; ++k) p.norm_part[((size_t)k * gridDim.x + blockIdx.x) * p.groups + g] = 0.0;
@@ -2512,7 +2273,7 @@ static void free_all(sfw_stepper* h) {
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
                     h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta, h->tcoef, h->UM[0], h->UM[1],
                     h->mfb, h->macc1, h->mnorm, h->mrows, h->shot_vec, h->shot_sub, h->shot_voff,
-                    h->shot_ftab, h->mbox, h->mmass, h->sflags, h->ucoef};
+                    h->shot_ftab, h->mbox, h->mmass, h->sflags, h->ucoef, h->swimg};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -2748,9 +2509,11 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
         if (d->scales) {
             TRY(dalloc(&h->scales, dense_n, errbuf, errlen));
             TRY(dalloc(&h->gam_dense, dense_n, errbuf, errlen));
-            SFW_CUDA_TRY(cudaMemcpy(h->scales, d->scales, dense_n * 8,
-                                    d->coef_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-            SFW_CUDA_TRY(cudaMemcpy(h->gam_dense, g_dev, dense_n * 8, cudaMemcpyDeviceToDevice));
+            if (d->coef_on_device)
+                SFW_CUDA_TRY(cudaMemcpyAsync(h->scales, d->scales, dense_n * 8, cudaMemcpyDeviceToDevice, h->stream));
+            else
+                SFW_CUDA_TRY(sfw_h2d(h->scales, d->scales, dense_n * 8));
+            SFW_CUDA_TRY(cudaMemcpyAsync(h->gam_dense, g_dev, dense_n * 8, cudaMemcpyDeviceToDevice, h->stream));
         }
         if (own_dense) {
             cudaFree(g_dev);
@@ -2829,9 +2592,9 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
         TRY(dalloc(&h->fbuf, (size_t)2 * n * W, errbuf, errlen));
         TRY(dalloc(&h->sub_norm, n, errbuf, errlen));
         TRY(dalloc(&h->bar, (size_t)h->grid, errbuf, errlen));
-        cudaMemset(h->U[0], 0, h->state_len * 8);
-        cudaMemset(h->U[1], 0, h->state_len * 8);
-        cudaMemset(h->fbuf, 0, (size_t)2 * n * W * 8);
+        SFW_CUDA_TRY(cudaMemsetAsync(h->U[0], 0, h->state_len * 8, h->stream));
+        SFW_CUDA_TRY(cudaMemsetAsync(h->U[1], 0, h->state_len * 8, h->stream));
+        SFW_CUDA_TRY(cudaMemsetAsync(h->fbuf, 0, (size_t)2 * n * W * 8, h->stream));
 
         // ---- sources ------------------------------------------------------------
         h->n_src = d->n_src;
@@ -2914,6 +2677,8 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
             if (getenv("SFW_STEP_VERBOSE"))
                 fprintf(stderr, "[sfw] k_step_sw: maxns=%d L=%d smem=%zu\n", maxns, L, need);
             if (maxns >= 1 && maxns <= 8 && need <= 220 * 1024) {
+                TRY(dalloc(&h->swimg, (size_t)n * 2 * L * 21 * m * m, errbuf, errlen));
+                k_expand_sw<4><<<(unsigned)(n * 2 * L), 128, 0, h->stream>>>(h->coef, h->BS, h->swimg);
                 h->klw = ksw[L];
                 h->lw_smem = (int)need;
                 h->lw_threads = 32 * maxns;
@@ -2921,8 +2686,8 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
                 h->res_pmax = pmax;
                 h->res_pdense = pdense;
                 SFW_CUDA_TRY(cudaFuncSetAttribute(h->klw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
-                SFW_CUDA_TRY(cudaMalloc(&h->mbox, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
-                SFW_CUDA_TRY(cudaMemset(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
+                TRY(dalloc(&h->mbox, (size_t)2 * n * W * 2, errbuf, errlen));
+                SFW_CUDA_TRY(cudaMemsetAsync(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long), h->stream));
                 h->tag_base = 0;
             }
         }
@@ -2936,8 +2701,8 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
                 k_repack_u2<<<(unsigned)h->n_blocks, 128, 0, h->stream>>>(h->coef, h->BS, m, BS2, h->ucoef,
                                                                         h->n_blocks);
                 if (!h->mbox) {
-                    SFW_CUDA_TRY(cudaMalloc(&h->mbox, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
-                    SFW_CUDA_TRY(cudaMemset(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
+                    TRY(dalloc(&h->mbox, (size_t)2 * n * W * 2, errbuf, errlen));
+                    SFW_CUDA_TRY(cudaMemsetAsync(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long), h->stream));
                     h->tag_base = 0;
                 }
                 h->BS2 = BS2;
@@ -2948,35 +2713,6 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
                 h->ustep = true;
                 SFW_CUDA_TRY(cudaFuncSetAttribute(h->klw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
                 if (getenv("SFW_STEP_VERBOSE")) fprintf(stderr, "[sfw] k_ustep: smem=%zu\n", need);
-            }
-        }
-        // layer-warp resident variant: one warp per (subdomain, layer), w <= 32
-        if (!h->klw && h->uniform && !getenv("SFW_NO_RESIDENT") && !getenv("SFW_NO_LW") && (m == 1 || m == 4)) {
-            int maxns = 0;
-            for (int b = 0; b < h->grid; ++b) maxns = std::max(maxns, cta_res_ns(h, b));
-            const int L = h->L, K = L * W, nthr = maxns * L * 32;
-            const int pmax = 256, pdense = 2;
-            const size_t need = 8 * ((size_t)maxns * 2 * L * 21 * m * m + (size_t)2 * maxns * K +
-                                     (size_t)maxns * 6 * m * m + (size_t)maxns * L +
-                                     (size_t)(nthr / 32) * (W + 42 * m) + (size_t)pdense * K) +
-                                4 * 2 * (size_t)pmax;
-            const void* kl = nullptr;
-            if (nthr <= 768) kl = (m == 1) ? (const void*)k_step_lw<1, 768> : (const void*)k_step_lw<4, 768>;
-            else if (nthr <= 896) kl = (m == 1) ? (const void*)k_step_lw<1, 896> : (const void*)k_step_lw<4, 896>;
-            else if (nthr <= 1024) kl = (m == 1) ? (const void*)k_step_lw<1, 1024> : (const void*)k_step_lw<4, 1024>;
-            if (getenv("SFW_STEP_VERBOSE"))
-                fprintf(stderr, "[sfw] k_step_lw: maxns=%d L=%d nthr=%d smem=%zu\n", maxns, L, nthr, need);
-            if (kl && maxns >= 1 && maxns <= 7 && need <= 220 * 1024) {
-                h->klw = kl;
-                h->lw_smem = (int)need;
-                h->lw_threads = nthr;
-                h->lw_groups = maxns;
-                h->res_pmax = pmax;
-                h->res_pdense = pdense;
-                SFW_CUDA_TRY(cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
-                SFW_CUDA_TRY(cudaMalloc(&h->mbox, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
-                SFW_CUDA_TRY(cudaMemset(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long)));
-                h->tag_base = 0;
             }
         }
         const void* kp = h->kfn;
@@ -3079,6 +2815,7 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
             h->tag_base = 0;
         }
         p.mbox = h->mbox;
+        p.swimg = h->swimg;
         p.tag_base = h->tag_base;
         p.groups = h->lw_groups;
         if (h->ustep) {  // k_ustep streams the 16-B-pair re-layout of the chain blocks

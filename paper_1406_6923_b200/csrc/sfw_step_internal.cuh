@@ -25,8 +25,10 @@ inline int dalloc(T** p, size_t n, char* errbuf, int errlen) {
     if (const char* pz = std::getenv("SFW_POISON")) {  // debug: fresh buffers read as NaN until written
         const bool w = g_wform_scope > 0;
         if (pz[0] == 'a' || (pz[0] == 'w' && w) || (pz[0] == 's' && !w)) {
+            // legacy-stream memset + a legacy-stream sync only: library kernels run on non-blocking
+            // streams and are not drained here (every H2D copy already syncs the legacy stream)
             cudaMemset(*p, 0xFF, n * sizeof(T));
-            cudaDeviceSynchronize();
+            cudaStreamSynchronize(cudaStreamLegacy);
         }
     }
     return 0;
@@ -111,10 +113,11 @@ struct sfw_stepper {
     const void* kfn = nullptr;
     const void* kres = nullptr;
     int res_smem = 0, res_nw = 0, res_pmax = 0, res_pdense = 0;
-    // k_step_lw (layer-warp resident kernel): launch shape + tagged face mailbox
+    // warp-per-subdomain kernels (k_step_sw, k_ustep): launch shape + tagged face mailbox
     const void* klw = nullptr;
     int lw_smem = 0, lw_threads = 0, lw_groups = 1;
     double* ucoef = nullptr;  // k_ustep: chain blocks in the 16-B-pair layout
+    double* swimg = nullptr;  // k_step_sw: every subdomain's 2L blocks pre-expanded to the SMEM image
     int BS2 = 0;
     bool ustep = false;
     int n_interior = 0;  // subdomains with all six faces shared
@@ -140,6 +143,7 @@ struct sfw_stepper {
     long long shot_ftab_cap = 0, mrows_cap = 0, mnorm_cap = 0;
     int mcur = 0;
     int shot_smem3 = 0;               // k_step_ms3 dynamic smem (0: not used)
+    int shot_smem4 = 0;               // k_step_ms4 dynamic smem (0: not used)
     int ms3_ng = 2, ms3_ns = 4;       // k_step_ms3 launch shape (subdomain groups, chain stages)
     unsigned int* sflags = nullptr;   // k_step_ms3: [n_sub][4] F_0 publication tags
     unsigned int stag = 0;            // k_step_ms3: last tag used

@@ -434,12 +434,14 @@ class CoupledStepper:
         self._baseline = base
         self._initialized = True
 
-    def _steps(self, n_steps: int, record_every: int, out: np.ndarray | None = None):
+    def _steps(self, n_steps: int, record_every: int, out: np.ndarray | None = None, check: bool = True):
         if not self._initialized:
             raise ProtocolError("stepper not initialized")
         dt = self.dt
         prof = self._profile_steps(self.steps_done, n_steps) if self.sources else None
         limits, base = self._limits(prof, self._src_norms, n_steps)
+        if not check:
+            limits = None
         n_rec = n_steps // record_every
         rows = out if out is not None else np.empty((max(1, n_rec), max(1, len(self._probes))))
         norms = np.empty(n_steps)
@@ -448,11 +450,13 @@ class CoupledStepper:
         if self.precision == "fp32":
             # W-form: |W| against the same detector rule with W-form source norms
             limits, base = self._limits(prof, self._src_norms_w, n_steps)
+            if not check:
+                limits = None
             ms = C.c_float(0.0)
             rc = self._lib.sfw_wform_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(rows),
                                          _lib.dptr(norms), C.byref(ms), eb, 1024)
             self.last_kernel_ms = ms.value
-            if rc == 0:
+            if rc == 0 and limits is not None:
                 over = np.nonzero(~(norms <= limits))[0]
                 if over.size:
                     rc = _lib.SFW_EINSTABLE
@@ -498,7 +502,17 @@ class CoupledStepper:
         out[0] = self._row0
         start = self.steps_done
         if n_steps > 0:
-            self._steps(n_steps, record_every, out=out[1:] if (n_p and n_rec) else None)
+            try:
+                self._steps(n_steps, record_every, out=out[1:] if (n_p and n_rec) else None)
+            except InstabilityError:
+                # the persistent launch ran past the first failing step k; replay the k steps from
+                # the same start (bitwise deterministic) so u_curr / u_prev / steps_done / time are
+                # the reference's at the raise (stepper.py:379-389 stops at step k)
+                k = self.steps_done - start
+                self.initialize(u0, v0, _probes=probes)
+                if k > 0:
+                    self._steps(k, 1, check=False)
+                raise
         times = np.concatenate([[0.0], (np.arange(record_every, n_steps + 1, record_every, dtype=np.float64)
                                         + float(start)) * self.dt]) if n_steps > 0 else np.zeros(1)
         return times, out

@@ -429,8 +429,29 @@ def golden_c5(workers=8):
     print("golden_c5.npz", alphas)
 
 
+def golden_states():
+    """Reference project_state / state_to_nodes (rom.py:437-459) on one config-1 subdomain model,
+    and the reference's interface masses (stepper.py:204-210) of the config-1 tiling."""
+    from sfwave.rom import project_state, state_to_nodes
+    wl = make_workload(1)
+    part, ops, models = workload_models(wl)
+    a = (1, 0, 1)
+    md = models[a]
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal(md.basis.shape[0])
+    u = rng.standard_normal(md.state_size)
+    with CoupledStepper(models, 1e-4) as st:
+        masses = np.stack([i.mass for i in st.interfaces])
+        pairs = np.array([[*i.low, i.low_face, *i.high, i.high_face] for i in st.interfaces])
+    np.savez_compressed(os.path.join(HERE, "golden_states.npz"), alpha=np.array(a), x=x, u=u,
+                        projected=project_state(md, x), nodes=state_to_nodes(md, u), masses=masses, pairs=pairs)
+    print("golden_states.npz", masses.shape)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["toy", "c1", "m9k8", "io", "fdtd", "ntd"]
+    if "states" in which:
+        golden_states()
     if "c2" in which:
         golden_c2()
     if "c5" in which:

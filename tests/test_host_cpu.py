@@ -177,3 +177,69 @@ def test_library_pulse_table_is_bit_identical_to_the_callable(name):
     # any other callable goes through the per-step path
     g = lambda t: 2.0 * t  # noqa: E731
     assert np.array_equal(profile_table([g], 3, 5, 0.5)[0], [2.0 * (3 + k) * 0.5 for k in range(5)])
+
+
+def test_resolve_dt_policy():
+    """sim.py:444-463 _resolve_dt semantics."""
+    from paper_1406_6923_b200 import resolve_dt
+    from paper_1406_6923_b200.stepper import _resolve_dt
+    assert resolve_dt("auto", 2.0, True, 1.0) == 0.9 * 2.0
+    assert resolve_dt("auto", 2.0, False, 1.0) == 0.9 * 1.0
+    assert resolve_dt("fine", 2.0, True, 1.0) == 0.9 * 1.0
+    assert resolve_dt(1.8, 2.0, True, 1.0) == 1.8
+    assert resolve_dt(1.8 * (1 + 5e-13), 2.0, True, 1.0) == 1.8 * (1 + 5e-13)
+    with pytest.raises(ConfigError) as ei:
+        resolve_dt(1.81, 2.0, True, 1.0)
+    assert ei.value.path == "time.dt"
+
+    class Cfg:
+        dt = "auto"
+    assert _resolve_dt(Cfg, 2.0, True, 1.0) == 0.9 * 2.0
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference tree absent (GPU box)")
+def test_public_signatures_match_reference():
+    """Every name we re-export that the reference also exports keeps the reference's parameters
+    (names, kinds, defaults, in order); ours may only append optional ones."""
+    import importlib
+    import inspect
+    import sys
+    sys.path.insert(0, REF_SRC)
+    try:
+        ref = importlib.import_module("sfwave")
+        ref_mods = {m: importlib.import_module("sfwave." + m) for m in ("rom", "stepper", "grid", "io", "reference")}
+    finally:
+        sys.path.remove(REF_SRC)
+    import paper_1406_6923_b200 as ours
+    from paper_1406_6923_b200 import rom, stepper
+    pairs = [(n, getattr(ours, n), getattr(ref, n)) for n in ours.__all__ if hasattr(ref, n)]
+    pairs += [(n, getattr(rom, n), getattr(ref_mods["rom"], n)) for n in ("project_state", "state_to_nodes")]
+    pairs += [(n, getattr(stepper, n), getattr(ref_mods["stepper"], n))
+              for n in ("project_source", "make_probe", "cfl_estimate_coupled", "stable_step_coupled",
+                        "chain_operator")]
+    checked = 0
+    for name, mine, theirs in pairs:
+        if not callable(theirs):
+            continue
+        try:
+            ps = list(inspect.signature(theirs).parameters.values())
+        except (TypeError, ValueError):
+            continue
+        mp = list(inspect.signature(mine).parameters.values())
+        assert len(mp) >= len(ps), name
+        for a, b in zip(ps, mp):
+            assert (a.name, a.kind) == (b.name, b.kind), (name, a, b)
+            assert a.default is inspect.Parameter.empty or a.default == b.default, (name, a, b)
+        for extra in mp[len(ps):]:
+            assert extra.default is not inspect.Parameter.empty or extra.kind == extra.VAR_KEYWORD, (name, extra)
+        checked += 1
+    methods = ["initialize", "advance", "run", "energy", "close"]
+    for meth in methods:
+        ps = list(inspect.signature(getattr(ref.CoupledStepper, meth)).parameters.values())
+        mp = list(inspect.signature(getattr(ours.CoupledStepper, meth)).parameters.values())
+        for a, b in zip(ps, mp):
+            assert (a.name, a.kind, a.default) == (b.name, b.kind, b.default), (meth, a, b)
+    assert checked >= 10, checked

@@ -211,6 +211,20 @@ def test_instability_detected():
     with CoupledStepper(models, dt) as st:
         with pytest.raises(InstabilityError):
             st.run(400, u0=u0)
+        # stops where the reference stops (stepper.py:379-389): same step, same state
+        omodels = {a: so.Model(alpha=a, lo=None, shape=None, spacing=None, modes_per_face=m.modes_per_face,
+                               layers=m.layers, shift=4.0, neighbors=m.neighbors, face_indices=(), gammas=m.gammas,
+                               gamma_hats=m.gamma_hats, scales=m.scales, basis=None, c=m.c, mu=m.mu)
+                   for a, m in models.items()}
+        ref = so.Coupled(omodels, dt)
+        with pytest.raises(so.OracleError) as ei:
+            ref.run(400, u0=u0)
+        assert ei.value.kind == "InstabilityError"
+        assert 0 < st.steps_done == ref.steps_done < 400
+        assert st.time == ref.time
+        uc = st.u_curr
+        for a in order:
+            assert rel(uc[a], ref.u_curr[a]) < 1e-8
 
 
 def test_advance_equals_run():
