@@ -2273,7 +2273,7 @@ static void free_all(sfw_stepper* h) {
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
                     h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta, h->tcoef, h->UM[0], h->UM[1],
                     h->mfb, h->macc1, h->mnorm, h->mrows, h->shot_vec, h->shot_sub, h->shot_voff,
-                    h->shot_ftab, h->mbox, h->mmass, h->sflags, h->ucoef, h->swimg};
+                    h->shot_ftab, h->mbox, h->mmass, h->ucoef, h->swimg};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);

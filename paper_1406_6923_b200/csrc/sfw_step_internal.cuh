@@ -130,7 +130,7 @@ struct sfw_stepper {
     double* flux = nullptr;
     double* sq = nullptr;
     // multi-shot mode (sfw_shots_*): S independent wavefields, DMMA tile-packed chain blocks
-    int n_shots = 0, shot_smem = 0, shot_smem2 = 0;
+    int n_shots = 0, shot_smem2 = 0;
     double* mmass = nullptr;  // multi-shot: per-subdomain interface mass blocks
     double* tcoef = nullptr;          // [n_blocks][TB] fragment-ordered 8x8 lower tiles
     int TB = 0;
@@ -142,11 +142,6 @@ struct sfw_stepper {
     double* shot_ftab = nullptr;
     long long shot_ftab_cap = 0, mrows_cap = 0, mnorm_cap = 0;
     int mcur = 0;
-    int shot_smem3 = 0;               // k_step_ms3 dynamic smem (0: not used)
-    int shot_smem4 = 0;               // k_step_ms4 dynamic smem (0: not used)
-    int ms3_ng = 2, ms3_ns = 4;       // k_step_ms3 launch shape (subdomain groups, chain stages)
-    unsigned int* sflags = nullptr;   // k_step_ms3: [n_sub][4] F_0 publication tags
-    unsigned int stag = 0;            // k_step_ms3: last tag used
 };
 
 namespace sfw {

@@ -34,10 +34,7 @@ def _shots(models, n, seed):
     return out
 
 
-@pytest.mark.parametrize("kernel", ["ms2", "ms3"])
-def test_shots_match_single_source_runs_config1(kernel, monkeypatch):
-    if kernel == "ms3":  # opt-in shot-group-per-warp kernel (k_step_ms3)
-        monkeypatch.setenv("SFW_MS3", "2,3")
+def test_shots_match_single_source_runs_config1():
     g = load_golden("golden_c1.npz")
     wl = make_workload(1)
     part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
