@@ -223,10 +223,13 @@ int sfw_wform_vectors(sfw_stepper* h, const double* src_vec, const double* probe
 /* Two-level start in W-form (u0/v0: HOST U-form or NULL). */
 int sfw_wform_init(sfw_stepper* h, const double* u0, const double* v0, const double* profile0,
                    double* row0_out, char* errbuf, int errlen);
-/* n_steps fp32 W-form steps in one launch; rows are physical probe values (fp64),
- * norms_out |W| per step; *kernel_ms the launch's CUDA-event time. */
-int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, const double* profile,
-                  double* rows_out, double* norms_out, float* kernel_ms, char* errbuf, int errlen);
+/* n_steps fp32 W-form steps; rows are physical probe values (fp64), norms_out |W| per step;
+ * *kernel_ms the CUDA-event time of the launches.  limits: HOST [n_steps] growth thresholds on |W|
+ * (the detector of stepper.py:379-389 in W-form norms) or NULL: with limits the run is launched in
+ * chunks of <= 512 steps whose |W| is checked on the way, and it stops launching at the first
+ * failing step (SFW_EINSTABLE, *bad_step 1-based; the state is at most one chunk past it). */
+int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, const double* profile, const double* limits,
+                  double* rows_out, double* norms_out, int* bad_step, float* kernel_ms, char* errbuf, int errlen);
 /* Current/previous state mapped back to U-form (fp64). */
 int sfw_wform_state(sfw_stepper* h, double* u_curr, double* u_prev, char* errbuf, int errlen);
 int sfw_wform_traffic(sfw_stepper* h, double* alg_bytes, double* streamed_bytes);

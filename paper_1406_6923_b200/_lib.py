@@ -80,7 +80,7 @@ SIGNATURES = {
     "sfw_wform_setup": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int]),
     "sfw_wform_vectors": (C.c_int, [C.c_void_p, PD, PD, PD, C.c_char_p, C.c_int]),
     "sfw_wform_init": (C.c_int, [C.c_void_p, PD, PD, PD, PD, C.c_char_p, C.c_int]),
-    "sfw_wform_run": (C.c_int, [C.c_void_p, C.c_int, C.c_int, PD, PD, PD, PF, C.c_char_p, C.c_int]),
+    "sfw_wform_run": (C.c_int, [C.c_void_p, C.c_int, C.c_int, PD, PD, PD, PD, PI, PF, C.c_char_p, C.c_int]),
     "sfw_wform_state": (C.c_int, [C.c_void_p, PD, PD, C.c_char_p, C.c_int]),
     "sfw_wform_traffic": (C.c_int, [C.c_void_p, PD, PD]),
     "sfw_wform_destroy": (C.c_int, [C.c_void_p]),

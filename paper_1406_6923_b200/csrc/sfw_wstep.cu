@@ -463,25 +463,25 @@ __global__ void __launch_bounds__(256, 1) k_wstep(const WParams p) {
                 const int s = s0 + warp + t * NW;
                 const float* U = ((p.mode == 1) ? Wc : Wn) + (size_t)s * K;
                 const int pa = p.prb_ptr[s], pb = p.prb_ptr[s + 1];
-                // many short probes (receiver-face coefficients, <= 64 weights): one per lane,
-                // 32 at a time; long ones (node receivers over the whole state) warp-cooperatively
-                const bool lanes = pb - pa >= 8;
-                if (lanes)
-                    for (int q0 = pa; q0 < pb; q0 += 32) {
-                        const int q = q0 + lane;
-                        if (q < pb) {
-                            const int pid = p.prb_ids[q];
-                            const int lo = p.prb_rng[2 * pid], cnt = p.prb_rng[2 * pid + 1];
-                            if (cnt <= 64) {
-                                const float* wv = p.prb_w + p.prb_woff[pid];
-                                double val = 0.0;
-                                for (int i = lo; i < lo + cnt; ++i) val = fma((double)wv[i], (double)U[i], val);
-                                p.rows[row * p.n_probe + pid] = val;
-                            }
+                // short probes (receiver-face coefficients, <= 64 weights): one per lane, 32 at a
+                // time, a sequential sum; long ones (node receivers over the whole state) warp-
+                // cooperatively.  The path depends on the probe's own length only, so a probe's value
+                // does not depend on which other probes share its subdomain.
+                for (int q0 = pa; q0 < pb; q0 += 32) {
+                    const int q = q0 + lane;
+                    if (q < pb) {
+                        const int pid = p.prb_ids[q];
+                        const int lo = p.prb_rng[2 * pid], cnt = p.prb_rng[2 * pid + 1];
+                        if (cnt <= 64) {
+                            const float* wv = p.prb_w + p.prb_woff[pid];
+                            double val = 0.0;
+                            for (int i = lo; i < lo + cnt; ++i) val = fma((double)wv[i], (double)U[i], val);
+                            p.rows[row * p.n_probe + pid] = val;
                         }
                     }
+                }
                 for (int pq = pa; pq < pb; ++pq) {
-                    if (lanes && p.prb_rng[2 * p.prb_ids[pq] + 1] <= 64) continue;
+                    if (p.prb_rng[2 * p.prb_ids[pq] + 1] <= 64) continue;
                     const int pid = p.prb_ids[pq];
                     const int lo = p.prb_rng[2 * pid], cnt = p.prb_rng[2 * pid + 1];
                     const float* wv = p.prb_w + p.prb_woff[pid];
@@ -887,17 +887,35 @@ extern "C" int sfw_wform_init(sfw_stepper* h, const double* u0, const double* v0
     return 0;
 }
 
-// n_steps fp32 W-form leapfrog steps (one launch).  Same table conventions as sfw_step_run;
-// norms are |W| (the W-form invariant scale), rows are the physical probe values.
+// |W| per step from the per-warp partials, summed in ascending partial order (one thread per step)
+__global__ void k_wnorms(const double* __restrict__ part, int n_steps, long long nwg, double* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_steps) return;
+    double t = 0.0;
+    for (long long c = 0; c < nwg; ++c) t += part[(size_t)k * nwg + c];
+    out[k] = sqrt(t);
+}
+
+// n_steps fp32 W-form leapfrog steps.  Same table conventions as sfw_step_run; norms are |W| (the
+// W-form invariant scale), rows are the physical probe values.  With limits (HOST [n_steps]) the
+// growth detector runs in the library's norm path: the run is launched in chunks of <= 512 steps,
+// each chunk's |W| is reduced on the device and checked while the next chunk computes, and no
+// further chunk is launched once a step exceeds its limit (SFW_EINSTABLE, *bad_step = first
+// failing step, 1-based); the state then has advanced at most one chunk past it.
 extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, const double* profile,
-                             double* rows_out, double* norms_out, float* kernel_ms, char* errbuf, int errlen) {
+                             const double* limits, double* rows_out, double* norms_out, int* bad_step,
+                             float* kernel_ms, char* errbuf, int errlen) {
     struct WScope { WScope() { ++sfw::g_wform_scope; } ~WScope() { --sfw::g_wform_scope; } } wscope_;
     WState* ws = g_wf.count(h) ? g_wf[h] : nullptr;
+    if (bad_step) *bad_step = 0;
     if (!ws) return fail(SFW_ECONFIG, "call sfw_wform_setup first", errbuf, errlen);
     if (n_steps <= 0) return 0;
+    if (record_every < 1) return fail(SFW_ECONFIG, "record_every must be >= 1", errbuf, errlen);
+    if (h->n_src && !profile)
+        return fail(SFW_ECONFIG, "a stepper with sources needs the f(t_k) profile table", errbuf, errlen);
     int rc = wf_ensure(&ws->ftab, &ws->ftab_cap, std::max(1LL, (long long)h->n_src * n_steps), errbuf, errlen);
     if (rc) return rc;
-    if (h->n_src && profile) {
+    if (h->n_src) {
         std::vector<float> f(profile, profile + (size_t)h->n_src * n_steps);
         sfw_h2d(ws->ftab, f.data(), f.size() * 4);
     }
@@ -909,18 +927,46 @@ extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, cons
         h->rows_cap = std::max(1LL, nrec * h->n_probe);
     }
     const long long nwg = (long long)h->grid * ws->nw;
-    if (ws->norm_cap < (long long)n_steps * nwg) {
+    if (ws->norm_cap < (long long)n_steps * nwg + n_steps) {
         if (ws->norm) cudaFree(ws->norm);
         ws->norm = nullptr;
-        if ((rc = dalloc(&ws->norm, (size_t)n_steps * nwg, errbuf, errlen))) return rc;
-        ws->norm_cap = (long long)n_steps * nwg;
+        if ((rc = dalloc(&ws->norm, (size_t)n_steps * nwg + n_steps, errbuf, errlen))) return rc;
+        ws->norm_cap = (long long)n_steps * nwg + n_steps;
     }
-    // large probe-row downloads overlap later chunks of the run (chunk_plan, as sfw_step_run)
-    const std::vector<long long> plan = chunk_plan(nrec, nrec * h->n_probe * 8, rows_out != nullptr);
+    double* dnorm = ws->norm + (size_t)n_steps * nwg;  // reduced |W| per step
+    // large probe-row downloads overlap later chunks of the run (chunk_plan, as sfw_step_run);
+    // with a growth limit, chunks are also capped at 512 steps (whole record intervals)
+    std::vector<long long> plan = chunk_plan(nrec, nrec * h->n_probe * 8, rows_out != nullptr);
+    if (limits && nrec > 0) {
+        const long long cap = std::max(1LL, 512LL / record_every);
+        std::vector<long long> fine{0};
+        for (size_t c = 1; c < plan.size(); ++c)
+            for (long long v = fine.back() + cap; ; v += cap) {
+                if (v >= plan[c]) {
+                    fine.push_back(plan[c]);
+                    break;
+                }
+                fine.push_back(v);
+            }
+        plan.swap(fine);
+    }
     const int n_chunks = (int)plan.size() - 1;
     if (n_chunks > 1 && !h->dstream) SFW_CUDA_TRY(cudaStreamCreateWithFlags(&h->dstream, cudaStreamNonBlocking));
-    if (n_chunks > 1) SFW_CUDA_TRY(ensure_row_staging(h, plan, h->n_probe));
+    if (n_chunks > 1 && rows_out) SFW_CUDA_TRY(ensure_row_staging(h, plan, h->n_probe));
     std::vector<cudaEvent_t> evs;
+    std::vector<int> bounds;  // first step of each launched chunk, then n_steps
+    std::vector<double> nrm(n_steps);
+    int bad = 0, checked = 0;  // steps [0, checked) verified against limits
+    auto check_upto = [&](int upto) -> cudaError_t {  // host copy + check of steps [checked, upto)
+        if (upto <= checked) return cudaSuccess;
+        cudaError_t e = cudaMemcpy(nrm.data() + checked, dnorm + checked, (size_t)(upto - checked) * 8,
+                                   cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return e;
+        for (int k = checked; k < upto && !bad; ++k)
+            if (!(nrm[k] <= limits[k])) bad = k + 1;  // NaN counts as divergence
+        checked = upto;
+        return cudaSuccess;
+    };
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
     for (int c = 0; c < n_chunks; ++c) {
         const long long r0 = plan[c], r1 = plan[c + 1];
@@ -928,33 +974,42 @@ extern "C" int sfw_wform_run(sfw_stepper* h, int n_steps, int record_every, cons
         const int s1 = (c == n_chunks - 1) ? n_steps : (int)(r1 * record_every);
         if ((rc = wf_launch(h, ws, 0, s1 - s0, record_every, n_steps, errbuf, errlen, s0))) return rc;
         ws->cur ^= ((s1 - s0) & 1);
-        if (n_chunks > 1) {
-            cudaEvent_t e;
-            SFW_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            SFW_CUDA_TRY(cudaEventRecord(e, h->stream));
-            evs.push_back(e);
+        k_wnorms<<<(s1 - s0 + 127) / 128, 128, 0, h->stream>>>(ws->norm + (size_t)s0 * nwg, s1 - s0, nwg, dnorm + s0);
+        bounds.push_back(s0);
+        cudaEvent_t e;
+        SFW_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        SFW_CUDA_TRY(cudaEventRecord(e, h->stream));
+        evs.push_back(e);
+        if (limits && c >= 1) {  // check the previous chunk while this one computes
+            SFW_CUDA_TRY(cudaEventSynchronize(evs[c - 1]));
+            SFW_CUDA_TRY(check_upto(s0));
+            if (bad) break;
         }
     }
+    bounds.push_back(n_steps);
     SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
-    std::vector<double> part((size_t)n_steps * nwg);
-    if (n_chunks > 1) {  // rows first: the pageable norm copy below blocks until the run ends
-        SFW_CUDA_TRY(download_rows_overlapped(h, plan, evs, h->rows, rows_out, h->n_probe));
-        for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    const int launched = (int)evs.size();
+    if (launched > 1 && rows_out) {  // rows of the launched chunks (the pageable norm copy blocks)
+        std::vector<long long> lplan(plan.begin(), plan.begin() + launched + 1);
+        SFW_CUDA_TRY(download_rows_overlapped(h, lplan, evs, h->rows, rows_out, h->n_probe));
     }
-    if (norms_out)
-        SFW_CUDA_TRY(cudaMemcpyAsync(part.data(), ws->norm, part.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-    if (n_chunks == 1 && rows_out && nrec * h->n_probe > 0) {
-        SFW_CUDA_TRY(cudaMemcpyAsync(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost, h->stream));
-    }
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
     SFW_CUDA_TRY(cudaGetLastError());
+    const int done = (launched == n_chunks) ? n_steps : bounds[launched];
+    if (launched == 1 && rows_out && nrec * h->n_probe > 0)
+        SFW_CUDA_TRY(cudaMemcpy(rows_out, h->rows, (size_t)nrec * h->n_probe * 8, cudaMemcpyDeviceToHost));
+    if (limits && !bad) SFW_CUDA_TRY(check_upto(done));
+    if (!limits || checked < done)
+        SFW_CUDA_TRY(cudaMemcpy(nrm.data(), dnorm, (size_t)done * 8, cudaMemcpyDeviceToHost));
     if (kernel_ms) cudaEventElapsedTime(kernel_ms, h->ev0, h->ev1);
-    if (norms_out)
-        for (int k = 0; k < n_steps; ++k) {
-            double t = 0.0;
-            for (long long c = 0; c < nwg; ++c) t += part[(size_t)k * nwg + c];
-            norms_out[k] = std::sqrt(t);
-        }
+    if (norms_out) std::memcpy(norms_out, nrm.data(), (size_t)done * 8);
+    if (bad) {
+        if (bad_step) *bad_step = bad;
+        char msg[256];
+        snprintf(msg, sizeof msg, "coupled stepping diverged: |W| = %.3e exceeds %.3e", nrm[bad - 1], limits[bad - 1]);
+        return fail(SFW_EINSTABLE, msg, errbuf, errlen);
+    }
     return 0;
 }
 

@@ -448,19 +448,15 @@ class CoupledStepper:
         bad = C.c_int(0)
         eb = _lib.errbuf()
         if self.precision == "fp32":
-            # W-form: |W| against the same detector rule with W-form source norms
+            # W-form: |W| against the same detector rule with W-form source norms, checked by the
+            # library chunk by chunk (it stops launching at the first failing step)
             limits, base = self._limits(prof, self._src_norms_w, n_steps)
             if not check:
                 limits = None
             ms = C.c_float(0.0)
-            rc = self._lib.sfw_wform_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(rows),
-                                         _lib.dptr(norms), C.byref(ms), eb, 1024)
+            rc = self._lib.sfw_wform_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(limits),
+                                         _lib.dptr(rows), _lib.dptr(norms), C.byref(bad), C.byref(ms), eb, 1024)
             self.last_kernel_ms = ms.value
-            if rc == 0 and limits is not None:
-                over = np.nonzero(~(norms <= limits))[0]
-                if over.size:
-                    rc = _lib.SFW_EINSTABLE
-                    bad.value = int(over[0]) + 1
         else:
             rc = self._lib.sfw_step_run(self._h, n_steps, record_every, _lib.dptr(prof), _lib.dptr(limits),
                                         _lib.dptr(rows), _lib.dptr(norms), C.byref(bad), eb, 1024)

@@ -119,3 +119,26 @@ def test_no_reads_of_unwritten_device_memory(monkeypatch):
     for prec in ("fp64", "fp32"):
         assert np.isfinite(out[("a", prec)]).all()
         assert np.array_equal(out[("a", prec)], out[("", prec)])
+
+
+def test_fp32_growth_detector_stops_early():
+    """An unstable dt (3x the CFL limit): the library checks |W| chunk by chunk and stops launching
+    at the first failing step; run() then replays to that step, so steps_done / u_curr are the
+    state at the raise, as the reference's detector leaves them (stepper.py:379-389)."""
+    from paper_1406_6923_b200 import InstabilityError
+    g = load_golden("golden_c1.npz")
+    wl = make_workload(1)
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    models = models_from_arrays(part, wl.c_field, 4, g["gammas"], g["hats"], g["scales"], shift=wl.shift)
+    src_alpha = tuple(int(x) for x in g["src_alpha"])
+    src = SourceTerm(src_alpha, g["src_vec"], so.ricker(wl.f0, wl.delay))
+    dt = 3.0 * 2.0 / math.sqrt(float(g["lam"]))
+    with CoupledStepper(models, dt, sources=(src,), precision="fp32") as st:
+        with pytest.raises(InstabilityError):
+            st.run(20000)
+        k = st.steps_done
+        assert 0 < k < 20000
+        uk = st.u_curr
+        st.run(k - 1)  # one step before the failing one: no raise
+        assert st.steps_done == k - 1
+    assert all(np.all(np.isfinite(v)) for v in uk.values())
