@@ -242,6 +242,9 @@ int sfw_step_masses(sfw_stepper* h, int* n_iface, double* out, char* errbuf, int
 
 /* Copy the current/previous state (HOST concat of L_s*w per subdomain). */
 int sfw_step_get_state(sfw_stepper* h, double* u_curr, double* u_prev);
+/* Overwrite the current / previous state (HOST concat of L_s*w per subdomain; NULL keeps that
+ * level): assignment to the reference's u_curr / u_prev dicts (stepper.py:164-165). */
+int sfw_step_set_state(sfw_stepper* h, const double* u_curr, const double* u_prev, char* errbuf, int errlen);
 
 /* Discrete energy (stepper.py:419-449), computed on the device. */
 int sfw_step_energy(sfw_stepper* h, double* energy, char* errbuf, int errlen);

@@ -69,6 +69,7 @@ SIGNATURES = {
     "sfw_step_power": (C.c_int, [C.c_void_p, PD, C.c_double, C.c_int, PD, PI, PI, C.c_char_p, C.c_int]),
     "sfw_step_masses": (C.c_int, [C.c_void_p, PI, PD, C.c_char_p, C.c_int]),
     "sfw_step_get_state": (C.c_int, [C.c_void_p, PD, PD]),
+    "sfw_step_set_state": (C.c_int, [C.c_void_p, PD, PD, C.c_char_p, C.c_int]),
     "sfw_step_energy": (C.c_int, [C.c_void_p, PD, C.c_char_p, C.c_int]),
     "sfw_step_traffic": (C.c_int, [C.c_void_p, PD, PD, PD]),
     "sfw_pulse_table": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_longlong, C.c_double, C.c_int, PD]),

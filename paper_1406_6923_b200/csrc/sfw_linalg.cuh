@@ -31,9 +31,12 @@ __device__ __forceinline__ void dmma8x8x4(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+#ifndef SFW_DGEMM_PAD
+#define SFW_DGEMM_PAD 4
+#endif
 template <bool TA>
 __global__ void __launch_bounds__(128) k_dgemm(const GemmArgs g) {
-    constexpr int BM = 64, BN = 64, BK = 16, PAD = 8;
+    constexpr int BM = 64, BN = 64, BK = 16, PAD = SFW_DGEMM_PAD;  // row stride = 4 mod 16 doubles: conflict-free fragments
     __shared__ __align__(16) double As[2][BK][BM + PAD];
     __shared__ __align__(16) double Bs[2][BK][BN + PAD];
     const int b = blockIdx.z;

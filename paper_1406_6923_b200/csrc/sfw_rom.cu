@@ -371,6 +371,285 @@ __global__ void __launch_bounds__(512, 1) k_pcg(const PcgArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_pcg2: the same preconditioned CG as k_pcg, two right-hand sides of one subdomain per CTA
+// (P = 17 only).  The two solves share c, the eigenbases and every barrier: the line passes deal
+// 2 x 289 lines over 12 warps (75% of the threads busy instead of 56%), the block reductions carry
+// both dot products through one barrier (ping-pong scratch, 1 barrier instead of 3), and r and 1/c
+// live in registers (13 nodes per thread), so p and z of both solves fit the 227 KB of shared
+// memory.  A solve that has converged stops updating (its lines are skipped) while the other runs.
+constexpr int PCG2_T = 384;
+constexpr int PCG2_NPT = (17 * 17 * 17 + PCG2_T - 1) / PCG2_T;  // nodes per thread
+
+__device__ __forceinline__ void block_sum2(double& v0, double& v1, double* red) {
+    // fixed-order: warp butterfly, then every thread sums the warp partials in warp order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) {
+        red[2 * warp] = v0;
+        red[2 * warp + 1] = v1;
+    }
+    __syncthreads();
+    double t0 = red[0], t1 = red[1];
+    for (int i = 1; i < nw; ++i) {
+        t0 += red[2 * i];
+        t1 += red[2 * i + 1];
+    }
+    v0 = t0;
+    v1 = t1;
+}
+
+__device__ __forceinline__ void line_pass2(double* z0, double* z1, const double* Q, int nlines, int stride,
+                                           int lstride_a, int lstride_b, int nb_inner, bool act0, bool act1) {
+    constexpr int PN = 17, QS = 18;
+    for (int l = threadIdx.x; l < 2 * nlines; l += blockDim.x) {
+        const int j = l >= nlines;
+        if (j ? !act1 : !act0) continue;
+        const int ll = j ? l - nlines : l;
+        double* z = j ? z1 : z0;
+        const int base = (ll / nb_inner) * lstride_a + (ll % nb_inner) * lstride_b;
+        double v[PN], y[PN];
+#pragma unroll
+        for (int i = 0; i < PN; ++i) v[i] = z[base + i * stride];
+#pragma unroll
+        for (int k = 0; k < PN; ++k) y[k] = 0.0;
+#pragma unroll
+        for (int i = 0; i < PN; ++i) {
+            const double* qr = Q + i * QS;
+#pragma unroll
+            for (int k = 0; k + 1 < PN; k += 2) {
+                const double2 q = *reinterpret_cast<const double2*>(qr + k);
+                y[k] = fma(q.x, v[i], y[k]);
+                y[k + 1] = fma(q.y, v[i], y[k + 1]);
+            }
+            y[PN - 1] = fma(qr[PN - 1], v[i], y[PN - 1]);
+        }
+#pragma unroll
+        for (int k = 0; k < PN; ++k) z[base + k * stride] = y[k];
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(PCG2_T, 1) k_pcg2(const PcgArgs a) {
+    extern __shared__ __align__(16) double sh[];
+    constexpr int PT = 17, QS = 18, QT = PT * QS, N = PT * PT * PT;
+    constexpr int px = PT, py = PT, pz = PT;
+    double* c = sh;
+    double* p0 = c + N;
+    double* p1 = p0 + N;
+    double* z0 = p1 + N;
+    double* z1 = z0 + N;
+    double* Q = sh + ((5 * N + 1) & ~1);  // [3 axes][fwd, bwd][PT][QS]
+    double* lam = Q + 6 * QT;
+    double* dd = lam + 3 * PMAX;
+    double* ee = dd + 3 * PMAX;
+    double* red = ee + 3 * PMAX;  // 2 x 2 x 32 (ping-pong)
+    const int ncp = (a.ncols + 1) / 2;
+    const int b = blockIdx.x / ncp, j0 = 2 * (blockIdx.x % ncp);
+    const bool two = j0 + 1 < a.ncols;
+    const int mask = a.mask[b];
+    for (int ax = 0; ax < 3; ++ax) {
+        const int pat = ((mask >> (2 * ax)) & 1) | (((mask >> (2 * ax + 1)) & 1) << 1);
+        const double* Qg = a.Qt + (size_t)(ax * 4 + pat) * PMAX * PMAX;
+        for (int idx = threadIdx.x; idx < PT * PT; idx += blockDim.x) {
+            const int i = idx / PT, k = idx % PT;
+            Q[(2 * ax) * QT + i * QS + k] = Qg[idx];
+            Q[(2 * ax + 1) * QT + k * QS + i] = Qg[idx];
+        }
+        for (int i = threadIdx.x; i < PT; i += blockDim.x) {
+            lam[ax * PMAX + i] = a.lamt[(ax * 4 + pat) * PMAX + i];
+            dd[ax * PMAX + i] = a.dt[(ax * 4 + pat) * PMAX + i];
+            ee[ax * PMAX + i] = a.et[(ax * 4 + pat) * PMAX + i];
+        }
+    }
+    const double* cg = a.c + (size_t)b * N;
+    const double* bg0 = a.rhs + (size_t)b * a.sR + (size_t)j0 * a.ldn;
+    const double* bg1 = bg0 + a.ldn;
+    double* og0 = a.out + (size_t)b * a.sO + (size_t)j0 * a.ldn;  // accumulates -x
+    double* og1 = og0 + a.ldn;
+    double r0[PCG2_NPT], r1[PCG2_NPT], ic[PCG2_NPT];
+    double cmin = 1e308, cmax = 0.0, bb0 = 0.0, bb1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < PCG2_NPT; ++t) {
+        const int i = threadIdx.x + t * PCG2_T;
+        r0[t] = r1[t] = ic[t] = 0.0;
+        if (i < N) {
+            const double ci = cg[i];
+            c[i] = ci;
+            ic[t] = 1.0 / ci;
+            cmin = fmin(cmin, ci);
+            cmax = fmax(cmax, ci);
+            r0[t] = bg0[i];
+            og0[i] = 0.0;
+            bb0 = fma(r0[t], r0[t], bb0);
+            if (two) {
+                r1[t] = bg1[i];
+                og1[i] = 0.0;
+                bb1 = fma(r1[t], r1[t], bb1);
+            }
+        }
+    }
+    cmax = block_max(cmax, red);
+    cmin = -block_max(-cmin, red);
+    int rb = 0;  // ping-pong reduction buffer
+    block_sum2(bb0, bb1, red + 64 * rb);
+    rb ^= 1;
+    const double sigma = a.shift / (cmin * cmax);
+    const double s = a.shift;
+    constexpr int sy = pz, sx = py * pz;
+    bool act0 = true, act1 = two;
+
+    auto precond = [&]() {  // z_j = P^-1 r_j for the active solves
+#pragma unroll
+        for (int t = 0; t < PCG2_NPT; ++t) {
+            const int i = threadIdx.x + t * PCG2_T;
+            if (i < N) {
+                if (act0) z0[i] = r0[t] * ic[t];
+                if (act1) z1[i] = r1[t] * ic[t];
+            }
+        }
+        __syncthreads();
+        line_pass2(z0, z1, Q + 0 * QT, py * pz, sx, 1, 1, py * pz, act0, act1);
+        line_pass2(z0, z1, Q + 2 * QT, px * pz, sy, sx, 1, pz, act0, act1);
+        line_pass2(z0, z1, Q + 4 * QT, px * py, 1, pz, 0, 1, act0, act1);
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            const int ix = i / sx, iy = (i / sy) % py, iz = i % pz;
+            const double d = __drcp_rn(((lam[ix] + lam[PMAX + iy]) + lam[2 * PMAX + iz]) + sigma);
+            if (act0) z0[i] = z0[i] * d;
+            if (act1) z1[i] = z1[i] * d;
+        }
+        __syncthreads();
+        line_pass2(z0, z1, Q + 5 * QT, px * py, 1, pz, 0, 1, act0, act1);
+        line_pass2(z0, z1, Q + 3 * QT, px * pz, sy, sx, 1, pz, act0, act1);
+        line_pass2(z0, z1, Q + 1 * QT, py * pz, sx, 1, 1, py * pz, act0, act1);
+#pragma unroll
+        for (int t = 0; t < PCG2_NPT; ++t) {
+            const int i = threadIdx.x + t * PCG2_T;
+            if (i < N) {
+                if (act0) z0[i] = z0[i] * ic[t];
+                if (act1) z1[i] = z1[i] * ic[t];
+            }
+        }
+        __syncthreads();
+    };
+
+    precond();
+    double rho0 = 0.0, rho1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < PCG2_NPT; ++t) {
+        const int i = threadIdx.x + t * PCG2_T;
+        if (i < N) {
+            p0[i] = z0[i];
+            rho0 = fma(r0[t], z0[i], rho0);
+            if (two) {
+                p1[i] = z1[i];
+                rho1 = fma(r1[t], z1[i], rho1);
+            }
+        }
+    }
+    block_sum2(rho0, rho1, red + 64 * rb);
+    rb ^= 1;
+    int st0 = -1, st1 = two ? -1 : 0;
+    const double tol0 = a.tol * a.tol * bb0, tol1 = a.tol * a.tol * bb1;
+    if (bb0 == 0.0) st0 = 0;
+    if (bb1 == 0.0) st1 = 0;
+    act0 = st0 < 0;
+    act1 = st1 < 0;
+    for (int it = 0; (act0 || act1) && it < a.maxit; ++it) {
+        // q = M p = c .* S (c .* p) + s p  -> stored in z
+        double pq0 = 0.0, pq1 = 0.0;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            const int ix = i / sx, iy = (i / sy) % py, iz = i % pz;
+            const double dsum = dd[ix] + dd[PMAX + iy] + dd[2 * PMAX + iz];
+            const double ci = c[i];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (j ? !act1 : !act0) continue;
+                const double* p = j ? p1 : p0;
+                const double ui = ci * p[i];
+                double su = dsum * ui;
+                if (ix + 1 < px) su = fma(ee[ix], c[i + sx] * p[i + sx], su);
+                if (ix > 0) su = fma(ee[ix - 1], c[i - sx] * p[i - sx], su);
+                if (iy + 1 < py) su = fma(ee[PMAX + iy], c[i + sy] * p[i + sy], su);
+                if (iy > 0) su = fma(ee[PMAX + iy - 1], c[i - sy] * p[i - sy], su);
+                if (iz + 1 < pz) su = fma(ee[2 * PMAX + iz], c[i + 1] * p[i + 1], su);
+                if (iz > 0) su = fma(ee[2 * PMAX + iz - 1], c[i - 1] * p[i - 1], su);
+                const double q = fma(ci, su, s * p[i]);
+                if (j) {
+                    z1[i] = q;
+                    pq1 = fma(p[i], q, pq1);
+                } else {
+                    z0[i] = q;
+                    pq0 = fma(p[i], q, pq0);
+                }
+            }
+        }
+        block_sum2(pq0, pq1, red + 64 * rb);
+        rb ^= 1;
+        if (act0 && !(pq0 > 0.0)) st0 = -2;  // not positive definite: shift too small
+        if (act1 && !(pq1 > 0.0)) st1 = -2;
+        if (st0 == -2 || st1 == -2) break;
+        const double al0 = act0 ? rho0 / pq0 : 0.0, al1 = act1 ? rho1 / pq1 : 0.0;
+        double rr0 = 0.0, rr1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < PCG2_NPT; ++t) {
+            const int i = threadIdx.x + t * PCG2_T;
+            if (i < N) {
+                if (act0) {
+                    og0[i] = fma(-al0, p0[i], og0[i]);
+                    r0[t] = fma(-al0, z0[i], r0[t]);
+                    rr0 = fma(r0[t], r0[t], rr0);
+                }
+                if (act1) {
+                    og1[i] = fma(-al1, p1[i], og1[i]);
+                    r1[t] = fma(-al1, z1[i], r1[t]);
+                    rr1 = fma(r1[t], r1[t], rr1);
+                }
+            }
+        }
+        block_sum2(rr0, rr1, red + 64 * rb);
+        rb ^= 1;
+        if (act0 && rr0 <= tol0) st0 = it + 1;
+        if (act1 && rr1 <= tol1) st1 = it + 1;
+        act0 = st0 < 0;
+        act1 = st1 < 0;
+        if (!act0 && !act1) break;
+        __syncthreads();  // z (q) reads above are done before the preconditioner overwrites z
+        precond();
+        double rz0 = 0.0, rz1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < PCG2_NPT; ++t) {
+            const int i = threadIdx.x + t * PCG2_T;
+            if (i < N) {
+                if (act0) rz0 = fma(r0[t], z0[i], rz0);
+                if (act1) rz1 = fma(r1[t], z1[i], rz1);
+            }
+        }
+        block_sum2(rz0, rz1, red + 64 * rb);
+        rb ^= 1;
+        const double be0 = act0 ? rz0 / rho0 : 0.0, be1 = act1 ? rz1 / rho1 : 0.0;
+        if (act0) rho0 = rz0;
+        if (act1) rho1 = rz1;
+#pragma unroll
+        for (int t = 0; t < PCG2_NPT; ++t) {
+            const int i = threadIdx.x + t * PCG2_T;
+            if (i < N) {
+                if (act0) p0[i] = fma(be0, p0[i], z0[i]);
+                if (act1) p1[i] = fma(be1, p1[i], z1[i]);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.iters[(size_t)b * a.ncols + j0] = st0;
+        if (two) a.iters[(size_t)b * a.ncols + j0 + 1] = st1;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Y[:, col] = A V[:, col] = -c .* S (c .* v)     (the grid.py operator as a stencil)
 __global__ void k_stencil(int px, int py, int pz, int N, int ncols, const double* __restrict__ c,
                           const int* __restrict__ mask, const double* __restrict__ dt, const double* __restrict__ et,
@@ -858,6 +1137,10 @@ extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf
     pa.et = det;
     pa.iters = it;
     const void* pcg_fn = p17 ? (const void*)k_pcg<17> : (const void*)k_pcg<0>;
+    // P = 17: two right-hand sides per CTA (k_pcg2); SFW_PCG1 selects the one-RHS kernel
+    const bool pcg2 = p17 && !getenv("SFW_PCG1");
+    const size_t pcg2_smem = (size_t)(((5 * 4913 + 1) & ~1) + 6 * 17 * 18 + 9 * PMAX + 128) * 8;
+    if (pcg2) cudaFuncSetAttribute(k_pcg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg2_smem);
     cudaFuncSetAttribute(pcg_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem);
     const size_t cq_smem = 2 * ww * 8;
     cudaFuncSetAttribute(k_cholqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cq_smem);
@@ -882,7 +1165,9 @@ extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf
             pa.sR = (long long)K * ldn;
             pa.out = X;
             pa.sO = (long long)w * ldn;
-            if (p17)
+            if (pcg2)
+                k_pcg2<<<nb * ((w + 1) / 2), PCG2_T, pcg2_smem, st>>>(pa);
+            else if (p17)
                 k_pcg<17><<<nb * w, 512, pcg_smem, st>>>(pa);
             else
                 k_pcg<0><<<nb * w, 512, pcg_smem, st>>>(pa);

@@ -3027,6 +3027,16 @@ extern "C" int sfw_step_masses(sfw_stepper* h, int* n_iface, double* out, char* 
     return 0;
 }
 
+extern "C" int sfw_step_set_state(sfw_stepper* h, const double* u_curr, const double* u_prev, char* errbuf,
+                                  int errlen) {
+    // overwrite the current / previous time level (HOST concat; NULL keeps a level): the attribute
+    // assignment of stepper.py:164-165 (u_curr / u_prev are plain mutable dicts in the reference)
+    SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (u_curr) SFW_CUDA_TRY(sfw_h2d(h->U[h->cur], u_curr, h->state_len * 8));
+    if (u_prev) SFW_CUDA_TRY(sfw_h2d(h->U[h->cur ^ 1], u_prev, h->state_len * 8));
+    return 0;
+}
+
 extern "C" int sfw_step_get_state(sfw_stepper* h, double* u_curr, double* u_prev) {
     char* errbuf = nullptr;
     int errlen = 0;

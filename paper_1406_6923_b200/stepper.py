@@ -123,6 +123,19 @@ def make_probe(model: SubdomainModel, local_row: int) -> Probe:
     return Probe(alpha=model.alpha, weights=out)
 
 
+class _StateView(dict):
+    """dict of a stepper's time level whose item assignment writes through to the device."""
+
+    def __init__(self, stepper, level, data):
+        super().__init__(data)
+        self._stepper = stepper
+        self._level = level
+
+    def __setitem__(self, alpha, value):
+        super().__setitem__(alpha, np.asarray(value, dtype=float).copy())
+        self._stepper._set_level(self._level, {alpha: value})
+
+
 class CoupledStepper:
     """Leapfrog integrator for a set of coupled subdomain models (stepper.py:144-449).
 
@@ -354,15 +367,44 @@ class CoupledStepper:
 
     @property
     def u_curr(self) -> dict:
+        """Current state per subdomain (stepper.py:164).  A copy of the device state; item or
+        attribute assignment writes back (the reference's dict is mutable)."""
         if not self._initialized:
             return {}
-        return self._split(self._state()[0])
+        return _StateView(self, 0, self._split(self._state()[0]))
+
+    @u_curr.setter
+    def u_curr(self, states: dict):
+        self._set_level(0, states)
 
     @property
     def u_prev(self) -> dict:
         if not self._initialized:
             return {}
-        return self._split(self._state()[1])
+        return _StateView(self, 1, self._split(self._state()[1]))
+
+    @u_prev.setter
+    def u_prev(self, states: dict):
+        self._set_level(1, states)
+
+    def _set_level(self, level: int, states: dict):
+        """Overwrite time level 0 (u_curr) or 1 (u_prev) for the subdomains in ``states``."""
+        if self.precision != "fp64":
+            raise ConfigError("assigning the state is defined for the fp64 U-form stepper")
+        if not self._initialized:
+            raise ProtocolError("stepper not initialized")
+        flat = self._state()[level]
+        for a, v in states.items():
+            i = self.index[a]
+            v = np.asarray(v, dtype=float).reshape(-1)
+            if v.size != self._sizes[i]:
+                raise ConfigError(f"state for {a} has the wrong length")
+            flat[self._offs[i]:self._offs[i + 1]] = v
+        flat = _f64(flat)
+        eb = _lib.errbuf()
+        rc = self._lib.sfw_step_set_state(self._h, _lib.dptr(flat) if level == 0 else None,
+                                          _lib.dptr(flat) if level == 1 else None, eb, 1024)
+        _lib.check(rc, eb)
 
     # -- physics -----------------------------------------------------------------
 

@@ -72,3 +72,32 @@ def test_build_checks_an_explicit_operator_matrix():
     bad.data = bad.data * 1.001
     with pytest.raises(ConfigError):
         build_models([dataclasses.replace(op, matrix=bad)], wl.modes_per_face, wl.n, wl.shift)
+
+
+def test_state_assignment_writes_through():
+    """u_curr / u_prev are mutable in the reference (stepper.py:164-165): assigning them (or an item)
+    sets the device state, and stepping continues from it exactly."""
+    wl, part, ops = _c1()
+    models = build_models(ops, wl.modes_per_face, wl.n, wl.shift)
+    rng = np.random.default_rng(11)
+    u0 = {a: rng.standard_normal(m.state_size) * 1e-3 for a, m in models.items()}
+    for a, m in models.items():  # shared-face replicas agree
+        for f, b in m.neighbors.items():
+            if b > a:
+                u0[b][models[b].face_slice(f ^ 1)] = u0[a][m.face_slice(f)]
+    with CoupledStepper(models, 1e-4) as st, CoupledStepper(models, 1e-4) as st2:
+        st.initialize(u0)
+        for _ in range(7):
+            st.advance()
+        uc, up = st.u_curr, st.u_prev
+        st2.initialize()
+        st2.u_curr = dict(uc)
+        view = st2.u_prev
+        for a in up:
+            view[a] = up[a]  # item assignment writes through
+        for _ in range(5):
+            st.advance()
+            st2.advance()
+        a_state, b_state = st.u_curr, st2.u_curr
+    for a in a_state:
+        assert np.array_equal(a_state[a], b_state[a])
