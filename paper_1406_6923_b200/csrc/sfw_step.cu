@@ -2273,7 +2273,7 @@ static void free_all(sfw_stepper* h) {
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
                     h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta, h->tcoef, h->UM[0], h->UM[1],
                     h->mfb, h->macc1, h->mnorm, h->mrows, h->shot_vec, h->shot_sub, h->shot_voff,
-                    h->shot_ftab, h->mbox, h->mmass, h->ucoef, h->swimg};
+                    h->shot_ftab, h->mbox, h->mmass, h->ucoef, h->swimg, h->src_subs};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -2620,6 +2620,10 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
             for (int i = 0; i < d->n_src; ++i) src_ids[fill[d->src_sub[i]]++] = i;
         }
         std::vector<double> sv(d->n_src ? d->src_vec : nullptr, d->n_src ? d->src_vec + vtot : nullptr);
+        h->src_subs_h.clear();
+        for (int s = 0; s < n; ++s)
+            if (src_ptr[s + 1] > src_ptr[s]) h->src_subs_h.push_back(s);
+        if (!h->src_subs_h.empty()) TRY(upload(&h->src_subs, h->src_subs_h, errbuf, errlen));
         TRY(upload(&h->src_ptr, src_ptr, errbuf, errlen));
         TRY(upload(&h->src_ids, src_ids, errbuf, errlen));
         TRY(upload(&h->src_voff, src_voff, errbuf, errlen));
@@ -2731,6 +2735,28 @@ error:
     free_all(h);
     delete h;
     return rc ? rc : SFW_ECUDA;
+}
+
+// Two-level start from rest (u0 = v0 = 0, stepper.py:347-353): acc(0) is a signed zero, so the
+// start leaves U_prev = (0 - dt*0) + ((0.5*dt)*dt) * (0 + sum_src vec f(0)) on source subdomains and
+// +0 elsewhere -- the mode-1 pass's arithmetic, without streaming every chain block once.
+__global__ void k_init_rest(const int* __restrict__ subs, const long long* __restrict__ soff,
+                            const int* __restrict__ src_ptr, const int* __restrict__ src_ids,
+                            const long long* __restrict__ src_voff, const double* __restrict__ src_vec,
+                            const double* __restrict__ ftab, double dt, double half, double* __restrict__ Uprev) {
+    const int s = subs[blockIdx.x];
+    const long long o = soff[s], len = soff[s + 1] - o;
+    const int a = src_ptr[s], b = src_ptr[s + 1];
+    for (long long idx = threadIdx.x; idx < len; idx += blockDim.x) {
+        double f = 0.0;
+        for (int q = a; q < b; ++q) {
+            const int src = src_ids[q];
+            const double term = __dmul_rn(src_vec[src_voff[src] + idx], ftab[src]);
+            f = (q == a) ? term : __dadd_rn(f, term);
+        }
+        const double tot = __dadd_rn(0.0, f);
+        Uprev[o + idx] = __dadd_rn(__dsub_rn(0.0, __dmul_rn(dt, 0.0)), __dmul_rn(half, tot));
+    }
 }
 
 static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, int ftab_stride,
@@ -2912,8 +2938,17 @@ extern "C" int sfw_step_init(sfw_stepper* h, const double* u0, const double* v0,
     if (rc) return rc;
     rc = ensure(h, &h->norm_part, &h->norm_cap, (long long)h->grid, errbuf, errlen);
     if (rc) return rc;
-    rc = launch_step(h, 1, 1, 1, 1, errbuf, errlen);
-    if (rc) return rc;
+    if (!u0 && !v0 && !getenv("SFW_INIT_FULL")) {  // from rest: no chain-block pass needed
+        SFW_CUDA_TRY(cudaMemsetAsync(h->U[1], 0, h->state_len * 8, h->stream));
+        if (!h->src_subs_h.empty())
+            k_init_rest<<<(unsigned)h->src_subs_h.size(), 128, 0, h->stream>>>(
+                h->src_subs, h->d_soff, h->src_ptr, h->src_ids, h->src_voff, h->src_vec, h->ftab, h->dt,
+                (0.5 * h->dt) * h->dt, h->U[1]);
+        if (h->n_probe) SFW_CUDA_TRY(cudaMemsetAsync(h->rows, 0, (size_t)h->n_probe * 8, h->stream));
+    } else {
+        rc = launch_step(h, 1, 1, 1, 1, errbuf, errlen);
+        if (rc) return rc;
+    }
     if (row0_out && h->n_probe)
         SFW_CUDA_TRY(cudaMemcpyAsync(row0_out, h->rows, h->n_probe * 8, cudaMemcpyDeviceToHost, h->stream));
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));

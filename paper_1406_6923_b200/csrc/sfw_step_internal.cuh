@@ -78,6 +78,8 @@ struct sfw_stepper {
     long long state_len = 0, n_blocks = 0;
     double dt = 0;
     std::vector<int> layers;
+    std::vector<int> src_subs_h;  // subdomains that carry a source (host copy, ascending)
+    int* src_subs = nullptr;      // same, on the device
     std::vector<long long> soff, src_len, prb_len;
     cudaStream_t stream = nullptr;
     cudaStream_t dstream = nullptr;  // probe-row downloads overlapped with later step chunks

@@ -90,7 +90,7 @@ def test_state_assignment_writes_through():
         for _ in range(7):
             st.advance()
         uc, up = st.u_curr, st.u_prev
-        st2.initialize()
+        st2.initialize(u0)  # same growth-detector baseline as st (stepper.py:357-360)
         st2.u_curr = dict(uc)
         view = st2.u_prev
         for a in up:

@@ -271,3 +271,25 @@ def test_chunked_run_equals_single_launch(record_every, env, monkeypatch):
     assert np.array_equal(ts, tc) and np.array_equal(rs, rc)
     for a in order:
         assert np.array_equal(us[a], uc[a])
+
+
+def test_start_from_rest_fast_path_is_bitwise(monkeypatch):
+    """From rest the start skips the acceleration pass (acc(0) = 0); traces and state equal the
+    full mode-1 start (SFW_INIT_FULL) bit for bit."""
+    g = load_golden("golden_c1.npz")
+    wl = make_workload(1)
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    models = models_from_arrays(part, wl.c_field, 4, g["gammas"], g["hats"], g["scales"], shift=wl.shift)
+    src_alpha = tuple(int(x) for x in g["src_alpha"])
+    src = SourceTerm(src_alpha, g["src_vec"], so.ricker(wl.f0, wl.delay))
+    probes = [Probe(a, w) for a, w in face_probes(models, wl)]
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("SFW_INIT_FULL", env)
+        with CoupledStepper(models, float(g["dt"]), sources=(src,)) as st:
+            _, rows = st.run(50, probes=probes)
+            out.append((rows, st.u_curr, st.u_prev))
+    assert np.array_equal(out[0][0], out[1][0])
+    for a in out[0][1]:
+        assert np.array_equal(out[0][1][a], out[1][1][a]) and np.array_equal(out[0][2][a], out[1][2][a])
