@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import logging
+import operator
 from dataclasses import dataclass
 from typing import Callable, Sequence
 
@@ -288,9 +289,11 @@ class CoupledStepper:
             self._wform_vectors()
 
     def _set_probes(self, probes: Sequence[Probe]):
-        key = tuple((p.alpha, id(p.weights)) for p in probes)
-        if key == self._probe_key:
+        # the same Probe objects as the last upload (identity, O(n) in C): nothing to do
+        prev = self._probe_key
+        if prev is not None and len(prev) == len(probes) and all(map(operator.is_, probes, prev)):
             return
+        key = tuple(probes)
         for p in probes:
             if p.alpha not in self.index:
                 raise ConfigError(f"probe subdomain {p.alpha} has no model")
