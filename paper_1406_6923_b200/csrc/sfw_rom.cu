@@ -295,20 +295,23 @@ __global__ void __launch_bounds__(512, 1) k_pcg(const PcgArgs a) {
     auto Qf = [&](int ax) { return PT > 0 ? Q + (2 * ax) * QT : Q + ax * QT; };
     auto Qb = [&](int ax) { return PT > 0 ? Q + (2 * ax + 1) * QT : Q + ax * QT; };
 
+    auto lpass = [&](const double* Qd, int n, int nl, int stride, int la, int lb, int nbi, bool fwd) {
+        line_pass<PT>(z, Qd, n, nl, stride, la, lb, nbi, fwd);
+    };
     auto precond = [&]() {  // z = P^-1 r
         for (int i = threadIdx.x; i < N; i += blockDim.x) z[i] = r[i] * ic[i];
         __syncthreads();
-        line_pass<PT>(z, Qf(0), px, py * pz, sx, 1, 1, py * pz, true);      // x lines: base = l
-        line_pass<PT>(z, Qf(1), py, px * pz, sy, sx, 1, pz, true);          // y lines
-        line_pass<PT>(z, Qf(2), pz, px * py, 1, pz, 0, 1, true);            // z lines: base = l*pz
+        lpass(Qf(0), px, py * pz, sx, 1, 1, py * pz, true);      // x lines: base = l
+        lpass(Qf(1), py, px * pz, sy, sx, 1, pz, true);          // y lines
+        lpass(Qf(2), pz, px * py, 1, pz, 0, 1, true);            // z lines: base = l*pz
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
             const int ix = i / sx, iy = (i / sy) % py, iz = i % pz;
             z[i] = z[i] * __drcp_rn(((lam[ix] + lam[PMAX + iy]) + lam[2 * PMAX + iz]) + sigma);
         }
         __syncthreads();
-        line_pass<PT>(z, Qb(2), pz, px * py, 1, pz, 0, 1, false);
-        line_pass<PT>(z, Qb(1), py, px * pz, sy, sx, 1, pz, false);
-        line_pass<PT>(z, Qb(0), px, py * pz, sx, 1, 1, py * pz, false);
+        lpass(Qb(2), pz, px * py, 1, pz, 0, 1, false);
+        lpass(Qb(1), py, px * pz, sy, sx, 1, pz, false);
+        lpass(Qb(0), px, py * pz, sx, 1, 1, py * pz, false);
         for (int i = threadIdx.x; i < N; i += blockDim.x) z[i] = z[i] * ic[i];
         __syncthreads();
     };
