@@ -436,6 +436,67 @@ __device__ __forceinline__ void line_pass2(double* z0, double* z1, const double*
     __syncthreads();
 }
 
+// The same line pass as one GEMM per 8-line tile on the DMMA pipe: Y (17 x 8 lines) = Qd^T V, with
+// Qd^T padded to 24 x 20 (3 row tiles x 5 k-steps of mma.m8n8k4.f64; its 15 A fragments live in
+// registers for the pass) and 37 tiles of 8 lines per solve, dealt over the CTA's warps.  Each tile's
+// lines are read into registers before its MMAs (warp-collective), then written back in place.
+__device__ __forceinline__ void line_pass2_dmma(double* z0, double* z1, const double* Q, int nlines, int stride,
+                                                int lstride_a, int lstride_b, int nb_inner, bool act0, bool act1) {
+    constexpr int PN = 17, QS = 18;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int q = lane & 3, r = lane >> 2;
+    double af[3][5];
+#pragma unroll
+    for (int I = 0; I < 3; ++I)
+#pragma unroll
+        for (int kap = 0; kap < 5; ++kap) {
+            const int kout = 8 * I + r, i = 4 * kap + q;
+            af[I][kap] = (kout < PN && i < PN) ? Q[i * QS + kout] : 0.0;  // A[kout][i] = Qd[i][kout]
+        }
+    const int ntile = (nlines + 7) / 8;
+    for (int t = warp; t < 2 * ntile; t += nw) {
+        const int j = t >= ntile;
+        if (j ? !act1 : !act0) continue;
+        double* z = j ? z1 : z0;
+        const int n0 = (t - j * ntile) * 8;
+        const int lb = n0 + r;  // this lane's B-fragment line
+        const int base_b = (lb / nb_inner) * lstride_a + (lb % nb_inner) * lstride_b;
+        double bf[5];
+#pragma unroll
+        for (int kap = 0; kap < 5; ++kap) {
+            const int i = 4 * kap + q;
+            bf[kap] = (lb < nlines && i < PN) ? z[base_b + i * stride] : 0.0;
+        }
+        double acc[3][2];
+#pragma unroll
+        for (int I = 0; I < 3; ++I) {
+            acc[I][0] = acc[I][1] = 0.0;
+#pragma unroll
+            for (int kap = 0; kap < 5; ++kap) dmma8x8x4(acc[I], af[I][kap], bf[kap]);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int lo = n0 + 2 * q + e;  // output line of acc[.][e]
+            if (lo >= nlines) continue;
+            const int base_o = (lo / nb_inner) * lstride_a + (lo % nb_inner) * lstride_b;
+#pragma unroll
+            for (int I = 0; I < 3; ++I) {
+                const int kout = 8 * I + r;
+                if (kout < PN) z[base_o + kout * stride] = acc[I][e];
+            }
+        }
+    }
+    __syncthreads();
+}
+
+#ifndef SFW_PCG_DMMA
+#define SFW_PCG_DMMA 1
+#endif
+#if SFW_PCG_DMMA
+#define LP2 line_pass2_dmma
+#else
+#define LP2 line_pass2
+#endif
 __global__ void __launch_bounds__(PCG2_T, 1) k_pcg2(const PcgArgs a) {
     extern __shared__ __align__(16) double sh[];
     constexpr int PT = 17, QS = 18, QT = PT * QS, N = PT * PT * PT;
@@ -515,9 +576,9 @@ __global__ void __launch_bounds__(PCG2_T, 1) k_pcg2(const PcgArgs a) {
             }
         }
         __syncthreads();
-        line_pass2(z0, z1, Q + 0 * QT, py * pz, sx, 1, 1, py * pz, act0, act1);
-        line_pass2(z0, z1, Q + 2 * QT, px * pz, sy, sx, 1, pz, act0, act1);
-        line_pass2(z0, z1, Q + 4 * QT, px * py, 1, pz, 0, 1, act0, act1);
+        LP2(z0, z1, Q + 0 * QT, py * pz, sx, 1, 1, py * pz, act0, act1);
+        LP2(z0, z1, Q + 2 * QT, px * pz, sy, sx, 1, pz, act0, act1);
+        LP2(z0, z1, Q + 4 * QT, px * py, 1, pz, 0, 1, act0, act1);
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
             const int ix = i / sx, iy = (i / sy) % py, iz = i % pz;
             const double d = __drcp_rn(((lam[ix] + lam[PMAX + iy]) + lam[2 * PMAX + iz]) + sigma);
@@ -525,9 +586,9 @@ __global__ void __launch_bounds__(PCG2_T, 1) k_pcg2(const PcgArgs a) {
             if (act1) z1[i] = z1[i] * d;
         }
         __syncthreads();
-        line_pass2(z0, z1, Q + 5 * QT, px * py, 1, pz, 0, 1, act0, act1);
-        line_pass2(z0, z1, Q + 3 * QT, px * pz, sy, sx, 1, pz, act0, act1);
-        line_pass2(z0, z1, Q + 1 * QT, py * pz, sx, 1, 1, py * pz, act0, act1);
+        LP2(z0, z1, Q + 5 * QT, px * py, 1, pz, 0, 1, act0, act1);
+        LP2(z0, z1, Q + 3 * QT, px * pz, sy, sx, 1, pz, act0, act1);
+        LP2(z0, z1, Q + 1 * QT, py * pz, sx, 1, 1, py * pz, act0, act1);
 #pragma unroll
         for (int t = 0; t < PCG2_NPT; ++t) {
             const int i = threadIdx.x + t * PCG2_T;
