@@ -548,7 +548,9 @@ def run_ours(args):
         except Exception as exc:  # the GPU line must still print
             cpu = {"value": None, "error": str(exc)[:300]}
     line["cpu_baseline"] = cpu
-    head_pp = pp if (args.extra and cfg == 5 and args.precision == "fp64") else None
+    # extras on one GPU only: under torchrun the other ranks have left (their measure_* barriers
+    # would never be matched), and the scaling line is the headline
+    head_pp = pp if (args.extra and cfg == 5 and args.precision == "fp64" and ws == 1) else None
     del pp
     torch.cuda.empty_cache()
     if head_pp is not None:
