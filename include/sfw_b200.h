@@ -198,7 +198,7 @@ int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub, const doub
 
 /* Run all shots from rest for n_steps in one persistent launch.  profile0: HOST
  * [S] f_q(0); profile: HOST [S][n_steps] f_q(k dt); rows_out: HOST
- * [n_steps/record_every][n_probe][S] or NULL; norms_out: HOST [n_steps][S]
+ * [n_steps/record_every][S][n_probe] or NULL; norms_out: HOST [n_steps][S]
  * |U_q| after each step or NULL; *kernel_ms: CUDA-event time of the launch. */
 int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, const double* profile0,
                   const double* profile, double* rows_out, double* norms_out, float* kernel_ms,

@@ -121,6 +121,116 @@ __global__ void __launch_bounds__(128) k_dgemm(const GemmArgs g) {
 }
 
 // ---------------------------------------------------------------------------
+// k_dgemm2: the same batched C = alpha op(A) B + beta C, with the tiles moved global -> shared by
+// cp.async (16-byte chunks, zero-filled at the edges) through a 3-stage ring, so no register
+// staging and two k-tiles in flight while the DMMA loop runs.  Shared layouts are chosen for
+// conflict-free fragment reads: A as [k][m] (row stride 68) when A is column-major in m, else
+// [m][k] (row stride 20); B as [n][k] (row stride 20).  Needs 16-byte aligned operands with even
+// leading dimensions (the host wrapper checks and otherwise uses k_dgemm).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int DG2_BM = 64, DG2_BN = 64, DG2_BK = 16, DG2_NS = 3, DG2_LDM = 68, DG2_LDK = 20;
+constexpr int DG2_ASZ = DG2_BK * DG2_LDM > DG2_BM * DG2_LDK ? DG2_BK * DG2_LDM : DG2_BM * DG2_LDK;
+constexpr int DG2_BSZ = DG2_BN * DG2_LDK;
+constexpr size_t DG2_SMEM = (size_t)DG2_NS * (DG2_ASZ + DG2_BSZ) * 8;
+
+template <bool TA>
+__global__ void __launch_bounds__(128) k_dgemm2(const GemmArgs g) {
+    extern __shared__ __align__(16) double dsm[];
+    double* As = dsm;                         // [NS][ASZ]
+    double* Bs = dsm + DG2_NS * DG2_ASZ;      // [NS][BSZ]
+    const int b = blockIdx.z;
+    const double* A = g.A + (size_t)b * g.sA;
+    const double* B = g.B + (size_t)b * g.sB;
+    double* C = g.C + (size_t)b * g.sC;
+    const int m0 = blockIdx.y * DG2_BM, n0 = blockIdx.x * DG2_BN;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+    const int nk = (g.K + DG2_BK - 1) / DG2_BK;
+    auto issue = [&](int kt, int buf) {
+        const int k0 = kt * DG2_BK;
+        double* as = As + buf * DG2_ASZ;
+        double* bs = Bs + buf * DG2_BSZ;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {  // 512 chunks of A, 4 per thread
+            const int c = tid + e * 128;
+            if (!TA) {  // A column-major (m fastest): chunk = 2 m at one k
+                const int k = c >> 5, m = (c & 31) * 2;
+                const int gm = m0 + m, gk = k0 + k;
+                const int valid = (gk < g.K) ? max(0, min(2, g.M - gm)) : 0;
+                cp_async16(as + k * DG2_LDM + m, valid ? A + gm + (size_t)gk * g.lda : A, 8 * valid);
+            } else {    // A^T: k fastest: chunk = 2 k at one m
+                const int m = c >> 3, k = (c & 7) * 2;
+                const int gm = m0 + m, gk = k0 + k;
+                const int valid = (gm < g.M) ? max(0, min(2, g.K - gk)) : 0;
+                cp_async16(as + m * DG2_LDK + k, valid ? A + gk + (size_t)gm * g.lda : A, 8 * valid);
+            }
+            {  // B (k fastest): chunk = 2 k at one n
+                const int n = c >> 3, k = (c & 7) * 2;
+                const int gn = n0 + n, gk = k0 + k;
+                const int valid = (gn < g.N) ? max(0, min(2, g.K - gk)) : 0;
+                cp_async16(bs + n * DG2_LDK + k, valid ? B + gk + (size_t)gn * g.ldb : B, 8 * valid);
+            }
+        }
+    };
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < DG2_NS - 1; ++s) {
+        if (s < nk) issue(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<DG2_NS - 2>();
+        __syncthreads();  // stage kt landed for every thread; everyone finished computing kt-1
+        if (kt + DG2_NS - 1 < nk) issue(kt + DG2_NS - 1, (kt + DG2_NS - 1) % DG2_NS);
+        cp_async_commit();
+        const double* as = As + (kt % DG2_NS) * DG2_ASZ;
+        const double* bs = Bs + (kt % DG2_NS) * DG2_BSZ;
+#pragma unroll
+        for (int kk = 0; kk < DG2_BK; kk += 4) {
+            double af[4], bf[4];
+            const int k = kk + (lane & 3);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int m = wm + i * 8 + (lane >> 2);
+                af[i] = TA ? as[m * DG2_LDK + k] : as[k * DG2_LDM + m];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = bs[(wn + j * 8 + (lane >> 2)) * DG2_LDK + k];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma8x8x4(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int gm = m0 + wm + i * 8 + (lane >> 2);
+                const int gn = n0 + wn + j * 8 + (lane & 3) * 2 + h;
+                if (gm < g.M && gn < g.N) {
+                    double* cp = C + gm + (size_t)gn * g.ldc;
+                    const double v = g.alpha * acc[i][j][h];
+                    *cp = (g.beta != 0.0) ? v + g.beta * *cp : v;
+                }
+            }
+}
+
+// ---------------------------------------------------------------------------
 // CTA-cooperative dense helpers on w x w row-major matrices in shared memory.
 // All routines must be called by every thread of the CTA.
 

@@ -993,12 +993,27 @@ __global__ void k_basis_rows(const double* __restrict__ V, long long ldn, long l
 // ---------------------------------------------------------------------------
 // host orchestration
 
+#ifndef SFW_DGEMM2
+#define SFW_DGEMM2 1
+#endif
 static void gemm(cudaStream_t st, bool ta, int M, int N, int K, double alpha, const double* A, long long lda,
                  long long sA, const double* B, long long ldb, long long sB, double beta, double* C, long long ldc,
                  long long sC, int batch) {
     GemmArgs g{M, N, K, alpha, beta, A, lda, sA, B, ldb, sB, C, ldc, sC};
     dim3 grid((N + 63) / 64, (M + 63) / 64, batch);
-    if (ta)
+    // the cp.async kernel needs 16-B aligned operands: even leading dimensions and batch strides
+    const bool al = !(((uintptr_t)A | (uintptr_t)B) & 15) && !((lda | ldb | sA | sB) & 1) && SFW_DGEMM2;
+    static bool attr = false;
+    if (al && !attr) {
+        cudaFuncSetAttribute(k_dgemm2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DG2_SMEM);
+        cudaFuncSetAttribute(k_dgemm2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DG2_SMEM);
+        attr = true;
+    }
+    if (al && ta)
+        k_dgemm2<true><<<grid, 128, DG2_SMEM, st>>>(g);
+    else if (al)
+        k_dgemm2<false><<<grid, 128, DG2_SMEM, st>>>(g);
+    else if (ta)
         k_dgemm<true><<<grid, 128, 0, st>>>(g);
     else
         k_dgemm<false><<<grid, 128, 0, st>>>(g);

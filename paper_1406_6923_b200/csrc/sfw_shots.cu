@@ -96,7 +96,7 @@ struct MsParams {
     const int* prb_tap;
     const double* prb_w;
     const long long* prb_woff;
-    double* rows;          // [n_rec][n_probe][S]
+    double* rows;          // [n_rec][S][n_probe]
     double* norm_part;     // [n_steps][grid][S]
     unsigned int* flags;
     const int* ncta_ptr;
@@ -494,7 +494,7 @@ __device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst
                         val = 0.0;
                         for (long long i = 0; i < K; ++i) val = fma(wv[i], us[i * S + q], val);
                     }
-                    p.rows[(row * p.n_probe + pid) * S + q] = val;
+                    p.rows[(row * S + q) * p.n_probe + pid] = val;  // [rec][shot][probe]
                 }
             }
         }
