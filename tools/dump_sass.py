@@ -15,14 +15,15 @@ KERNELS = {  # file name -> mangled-name pattern
     "k_ustep_9_2": r"_ZN3sfw7k_ustepILi9ELi2EEEvNS_10StepParamsE",
     "k_wstep_9_2": r"_ZN3sfw7k_wstepILi9ELi2EEEvNS_7WParamsE",
     "k_step_ms2_9": r"_ZN3sfw10k_step_ms2ILi9EEEvNS_8MsParamsE",
-    "k_pcg_17": r"_ZN3sfw5k_pcgILi17EEEvNS_7PcgArgsE",
-    "k_dgemm_T": r"_ZN3sfw7k_dgemmILb1EEEvNS_8GemmArgsE",
+    "k_pcg2": r"_ZN3sfw6k_pcg2ENS_7PcgArgsE",
+    "k_dgemm2_T": r"_ZN3sfw8k_dgemm2ILb1EEEvNS_8GemmArgsE",
+    "k_dgemm2_N": r"_ZN3sfw8k_dgemm2ILb0EEEvNS_8GemmArgsE",
     "k_cholqr": r"_ZN3sfw8k_cholqr\w*",
     "k_sfraction": r"_ZN3sfw11k_sfraction\w*",
     "k_stencil": r"_ZN3sfw9k_stencil\w*",
     "k_fdtd_0": r"_ZN3sfw6k_fdtdILi0EEEvNS_8FdParamsE",
 }
-MNEM = ["DMMA", "UBLKCP", "SYNCS", "LDS", "STS", "LDG", "STG", "DFMA", "DADD", "DMUL", "BAR", "SHFL"]
+MNEM = ["DMMA", "UBLKCP", "LDGSTS", "SYNCS", "LDS", "STS", "LDG", "STG", "DFMA", "DADD", "DMUL", "BAR", "SHFL"]
 
 
 def main():
