@@ -41,6 +41,9 @@ struct FdParams {
     const double* src_val;
     double f;              // source profile value of this step
     double* part;          // per-block partial sums: mode 0/1 |out|^2, mode 2 unused
+    int n_rec;             // mode 0: receivers written by the kernel into rows (when rows != null)
+    const long long* rec;
+    double* rows;          // mode 0: this step's receiver row, or null
 };
 
 // 2.5-D blocking: a CTA owns a 32 (z) x 8 (y) column of XC consecutive x-planes.  The thread's
@@ -49,15 +52,14 @@ struct FdParams {
 // formed in the reference's order (x-, y-, z-, diag, z+, y+, x+) whatever the operands' source.
 constexpr int FD_XC = 16;
 
-template <int MODE>
-__global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
-    __shared__ double su[10][34], sc[10][34];
-    __shared__ double red[8];
+template <int MODE, bool INT>
+__device__ __forceinline__ void fdtd_tile(const FdParams& p, double (&su)[10][34], double (&sc)[10][34],
+                                          double* red) {
     const int tz = threadIdx.x, ty = threadIdx.y;
     const int z = blockIdx.x * 32 + tz, y = blockIdx.y * 8 + ty;
     const int x0 = blockIdx.z * FD_XC, x1 = min(p.nx, x0 + FD_XC);
     const int sx = p.ny * p.nz, sy = p.nz;  // 32-bit offsets: grids up to 2^31 nodes (checked at create)
-    const bool in = z < p.nz && y < p.ny;
+    const bool in = INT || (z < p.nz && y < p.ny);
     const int col = y * p.nz + z;
     // does this CTA's column hold a source node?  (block-uniform; the per-node test runs only there)
     bool src_here = false;
@@ -66,22 +68,30 @@ __global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
         const int sxq = (int)(s / sx), rem = (int)(s % sx), syq = rem / p.nz, szq = rem % p.nz;
         src_here |= sxq >= x0 && sxq < x1 && syq / 8 == (int)blockIdx.y && szq / 32 == (int)blockIdx.x;
     }
+    // does this CTA's column hold a receiver that is recorded this step?  (block-uniform)
+    bool rec_here = false;
+    if (MODE == 0 && p.rows)
+        for (int q = 0; q < p.n_rec; ++q) {
+            const long long r = p.rec[q];
+            const int rx = (int)(r / sx), rem = (int)(r % sx), ry = rem / p.nz, rz = rem % p.nz;
+            rec_here |= rx >= x0 && rx < x1 && ry / 8 == (int)blockIdx.y && rz / 32 == (int)blockIdx.x;
+        }
     // halo duty of this thread: row y-1 (ty == 0), row y+1 (ty == 7), column z-1 (tz == 0), z+1 (tz == 31)
-    const int hy = (ty == 0 && y > 0) ? -1 : (ty == 7 && y + 1 < p.ny) ? 1 : 0;
-    const int hz = (tz == 0 && z > 0) ? -1 : (tz == 31 && z + 1 < p.nz) ? 1 : 0;
+    const int hy = (ty == 0 && (INT || y > 0)) ? -1 : (ty == 7 && (INT || y + 1 < p.ny)) ? 1 : 0;
+    const int hz = (tz == 0 && (INT || z > 0)) ? -1 : (tz == 31 && (INT || z + 1 < p.nz)) ? 1 : 0;
     // software pipeline, two planes deep: centre (u, c) of x+1 and x+2, halos and u_prev of x+1
     auto ld = [&](const double* a, int i) { return __ldg(a + i); };
     double um = 0.0, uc = 0.0, up = 0.0, u2 = 0.0, cm = 0.0, cc = 0.0, cp = 0.0, c2 = 0.0;
     double hyu = 0.0, hyc = 0.0, hzu = 0.0, hzc = 0.0, prv = 0.0, vel = 0.0;
     if (in) {
         const int i0 = x0 * sx + col;
-        if (x0 > 0) {
+        if (INT || x0 > 0) {
             um = ld(p.u, i0 - sx);
             cm = ld(p.c, i0 - sx);
         }
         uc = ld(p.u, i0);
         cc = ld(p.c, i0);
-        if (x0 + 1 < p.nx) {
+        if (INT || x0 + 1 < p.nx) {
             up = ld(p.u, i0 + sx);
             cp = ld(p.c, i0 + sx);
         }
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
         const double prev = prv, v0 = vel;
         // next loads: plane x+2 centre, plane x+1 halos and u_prev
         if (in) {
-            if (x + 2 < p.nx) {
+            if (INT || x + 2 < p.nx) {
                 u2 = ld(p.u, i + 2 * sx);
                 c2 = ld(p.c, i + 2 * sx);
             }
@@ -135,29 +145,29 @@ __global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
             const double ci = cc, ui = uc;
             const double cn = __dmul_rn(-ci, ci);
             double diag = 0.0;  // np.add.at order: x lower/upper end, y, z
-            if (p.nx > 1) {
-                if (x + 1 < p.nx) diag = __dadd_rn(diag, __dmul_rn(cn, p.s0));
-                if (x > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s0));
+            if (INT || p.nx > 1) {
+                if (INT || x + 1 < p.nx) diag = __dadd_rn(diag, __dmul_rn(cn, p.s0));
+                if (INT || x > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s0));
             }
-            if (p.ny > 1) {
-                if (y + 1 < p.ny) diag = __dadd_rn(diag, __dmul_rn(cn, p.s1));
-                if (y > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s1));
+            if (INT || p.ny > 1) {
+                if (INT || y + 1 < p.ny) diag = __dadd_rn(diag, __dmul_rn(cn, p.s1));
+                if (INT || y > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s1));
             }
-            if (p.nz > 1) {
-                if (z + 1 < p.nz) diag = __dadd_rn(diag, __dmul_rn(cn, p.s2));
-                if (z > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s2));
+            if (INT || p.nz > 1) {
+                if (INT || z + 1 < p.nz) diag = __dadd_rn(diag, __dmul_rn(cn, p.s2));
+                if (INT || z > 0) diag = __dadd_rn(diag, __dmul_rn(cn, p.s2));
             }
             double acc = 0.0;
             auto term = [&](double cj, double uj, double s) {
                 acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(__dmul_rn(cj, ci), s), uj));
             };
-            if (x > 0) term(cm, um, p.s0);
-            if (y > 0) term(sc[ty][tz + 1], su[ty][tz + 1], p.s1);
-            if (z > 0) term(sc[ty + 1][tz], su[ty + 1][tz], p.s2);
+            if (INT || x > 0) term(cm, um, p.s0);
+            if (INT || y > 0) term(sc[ty][tz + 1], su[ty][tz + 1], p.s1);
+            if (INT || z > 0) term(sc[ty + 1][tz], su[ty + 1][tz], p.s2);
             acc = __dadd_rn(acc, __dmul_rn(diag, ui));
-            if (z + 1 < p.nz) term(sc[ty + 1][tz + 2], su[ty + 1][tz + 2], p.s2);
-            if (y + 1 < p.ny) term(sc[ty + 2][tz + 1], su[ty + 2][tz + 1], p.s1);
-            if (x + 1 < p.nx) term(cp, up, p.s0);
+            if (INT || z + 1 < p.nz) term(sc[ty + 1][tz + 2], su[ty + 1][tz + 2], p.s2);
+            if (INT || y + 1 < p.ny) term(sc[ty + 2][tz + 1], su[ty + 2][tz + 1], p.s1);
+            if (INT || x + 1 < p.nx) term(cp, up, p.s0);
             if (MODE == 2) {
                 p.out[i] = -acc;
             } else {
@@ -173,6 +183,9 @@ __global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
                 }
                 p.out[i] = v;
                 sq = fma(v, v, sq);
+                if (MODE == 0 && rec_here)  // receiver rows straight from the new level
+                    for (int q = 0; q < p.n_rec; ++q)
+                        if (p.rec[q] == i) p.rows[q] = v;
             }
         }
         __syncthreads();
@@ -192,6 +205,37 @@ __global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
             for (int k = 0; k < 8; ++k) t += red[k];
             p.part[((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
         }
+    }
+}
+
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_fdtd(const FdParams p) {
+    __shared__ double su[10][34], sc[10][34];
+    __shared__ double red[8];
+    // block-uniform: a tile that touches no face of the grid takes the branch-free path (every
+    // neighbour exists, so the same multiplies and adds run in the same order: bit-identical)
+    const int z0 = blockIdx.x * 32, y0 = blockIdx.y * 8, x0 = blockIdx.z * FD_XC;
+    const bool interior = z0 > 0 && z0 + 32 < p.nz && y0 > 0 && y0 + 8 < p.ny && x0 > 0 && x0 + FD_XC + 1 < p.nx;
+    if (interior)
+        fdtd_tile<MODE, true>(p, su, sc, red);
+    else
+        fdtd_tile<MODE, false>(p, su, sc, red);
+}
+
+// one block per step: the fixed-order sum of that step's block partials (the order k_fd_finish uses)
+__global__ void k_fd_norms(const double* __restrict__ part, long long nparts, double* __restrict__ out) {
+    __shared__ double red[32];
+    const double* pk = part + (size_t)blockIdx.x * nparts;
+    double t = 0.0;
+    for (long long k = threadIdx.x; k < nparts; k += blockDim.x) t += pk[k];
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        out[blockIdx.x] = s;
     }
 }
 
@@ -296,6 +340,8 @@ struct sfw_fdtd {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     dim3 grid, block;
     long long nparts = 0;
+    double* part_steps = nullptr;  // [steps][nparts] block partials of a run
+    long long part_steps_cap = 0;
 };
 
 namespace {
@@ -492,17 +538,28 @@ extern "C" int sfw_fdtd_run(sfw_fdtd* h, double dt, int n_steps, const double* f
     p.n_src = h->n_src;
     p.src_idx = h->src;
     p.src_val = h->srcv;
+    if (h->part_steps_cap < (long long)n_steps * h->nparts) {
+        cudaFree(h->part_steps);
+        h->part_steps = nullptr;
+        if ((rc = fd_alloc(&h->part_steps, (size_t)n_steps * h->nparts, errbuf, errlen))) return rc;
+        h->part_steps_cap = (long long)n_steps * h->nparts;
+    }
+    p.n_rec = h->n_rec;
+    p.rec = h->rec;
+    // one launch per step: receivers are written by the stepping kernel and the per-step norm
+    // partials kept, so the norms are reduced once after the loop (no per-step finish kernel)
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
     for (int k = 1; k <= n_steps; ++k) {
         p.u = h->U[h->cur];
         p.out = h->U[h->cur ^ 1];  // holds level k-2, receives level k
         p.f = h->n_src ? ftab[k - 1] : 0.0;
+        p.part = h->part_steps + (size_t)(k - 1) * h->nparts;
+        const bool rec = (k % record_every) == 0 && h->n_rec > 0;
+        p.rows = rec ? h->rows + (k / record_every - 1) * h->n_rec : nullptr;
         k_fdtd<0><<<h->grid, h->block, 0, h->stream>>>(p);
         h->cur ^= 1;
-        const bool rec = (k % record_every) == 0 && h->n_rec > 0;
-        k_fd_finish<<<1, 1024, 0, h->stream>>>(h->part, h->nparts, h->norms, k - 1, h->U[h->cur], h->rec, h->n_rec,
-                                               rec ? h->rows + (k / record_every - 1) * h->n_rec : nullptr);
     }
+    k_fd_norms<<<n_steps, 1024, 0, h->stream>>>(h->part_steps, h->nparts, h->norms);
     SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
     if (norms_out) SFW_CUDA_TRY(cudaMemcpyAsync(norms_out, h->norms, n_steps * 8, cudaMemcpyDeviceToHost, h->stream));
     if (rows_out && nrec * h->n_rec)
@@ -522,7 +579,8 @@ extern "C" int sfw_fdtd_state(sfw_fdtd* h, double* u_curr, double* u_prev, char*
 
 extern "C" int sfw_fdtd_destroy(sfw_fdtd* h) {
     if (!h) return 0;
-    void* ptrs[] = {h->c, h->U[0], h->U[1], h->W, h->part, h->acc, h->norms, h->rows, h->src, h->srcv, h->rec, h->damp};
+    void* ptrs[] = {h->c, h->U[0], h->U[1], h->W, h->part, h->acc, h->norms, h->rows, h->src, h->srcv, h->rec, h->damp,
+                    h->part_steps};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
