@@ -298,7 +298,7 @@ int sfw_fdtd_power(sfw_fdtd* h, const double* v0, double tol, int max_iter, doub
 /* source_vec nonzeros (node, value), receiver rows, optional damping (HOST n). */
 int sfw_fdtd_setup(sfw_fdtd* h, int n_src, const long long* src_idx, const double* src_val, int n_rec,
                    const long long* rec_idx, const double* damping, char* errbuf, int errlen);
-/* second-order start (reference.py:123-124); v0 may be NULL; f0 = source_fn(0). */
+/* second-order start (reference.py:123-124); u0 / v0 may be NULL (zeros); f0 = source_fn(0). */
 int sfw_fdtd_init(sfw_fdtd* h, double dt, const double* u0, const double* v0, double f0, char* errbuf,
                   int errlen);
 /* n_steps steps (reference.py:129-150): ftab[k-1] = source_fn((k-1) dt);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/sfw_b200.h"
@@ -31,6 +32,29 @@ inline cudaError_t sfw_h2d(void* dst, const void* src, size_t bytes) {
             return ::sfw::fail(SFW_ECUDA, std::string(#expr ": ") + cudaGetErrorString(_e), \
                                errbuf, errlen);                                       \
     } while (0)
+
+// ---- device allocation (every library buffer; SFW_POISON debug fill) ---------
+
+inline int g_wform_scope = 0;  // debug poisoning: > 0 while a W-form entry point allocates
+
+template <typename T>
+inline int dalloc(T** p, size_t n, char* errbuf, int errlen) {
+    *p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+    if (e != cudaSuccess)
+        return fail(SFW_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e), errbuf, errlen);
+    if (const char* pz = std::getenv("SFW_POISON")) {  // debug: fresh buffers read as NaN until written
+        const bool w = g_wform_scope > 0;
+        if (pz[0] == 'a' || (pz[0] == 'w' && w) || (pz[0] == 's' && !w)) {
+            // legacy-stream memset + a legacy-stream sync only: library kernels run on non-blocking
+            // streams and are not drained here (every H2D copy already syncs the legacy stream)
+            cudaMemset(*p, 0xFF, n * sizeof(T));
+            cudaStreamSynchronize(cudaStreamLegacy);
+        }
+    }
+    return 0;
+}
 
 // ---- PTX wrappers: mbarrier + 1-D bulk async copy (TMA engine) -------------
 

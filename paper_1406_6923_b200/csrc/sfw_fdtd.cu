@@ -494,7 +494,10 @@ extern "C" int sfw_fdtd_setup(sfw_fdtd* h, int n_src, const long long* src_idx, 
 extern "C" int sfw_fdtd_init(sfw_fdtd* h, double dt, const double* u0, const double* v0, double f0, char* errbuf,
                              int errlen) {
     h->cur = 0;
-    SFW_CUDA_TRY(cudaMemcpyAsync(h->U[0], u0, h->n * 8, cudaMemcpyHostToDevice, h->stream));
+    if (u0)
+        SFW_CUDA_TRY(cudaMemcpyAsync(h->U[0], u0, h->n * 8, cudaMemcpyHostToDevice, h->stream));
+    else  // from rest: no host zeros to upload
+        SFW_CUDA_TRY(cudaMemsetAsync(h->U[0], 0, h->n * 8, h->stream));
     if (v0) SFW_CUDA_TRY(cudaMemcpyAsync(h->W, v0, h->n * 8, cudaMemcpyHostToDevice, h->stream));
     FdParams p = fd_params(h);
     p.u = h->U[0];

@@ -144,11 +144,10 @@ static int maps_common(int L, int w, const double* G, const double* row, double 
         cudaFree(dn);
         cudaFree(dst);
     };
-    if (cudaMalloc(&dG, K * w * 8) != cudaSuccess || cudaMalloc(&dv, K * 8) != cudaSuccess ||
-        cudaMalloc(&dc, K * 8) != cudaSuccess || cudaMalloc(&dout, K * 8) != cudaSuccess ||
-        cudaMalloc(&dn, 16) != cudaSuccess || cudaMalloc(&dst, L * sizeof(int)) != cudaSuccess) {
+    if (dalloc(&dG, K * w, errbuf, errlen) || dalloc(&dv, K, errbuf, errlen) || dalloc(&dc, K, errbuf, errlen) ||
+        dalloc(&dout, K, errbuf, errlen) || dalloc(&dn, 2, errbuf, errlen) || dalloc(&dst, L, errbuf, errlen)) {
         cleanup();
-        return fail(SFW_ECUDA, "cudaMalloc failed in chain maps", errbuf, errlen);
+        return SFW_ECUDA;
     }
     sfw_h2d(dG, G, K * w * 8);
     sfw_h2d(dv, row, K * 8);
@@ -206,11 +205,11 @@ static int state_map(int dir, int N, int L, int w, const double* basis, const do
         cudaFree(dout);
         cudaFree(dst);
     };
-    if (cudaMalloc(&dB, (size_t)N * K * 8) != cudaSuccess || cudaMalloc(&dG, (size_t)K * w * 8) != cudaSuccess ||
-        cudaMalloc(&dx, (size_t)std::max(N, K) * 8) != cudaSuccess || cudaMalloc(&dc, (size_t)K * 8) != cudaSuccess ||
-        cudaMalloc(&dout, (size_t)std::max(N, K) * 8) != cudaSuccess || cudaMalloc(&dst, L * sizeof(int)) != cudaSuccess) {
+    if (dalloc(&dB, (size_t)N * K, errbuf, errlen) || dalloc(&dG, (size_t)K * w, errbuf, errlen) ||
+        dalloc(&dx, (size_t)std::max(N, K), errbuf, errlen) || dalloc(&dc, (size_t)K, errbuf, errlen) ||
+        dalloc(&dout, (size_t)std::max(N, K), errbuf, errlen) || dalloc(&dst, (size_t)L, errbuf, errlen)) {
         cleanup();
-        return fail(SFW_ECUDA, "cudaMalloc failed in the state maps", errbuf, errlen);
+        return SFW_ECUDA;
     }
     sfw_h2d(dB, basis, (size_t)N * K * 8);
     sfw_h2d(dG, scales, (size_t)K * w * 8);

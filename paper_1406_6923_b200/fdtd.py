@@ -158,7 +158,7 @@ def run_leapfrog(a, dt: float, n_steps: int, *, u0=None, v0=None, source_vec=Non
     n = op.n
     if record_every < 1:
         raise ConfigError("record_every must be >= 1")
-    u_curr = np.zeros(n) if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)
+    u_curr = None if u0 is None else np.ascontiguousarray(u0, dtype=np.float64)  # None: from rest
     vel = None if v0 is None else np.ascontiguousarray(v0, dtype=np.float64)
     forced = source_vec is not None and source_fn is not None
     if forced:
@@ -183,9 +183,10 @@ def run_leapfrog(a, dt: float, n_steps: int, *, u0=None, v0=None, source_vec=Non
                "sfw_fdtd_init")
     samples, times = [], []
     if rec is not None:
-        samples.append(u_curr[rec].copy())
+        samples.append(u_curr[rec].copy() if u_curr is not None else np.zeros(n_rec))
         times.append(0.0)
-    baseline = float(np.linalg.norm(u_curr)) + dt * float(np.linalg.norm(vel if vel is not None else np.zeros(1)))
+    baseline = (float(np.linalg.norm(u_curr)) if u_curr is not None else 0.0) + \
+        dt * float(np.linalg.norm(vel if vel is not None else np.zeros(1)))
     step_chunk = record_every * max(1, int(chunk) // record_every)
     done = 0
     ms_total = 0.0
