@@ -1567,6 +1567,380 @@ __global__ void __launch_bounds__(256, 1) k_step_sw(const StepParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// k_step_sw4: the SMEM-resident small-m step with the layers of a subdomain split over
+// NQ = 1 + ceil((L-1)/NLW) warps (config 2: 512 x m4k6, <= 4 subdomains per CTA).
+//
+// k_step_sw runs the 2L block mat-vecs of a subdomain back to back in one warp, one warp per
+// SMSP: the step is the latency of that chain (3.9 us at m4k6).  Here warp 0 of a subdomain
+// owns layer 0 (the face exchange: flux put, neighbour poll, interface masses, probes and
+// norms), warps 1.. own NLW consecutive layers each.  A step is two phases separated by a
+// named barrier of the subdomain's warps:
+//   P1: flux_j = Gamma_j (U_{j+1} - U_j)   (U_{hi} of the next warp's first layer from SMEM)
+//   P2: acc_j  = Gamma-hat_j (flux_j - flux_{j-1}) (flux_{lo-1} from SMEM), leapfrog
+// Every product is the same sym_matvec_multi call on the same data as in k_step_sw, so the
+// results are bitwise those of k_step_sw / k_step2.
+template <int L, int NLW>
+struct Sw4Shape {
+    static constexpr int NQ = 1 + (L - 1 + NLW - 1) / NLW;
+};
+
+template <int M, int L, int NLW, int NL, bool ZERO>
+__device__ __forceinline__ void sw4_warp(const StepParams& p, const double* cfg, double* wbase, double* ubuf,
+                                         double* fbuf, const double* msub, const double* pwv, const int* pmeta,
+                                         const int* s_src, const int* s_prb, const int* s_nbr, int g, int s, int lo,
+                                         int lane, int bar_id, int bar_n, const RedOff7<M>& ro) {
+    constexpr int W = 6 * M;
+    constexpr int K = L * W;
+    constexpr int FB = 21 * M * M;
+    constexpr int PW = 42 * M;
+    constexpr unsigned FULL = 0xffffffffu;
+    const bool act = lane < W;
+    double* xw = wbase;
+    double* pw = xw + NL * 32;
+    double* ob = pw + NL * PW;  // ZERO warp only
+    auto sub_bar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_n) : "memory"); };
+
+    double uc[NL], up[NL];
+    {
+        const double* Ug0 = p.cur ? p.U1 : p.U0;
+        const double* Ug1 = p.cur ? p.U0 : p.U1;
+#pragma unroll
+        for (int t = 0; t < NL; ++t) {
+            uc[t] = act ? Ug0[(size_t)s * K + (lo + t) * W + lane] : 0.0;
+            up[t] = act ? Ug1[(size_t)s * K + (lo + t) * W + lane] : 0.0;
+            ubuf[(lo + t) * 32 + lane] = uc[t];
+        }
+    }
+    const int src_a = s_src[g], nsrc = s_src[g + 1] - s_src[g];
+    double sv0[NL], sv1[NL];
+    const double *ft0 = p.ftab, *ft1 = p.ftab;
+#pragma unroll
+    for (int t = 0; t < NL; ++t) sv0[t] = sv1[t] = 0.0;
+    if (nsrc >= 1 && nsrc <= 2) {
+        const int q0 = p.src_ids[src_a];
+        ft0 = p.ftab + (long long)q0 * p.ftab_stride;
+#pragma unroll
+        for (int t = 0; t < NL; ++t) sv0[t] = act ? p.src_vec[p.src_voff[q0] + (long long)(lo + t) * W + lane] : 0.0;
+        if (nsrc == 2) {
+            const int q1 = p.src_ids[src_a + 1];
+            ft1 = p.ftab + (long long)q1 * p.ftab_stride;
+#pragma unroll
+            for (int t = 0; t < NL; ++t)
+                sv1[t] = act ? p.src_vec[p.src_voff[q1] + (long long)(lo + t) * W + lane] : 0.0;
+        }
+    }
+    // ---- layer-0 warp: face exchange and the probe / norm record (k_step_sw's record) ----
+    int tj0 = -1, tp0 = -1, tj1 = -1, tp1 = -1, dp0 = -1, dp1 = -1;
+    const double *dw0 = pwv, *dw1 = pwv;
+    bool generic = false;
+    const int pa0 = s_prb[0], pq0 = s_prb[g], pq1 = s_prb[g + 1];
+    const int f = lane / M, r = lane % M;
+    int nb = -1;
+    unsigned long long* mb_out = nullptr;
+    const unsigned long long* mb_in = nullptr;
+    const size_t mb_par = (size_t)p.n_sub * W * 2;
+    const double* mrow = msub;
+    if (ZERO) {
+        for (int q = pq0; q < pq1; ++q) {
+            const bool staged = q - pa0 < p.res_pmax;
+            const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
+            const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
+            if (tap < 0) {
+                if (!staged || tap <= -1000000) {
+                    generic = true;
+                } else if (dp0 < 0) {
+                    dp0 = pid;
+                    dw0 = pwv + (size_t)(-1 - tap) * K;
+                } else if (dp1 < 0) {
+                    dp1 = pid;
+                    dw1 = pwv + (size_t)(-1 - tap) * K;
+                } else {
+                    generic = true;
+                }
+            } else if (tap % W == lane) {
+                if (tp0 < 0) {
+                    tj0 = tap / W;
+                    tp0 = pid;
+                } else if (tp1 < 0) {
+                    tj1 = tap / W;
+                    tp1 = pid;
+                } else {
+                    generic = true;
+                }
+            }
+        }
+        generic = __any_sync(FULL, generic);
+        nb = act ? s_nbr[g * 6 + f] : -1;
+        mb_out = p.mbox + ((size_t)s * W + lane) * 2;
+        mb_in = p.mbox + ((size_t)(nb < 0 ? 0 : nb) * W + (f ^ 1) * M + r) * 2;
+        mrow = msub + (f < 6 ? f : 0) * M * M + r * M;
+    }
+    // rows / norm of the state after step kd, read from the subdomain's SMEM copy of U
+    // (same order as k_step_sw's register version)
+    auto record = [&](int kd) {
+        const bool rows_now = (kd % p.record_every == 0) && p.rows;
+        const long long row = kd / p.record_every - 1;
+        double sq = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+            const double u = ubuf[j * 32 + lane];
+            sq = fma(u, u, sq);
+        }
+        if (rows_now && !generic && dp0 >= 0) {
+#pragma unroll
+            for (int j = 0; j < L; ++j)
+                if (act) d0 = fma(dw0[j * W + lane], ubuf[j * 32 + lane], d0);
+            if (dp1 >= 0) {
+#pragma unroll
+                for (int j = 0; j < L; ++j)
+                    if (act) d1 = fma(dw1[j * W + lane], ubuf[j * 32 + lane], d1);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sq += __shfl_xor_sync(FULL, sq, o);
+            d0 += __shfl_xor_sync(FULL, d0, o);
+            d1 += __shfl_xor_sync(FULL, d1, o);
+        }
+        if (lane == 0) p.norm_part[((size_t)(kd - 1) * gridDim.x + blockIdx.x) * p.groups + g] = sq;
+        if (!rows_now) return;
+        if (!generic) {
+            if (lane == 0 && dp0 >= 0) p.rows[row * p.n_probe + dp0] = d0;
+            if (lane == 0 && dp1 >= 0) p.rows[row * p.n_probe + dp1] = d1;
+            if (tp0 >= 0) p.rows[row * p.n_probe + tp0] = ubuf[tj0 * 32 + lane];
+            if (tp1 >= 0) p.rows[row * p.n_probe + tp1] = ubuf[tj1 * 32 + lane];
+            return;
+        }
+        for (int q = pq0; q < pq1; ++q) {
+            const bool staged = q - pa0 < p.res_pmax;
+            const int pid = staged ? pmeta[2 * (q - pa0)] : p.prb_ids[q];
+            const int tap = staged ? pmeta[2 * (q - pa0) + 1] : p.prb_tap[pid];
+            double v;
+            if (tap >= 0) {
+                v = ubuf[(tap / W) * 32 + tap % W];
+            } else {
+                const double* wv = (tap > -1000000) ? pwv + (size_t)(-1 - tap) * K : p.prb_w + p.prb_woff[pid];
+                double acc = 0.0;
+#pragma unroll
+                for (int j = 0; j < L; ++j)
+                    if (act) acc = fma(wv[j * W + lane], ubuf[j * 32 + lane], acc);
+                v = warp_sum(acc);
+            }
+            if (lane == 0) p.rows[row * p.n_probe + pid] = v;
+        }
+    };
+
+#ifdef SFW_LW_CLK
+    long long clk_prev = clock64(), clk_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define SW4_CLK(ph)                     \
+    {                                   \
+        const long long c_ = clock64(); \
+        clk_acc[ph] += c_ - clk_prev;   \
+        clk_prev = c_;                  \
+    }
+#else
+#define SW4_CLK(ph)
+#endif
+    const double dt2 = p.dt2;
+    const double* gam = cfg + (size_t)lo * 2 * FB;       // Gamma_lo, stride 2 FB
+    const double* hat = cfg + (size_t)lo * 2 * FB + FB;  // Gamma-hat_lo
+    sub_bar();  // every warp's U in ubuf
+    SW4_CLK(7);
+    for (int k = 1; k <= p.n_steps; ++k) {
+        const int par = k & 1;
+        const unsigned int tag = p.tag_base + (unsigned int)k;
+        const int kk = k - 1;
+        const double fa0 = (nsrc >= 1 && nsrc <= 2) ? ft0[kk] : 0.0;
+        const double fa1 = (nsrc == 2) ? ft1[kk] : 0.0;
+        // ---- P1: flux_j = Gamma_j (U_{j+1} - U_j) ----
+        {
+            const double unext = (lo + NL < L) ? ubuf[(lo + NL) * 32 + lane] : 0.0;
+#pragma unroll
+            for (int t = 0; t < NL; ++t) xw[t * 32 + lane] = (t + 1 < NL ? uc[t + 1] : unext) - uc[t];
+        }
+        __syncwarp();
+        double fl[NL];
+        sym_matvec_multi<M, NL>(gam, 2 * FB, xw, pw, fl, lane, ro);
+        if (ZERO && nb >= 0) mbox_put(mb_out + par * mb_par, fl[0], tag);
+        fbuf[(lo + NL - 1) * 32 + lane] = fl[NL - 1];
+        SW4_CLK(0);
+        if (ZERO && k > 1) record(k - 1);
+        SW4_CLK(1);
+        sub_bar();
+        SW4_CLK(2);
+        // ---- P2: acc_j = Gamma-hat_j (flux_j - flux_{j-1}), leapfrog ----
+        {
+            const double fprev = lo > 0 ? fbuf[(lo - 1) * 32 + lane] : 0.0;
+#pragma unroll
+            for (int t = 0; t < NL; ++t)
+                xw[t * 32 + lane] = (lo + t > 0) ? fl[t] - (t > 0 ? fl[t - 1] : fprev) : fl[0];
+        }
+        __syncwarp();
+        double acc[NL];
+        sym_matvec_multi<M, NL>(hat, 2 * FB, xw, pw, acc, lane, ro);
+        SW4_CLK(3);
+#pragma unroll
+        for (int t = NL - 1; t >= 0; --t) {
+            double a = acc[t];
+            if (ZERO && t == 0) {
+                // interface faces: seg = mass (own + nbr)  (stepper.py:283-300)
+                const double oth = mbox_take_warp(mb_in + par * mb_par, tag, nb >= 0);
+                SW4_CLK(4);
+                if (nb >= 0) ob[lane] = oth;
+                __syncwarp();
+                double acc_if = 0.0;
+#pragma unroll
+                for (int c = 0; c < M; ++c) acc_if = fma(mrow[c], __dadd_rn(xw[f * M + c], ob[f * M + c]), acc_if);
+                if (nb >= 0) a = acc_if;
+            }
+            double tot = a;
+            if (nsrc == 1) {
+                tot = __dadd_rn(a, __dmul_rn(sv0[t], fa0));
+            } else if (nsrc == 2) {
+                tot = __dadd_rn(a, __dadd_rn(__dmul_rn(sv0[t], fa0), __dmul_rn(sv1[t], fa1)));
+            }
+            const double un = act ? __dadd_rn(__dsub_rn(__dmul_rn(2.0, uc[t]), up[t]), __dmul_rn(dt2, tot)) : 0.0;
+            up[t] = uc[t];
+            uc[t] = un;
+            ubuf[(lo + t) * 32 + lane] = un;
+        }
+        SW4_CLK(5);
+        sub_bar();
+        SW4_CLK(6);
+    }
+    if (ZERO && p.n_steps > 0) record(p.n_steps);
+#ifdef SFW_LW_CLK
+    if (p.tprof && lane < 8) {
+        long long v = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (lane == q) v = clk_acc[q];
+        p.tprof[((size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 16 + lane] = v;
+    }
+#endif
+#undef SW4_CLK
+    if (act) {
+        double* Gc = (p.cur ^ (p.n_steps & 1)) ? p.U1 : p.U0;
+        double* Go = (p.cur ^ (p.n_steps & 1)) ? p.U0 : p.U1;
+#pragma unroll
+        for (int t = 0; t < NL; ++t) {
+            Gc[(size_t)s * K + (lo + t) * W + lane] = uc[t];
+            Go[(size_t)s * K + (lo + t) * W + lane] = up[t];
+        }
+    }
+}
+
+template <int M, int L, int NLW>
+__host__ __device__ constexpr int sw4_sub_words() {  // per-subdomain scratch doubles (warps + ubuf/fbuf)
+    return (32 + 42 * M + 32) + (Sw4Shape<L, NLW>::NQ - 1) * NLW * (32 + 42 * M) + 2 * L * 32;
+}
+
+template <int M, int L, int NLW>
+__global__ void __launch_bounds__(Sw4Shape<L, NLW>::NQ * 32 * 4, 1) k_step_sw4(const StepParams p) {  // <= 4 subdomains
+    constexpr int NQ = Sw4Shape<L, NLW>::NQ;
+    constexpr int FB = 21 * M * M;
+    constexpr int K = L * 6 * M;
+    constexpr int PW = 42 * M;
+    constexpr int SUBW = sw4_sub_words<M, L, NLW>();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    const RedOff7<M> ro(lane);
+    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int ns = s1 - s0;
+    const int nslot = nwarps / NQ;
+    double* cf = reinterpret_cast<double*>(smem_raw);          // [ns][2L][FB]
+    double* ms = cf + (size_t)nslot * 2 * L * FB;              // [nslot][6][M*M]
+    double* wsb = ms + (size_t)nslot * 6 * M * M;              // [nslot][SUBW]
+    double* pwv = wsb + (size_t)nslot * SUBW;                  // [npd][K]
+    int* pmeta = reinterpret_cast<int*>(pwv + (size_t)p.res_pdense * K);
+    __shared__ int s_nbr[8 * 6];
+    __shared__ int s_src[8 + 1];
+    __shared__ int s_prb[8 + 1];
+    __shared__ __align__(8) uint64_t s_bar;
+    const uint32_t img_bytes = (uint32_t)ns * 2 * L * FB * 8;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&s_bar, img_bytes);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(p.swimg + (size_t)s0 * 2 * L * FB);
+        for (uint32_t off = 0; off < img_bytes; off += 32768u)
+            bulk_g2s(reinterpret_cast<unsigned char*>(cf) + off, src + off, min(32768u, img_bytes - off), &s_bar,
+                     l2_policy_evict_last());
+    }
+    {
+        const int pa = p.prb_ptr[s0], pb = p.prb_ptr[s1];
+        if (threadIdx.x == 0) {
+            int nd = 0;
+            for (int q = pa; q < pb && q - pa < p.res_pmax; ++q) {
+                const int pid = p.prb_ids[q];
+                const int tap = p.prb_tap[pid];
+                pmeta[2 * (q - pa)] = pid;
+                if (tap >= 0) {
+                    pmeta[2 * (q - pa) + 1] = tap;
+                } else if (nd < p.res_pdense) {
+                    pmeta[2 * (q - pa) + 1] = -1 - nd;
+                    ++nd;
+                } else {
+                    pmeta[2 * (q - pa) + 1] = -1000000;
+                }
+            }
+        }
+        __syncthreads();
+        for (int q = pa + warp; q < pb && q - pa < p.res_pmax; q += nwarps) {
+            const int slot = pmeta[2 * (q - pa) + 1];
+            if (slot < 0 && slot > -1000000) {
+                const double* wv = p.prb_w + p.prb_woff[pmeta[2 * (q - pa)]];
+                for (int i = lane; i < K; i += 32) pwv[(size_t)(-1 - slot) * K + i] = wv[i];
+            }
+        }
+    }
+    for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nbr[i] = p.nbr[s0 * 6 + i];
+    for (int i = threadIdx.x; i <= ns; i += blockDim.x) {
+        s_src[i] = p.src_ptr[s0 + i];
+        s_prb[i] = p.prb_ptr[s0 + i];
+    }
+    for (int i = threadIdx.x; i < ns * 6 * M * M; i += blockDim.x) {
+        const int sl = i / (6 * M * M), fc = (i / (M * M)) % 6, e = i % (M * M);
+        const int mi = p.mass_idx[(s0 + sl) * 6 + fc];
+        ms[i] = mi >= 0 ? p.mass[(size_t)mi * M * M + e] : 0.0;
+    }
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+    const int g = warp / NQ, q = warp % NQ;
+    if (g >= ns) {  // no subdomain for this slot: zero its norm partials
+        if (q == 0 && lane == 0 && g < p.groups)
+            for (int k = 0; k < p.n_steps; ++k) p.norm_part[((size_t)k * gridDim.x + blockIdx.x) * p.groups + g] = 0.0;
+        return;
+    }
+    const int s = s0 + g;
+    const double* cfg = cf + (size_t)g * 2 * L * FB;
+    double* sub = wsb + (size_t)g * SUBW;
+    double* ubuf = sub + SUBW - 2 * L * 32;
+    double* fbuf = ubuf + L * 32;
+    const double* msub = ms + (size_t)g * 6 * M * M;
+    const int bar_id = 1 + g, bar_n = NQ * 32;
+    if (q == 0) {
+        sw4_warp<M, L, NLW, 1, true>(p, cfg, sub, ubuf, fbuf, msub, pwv, pmeta, s_src, s_prb, s_nbr, g, s, 0, lane,
+                                     bar_id, bar_n, ro);
+        return;
+    }
+    const int lo = 1 + (q - 1) * NLW;
+    const int nl = min(NLW, L - lo);
+    double* wb = sub + (32 + PW + 32) + (size_t)(q - 1) * NLW * (32 + PW);
+    if (nl == NLW) {
+        sw4_warp<M, L, NLW, NLW, false>(p, cfg, wb, ubuf, fbuf, msub, pwv, pmeta, s_src, s_prb, s_nbr, g, s, lo, lane,
+                                        bar_id, bar_n, ro);
+    } else if (NLW >= 2 && nl == 1) {
+        sw4_warp<M, L, NLW, 1, false>(p, cfg, wb, ubuf, fbuf, msub, pwv, pmeta, s_src, s_prb, s_nbr, g, s, lo, lane,
+                                      bar_id, bar_n, ro);
+    } else if (NLW >= 3 && nl == 2) {
+        sw4_warp<M, L, NLW, (NLW >= 3 ? 2 : 1), false>(p, cfg, wb, ubuf, fbuf, msub, pwv, pmeta, s_src, s_prb, s_nbr, g,
+                                                        s, lo, lane, bar_id, bar_n, ro);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_ustep: fp64 U-form stepping, warp per subdomain (configs 3 and 5).
 //
 // Same physics and arithmetic order per element as k_step2 (stepper.py:243-373), organised as
@@ -2680,16 +3054,45 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
                                                (const void*)k_step_sw<4, 7>, (const void*)k_step_sw<4, 8>};
             if (getenv("SFW_STEP_VERBOSE"))
                 fprintf(stderr, "[sfw] k_step_sw: maxns=%d L=%d smem=%zu\n", maxns, L, need);
-            if (maxns >= 1 && maxns <= 8 && need <= 220 * 1024) {
+            // layer-split variant: NLW layers per warp, NQ = 1 + ceil((L-1)/NLW) warps per subdomain
+            static const void* const ksw4[3][9] = {
+                {nullptr, nullptr, (const void*)k_step_sw4<4, 2, 1>, (const void*)k_step_sw4<4, 3, 1>,
+                 (const void*)k_step_sw4<4, 4, 1>, (const void*)k_step_sw4<4, 5, 1>, (const void*)k_step_sw4<4, 6, 1>,
+                 (const void*)k_step_sw4<4, 7, 1>, (const void*)k_step_sw4<4, 8, 1>},
+                {nullptr, nullptr, (const void*)k_step_sw4<4, 2, 2>, (const void*)k_step_sw4<4, 3, 2>,
+                 (const void*)k_step_sw4<4, 4, 2>, (const void*)k_step_sw4<4, 5, 2>, (const void*)k_step_sw4<4, 6, 2>,
+                 (const void*)k_step_sw4<4, 7, 2>, (const void*)k_step_sw4<4, 8, 2>},
+                {nullptr, nullptr, (const void*)k_step_sw4<4, 2, 3>, (const void*)k_step_sw4<4, 3, 3>,
+                 (const void*)k_step_sw4<4, 4, 3>, (const void*)k_step_sw4<4, 5, 3>, (const void*)k_step_sw4<4, 6, 3>,
+                 (const void*)k_step_sw4<4, 7, 3>, (const void*)k_step_sw4<4, 8, 3>}};
+            int nlw = 0;  // 0: one warp per subdomain (k_step_sw)
+            if (const char* e = getenv("SFW_SW_NLW")) {
+                nlw = atoi(e);
+            } else {
+                if (maxns <= 4) nlw = 2;  // measured at config 2: nlw 1 / 2 / 3 -> 3.71 / 2.86 / 2.99 us per step
+            }
+            nlw = std::max(0, std::min(3, nlw));
+            const int nq = nlw ? 1 + (L - 1 + nlw - 1) / nlw : 1;
+            const size_t sub_words = nlw ? (size_t)(32 + 42 * m + 32) + (size_t)(nq - 1) * nlw * (32 + 42 * m) +
+                                               (size_t)2 * L * 32
+                                         : 0;
+            const size_t need4 = 8 * ((size_t)maxns * 2 * L * 21 * m * m + (size_t)maxns * 6 * m * m +
+                                      (size_t)maxns * sub_words + (size_t)pdense * K) +
+                                 4 * 2 * (size_t)pmax;
+            if (nlw && (maxns > 4 || need4 > 220 * 1024)) nlw = 0;
+            if (maxns >= 1 && maxns <= 8 && (nlw ? need4 : need) <= 220 * 1024) {
                 TRY(dalloc(&h->swimg, (size_t)n * 2 * L * 21 * m * m, errbuf, errlen));
                 k_expand_sw<4><<<(unsigned)(n * 2 * L), 128, 0, h->stream>>>(h->coef, h->BS, h->swimg);
-                h->klw = ksw[L];
-                h->lw_smem = (int)need;
-                h->lw_threads = 32 * maxns;
+                h->klw = nlw ? ksw4[nlw - 1][L] : ksw[L];
+                h->lw_smem = (int)(nlw ? need4 : need);
+                h->lw_threads = 32 * maxns * nq;
+                if (getenv("SFW_STEP_VERBOSE"))
+                    fprintf(stderr, "[sfw] k_step_sw%s: nlw=%d nq=%d threads=%d smem=%d\n", nlw ? "4" : "", nlw, nq,
+                            h->lw_threads, h->lw_smem);
                 h->lw_groups = maxns;
                 h->res_pmax = pmax;
                 h->res_pdense = pdense;
-                SFW_CUDA_TRY(cudaFuncSetAttribute(h->klw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+                SFW_CUDA_TRY(cudaFuncSetAttribute(h->klw, cudaFuncAttributeMaxDynamicSharedMemorySize, h->lw_smem));
                 TRY(dalloc(&h->mbox, (size_t)2 * n * W * 2, errbuf, errlen));
                 SFW_CUDA_TRY(cudaMemsetAsync(h->mbox, 0, (size_t)2 * n * W * 2 * sizeof(unsigned long long), h->stream));
                 h->tag_base = 0;
@@ -2810,8 +3213,7 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
     p.rows = h->rows + (size_t)(step0 / record_every) * h->n_probe;
     p.sub_norm = h->sub_norm;
     p.norm_part = h->norm_part + (size_t)step0 * h->grid * (h->klw ? h->lw_groups : 1);
-    p.bar = h->bar;
-    SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int) * h->grid, h->stream));
+    p.bar = h->bar;  // step flags of the grid-barrier kernels (zeroed below; the mailbox kernels use tags)
     p.ncta_ptr = h->ncta_ptr;
     p.ncta = h->ncta;
     p.L = h->L;
@@ -2868,6 +3270,7 @@ static int launch_step(sfw_stepper* h, int mode, int n_steps, int record_every, 
         h->tag_base += (unsigned int)n_steps;
         return 0;
     }
+    SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int) * h->grid, h->stream));
     if (mode == 0 && h->kres && !Ucur) {
         SFW_CUDA_TRY(cudaLaunchCooperativeKernel(h->kres, dim3(h->grid), dim3(h->res_nw * 32), args, h->res_smem,
                                                  h->stream));

@@ -140,3 +140,25 @@ def test_config4_full_size_shots(cfg3):
         print(f"config4 shot {q}: vs single-source GPU run {e:.2e}, vs CPU oracle {eo:.2e}")
         assert e <= 1e-10
         assert eo <= 1e-9
+
+
+@pytest.mark.parametrize("nlw", ["1", "2", "3"])
+def test_config2_layer_split_bitwise(cfg2, nlw, monkeypatch):
+    """k_step_sw4 (a subdomain's layers split over 1 + ceil((L-1)/nlw) warps) runs the same block
+    products on the same data as the one-warp-per-subdomain k_step_sw: probe rows (face taps and
+    dense node weights, record_every 1 and 3), norms and both time levels are bit for bit equal."""
+    wl, models, dt, src, probes = cfg2
+    order = sorted(models)
+    rng = np.random.default_rng(5)
+    dense = [Probe(a, rng.standard_normal(models[a].state_size)) for a in (order[0], order[7], order[7], order[300])]
+    out = []
+    for env in ("0", nlw):
+        monkeypatch.setenv("SFW_SW_NLW", env)
+        with CoupledStepper(models, dt, sources=(src,)) as st:
+            r1 = st.run(97, probes=probes + dense)[1]
+            r3 = st.run(61, probes=probes + dense, record_every=3)[1]
+            out.append((r1, r3, st.u_curr, st.u_prev))
+    a, b = out
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for al in order:
+        assert np.array_equal(a[2][al], b[2][al]) and np.array_equal(a[3][al], b[3][al])
