@@ -1,29 +1,44 @@
-// Multi-shot stepping (BASELINE config 4): S independent wavefields advanced in
+// Multi-shot stepping (BASELINE config 4): S = 32 independent wavefields advanced in
 // one persistent launch.  The reference runs one CoupledStepper per shot
-// (stepper.py:144-449 with a single SourceTerm); here the
-// state of a subdomain layer is a w x S block and every chain block product
-// Gamma_j X / Gamma-hat_j X is a (w x w)(w x S) fp64 GEMM on the DMMA pipe
+// (stepper.py:144-449 with a single SourceTerm); here every chain
+// block product Gamma_j X / Gamma-hat_j X over the shots is an fp64 GEMM on the DMMA pipe
 // (mma.sync.m8n8k4.f64).
 //
-// Block storage: the lower 8 x 8 tiles (I >= K) of the padded w x w symmetric
-// block, each tile stored in DMMA A-fragment order (half h, lane l) ->
-// element (l/4, 4h + l%4).  Warp I owns output row-tile I and applies tile
-// (I,K) for K <= I and the transpose of tile (K,I) for K > I, so the symmetric
-// block is streamed once (+20% bytes over w(w+1)/2 for w = 54) and no
-// cross-warp reduction is needed.
+// Orientation.  The product is computed transposed, Y^T = X^T B (B symmetric): the shots
+// are the M dimension of the MMA, the rows of the block its K and N dimensions.  The
+// accumulator fragment of m8n8k4 gives lane l the elements (shot l/4, rows 8t + 2(l%4) + e),
+// e = 0, 1, of row tile t; the A fragment of a k-step wants (shot l/4, k = l%4).  Numbering
+// the k-steps kappa = 2T + e and letting position c of k-step kappa stand for row
+// 8T + 2c + e makes the accumulator of one GEMM, element for element in the same lane, the
+// A operand of the next: differences, leapfrog and the whole layer sweep of a subdomain
+// stay in registers.  One warp owns 8 shots of a subdomain and sweeps its layers alone; no
+// X tile goes through shared memory and no warp waits for another inside a sweep.  The row
+// permutation of the k-steps is folded into the stored chain blocks (the B operand).
 //
-// One CTA walks its subdomains; per step:
-//   phase A  flux_1, acc_1 = Gamma-hat_1 flux_1 of every subdomain (published)
-//   phase B  layers 2..L by a sliding window (U_j, U_{j+1}, flux_{j-1} in SMEM),
-//            leapfrog fused into the Gamma-hat epilogue
-//   phase C  (after the neighbour flags) layer-1 face coupling + leapfrog,
-//            per-shot |U|^2 partials and probe rows
+// Chain block storage: the lower 8 x 8 tiles (T >= t) of the padded symmetric block, each
+// tile's 64 doubles at the swizzled positions mt_pos(r, c), so that the B fragment of tile
+// (T, t) -- element (2(l%4) + e, l/4) -- and that of its transpose -- element (l/4, 2(l%4) + e)
+// of tile (t, T) -- are both conflict-free 8-byte shared loads.  A block is streamed once.
+//
+// CTA = 4 compute warps (shots 8w .. 8w+7) + 1 producer warp; two CTAs per SM.  One lane of
+// the producer warp streams chain blocks and 32-shot state blocks, in the order the sweep
+// consumes them, through a single ring of equal stages (cp.async.bulk + mbarrier).  Per step:
+//   sweep   per subdomain F_0 = G_0 (U_1 - U_0) -> face buffer (global); boundary subdomains
+//           also acc_0 = H_0 F_0; layers j = 1..L-1: F_j, A_j = H_j (F_j - F_{j-1}), leapfrog
+//   flags   CTA barrier, step flag, wait for the CTAs owning face neighbours
+//   faces   layer 0: T = F_0 + neighbour's F_0 on shared faces, acc_0 = mass T as a GEMM
+//           over the tiles that meet a face block (block-diagonal mass), leapfrog
+// State layout in HBM: [subdomain][layer][shot][WP rows] (rows padded to 8 RT, pad = 0), so a
+// lane's two adjacent rows are one 16-byte access and a warp's 8 shots of a row tile are
+// eight 64-byte segments.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "sfw_common.cuh"
@@ -53,7 +68,44 @@ __host__ __device__ inline int ms_packed_pos(int m, int row, int col) {
     return 15 * m * m + e * 6 + I;
 }
 
-// 6-group packed blocks -> fragment-ordered lower 8x8 tiles
+// position of element (r, c) inside a stored 8 x 8 tile.  Over the 16 lanes of a half-warp the
+// direct fragment {(2a + e, b)} and the transposed one {(b, 2a + e)}, a, b in 0..3, both hit 16
+// distinct 8-byte banks (low four bits: r1, c1, r2 ^ c2, r0 ^ c0).
+__host__ __device__ constexpr int mt_pos(int r, int c) {
+    return 16 * (2 * (r >> 2) + (r & 1)) + 8 * ((r >> 1) & 1) + 4 * ((c >> 1) & 1) + 2 * ((r >> 2) ^ (c >> 2)) +
+           ((r & 1) ^ (c & 1));
+}
+
+// does tile (T, t) of the block-diagonal interface mass (6 face blocks of m x m) hold a nonzero?
+__host__ __device__ constexpr bool mt_face_tile(int m, int T, int t) {
+    for (int f = 0; f < 6; ++f) {
+        const int lo = f * m, hi = lo + m;
+        if (lo < 8 * T + 8 && hi > 8 * T && lo < 8 * t + 8 && hi > 8 * t) return true;
+    }
+    return false;
+}
+
+// compact index of lower tile (T, t), T >= t, among the mass tiles (row-major lower order)
+__host__ __device__ constexpr int mt_mass_idx(int m, int T, int t) {
+    int n = 0;
+    for (int I = 0; I <= T; ++I)
+        for (int K = 0; K <= I; ++K) {
+            if (I == T && K == t) return n;
+            if (mt_face_tile(m, I, K)) ++n;
+        }
+    return n;
+}
+
+__host__ __device__ constexpr int mt_mass_count(int m) {
+    const int RT = (6 * m + 7) / 8;
+    int n = 0;
+    for (int I = 0; I < RT; ++I)
+        for (int K = 0; K <= I; ++K)
+            if (mt_face_tile(m, I, K)) ++n;
+    return n;
+}
+
+// 6-group packed blocks -> swizzled lower 8 x 8 tiles
 __global__ void k_tilepack(const double* __restrict__ packed, int BS, int m, int RT, int TB,
                            double* __restrict__ out, long long n_blocks) {
     const long long b = blockIdx.x;
@@ -63,29 +115,50 @@ __global__ void k_tilepack(const double* __restrict__ packed, int BS, int m, int
     double* dst = out + b * TB;
     const int ntl = RT * (RT + 1) / 2;
     for (int idx = threadIdx.x; idx < ntl * 64; idx += blockDim.x) {
-        const int t = idx / 64, within = idx % 64;
+        const int tl = idx / 64, within = idx % 64;
         int I = 0;
-        while ((I + 1) * (I + 2) / 2 <= t) ++I;
-        const int K = t - I * (I + 1) / 2;
-        const int h = within / 32, l = within % 32;
-        const int r = l >> 2, c = 4 * h + (l & 3);
+        while ((I + 1) * (I + 2) / 2 <= tl) ++I;
+        const int K = tl - I * (I + 1) / 2;
+        const int r = within / 8, c = within % 8;
         const int row = I * 8 + r, col = K * 8 + c;
-        dst[idx] = (row < w && col < w) ? src[ms_packed_pos(m, row, col)] : 0.0;
+        dst[tl * 64 + mt_pos(r, c)] = (row < w && col < w) ? src[ms_packed_pos(m, row, col)] : 0.0;
     }
 }
 
-struct MsParams {
-    int n_sub, L, W, WP, RT, TB, S, n_steps, record_every, n_probe, ftab_stride;
-    long long K;  // L*W
+// per-subdomain interface mass as swizzled tiles [n_sub][NMT][64] (zeros on outer faces; the mass
+// of an interface is symmetric, stepper.py:209)
+__global__ void k_mt_masstiles(const double* __restrict__ mass, const int* __restrict__ mass_idx, int n_sub, int m,
+                               int RT, int NMT, double* __restrict__ out) {
+    const int s = blockIdx.x;
+    if (s >= n_sub) return;
+    const int w = 6 * m;
+    for (int I = 0; I < RT; ++I)
+        for (int K = 0; K <= I; ++K) {
+            if (!mt_face_tile(m, I, K)) continue;
+            const int tl = mt_mass_idx(m, I, K);
+            for (int e = threadIdx.x; e < 64; e += blockDim.x) {
+                const int r = e / 8, c = e % 8, row = I * 8 + r, col = K * 8 + c;
+                double v = 0.0;
+                if (row < w && col < w && row / m == col / m) {
+                    const int mi = mass_idx[s * 6 + row / m];
+                    if (mi >= 0) v = mass[(size_t)mi * m * m + (row % m) * m + (col % m)];
+                }
+                out[((size_t)s * NMT + tl) * 64 + mt_pos(r, c)] = v;
+            }
+        }
+}
+
+struct MtParams {
+    int n_sub, L, n_steps, record_every, n_probe, ftab_stride, nst;
+    int n_team, team_smem;  // teams in the launch (two per CTA); shared-memory bytes of one team
     double dt2;
-    const double* tcoef;
+    const double* tcoef;   // [n_blocks][TB] swizzled lower tiles; block 2j = Gamma_j, 2j+1 = Gamma-hat_j
+    const double* mtiles;  // [n_sub][NMT][64]
     double* U0;
-    double* U1;
-    double* flux;   // [n_sub][W][S] layer-1 flux (face mailbox), double-buffered by parity
-    double* acc1;   // [n_sub][W][S]
+    double* U1;            // [n_sub][L][S][WP]
+    double* flux;          // [2][n_sub][S][WP] layer-0 flux F_0 (face mailbox), double-buffered by parity
+    double* acc1;          // [n_sub][S][WP] H_0 F_0 of boundary subdomains
     const int* nbr;
-    const int* mass_idx;
-    const double* mass;
     const int* cta_sub_ptr;
     const int* shot_sub;   // [S] source subdomain of each shot (-1: none)
     const double* shot_vec;
@@ -101,594 +174,419 @@ struct MsParams {
     unsigned int* flags;
     const int* ncta_ptr;
     const int* ncta;
-    int evict_first;
-    unsigned long long* dbg;  // debug cycle counters (SFW_MS_CLK builds) or null
-    const double* mblk;       // [n_sub][6][M*M] interface mass per face (0 for outer faces)
 };
 
-// ---------------------------------------------------------------------------
-// k_step_ms2: shot-column-parallel multi-shot stepping.  8 compute warps: warp
-// (c, hh) owns shots 8c..8c+7 and output row tiles [hh*RH, hh*RH+RH) of every
-// layer GEMM B X (B = Gamma_j or Gamma-hat_j, 56 x 56 symmetric, X 56 x 8), two
-// warps per SMSP (the FP64 tensor pipe needs two LDS-fed DMMA streams per SMSP:
-// measured 1 DMMA / 4.0 SM cycles with 8 warps vs 5.3 with 4).  Shots are
-// independent: the two warps of a column pair exchange only their X rows
-// (double-buffered, one 64-thread named barrier per GEMM); all warps share the
-// TMA-streamed chain blocks and state blocks (full/empty mbarriers, 8 consumer
-// arrivals per stage).  The lane's output fragment (row 8I + l/4, shots q0, q0+1)
-// is also the slice of U / flux it owns in registers across the layer sweep.
-//   per subdomain (A+B): F_0 = G_0 (U_1 - U_0) -> face buffer; acc_0 = H_0 F_0;
-//     j = 1..L-1: F_j = G_j (U_{j+1} - U_j); A_j = H_j (F_j - F_{j-1}); leapfrog.
-//   after all subdomains: step flag; neighbour flags; C: layer-1 coupling + leapfrog.
-constexpr int M2_NC = 4;    // chain-block stages (5 with a swizzled 8-wide X tile measured 4% slower)
-constexpr int M2_NSS = 8;   // state-block stages
-constexpr int M2_LDX = 12;  // padded X row stride (conflict-free fragment reads)
-__device__ __forceinline__ int m2_xs(int row, int col) { return row * M2_LDX + col; }
-constexpr int M2_NQ = 4;    // warps per shot column tile (row-tile groups)
-constexpr int M2_NW = 4 * M2_NQ;  // compute warps
+constexpr int MT_NCW = 4;  // compute warps per CTA (8 shots each)
 
-template <int M, int HH>  // HH: row-tile group of this warp (0..M2_NQ-1)
-__device__ __forceinline__ void ms2_compute(const MsParams& p, const double* cst, const double* sst, double* Xpair,
-                                            uint64_t* cfull, uint64_t* cempty, uint64_t* sfull, uint64_t* sempty,
-                                            uint64_t* stepdone, const int* ssub, const int* s_nb, int s0, int ns,
-                                            int cw, int lane) {
-    constexpr int S = 32;
-    constexpr int RT = (6 * M + 7) / 8;
-    constexpr int RH = (RT + M2_NQ - 1) / M2_NQ;  // row tiles per group
-    constexpr int I0 = HH * RH;                   // first row tile of this warp
-    constexpr int NI = (RT - I0 >= RH) ? RH : (RT - I0 > 0 ? RT - I0 : 1);  // row tiles of this warp (>= 1 slot)
-    constexpr int WP = 8 * RT;
-    constexpr int W = 6 * M;
-    const int TB = p.TB, L = p.L;
-    const long long K = p.K;
-    const long long WS = (long long)W * S, KS = K * S;
-    const int barP = 2 + cw;                    // named barrier of the column group (NQ warps)
-    int tr[2];
+template <int M>
+struct MtDims {
+    static constexpr int S = 32;
+    static constexpr int W = 6 * M;
+    static constexpr int RT = (W + 7) / 8;
+    static constexpr int WP = 8 * RT;
+    static constexpr int TB = RT * (RT + 1) / 2 * 64;  // doubles per chain block
+    static constexpr int SB = S * WP;                  // doubles per 32-shot state block
+    static constexpr int STG = TB > SB ? TB : SB;      // ring stage (doubles)
+    static constexpr int NMT = mt_mass_count(M);
+};
+
+// compile-time loop: f(std::integral_constant<int, 0>{}), ..., f(std::integral_constant<int, N - 1>{})
+template <typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// acc^T = x^T B over all row tiles; x, acc in accumulator-fragment layout (see the header comment).
+// MASS: B = block-diagonal interface mass, only the tiles that meet a face block.  RT independent
+// accumulator chains; every tile offset is an immediate.
+template <int M, bool MASS>
+__device__ __forceinline__ void mt_gemm(const double* __restrict__ tiles, const double (&x)[MtDims<M>::RT][2],
+                                        double (&acc)[MtDims<M>::RT][2], const int (&dir)[2], const int (&trn)[2]) {
+    constexpr int RT = MtDims<M>::RT;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int r = 4 * h + (lane & 3), c = lane >> 2;
-        tr[h] = (c >> 2) * 32 + r * 4 + (c & 3);
+    for (int t = 0; t < RT; ++t) acc[t][0] = acc[t][1] = 0.0;
+    static_for<2 * RT>([&](auto kc) {
+        constexpr int T = decltype(kc)::value / 2, e = decltype(kc)::value % 2;
+        const double a = x[T][e];
+        static_for<RT>([&](auto tc) {
+            constexpr int t = decltype(tc)::value;
+            if constexpr (!MASS || mt_face_tile(M, T, t)) {
+                constexpr int hi = T >= t ? T : t, lo = T >= t ? t : T;
+                constexpr int tl = MASS ? mt_mass_idx(M, hi, lo) : hi * (hi + 1) / 2 + lo;
+                const double b = tiles[tl * 64 + (T >= t ? dir[e] : trn[e])];
+                dmma8x8x4(acc[t], a, b);
+            }
+        });
+    });
+}
+
+template <int M>
+__device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring, uint64_t* full, uint64_t* empty,
+                                           uint64_t* stepdone, const int* ssub, const int* s_nb, int s0, int ns,
+                                           int team, int w, int lane) {
+    using D = MtDims<M>;
+    constexpr int S = D::S, W = D::W, RT = D::RT, WP = D::WP, SB = D::SB, STG = D::STG;
+    const int L = p.L, NST = p.nst;
+    const long long KS = (long long)L * SB;
+    const int g = lane >> 2, c = lane & 3;
+    const int q = 8 * w + g;              // this lane's shot
+    const int lo = q * WP + 2 * c;        // offset of (shot q, row 2c) in a state block
+    int dir[2], trn[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        dir[e] = mt_pos(2 * c + e, g);
+        trn[e] = mt_pos(g, 2 * c + e);
     }
-    long long c_con = 0, s_con = 0;
-    int xb = 0;  // X double buffer
-#ifdef SFW_MS_CLK
-    long long clk[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // c-wait, s-wait, gemm, total, flags, C, tail
-    const long long clk_start = clock64();
-#define MS_T0 const long long t0_ = clock64();
-#define MS_T1(i) clk[i] += clock64() - t0_;
-#else
-#define MS_T0
-#define MS_T1(i)
-#endif
-    auto c_acquire = [&]() -> const double* {
-        const int st = (int)(c_con % M2_NC);
-        MS_T0
-        mbar_wait(&cfull[st], (uint32_t)((c_con / M2_NC) & 1));
-        MS_T1(0)
-        return cst + (size_t)st * TB;
+    // ring cursor (same item sequence in every compute warp and in the producer)
+    int st = 0;
+    uint32_t ph = 0;
+    auto acquire = [&](int o) -> const double* {
+        int s2 = st + o;
+        uint32_t p2 = ph;
+        if (s2 >= NST) {
+            s2 -= NST;
+            p2 ^= 1;
+        }
+        mbar_wait(&full[s2], p2);
+        return ring + (size_t)s2 * STG;
     };
-    auto c_release = [&]() {
+    auto release = [&]() {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&cempty[c_con % M2_NC]);
-        ++c_con;
-    };
-    auto s_acquire_at = [&](int o) -> const double* {  // o-th stage after the next unreleased one
-        const long long c = s_con + o;
-        const int st = (int)(c % M2_NSS);
-        MS_T0
-        mbar_wait(&sfull[st], (uint32_t)((c / M2_NSS) & 1));
-        MS_T1(1)
-        return sst + (size_t)st * WS;
-    };
-    auto s_release = [&]() {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[s_con % M2_NSS]);
-        ++s_con;
-    };
-    const int r0 = lane >> 2;              // fragment row within a row tile
-    const int q0 = 8 * cw + 2 * (lane & 3);  // first of the lane's two shots
-    auto load_slice = [&](const double* blk, double (&v)[NI][2]) {
-#pragma unroll
-        for (int i = 0; i < NI; ++i) {
-            const int row = 8 * (I0 + i) + r0;
-            if (row < W) {
-                const double2 t = *reinterpret_cast<const double2*>(blk + (size_t)row * S + q0);
-                v[i][0] = t.x;
-                v[i][1] = t.y;
-            } else {
-                v[i][0] = v[i][1] = 0.0;
-            }
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == NST) {
+            st = 0;
+            ph ^= 1;
         }
     };
-    // write this warp's rows of X into the pair's next buffer, then meet the partner
-    auto put_x = [&](const double (&v)[NI][2]) -> const double* {
-        xb ^= 1;
-        double* Xw = Xpair + (size_t)xb * WP * M2_LDX;
+    auto load_slice = [&](const double* blk, double (&v)[RT][2]) {
 #pragma unroll
-        for (int i = 0; i < NI; ++i)
-            if (I0 + i < RT)
-                *reinterpret_cast<double2*>(Xw + m2_xs(8 * (I0 + i) + r0, 2 * (lane & 3))) =
-                    make_double2(v[i][0], v[i][1]);
-        asm volatile("bar.sync %0, %1;" ::"r"(barP), "r"(M2_NQ * 32) : "memory");
-        return Xw;
+        for (int t = 0; t < RT; ++t) {
+            const double2 d = *reinterpret_cast<const double2*>(blk + lo + 8 * t);
+            v[t][0] = d.x;
+            v[t][1] = d.y;
+        }
     };
-    // acc = B X over this warp's row tiles, B symmetric (lower tiles, fragment order)
-    // two accumulator chains per row tile (even / odd k-steps, summed at the end): 2 NI independent
-    // DMMA chains per warp, so one warp alone keeps its SMSP's FP64 tensor pipe fed
-    auto gemm = [&](const double* tiles, const double* Xw, double (&acc)[NI][2]) {
-        MS_T0
-        double acc2[NI][2];
+    auto store_slice = [&](double* blk, const double (&v)[RT][2]) {
 #pragma unroll
-        for (int i = 0; i < NI; ++i) acc[i][0] = acc[i][1] = acc2[i][0] = acc2[i][1] = 0.0;
-#pragma unroll
-        for (int kap = 0; kap < 2 * RT; ++kap) {
-            const int Kt = kap >> 1, h = kap & 1;
-            const double b = Xw[m2_xs(4 * kap + (lane & 3), r0)];
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-                const int I = I0 + i;
-                if (I >= RT) break;
-                const double a = (I >= Kt) ? tiles[(I * (I + 1) / 2 + Kt) * 64 + h * 32 + lane]
-                                           : tiles[(Kt * (Kt + 1) / 2 + I) * 64 + tr[h]];
-                if (h)
-                    dmma8x8x4(acc2[i], a, b);
-                else
-                    dmma8x8x4(acc[i], a, b);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < NI; ++i) {
-            acc[i][0] += acc2[i][0];
-            acc[i][1] += acc2[i][1];
-        }
-#ifdef SFW_MS_CLK
-        for (int i = 0; i < NI; ++i) asm volatile("" ::"d"(acc[i][0]), "d"(acc[i][1]));
-#endif
-        MS_T1(2)
-    };
-    auto store_global = [&](double* blk, const double (&v)[NI][2]) {
-#pragma unroll
-        for (int i = 0; i < NI; ++i) {
-            const int row = 8 * (I0 + i) + r0;
-            if (row < W) *reinterpret_cast<double2*>(blk + (size_t)row * S + q0) = make_double2(v[i][0], v[i][1]);
-        }
+        for (int t = 0; t < RT; ++t)
+            *reinterpret_cast<double2*>(blk + lo + 8 * t) = make_double2(v[t][0], v[t][1]);
     };
     const double dt2 = p.dt2;
-    const bool src0 = ssub[q0] >= 0, src1 = ssub[q0 + 1] >= 0;
+    const int barT = 1 + (int)(threadIdx.x >= (MT_NCW + 1) * 32);  // named barrier of the team's compute warps
+    const int my_src = ssub[q];           // source subdomain of this lane's shot
+    const double* svec = my_src >= 0 ? p.shot_vec + p.shot_voff[q] : nullptr;
 
     for (int k = 1; k <= p.n_steps; ++k) {
         const int par = k & 1;
         const int cb = (k - 1) & 1;
         double* Un = cb ? p.U0 : p.U1;
-        double* fx = p.flux + (size_t)par * p.n_sub * WS;
+        double* fx = p.flux + (size_t)par * p.n_sub * SB;
         const int kk = k - 1;
-        const double f0 = src0 ? p.ftab[(size_t)q0 * p.ftab_stride + kk] : 0.0;
-        const double f1 = src1 ? p.ftab[(size_t)(q0 + 1) * p.ftab_stride + kk] : 0.0;
-        double sq0 = 0.0, sq1 = 0.0;
-        auto force = [&](int s, long long idx, int e) -> double {  // shot source term (ssub[q] == s)
-            const int q = q0 + e;
-            return __dmul_rn(p.shot_vec[p.shot_voff[q] + idx], e ? f1 : f0);
-        };
+        const double fq = my_src >= 0 ? p.ftab[(size_t)q * p.ftab_stride + kk] : 0.0;
+        double sq = 0.0;
 
-        // ---------------- A + B: every subdomain's layer sweep --------------------------
+        // ---------------- sweep: layers of every subdomain, all in registers ---------------
         for (int sl = 0; sl < ns; ++sl) {
             const int s = s0 + sl;
-            double ua[NI][2], ub[NI][2], fp[NI][2], acc[NI][2];
-            const double* Xw;
+            const bool mine = my_src == s;
+            double ua[RT][2], ub[RT][2], fp[RT][2], x[RT][2], acc[RT][2];
             {
-                double u0[NI][2];
-                load_slice(s_acquire_at(0), u0);
-                load_slice(s_acquire_at(1), ua);  // U_1
-                s_release();
-                s_release();
+                const double* b0 = acquire(0);
+                const double* b1 = acquire(1);
+                load_slice(b0, x);   // U_0
+                load_slice(b1, ua);  // U_1
+                release();
+                release();
 #pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    u0[i][0] = ua[i][0] - u0[i][0];
-                    u0[i][1] = ua[i][1] - u0[i][1];
+                for (int t = 0; t < RT; ++t) {
+                    x[t][0] = ua[t][0] - x[t][0];
+                    x[t][1] = ua[t][1] - x[t][1];
                 }
-                Xw = put_x(u0);
             }
-            gemm(c_acquire(), Xw, fp);  // F_0
-            c_release();
-            store_global(fx + (size_t)s * WS, fp);
-            const bool interior = s_nb[sl * 6] >= 0 && s_nb[sl * 6 + 1] >= 0 && s_nb[sl * 6 + 2] >= 0 &&
-                                  s_nb[sl * 6 + 3] >= 0 && s_nb[sl * 6 + 4] >= 0 && s_nb[sl * 6 + 5] >= 0;
-            if (!interior) {  // acc_0 = H_0 F_0: only outer-face rows are ever read back
-                Xw = put_x(fp);
-                gemm(c_acquire(), Xw, acc);
-                c_release();
-#pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    const int row = 8 * (I0 + i) + r0;
-                    if (row < W && s_nb[sl * 6 + row / M] < 0)
-                        *reinterpret_cast<double2*>(p.acc1 + ((size_t)s * W + row) * S + q0) =
-                            make_double2(acc[i][0], acc[i][1]);
-                }
+            mt_gemm<M, false>(acquire(0), x, fp, dir, trn);  // F_0
+            release();
+            store_slice(fx + (size_t)s * SB, fp);
+            const bool interior = (s_nb[sl * 6] | s_nb[sl * 6 + 1] | s_nb[sl * 6 + 2] | s_nb[sl * 6 + 3] |
+                                   s_nb[sl * 6 + 4] | s_nb[sl * 6 + 5]) >= 0;
+            if (!interior) {  // acc_0 = H_0 F_0: only outer-face rows are read back
+                mt_gemm<M, false>(acquire(0), fp, acc, dir, trn);
+                release();
+                store_slice(p.acc1 + (size_t)s * SB, acc);
             }
             for (int j = 1; j < L; ++j) {
                 if (j + 1 < L) {
-                    load_slice(s_acquire_at(0), ub);  // U_{j+1}
-                    s_release();
+                    load_slice(acquire(0), ub);  // U_{j+1}
+                    release();
                 } else {
 #pragma unroll
-                    for (int i = 0; i < NI; ++i) ub[i][0] = ub[i][1] = 0.0;
+                    for (int t = 0; t < RT; ++t) ub[t][0] = ub[t][1] = 0.0;
                 }
-                {
-                    double x[NI][2];
 #pragma unroll
-                    for (int i = 0; i < NI; ++i) {
-                        x[i][0] = ub[i][0] - ua[i][0];
-                        x[i][1] = ub[i][1] - ua[i][1];
-                    }
-                    Xw = put_x(x);
+                for (int t = 0; t < RT; ++t) {
+                    x[t][0] = ub[t][0] - ua[t][0];
+                    x[t][1] = ub[t][1] - ua[t][1];
                 }
-                gemm(c_acquire(), Xw, acc);  // F_j
-                c_release();
-                {
-                    double x[NI][2];
+                mt_gemm<M, false>(acquire(0), x, acc, dir, trn);  // F_j
+                release();
 #pragma unroll
-                    for (int i = 0; i < NI; ++i) {
-                        x[i][0] = acc[i][0] - fp[i][0];
-                        x[i][1] = acc[i][1] - fp[i][1];
-                        fp[i][0] = acc[i][0];
-                        fp[i][1] = acc[i][1];
-                    }
-                    Xw = put_x(x);
+                for (int t = 0; t < RT; ++t) {
+                    x[t][0] = acc[t][0] - fp[t][0];
+                    x[t][1] = acc[t][1] - fp[t][1];
+                    fp[t][0] = acc[t][0];
+                    fp[t][1] = acc[t][1];
                 }
-                double uo[NI][2];
-                load_slice(s_acquire_at(0), uo);  // Uprev_j
-                s_release();
-                gemm(c_acquire(), Xw, acc);  // A_j
-                c_release();
-                double* un = Un + (size_t)s * KS + (size_t)j * WS;
+                mt_gemm<M, false>(acquire(0), x, acc, dir, trn);  // A_j
+                release();
+                const double* uo = acquire(0);  // Uprev_j
+                double* un = Un + (size_t)s * KS + (size_t)j * SB;
 #pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    const int row = 8 * (I0 + i) + r0;
+                for (int t = 0; t < RT; ++t) {
+                    const double2 o = *reinterpret_cast<const double2*>(uo + lo + 8 * t);
                     double v[2];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        double tot = acc[i][e];
-                        if ((e ? src1 : src0) && row < W && ssub[q0 + e] == s)
-                            tot = __dadd_rn(tot, force(s, (long long)j * W + row, e));
-                        v[e] = __dadd_rn(__dsub_rn(__dmul_rn(2.0, ua[i][e]), uo[i][e]), __dmul_rn(dt2, tot));
+                        double tot = acc[t][e];
+                        const int row = 8 * t + 2 * c + e;
+                        if (mine && row < W) tot = __dadd_rn(tot, __dmul_rn(svec[(long long)j * W + row], fq));
+                        v[e] = fma(dt2, tot, fma(2.0, ua[t][e], e ? -o.y : -o.x));
+                        sq = fma(v[e], v[e], sq);
                     }
-                    if (row < W) {
-                        *reinterpret_cast<double2*>(un + (size_t)row * S + q0) = make_double2(v[0], v[1]);
-                        sq0 = fma(v[0], v[0], sq0);
-                        sq1 = fma(v[1], v[1], sq1);
-                    }
+                    *reinterpret_cast<double2*>(un + lo + 8 * t) = make_double2(v[0], v[1]);
                 }
+                release();
 #pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    ua[i][0] = ub[i][0];
-                    ua[i][1] = ub[i][1];
+                for (int t = 0; t < RT; ++t) {
+                    ua[t][0] = ub[t][0];
+                    ua[t][1] = ub[t][1];
                 }
             }
         }
         // ---------------- step flag, neighbour flags ------------------------------------
-#ifdef SFW_MS_CLK
-        long long tf0 = clock64();
-#endif
-        asm volatile("bar.sync 1, %0;" ::"r"(M2_NW * 32) : "memory");
-        if (cw == 0 && HH == 0 && lane == 0) flag_publish(p.flags, (unsigned int)k);
-        if (cw == 0 && HH == 0)
-            flags_wait(p.flags, p.ncta + p.ncta_ptr[blockIdx.x], p.ncta_ptr[blockIdx.x + 1] - p.ncta_ptr[blockIdx.x],
-                       (unsigned int)k, lane);
-        asm volatile("bar.sync 1, %0;" ::"r"(M2_NW * 32) : "memory");
-#ifdef SFW_MS_CLK
-        clk[4] += clock64() - tf0;
-        tf0 = clock64();
-#endif
-        // ---------------- C: layer-1 face coupling + leapfrog ---------------------------
+        // (bar.sync orders the team's face-buffer writes before lane 0's release store: cumulativity)
+        asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
+        if (w == 0 && lane == 0) st_release(p.flags + team, (unsigned int)k);
+        if (w == 0)
+            flags_wait(p.flags, p.ncta + p.ncta_ptr[team], p.ncta_ptr[team + 1] - p.ncta_ptr[team], (unsigned int)k,
+                       lane);
+        asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
+        // ---------------- faces: layer-0 coupling + leapfrog -----------------------------
         for (int sl = 0; sl < ns; ++sl) {
             const int s = s0 + sl;
-            const double* mb = s_acquire_at(0);  // [6][M][M] interface mass
-            // own + neighbour layer-1 flux of every face row, the pair's 8 shots; each warp
-            // of the pair stages half of the rows (independent loads: one L2 round trip)
-            xb ^= 1;
-            double* T = Xpair + (size_t)xb * WP * M2_LDX;
-            {
-                constexpr int NROW = (6 * M + M2_NQ - 1) / M2_NQ;  // rows per warp
-                constexpr int NIT = (NROW * 4 + 31) / 32;
-                double2 ow[NIT], ot[NIT];
+            const bool mine = my_src == s;
+            double x[RT][2], acc[RT][2], a1[RT][2];
+            const double* fo = fx + (size_t)s * SB + lo;
+            const double* ao = p.acc1 + (size_t)s * SB + lo;
 #pragma unroll
-                for (int t = 0; t < NIT; ++t) {
-                    const int it = lane + 32 * t, row = HH * NROW + (it >> 2), pr = it & 3;
-                    ow[t] = ot[t] = make_double2(0.0, 0.0);
-                    if ((it >> 2) < NROW && row < 6 * M) {
-                        const int f = row / M, c = row % M, nb = s_nb[sl * 6 + f];
-                        if (nb >= 0) {
-                            ow[t] = __ldcg(reinterpret_cast<const double2*>(fx + ((size_t)s * W + row) * S + 8 * cw + 2 * pr));
-                            ot[t] = __ldcg(reinterpret_cast<const double2*>(fx + ((size_t)nb * W + (f ^ 1) * M + c) * S +
-                                                                           8 * cw + 2 * pr));
-                        }
+            for (int t = 0; t < RT; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = 8 * t + 2 * c + e;
+                    x[t][e] = 0.0;
+                    a1[t][e] = 0.0;
+                    if (row < W) {
+                        const int f = row / M, nb = s_nb[sl * 6 + f];
+                        if (nb >= 0)
+                            x[t][e] = __dadd_rn(__ldcg(fo + 8 * t + e),
+                                                __ldcg(fx + (size_t)nb * SB + q * WP + (f ^ 1) * M + row % M));
+                        else
+                            a1[t][e] = __ldcg(ao + 8 * t + e);
                     }
                 }
-#pragma unroll
-                for (int t = 0; t < NIT; ++t) {
-                    const int it = lane + 32 * t, row = HH * NROW + (it >> 2), pr = it & 3;
-                    if ((it >> 2) < NROW && row < 6 * M)
-                        *reinterpret_cast<double2*>(T + m2_xs(row, 2 * pr)) =
-                            make_double2(__dadd_rn(ow[t].x, ot[t].x), __dadd_rn(ow[t].y, ot[t].y));
-                }
-            }
-            double a1[NI][2];
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {  // boundary-face accelerations (prefetch)
-                const int row = 8 * (I0 + i) + r0;
-                a1[i][0] = a1[i][1] = 0.0;
-                if (row < W && s_nb[sl * 6 + row / M] < 0) {
-                    const double2 t = __ldcg(reinterpret_cast<const double2*>(p.acc1 + ((size_t)s * W + row) * S + q0));
-                    a1[i][0] = t.x;
-                    a1[i][1] = t.y;
-                }
-            }
-            asm volatile("bar.sync %0, %1;" ::"r"(barP), "r"(M2_NQ * 32) : "memory");
-            double u0[NI][2], uo[NI][2];
-            load_slice(s_acquire_at(1), u0);
-            load_slice(s_acquire_at(2), uo);
+            mt_gemm<M, true>(acquire(0), x, acc, dir, trn);
+            const double* u0 = acquire(1);
+            const double* uo = acquire(2);
             double* un = Un + (size_t)s * KS;
 #pragma unroll
-            for (int i = 0; i < NI; ++i) {
-                const int row = 8 * (I0 + i) + r0;
-                if (row >= W) continue;
-                const int f = row / M, r = row % M;
-                double a[2] = {a1[i][0], a1[i][1]};
-                if (s_nb[sl * 6 + f] >= 0) {
-                    a[0] = a[1] = 0.0;
-                    const double* mx = mb + (f * M + r) * M;
-#pragma unroll
-                    for (int c = 0; c < M; ++c) {
-                        const double mc = mx[c];
-                        const double2 t = *reinterpret_cast<const double2*>(T + m2_xs(f * M + c, 2 * (lane & 3)));
-                        a[0] = fma(mc, t.x, a[0]);
-                        a[1] = fma(mc, t.y, a[1]);
-                    }
-                }
+            for (int t = 0; t < RT; ++t) {
+                const double2 u = *reinterpret_cast<const double2*>(u0 + lo + 8 * t);
+                const double2 o = *reinterpret_cast<const double2*>(uo + lo + 8 * t);
                 double v[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    double tot = a[e];
-                    if ((e ? src1 : src0) && ssub[q0 + e] == s) tot = __dadd_rn(tot, force(s, row, e));
-                    v[e] = __dadd_rn(__dsub_rn(__dmul_rn(2.0, u0[i][e]), uo[i][e]), __dmul_rn(dt2, tot));
+                    const int row = 8 * t + 2 * c + e;
+                    double tot = __dadd_rn(acc[t][e], a1[t][e]);  // one of the two is zero
+                    if (mine && row < W) tot = __dadd_rn(tot, __dmul_rn(svec[row], fq));
+                    v[e] = fma(dt2, tot, fma(2.0, e ? u.y : u.x, e ? -o.y : -o.x));
+                    sq = fma(v[e], v[e], sq);
                 }
-                *reinterpret_cast<double2*>(un + (size_t)row * S + q0) = make_double2(v[0], v[1]);
-                sq0 = fma(v[0], v[0], sq0);
-                sq1 = fma(v[1], v[1], sq1);
+                *reinterpret_cast<double2*>(un + lo + 8 * t) = make_double2(v[0], v[1]);
             }
-            s_release();  // mass
-            s_release();  // U_0
-            s_release();  // Uprev_0
+            release();  // mass tiles
+            release();  // U_0
+            release();  // Uprev_0
         }
-#ifdef SFW_MS_CLK
-        clk[5] += clock64() - tf0;
-        tf0 = clock64();
-#endif
-        // per-shot |U|^2 of this warp's rows: lanes with equal (lane & 3) hold the same shots;
-        // the pair's two halves go to separate partial slots (k_ms_norms sums them)
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-            sq0 += __shfl_xor_sync(0xffffffffu, sq0, o);
-            sq1 += __shfl_xor_sync(0xffffffffu, sq1, o);
-        }
-        if (lane < 4) {
-            double* np = p.norm_part + (((size_t)kk * gridDim.x + blockIdx.x) * M2_NQ + HH) * S + q0;
-            np[0] = sq0;
-            np[1] = sq1;
-        }
-        // probes (this warp: its pair's 8 shots, every other probe): rows of U after the step
+        // per-shot |U|^2 of this CTA: the 4 lanes of a shot hold its rows
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+        if (c == 0) p.norm_part[((size_t)kk * p.n_team + team) * S + q] = sq;
+        // probes: rows of U after the step (thread = shot x every 4th probe)
         if (k % p.record_every == 0 && p.rows) {
-            asm volatile("bar.sync %0, %1;" ::"r"(barP), "r"(M2_NQ * 32) : "memory");  // group's U rows written
-            const long long row = k / p.record_every - 1;
-            const int q = 8 * cw + (lane & 7);
+            asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");  // the team's U rows are written
+            const long long rec = k / p.record_every - 1;
+            const int pq0 = w, qs = lane;  // thread (w, lane): shot lane, probes w, w+4, ...
             for (int s = s0; s < s0 + ns; ++s) {
-                const double* us = Un + (size_t)s * KS;
-                for (int pq = p.prb_ptr[s] + M2_NQ * (lane >> 3) + HH; pq < p.prb_ptr[s + 1]; pq += 4 * M2_NQ) {
+                const double* us = Un + (size_t)s * KS + (size_t)qs * WP;
+                for (int pq = p.prb_ptr[s] + pq0; pq < p.prb_ptr[s + 1]; pq += MT_NCW) {
                     const int pid = p.prb_ids[pq];
                     const int tap = p.prb_tap[pid];
                     double val;
                     if (tap >= 0) {
-                        val = us[(size_t)tap * S + q];
+                        val = us[(size_t)(tap / W) * SB + tap % W];
                     } else {
                         const double* wv = p.prb_w + p.prb_woff[pid];
                         val = 0.0;
-                        for (long long i = 0; i < K; ++i) val = fma(wv[i], us[i * S + q], val);
+                        for (int j = 0; j < L; ++j)
+                            for (int r = 0; r < W; ++r) val = fma(wv[j * W + r], us[(size_t)j * SB + r], val);
                     }
-                    p.rows[(row * S + q) * p.n_probe + pid] = val;  // [rec][shot][probe]
+                    p.rows[(rec * S + qs) * p.n_probe + pid] = val;  // [rec][shot][probe]
                 }
             }
         }
-        // this step's state writes feed the next step's TMA reads (async proxy)
+        // this step's state writes feed the next step's bulk-copy reads (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(stepdone);
-#ifdef SFW_MS_CLK
-        clk[6] += clock64() - tf0;
-#endif
     }
-#ifdef SFW_MS_CLK
-    clk[3] = clock64() - clk_start;
-    if (lane < 8 && p.dbg) {
-        long long v = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (lane == i) v = clk[i];
-        p.dbg[(blockIdx.x * M2_NW + M2_NQ * cw + HH) * 8 + lane] = v;
-    }
-#endif
-#undef MS_T0
-#undef MS_T1
 }
 
 template <int M>
-__global__ void __launch_bounds__((M2_NW + 2) * 32, 1) k_step_ms2(const MsParams p) {
-    constexpr int S = 32;
-    constexpr int RT = (6 * M + 7) / 8;
-    constexpr int WP = 8 * RT;
-    constexpr int W = 6 * M;
+__global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtParams p) {
+    using D = MtDims<M>;
+    constexpr int S = D::S, TB = D::TB, SB = D::SB, STG = D::STG, NMT = D::NMT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int L = p.L, TB = p.TB;
-    const long long K = p.K;
-    const long long WS = (long long)W * S, KS = K * S;
-    double* cst = reinterpret_cast<double*>(smem_raw);   // [NC][TB]
-    double* sst = cst + (size_t)M2_NC * TB;              // [NSS][W*S]
-    double* Xall = sst + (size_t)M2_NSS * WS;            // [4 column groups][2][WP][LDX]
-    uint64_t* cfull = reinterpret_cast<uint64_t*>(Xall + (size_t)4 * 2 * WP * M2_LDX);
-    uint64_t* cempty = cfull + M2_NC;
-    uint64_t* sfull = cempty + M2_NC;
-    uint64_t* sempty = sfull + M2_NSS;
-    uint64_t* stepdone = sempty + M2_NSS;
+    // a CTA hosts two independent teams (5 warps each: 4 compute + 1 producer) with their own rings,
+    // subdomain ranges and step flags: two sweeps in flight per SM, two compute warps per SMSP
+    const int tw = threadIdx.x / ((MT_NCW + 1) * 32);
+    const int team = 2 * blockIdx.x + tw;
+    if (team >= p.n_team) return;
+    const int tid = threadIdx.x - tw * (MT_NCW + 1) * 32;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int L = p.L, NST = p.nst;
+    const long long KS = (long long)L * SB;
+    double* ring = reinterpret_cast<double*>(smem_raw + (size_t)tw * p.team_smem);  // [NST][STG]
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NST * STG);
+    uint64_t* empty = full + NST;
+    uint64_t* stepdone = empty + NST;
     int* ssub = reinterpret_cast<int*>(stepdone + 1);
-    int* s_nb = ssub + S;  // [ns][6] face neighbours of the CTA's subdomains
+    int* s_nb = ssub + S;  // [ns][6] face neighbours of the team's subdomains
 
-    for (int q = threadIdx.x; q < S; q += blockDim.x) ssub[q] = p.shot_sub[q];
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < M2_NC; ++i) {
-            mbar_init(&cfull[i], 1);
-            mbar_init(&cempty[i], M2_NW);
+    for (int i = tid; i < S; i += (MT_NCW + 1) * 32) ssub[i] = p.shot_sub[i];
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], MT_NCW);
         }
-        for (int i = 0; i < M2_NSS; ++i) {
-            mbar_init(&sfull[i], 1);
-            mbar_init(&sempty[i], M2_NW);
-        }
-        mbar_init(stepdone, M2_NW);
+        mbar_init(stepdone, MT_NCW);
         fence_mbar_init();
     }
-    for (int i = threadIdx.x; i < 4 * 2 * WP * M2_LDX; i += blockDim.x) Xall[i] = 0.0;
-    const int s0 = p.cta_sub_ptr[blockIdx.x], s1 = p.cta_sub_ptr[blockIdx.x + 1];
+    const int s0 = p.cta_sub_ptr[team], s1 = p.cta_sub_ptr[team + 1];
     const int ns = s1 - s0;
-    for (int i = threadIdx.x; i < ns * 6; i += blockDim.x) s_nb[i] = p.nbr[s0 * 6 + i];
-    __syncthreads();
+    for (int i = tid; i < ns * 6; i += (MT_NCW + 1) * 32) s_nb[i] = p.nbr[s0 * 6 + i];
+    asm volatile("bar.sync %0, %1;" ::"r"(3 + tw), "r"((MT_NCW + 1) * 32) : "memory");
 
-    // ======== producer warps: chain blocks (ungated) and state blocks (gated per step) ====
-    // one warp per ring (lane 0 issues); waits are blocking mbarrier try_waits, so the producers
-    // take no issue slots from the compute warps while their ring is full.  Interior subdomains
-    // never read acc_0 (only outer-face rows do), so their Gamma-hat_0 block is not streamed.
-    if (warp >= M2_NW) {
-        if (lane == 0 && warp == M2_NW) {  // chain-block ring
-            const uint64_t pol = l2_policy_evict_first();
-            const uint32_t cbytes = (uint32_t)TB * 8u;
-            long long c_iss = 0;
-            for (int k = 0; k < p.n_steps; ++k)
-                for (int sl = 0; sl < ns; ++sl) {
-                    const bool interior = s_nb[sl * 6] >= 0 && s_nb[sl * 6 + 1] >= 0 && s_nb[sl * 6 + 2] >= 0 &&
-                                          s_nb[sl * 6 + 3] >= 0 && s_nb[sl * 6 + 4] >= 0 && s_nb[sl * 6 + 5] >= 0;
-                    for (int b = 0; b < 2 * L; ++b) {
-                        if (b == 1 && interior) continue;
-                        const int st = (int)(c_iss % M2_NC);
-                        mbar_wait(&cempty[st], (uint32_t)(((c_iss / M2_NC) & 1) ^ 1));
-                        mbar_arrive_expect_tx(&cfull[st], cbytes);
-                        bulk_g2s(cst + (size_t)st * TB, p.tcoef + ((long long)(s0 + sl) * 2 * L + b) * TB, cbytes,
-                                 &cfull[st], pol);
-                        ++c_iss;
-                    }
-                }
-        } else if (lane == 0 && warp == M2_NW + 1) {  // state-block ring, gated per step
-            const uint64_t pol_state = l2_policy_evict_first();  // measured 1-1.5% faster than evict_last
-            const uint32_t mbytes = (uint32_t)(6 * M * M * 8);
-            const uint32_t sbytes = (uint32_t)(WS * 8);
-            const int nab = 2 * L - 1;
-            long long s_iss = 0;
-            for (int k = 0; k < p.n_steps; ++k) {
-                // step k >= 1 reads what step k-1 wrote: wait for all compute warps
-                if (k > 0) mbar_wait(stepdone, (uint32_t)((k - 1) & 1));
-                const int cb = k & 1;
-                const double* cur = cb ? p.U1 : p.U0;
-                const double* prv = cb ? p.U0 : p.U1;
-                for (int spos = 0; spos < ns * (nab + 3); ++spos) {
-                    const double* src;
-                    uint32_t bytes = sbytes;
-                    if (spos < ns * nab) {
-                        const int sl = spos / nab, r = spos % nab;
-                        const long long base = (long long)(s0 + sl) * KS;
-                        if (r < 2) {
-                            src = cur + base + r * WS;  // U_0, U_1
-                        } else {
-                            const int rp = r - 2;  // j = 1..L-1: [U_{j+1}], Uprev_j
-                            if (rp < 2 * (L - 2)) {
-                                const int j = 1 + rp / 2;
-                                src = (rp & 1) ? prv + base + j * WS : cur + base + (j + 1) * WS;
-                            } else {
-                                src = prv + base + (L - 1) * WS;
-                            }
-                        }
-                    } else {
-                        const int r = spos - ns * nab, sl = r / 3, w3 = r % 3;
-                        if (w3 == 0) {  // interface mass of the 6 faces
-                            src = p.mblk + (size_t)(s0 + sl) * 6 * M * M;
-                            bytes = mbytes;
-                        } else {
-                            src = ((w3 == 2) ? prv : cur) + (long long)(s0 + sl) * KS;  // U_0, Uprev_0
-                        }
-                    }
-                    const int st = (int)(s_iss % M2_NSS);
-                    mbar_wait(&sempty[st], (uint32_t)(((s_iss / M2_NSS) & 1) ^ 1));
-                    mbar_arrive_expect_tx(&sfull[st], bytes);
-                    bulk_g2s(sst + (size_t)st * WS, src, bytes, &sfull[st], pol_state);
-                    ++s_iss;
-                }
-            }
-        }
+    if (warp < MT_NCW) {
+        mt_compute<M>(p, ring, full, empty, stepdone, ssub, s_nb, s0, ns, team, warp, lane);
         return;
     }
-    // ======== compute warps: (column tile cw, row half hh) ========
-    // SMSP (warp % 4) hosts one warp of every row-tile group -> equal DMMA work per SMSP
-    const int cw = warp / M2_NQ, hh = (warp / M2_NQ + warp) % M2_NQ;
-    double* Xpair = Xall + (size_t)cw * 2 * WP * M2_LDX;
-    switch (hh) {
-        case 0: ms2_compute<M, 0>(p, cst, sst, Xpair, cfull, cempty, sfull, sempty, stepdone, ssub, s_nb, s0, ns, cw, lane); break;
-        case 1: ms2_compute<M, 1>(p, cst, sst, Xpair, cfull, cempty, sfull, sempty, stepdone, ssub, s_nb, s0, ns, cw, lane); break;
-        case 2: ms2_compute<M, 2>(p, cst, sst, Xpair, cfull, cempty, sfull, sempty, stepdone, ssub, s_nb, s0, ns, cw, lane); break;
-        default: ms2_compute<M, 3>(p, cst, sst, Xpair, cfull, cempty, sfull, sempty, stepdone, ssub, s_nb, s0, ns, cw, lane); break;
+    // ======== producer: one lane streams every item in consumption order ========
+    // Interior subdomains never read acc_0 (only outer-face rows do), so their Gamma-hat_0
+    // block is not streamed.  State items of step k wait for the compute warps' step k-1.
+    if (lane != 0) return;
+    const uint64_t pol = l2_policy_evict_first();
+    constexpr uint32_t cbytes = (uint32_t)TB * 8u, sbytes = (uint32_t)SB * 8u, mbytes = (uint32_t)NMT * 512u;
+    int st = 0;
+    uint32_t ph = 0;
+    auto issue = [&](const double* src, uint32_t bytes) {
+        mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], bytes);
+        bulk_g2s(ring + (size_t)st * STG, src, bytes, &full[st], pol);
+        if (++st == NST) {
+            st = 0;
+            ph ^= 1;
+        }
+    };
+    for (int k = 0; k < p.n_steps; ++k) {
+        if (k > 0) mbar_wait(stepdone, (uint32_t)((k - 1) & 1));
+        const double* cur = (k & 1) ? p.U1 : p.U0;
+        const double* prv = (k & 1) ? p.U0 : p.U1;
+        for (int sl = 0; sl < ns; ++sl) {
+            const bool interior = (s_nb[sl * 6] | s_nb[sl * 6 + 1] | s_nb[sl * 6 + 2] | s_nb[sl * 6 + 3] |
+                                   s_nb[sl * 6 + 4] | s_nb[sl * 6 + 5]) >= 0;
+            const double* uc = cur + (long long)(s0 + sl) * KS;
+            const double* up = prv + (long long)(s0 + sl) * KS;
+            const double* cf = p.tcoef + (long long)(s0 + sl) * 2 * L * TB;
+            issue(uc, sbytes);
+            issue(uc + SB, sbytes);
+            issue(cf, cbytes);
+            if (!interior) issue(cf + TB, cbytes);
+            for (int j = 1; j < L; ++j) {
+                if (j + 1 < L) issue(uc + (long long)(j + 1) * SB, sbytes);
+                issue(cf + (long long)(2 * j) * TB, cbytes);
+                issue(cf + (long long)(2 * j + 1) * TB, cbytes);
+                issue(up + (long long)j * SB, sbytes);
+            }
+        }
+        for (int sl = 0; sl < ns; ++sl) {
+            issue(p.mtiles + (size_t)(s0 + sl) * NMT * 64, mbytes);
+            issue(cur + (long long)(s0 + sl) * KS, sbytes);
+            issue(prv + (long long)(s0 + sl) * KS, sbytes);
+        }
     }
 }
 
-static size_t ms2_smem_bytes(int RT, int TB, int W, int nsmax) {
-    return 8 * ((size_t)M2_NC * TB + (size_t)M2_NSS * W * 32 + (size_t)4 * 2 * 8 * RT * M2_LDX + 2 * M2_NC +
-                2 * M2_NSS + 1) +
-           4 * (32 + 6 * (size_t)nsmax) + 64;
-}
-
-// per-subdomain interface mass blocks [n_sub][6][m*m] (zeros on outer faces)
-__global__ void k_ms_massblocks(const double* __restrict__ mass, const int* __restrict__ mass_idx, int n_sub, int m,
-                                double* __restrict__ out) {
-    const long long total = (long long)n_sub * 6 * m * m;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long sf = i / (m * m);
-        const int e = (int)(i % (m * m));
-        const int mi = mass_idx[sf];
-        out[i] = mi >= 0 ? mass[(size_t)mi * m * m + e] : 0.0;
-    }
-}
-
-static const void* ms2_kernel(int m) {
+static const void* mt_kernel(int m) {
     static const void* const tab[10] = {nullptr,
-                                        (const void*)k_step_ms2<1>,
-                                        (const void*)k_step_ms2<2>,
-                                        (const void*)k_step_ms2<3>,
-                                        (const void*)k_step_ms2<4>,
-                                        (const void*)k_step_ms2<5>,
-                                        (const void*)k_step_ms2<6>,
-                                        (const void*)k_step_ms2<7>,
-                                        (const void*)k_step_ms2<8>,
-                                        (const void*)k_step_ms2<9>};
+                                        (const void*)k_step_mt<1>,
+                                        (const void*)k_step_mt<2>,
+                                        (const void*)k_step_mt<3>,
+                                        (const void*)k_step_mt<4>,
+                                        (const void*)k_step_mt<5>,
+                                        (const void*)k_step_mt<6>,
+                                        (const void*)k_step_mt<7>,
+                                        (const void*)k_step_mt<8>,
+                                        (const void*)k_step_mt<9>};
     return (m >= 1 && m <= 9) ? tab[m] : nullptr;
 }
 
+struct MtShape {
+    int W, RT, WP, TB, SB, STG, NMT;
+};
+
+static MtShape mt_shape(int m) {
+    MtShape d;
+    d.W = 6 * m;
+    d.RT = (d.W + 7) / 8;
+    d.WP = 8 * d.RT;
+    d.TB = d.RT * (d.RT + 1) / 2 * 64;
+    d.SB = 32 * d.WP;
+    d.STG = std::max(d.TB, d.SB);
+    d.NMT = mt_mass_count(m);
+    return d;
+}
+
+static size_t mt_smem_bytes(const MtShape& d, int nst, int nsmax) {
+    const size_t b = (size_t)nst * d.STG * 8 + (2 * (size_t)nst + 1) * 8 + 4 * (32 + 6 * (size_t)nsmax);
+    return (b + 127) & ~(size_t)127;  // one team
+}
+
 // shots start from rest (u0 = v0 = 0): U_curr = 0, U_prev = ((0.5 dt) dt) (vec_q f_q(0))  (stepper.py:347-353)
-__global__ void k_ms_init(double* U0, double* U1, long long total, int S, const int* shot_sub,
-                          const double* shot_vec, const long long* shot_voff, const double* f0, double half,
-                          long long K) {
+__global__ void k_ms_init(double* U0, double* U1, long long total, int S, int W, int WP, int L, const int* shot_sub,
+                          const double* shot_vec, const long long* shot_voff, const double* f0, double half) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int q = (int)(i % S);
-        const long long rest = i / S;
-        const long long s = rest / K, idx = rest % K;
+        const int r = (int)(i % WP);
+        long long rest = i / WP;
+        const int q = (int)(rest % S);
+        rest /= S;
+        const int j = (int)(rest % L);
+        const long long s = rest / L;
         U0[i] = 0.0;
         double v = 0.0;
-        if (shot_sub[q] == s) v = __dmul_rn(half, __dmul_rn(shot_vec[shot_voff[q] + idx], f0[q]));
+        if (r < W && shot_sub[q] == s) v = __dmul_rn(half, __dmul_rn(shot_vec[shot_voff[q] + (long long)j * W + r], f0[q]));
         U1[i] = v;
     }
 }
@@ -700,6 +598,17 @@ __global__ void k_ms_norms(const double* __restrict__ part, int n_steps, int n_c
     double t = 0.0;
     for (int c = 0; c < n_cta; ++c) t += part[((size_t)k * n_cta + c) * S + q];
     out[i] = sqrt(t);
+}
+
+// one shot of the [sub][layer][shot][WP] state as the reference's concatenated [sub][L*W] vector
+__global__ void k_mt_gather(const double* __restrict__ U, long long total, int q, int S, int W, int WP,
+                            double* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(i % W);
+        const long long sj = i / W;  // s * L + j
+        out[i] = U[(sj * S + q) * WP + r];
+    }
 }
 
 }  // namespace sfw
@@ -722,26 +631,33 @@ extern "C" int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub,
                                char* errbuf, int errlen) {
     if (n_shots != 32) return fail(SFW_ECONFIG, "multi-shot stepping supports exactly 32 shots", errbuf, errlen);
     if (!h->uniform) return fail(SFW_ECONFIG, "multi-shot stepping needs one layer count for all models", errbuf, errlen);
-    const int S = n_shots, W = h->W, L = h->L;
-    const int WP = (W + 7) & ~7, RT = WP / 8;
-    h->TB = RT * (RT + 1) / 2 * 64;
+    if (h->L < 2) return fail(SFW_ECONFIG, "multi-shot stepping needs at least 2 layers", errbuf, errlen);
+    const void* kfn = mt_kernel(h->m);
+    if (!kfn) return fail(SFW_ECONFIG, "multi-shot stepping supports 1 <= modes per face <= 9", errbuf, errlen);
+    const int S = n_shots, L = h->L, n = h->n_sub;
+    const MtShape d = mt_shape(h->m);
+    h->TB = d.TB;
     h->n_shots = S;
     int rc = 0;
     if (!h->tcoef) {
-        if ((rc = dalloc(&h->tcoef, (size_t)h->n_blocks * h->TB, errbuf, errlen))) return rc;
-        k_tilepack<<<(unsigned)h->n_blocks, 256, 0, h->stream>>>(h->coef, h->BS, h->m, RT, h->TB, h->tcoef,
+        if ((rc = dalloc(&h->tcoef, (size_t)h->n_blocks * d.TB, errbuf, errlen))) return rc;
+        k_tilepack<<<(unsigned)h->n_blocks, 256, 0, h->stream>>>(h->coef, h->BS, h->m, d.RT, d.TB, h->tcoef,
                                                                  h->n_blocks);
     }
-    const size_t st = (size_t)h->n_sub * L * W * S;
+    if (!h->mmass) {
+        if ((rc = dalloc(&h->mmass, (size_t)n * d.NMT * 64, errbuf, errlen))) return rc;
+        k_mt_masstiles<<<(unsigned)n, 64, 0, h->stream>>>(h->mass, h->mass_idx, n, h->m, d.RT, d.NMT, h->mmass);
+    }
+    const size_t st = (size_t)n * L * d.SB;
     for (int b = 0; b < 2; ++b)
         if (!h->UM[b] && (rc = dalloc(&h->UM[b], st, errbuf, errlen))) return rc;
-    if (!h->mfb && (rc = dalloc(&h->mfb, (size_t)2 * h->n_sub * W * S, errbuf, errlen))) return rc;
-    if (!h->macc1 && (rc = dalloc(&h->macc1, (size_t)h->n_sub * W * S, errbuf, errlen))) return rc;
+    if (!h->mfb && (rc = dalloc(&h->mfb, (size_t)2 * n * d.SB, errbuf, errlen))) return rc;
+    if (!h->macc1 && (rc = dalloc(&h->macc1, (size_t)n * d.SB, errbuf, errlen))) return rc;
     std::vector<long long> voff(S);
     long long vt = 0;
     for (int q = 0; q < S; ++q) {
         const int s = shot_sub[q];
-        if (s < -1 || s >= h->n_sub) return fail(SFW_ECONFIG, "shot source subdomain has no model", errbuf, errlen);
+        if (s < -1 || s >= n) return fail(SFW_ECONFIG, "shot source subdomain has no model", errbuf, errlen);
         voff[q] = vt;
         if (s >= 0) vt += h->soff[s + 1] - h->soff[s];
     }
@@ -756,31 +672,69 @@ extern "C" int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub,
     if ((rc = upload(&h->shot_sub, ss, errbuf, errlen))) return rc;
     if ((rc = upload(&h->shot_voff, voff, errbuf, errlen))) return rc;
     if ((rc = upload(&h->shot_vec, sv, errbuf, errlen))) return rc;
-    if (L < 2) return fail(SFW_ECONFIG, "multi-shot stepping needs at least 2 layers", errbuf, errlen);
-    if (!ms2_kernel(h->m))
-        return fail(SFW_ECONFIG, "multi-shot stepping supports 1 <= modes per face <= 9", errbuf, errlen);
-    {
-        const void* k2 = ms2_kernel(h->m);
+    if (!h->mt_grid) {
+        // work decomposition: two teams per SM, each a contiguous subdomain range; a team waits per
+        // step only for the teams that own face neighbours of its subdomains
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        int G = std::min(2 * nsm, n);
+        if (const char* e = getenv("SFW_STEP_MAXGRID")) G = std::max(1, std::min(G, atoi(e)));  // test hook
+        std::vector<int> cta_ptr(G + 1), owner(n), nptr(G + 1, 0), nlist;
+        for (int b = 0; b <= G; ++b) cta_ptr[b] = (int)((long long)b * n / G);
         int nsmax = 0;
-        for (int b = 0; b < h->grid; ++b) nsmax = std::max(nsmax, h->cta_ptr_h[b + 1] - h->cta_ptr_h[b]);
-        h->shot_smem2 = (int)ms2_smem_bytes(RT, h->TB, W, nsmax);
-        if (!h->mmass && (rc = dalloc(&h->mmass, (size_t)h->n_sub * 6 * h->m * h->m, errbuf, errlen))) return rc;
-        k_ms_massblocks<<<592, 256, 0, h->stream>>>(h->mass, h->mass_idx, h->n_sub, h->m, h->mmass);
-        if (h->shot_smem2 <= 220 * 1024)
-            SFW_CUDA_TRY(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, h->shot_smem2));
-        else
-            h->shot_smem2 = 0;
+        for (int b = 0; b < G; ++b) {
+            nsmax = std::max(nsmax, cta_ptr[b + 1] - cta_ptr[b]);
+            for (int s = cta_ptr[b]; s < cta_ptr[b + 1]; ++s) owner[s] = b;
+        }
+        for (int b = 0; b < G; ++b) {
+            std::vector<int> mine;
+            for (int s = cta_ptr[b]; s < cta_ptr[b + 1]; ++s)
+                for (int f = 0; f < 6; ++f) {
+                    const int t = h->nbr_h[6 * s + f];
+                    if (t >= 0 && owner[t] != b) mine.push_back(owner[t]);
+                }
+            std::sort(mine.begin(), mine.end());
+            mine.erase(std::unique(mine.begin(), mine.end()), mine.end());
+            nlist.insert(nlist.end(), mine.begin(), mine.end());
+            nptr[b + 1] = (int)nlist.size();
+        }
+        if (nlist.empty()) nlist.push_back(0);
+        if ((rc = upload(&h->mt_cta_ptr, cta_ptr, errbuf, errlen))) return rc;
+        if ((rc = upload(&h->mt_ncta_ptr, nptr, errbuf, errlen))) return rc;
+        if ((rc = upload(&h->mt_ncta, nlist, errbuf, errlen))) return rc;
+        if ((rc = dalloc(&h->mt_flags, (size_t)G, errbuf, errlen))) return rc;
+        // ring depth: two teams share the 227 KB of a CTA
+        int nst = 12;
+        while (nst > 4 && 2 * mt_smem_bytes(d, nst, nsmax) > 226 * 1024) --nst;
+        const size_t smem = 2 * mt_smem_bytes(d, nst, nsmax);
+        if (smem > 227 * 1024)
+            return fail(SFW_ECONFIG, "multi-shot stepping: too many subdomains per CTA for shared memory", errbuf,
+                        errlen);
+        SFW_CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        SFW_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 2 * (MT_NCW + 1) * 32, smem));
+        if (per_sm * nsm < (G + 1) / 2) {
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kfn);
+            return fail(SFW_ECONFIG,
+                        "multi-shot stepping: the persistent grid is not co-resident (registers " +
+                            std::to_string(fa.numRegs) + ", max threads " + std::to_string(fa.maxThreadsPerBlock) +
+                            ", shared " + std::to_string(smem) + " B, CTAs per SM " + std::to_string(per_sm) + ")",
+                        errbuf, errlen);
+        }
+        h->mt_team_smem = (int)mt_smem_bytes(d, nst, nsmax);
+        h->mt_nst = nst;
+        h->shot_smem2 = (int)smem;
+        h->mt_grid = G;
     }
-    if (!h->shot_smem2)
-        return fail(SFW_ECONFIG, "multi-shot stepping: too many subdomains per CTA for the shared-memory rings",
-                    errbuf, errlen);
     SFW_CUDA_TRY(cudaStreamSynchronize(h->stream));
     SFW_CUDA_TRY(cudaGetLastError());
     return 0;
 }
 
 // Run n_steps from rest for all shots.  profile: HOST [S][n_steps] f_q(t_k), t_k = k dt;
-// profile0: HOST [S] f_q(0).  rows_out: HOST [n_steps/record_every][n_probe][S] (or NULL);
+// profile0: HOST [S] f_q(0).  rows_out: HOST [n_steps/record_every][S][n_probe] (or NULL);
 // norms_out: HOST [n_steps][S] (or NULL); *kernel_ms: CUDA-event time of the launch.
 extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, const double* profile0,
                              const double* profile, double* rows_out, double* norms_out, float* kernel_ms,
@@ -788,8 +742,8 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
     if (!h->n_shots) return fail(SFW_ECONFIG, "call sfw_shots_setup first", errbuf, errlen);
     if (n_steps <= 0) return 0;
     if (record_every < 1) return fail(SFW_ECONFIG, "record_every must be >= 1", errbuf, errlen);
-    const int S = h->n_shots, W = h->W, L = h->L;
-    const int WP = (W + 7) & ~7, RT = WP / 8;
+    const int S = h->n_shots, L = h->L;
+    const MtShape d = mt_shape(h->m);
     int rc = ms_ensure(&h->shot_ftab, &h->shot_ftab_cap, (long long)S * n_steps + S, errbuf, errlen);
     if (rc) return rc;
     SFW_CUDA_TRY(cudaMemcpyAsync(h->shot_ftab, profile, (size_t)S * n_steps * 8, cudaMemcpyHostToDevice, h->stream));
@@ -797,39 +751,34 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
                                  h->stream));
     const long long nrec = n_steps / record_every;
     if ((rc = ms_ensure(&h->mrows, &h->mrows_cap, std::max(1LL, nrec * h->n_probe * S), errbuf, errlen))) return rc;
-    // norm partials per step: one per (CTA, row-tile group)
-    const int nparts = M2_NQ * h->grid;
+    const int nparts = h->mt_grid;  // |U|^2 partials per step: one per CTA
     if ((rc = ms_ensure(&h->mnorm, &h->mnorm_cap, (long long)n_steps * nparts * S + (long long)n_steps * S, errbuf,
                         errlen)))
         return rc;
-    const long long total = (long long)h->n_sub * L * W * S;
+    const long long total = (long long)h->n_sub * L * d.SB;
     const double half = (0.5 * h->dt) * h->dt;
-    k_ms_init<<<1184, 256, 0, h->stream>>>(h->UM[0], h->UM[1], total, S, h->shot_sub, h->shot_vec, h->shot_voff,
-                                           h->shot_ftab + (size_t)S * n_steps, half, (long long)L * W);
-    SFW_CUDA_TRY(cudaMemsetAsync(h->bar, 0, sizeof(unsigned int) * h->grid, h->stream));
-    MsParams p{};
+    k_ms_init<<<1184, 256, 0, h->stream>>>(h->UM[0], h->UM[1], total, S, d.W, d.WP, L, h->shot_sub, h->shot_vec,
+                                           h->shot_voff, h->shot_ftab + (size_t)S * n_steps, half);
+    SFW_CUDA_TRY(cudaMemsetAsync(h->mt_flags, 0, sizeof(unsigned int) * h->mt_grid, h->stream));
+    MtParams p{};
     p.n_sub = h->n_sub;
     p.L = L;
-    p.W = W;
-    p.WP = WP;
-    p.RT = RT;
-    p.TB = h->TB;
-    p.S = S;
     p.n_steps = n_steps;
     p.record_every = record_every;
     p.n_probe = h->n_probe;
     p.ftab_stride = n_steps;
-    p.K = (long long)L * W;
+    p.nst = h->mt_nst;
+    p.n_team = h->mt_grid;
+    p.team_smem = h->mt_team_smem;
     p.dt2 = h->dt * h->dt;
     p.tcoef = h->tcoef;
+    p.mtiles = h->mmass;
     p.U0 = h->UM[0];
     p.U1 = h->UM[1];
     p.flux = h->mfb;
     p.acc1 = h->macc1;
     p.nbr = h->nbr;
-    p.mass_idx = h->mass_idx;
-    p.mass = h->mass;
-    p.cta_sub_ptr = h->cta_sub_ptr;
+    p.cta_sub_ptr = h->mt_cta_ptr;
     p.shot_sub = h->shot_sub;
     p.shot_vec = h->shot_vec;
     p.shot_voff = h->shot_voff;
@@ -841,25 +790,12 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
     p.prb_woff = h->prb_woff;
     p.rows = h->mrows;
     p.norm_part = h->mnorm;
-    p.flags = h->bar;
-    p.ncta_ptr = h->ncta_ptr;
-    p.ncta = h->ncta;
-    p.evict_first = 1;
-    p.dbg = nullptr;
-    p.mblk = h->mmass;
-    if (getenv("SFW_STEP_PROF")) {
-        const size_t need = (size_t)h->grid * M2_NW * 8;
-        if (h->tprof_n < need) {
-            if (h->tprof) cudaFree(h->tprof);
-            cudaMalloc(&h->tprof, need * 8);
-            h->tprof_n = need;
-        }
-        cudaMemsetAsync(h->tprof, 0, need * 8, h->stream);
-        p.dbg = h->tprof;
-    }
+    p.flags = h->mt_flags;
+    p.ncta_ptr = h->mt_ncta_ptr;
+    p.ncta = h->mt_ncta;
     void* args[] = {&p};
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
-    SFW_CUDA_TRY(cudaLaunchCooperativeKernel(ms2_kernel(h->m), dim3(h->grid), dim3((M2_NW + 2) * 32), args,
+    SFW_CUDA_TRY(cudaLaunchCooperativeKernel(mt_kernel(h->m), dim3((h->mt_grid + 1) / 2), dim3(2 * (MT_NCW + 1) * 32), args,
                                              h->shot_smem2, h->stream));
     SFW_CUDA_TRY(cudaEventRecord(h->ev1, h->stream));
     double* dn = h->mnorm + (size_t)n_steps * nparts * S;
@@ -881,28 +817,38 @@ extern "C" int sfw_shots_state(sfw_stepper* h, int q, double* u_curr, double* u_
     char* errbuf = nullptr;
     int errlen = 0;
     if (!h->n_shots || q < 0 || q >= h->n_shots) return SFW_ECONFIG;
-    const int S = h->n_shots;
-    const long long total = (long long)h->n_sub * h->L * h->W;
-    std::vector<double> buf((size_t)total * S);
+    const MtShape d = mt_shape(h->m);
+    const long long total = (long long)h->n_sub * h->L * d.W;
+    double* tmp = nullptr;
+    int rc = dalloc(&tmp, (size_t)total, errbuf, errlen);
+    if (rc) return rc;
     for (int lvl = 0; lvl < 2; ++lvl) {
         double* dst = lvl == 0 ? u_curr : u_prev;
         if (!dst) continue;
         const double* src = h->UM[lvl == 0 ? h->mcur : h->mcur ^ 1];
-        SFW_CUDA_TRY(cudaMemcpy(buf.data(), src, buf.size() * 8, cudaMemcpyDeviceToHost));
-        for (long long i = 0; i < total; ++i) dst[i] = buf[(size_t)i * S + q];
+        k_mt_gather<<<592, 256, 0, h->stream>>>(src, total, q, h->n_shots, d.W, d.WP, tmp);
+        cudaError_t e = cudaMemcpyAsync(dst, tmp, (size_t)total * 8, cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) {
+            cudaFree(tmp);
+            return SFW_ECUDA;
+        }
     }
+    cudaFree(tmp);
     return 0;
 }
 
-// algorithmic bytes / flops per step of the multi-shot launch (SURVEY 8d, S shots)
+// algorithmic bytes / flops per step of the multi-shot launch (SURVEY 8d, S shots), and the
+// bytes the kernel streams (tile-padded blocks, padded state rows, mass tiles, face buffer)
 extern "C" int sfw_shots_traffic(sfw_stepper* h, double* alg_bytes, double* alg_flops, double* streamed) {
     const double w = h->W, S = h->n_shots ? h->n_shots : 32;
+    const MtShape d = mt_shape(h->m);
     double b = 0, f = 0, s = 0;
     for (int i = 0; i < h->n_sub; ++i) {
         const double L = h->layers[i];
         b += 8.0 * ((2 * L - 1) * w * (w + 1) / 2 + 3 * L * w * S);
         f += S * (2.0 * (2 * L - 1) * w * w + 5 * L * w);
-        s += 8.0 * (2 * L * h->TB + 3 * L * w * S);
+        s += 8.0 * ((2 * L - 1) * d.TB + d.NMT * 64 + (3 * L + 2) * (double)d.SB);
     }
     if (alg_bytes) *alg_bytes = b;
     if (alg_flops) *alg_flops = f;

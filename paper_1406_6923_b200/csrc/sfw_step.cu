@@ -2647,7 +2647,8 @@ static void free_all(sfw_stepper* h) {
                     h->prb_ids, h->prb_tap, h->prb_w, h->prb_woff, h->rows, h->sub_norm,
                     h->norm_part, h->norms, h->bar, h->scales, h->gam_dense, h->flux, h->sq, h->ncta_ptr, h->ncta, h->tcoef, h->UM[0], h->UM[1],
                     h->mfb, h->macc1, h->mnorm, h->mrows, h->shot_vec, h->shot_sub, h->shot_voff,
-                    h->shot_ftab, h->mbox, h->mmass, h->ucoef, h->swimg, h->src_subs};
+                    h->shot_ftab, h->mbox, h->mmass, h->ucoef, h->swimg, h->src_subs, h->mt_cta_ptr, h->mt_ncta_ptr,
+                    h->mt_ncta, h->mt_flags};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (h->ev0) cudaEventDestroy(h->ev0);
@@ -2957,6 +2958,7 @@ extern "C" int sfw_step_create(const sfw_step_desc* d, sfw_stepper** out, char* 
         TRY(upload(&h->d_layers, h->layers, errbuf, errlen));
         TRY(upload(&h->d_soff, h->soff, errbuf, errlen));
         TRY(upload(&h->nbr, nbr, errbuf, errlen));
+        h->nbr_h = nbr;
         TRY(upload(&h->mass_idx, mass_idx, errbuf, errlen));
 
         // ---- state and scratch ------------------------------------------------

@@ -112,8 +112,12 @@ struct sfw_stepper {
     double* sq = nullptr;
     // multi-shot mode (sfw_shots_*): S independent wavefields, DMMA tile-packed chain blocks
     int n_shots = 0, shot_smem2 = 0;
-    double* mmass = nullptr;  // multi-shot: per-subdomain interface mass blocks
-    double* tcoef = nullptr;          // [n_blocks][TB] fragment-ordered 8x8 lower tiles
+    std::vector<int> nbr_h;           // host copy of the face-neighbour table [n_sub][6]
+    int mt_grid = 0, mt_nst = 0, mt_team_smem = 0;  // k_step_mt: teams (two per CTA), ring stages, bytes per team
+    int *mt_cta_ptr = nullptr, *mt_ncta_ptr = nullptr, *mt_ncta = nullptr;
+    unsigned int* mt_flags = nullptr;
+    double* mmass = nullptr;  // multi-shot: per-subdomain interface mass tiles
+    double* tcoef = nullptr;          // [n_blocks][TB] swizzled 8x8 lower tiles
     int TB = 0;
     double *UM[2] = {nullptr, nullptr};
     double *mflux = nullptr, *macc1 = nullptr, *mfb = nullptr, *mnorm = nullptr, *mrows = nullptr;
