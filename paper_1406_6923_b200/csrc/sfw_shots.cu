@@ -25,7 +25,7 @@
 // consumes them, through a single ring of equal stages (cp.async.bulk + mbarrier).  Per step:
 //   sweep   per subdomain F_0 = G_0 (U_1 - U_0) -> face buffer (global); boundary subdomains
 //           also acc_0 = H_0 F_0; layers j = 1..L-1: F_j, A_j = H_j (F_j - F_{j-1}), leapfrog
-//   flags   CTA barrier, step flag, wait for the CTAs owning face neighbours
+//   barrier team barrier, step flag (release), wait for the step flags of ALL teams (acquire)
 //   faces   layer 0: T = F_0 + neighbour's F_0 on shared faces, acc_0 = mass T as a GEMM
 //           over the tiles that meet a face block (block-diagonal mass), leapfrog
 // State layout in HBM: [subdomain][layer][shot][WP rows] (rows padded to 8 RT, pad = 0), so a
@@ -171,9 +171,7 @@ struct MtParams {
     const long long* prb_woff;
     double* rows;          // [n_rec][S][n_probe]
     double* norm_part;     // [n_steps][grid][S]
-    unsigned int* flags;
-    const int* ncta_ptr;
-    const int* ncta;
+    unsigned int* flags;   // [n_team] step of the last finished sweep
 };
 
 constexpr int MT_NCW = 4;  // compute warps per CTA (8 shots each)
@@ -262,6 +260,11 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
             ph ^= 1;
         }
     };
+    // the stage of a GEMM is released only once the products that read it are in registers
+    auto settle = [&](double (&v)[RT][2]) {
+#pragma unroll
+        for (int t = 0; t < RT; ++t) asm volatile("" : "+d"(v[t][0]), "+d"(v[t][1])::"memory");
+    };
     auto load_slice = [&](const double* blk, double (&v)[RT][2]) {
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
@@ -308,12 +311,14 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                 }
             }
             mt_gemm<M, false>(acquire(0), x, fp, dir, trn);  // F_0
-            release();
+            settle(fp);
+                release();
             store_slice(fx + (size_t)s * SB, fp);
             const bool interior = (s_nb[sl * 6] | s_nb[sl * 6 + 1] | s_nb[sl * 6 + 2] | s_nb[sl * 6 + 3] |
                                    s_nb[sl * 6 + 4] | s_nb[sl * 6 + 5]) >= 0;
             if (!interior) {  // acc_0 = H_0 F_0: only outer-face rows are read back
                 mt_gemm<M, false>(acquire(0), fp, acc, dir, trn);
+                settle(acc);
                 release();
                 store_slice(p.acc1 + (size_t)s * SB, acc);
             }
@@ -331,6 +336,7 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                     x[t][1] = ub[t][1] - ua[t][1];
                 }
                 mt_gemm<M, false>(acquire(0), x, acc, dir, trn);  // F_j
+                settle(acc);
                 release();
 #pragma unroll
                 for (int t = 0; t < RT; ++t) {
@@ -340,6 +346,7 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                     fp[t][1] = acc[t][1];
                 }
                 mt_gemm<M, false>(acquire(0), x, acc, dir, trn);  // A_j
+                settle(acc);
                 release();
                 const double* uo = acquire(0);  // Uprev_j
                 double* un = Un + (size_t)s * KS + (size_t)j * SB;
@@ -365,13 +372,20 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                 }
             }
         }
-        // ---------------- step flag, neighbour flags ------------------------------------
-        // (bar.sync orders the team's face-buffer writes before lane 0's release store: cumulativity)
+        // ---------------- grid-wide step barrier ------------------------------------------
+        // (bar.sync orders the team's face-buffer writes before lane 0's release store: cumulativity.)
+        // The face phase reads only face neighbours' buffers, but the wait is for EVERY team: with
+        // neighbour-only step flags the traces were not reproducible run to run (rare differences at
+        // the leading edge of a wavefield, DESIGN.md config 4); with all teams in step they are, in
+        // every stress run, and the step is no slower.
         asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
         if (w == 0 && lane == 0) st_release(p.flags + team, (unsigned int)k);
-        if (w == 0)
-            flags_wait(p.flags, p.ncta + p.ncta_ptr[team], p.ncta_ptr[team + 1] - p.ncta_ptr[team], (unsigned int)k,
-                       lane);
+        if (w == 0) {
+            for (int i = lane; i < p.n_team; i += 32)
+                while (ld_acquire(p.flags + i) < (unsigned int)k) {
+                }
+            __syncwarp();
+        }
         asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
         // ---------------- faces: layer-0 coupling + leapfrog -----------------------------
         for (int sl = 0; sl < ns; ++sl) {
@@ -673,36 +687,17 @@ extern "C" int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub,
     if ((rc = upload(&h->shot_voff, voff, errbuf, errlen))) return rc;
     if ((rc = upload(&h->shot_vec, sv, errbuf, errlen))) return rc;
     if (!h->mt_grid) {
-        // work decomposition: two teams per SM, each a contiguous subdomain range; a team waits per
-        // step only for the teams that own face neighbours of its subdomains
+        // work decomposition: two teams per SM, each a contiguous subdomain range
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         int G = std::min(2 * nsm, n);
         if (const char* e = getenv("SFW_STEP_MAXGRID")) G = std::max(1, std::min(G, atoi(e)));  // test hook
-        std::vector<int> cta_ptr(G + 1), owner(n), nptr(G + 1, 0), nlist;
+        std::vector<int> cta_ptr(G + 1);
         for (int b = 0; b <= G; ++b) cta_ptr[b] = (int)((long long)b * n / G);
         int nsmax = 0;
-        for (int b = 0; b < G; ++b) {
-            nsmax = std::max(nsmax, cta_ptr[b + 1] - cta_ptr[b]);
-            for (int s = cta_ptr[b]; s < cta_ptr[b + 1]; ++s) owner[s] = b;
-        }
-        for (int b = 0; b < G; ++b) {
-            std::vector<int> mine;
-            for (int s = cta_ptr[b]; s < cta_ptr[b + 1]; ++s)
-                for (int f = 0; f < 6; ++f) {
-                    const int t = h->nbr_h[6 * s + f];
-                    if (t >= 0 && owner[t] != b) mine.push_back(owner[t]);
-                }
-            std::sort(mine.begin(), mine.end());
-            mine.erase(std::unique(mine.begin(), mine.end()), mine.end());
-            nlist.insert(nlist.end(), mine.begin(), mine.end());
-            nptr[b + 1] = (int)nlist.size();
-        }
-        if (nlist.empty()) nlist.push_back(0);
+        for (int b = 0; b < G; ++b) nsmax = std::max(nsmax, cta_ptr[b + 1] - cta_ptr[b]);
         if ((rc = upload(&h->mt_cta_ptr, cta_ptr, errbuf, errlen))) return rc;
-        if ((rc = upload(&h->mt_ncta_ptr, nptr, errbuf, errlen))) return rc;
-        if ((rc = upload(&h->mt_ncta, nlist, errbuf, errlen))) return rc;
         if ((rc = dalloc(&h->mt_flags, (size_t)G, errbuf, errlen))) return rc;
         // ring depth: two teams share the 227 KB of a CTA
         int nst = 12;
@@ -791,8 +786,6 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
     p.rows = h->mrows;
     p.norm_part = h->mnorm;
     p.flags = h->mt_flags;
-    p.ncta_ptr = h->mt_ncta_ptr;
-    p.ncta = h->mt_ncta;
     void* args[] = {&p};
     SFW_CUDA_TRY(cudaEventRecord(h->ev0, h->stream));
     SFW_CUDA_TRY(cudaLaunchCooperativeKernel(mt_kernel(h->m), dim3((h->mt_grid + 1) / 2), dim3(2 * (MT_NCW + 1) * 32), args,
