@@ -14,7 +14,8 @@ KERNELS = {  # file name -> mangled-name pattern
     "k_step_sw_4_7": r"_ZN3sfw9k_step_swILi4ELi7EEEvNS_10StepParamsE",
     "k_ustep_9_2": r"_ZN3sfw7k_ustepILi9ELi2EEEvNS_10StepParamsE",
     "k_wstep_9_2": r"_ZN3sfw7k_wstepILi9ELi2EEEvNS_7WParamsE",
-    "k_step_ms2_9": r"_ZN3sfw10k_step_ms2ILi9EEEvNS_8MsParamsE",
+    "k_step_sw4_4_7_2": r"_ZN3sfw10k_step_sw4ILi4ELi7ELi2EEEvNS_10StepParamsE",
+    "k_step_mt_9": r"_ZN3sfw9k_step_mtILi9EEEvNS_8MtParamsE",
     "k_pcg2": r"_ZN3sfw6k_pcg2ENS_7PcgArgsE",
     "k_dgemm2_T": r"_ZN3sfw8k_dgemm2ILb1EEEvNS_8GemmArgsE",
     "k_dgemm2_N": r"_ZN3sfw8k_dgemm2ILb0EEEvNS_8GemmArgsE",
