@@ -159,7 +159,9 @@ struct MtParams {
     double* flux;          // [2][n_sub][S][WP] layer-0 flux F_0 (face mailbox), double-buffered by parity
     double* acc1;          // [n_sub][S][WP] H_0 F_0 of boundary subdomains
     const int* nbr;
-    const int* cta_sub_ptr;
+    const int* cta_sub_ptr;  // [n_team + 1] offsets into team_subs
+    const int* team_subs;    // subdomains of every team (ascending within a team)
+    int nsmax;               // most subdomains in a team
     const int* shot_sub;   // [S] source subdomain of each shot (-1: none)
     const double* shot_vec;
     const long long* shot_voff;
@@ -224,7 +226,7 @@ __device__ __forceinline__ void mt_gemm(const double* __restrict__ tiles, const 
 
 template <int M>
 __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring, uint64_t* full, uint64_t* empty,
-                                           uint64_t* stepdone, const int* ssub, const int* s_nb, int s0, int ns,
+                                           uint64_t* stepdone, const int* ssub, const int* s_id, const int* s_nb, int ns,
                                            int team, int w, int lane) {
     using D = MtDims<M>;
     constexpr int S = D::S, W = D::W, RT = D::RT, WP = D::WP, SB = D::SB, STG = D::STG;
@@ -294,7 +296,7 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
 
         // ---------------- sweep: layers of every subdomain, all in registers ---------------
         for (int sl = 0; sl < ns; ++sl) {
-            const int s = s0 + sl;
+            const int s = s_id[sl];
             const bool mine = my_src == s;
             double ua[RT][2], ub[RT][2], fp[RT][2], x[RT][2], acc[RT][2];
             {
@@ -389,7 +391,7 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
         asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
         // ---------------- faces: layer-0 coupling + leapfrog -----------------------------
         for (int sl = 0; sl < ns; ++sl) {
-            const int s = s0 + sl;
+            const int s = s_id[sl];
             const bool mine = my_src == s;
             double x[RT][2], acc[RT][2], a1[RT][2];
             const double* fo = fx + (size_t)s * SB + lo;
@@ -442,7 +444,8 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
             asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");  // the team's U rows are written
             const long long rec = k / p.record_every - 1;
             const int pq0 = w, qs = lane;  // thread (w, lane): shot lane, probes w, w+4, ...
-            for (int s = s0; s < s0 + ns; ++s) {
+            for (int sl = 0; sl < ns; ++sl) {
+                const int s = s_id[sl];
                 const double* us = Un + (size_t)s * KS + (size_t)qs * WP;
                 for (int pq = p.prb_ptr[s] + pq0; pq < p.prb_ptr[s + 1]; pq += MT_NCW) {
                     const int pid = p.prb_ids[pq];
@@ -486,7 +489,8 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
     uint64_t* empty = full + NST;
     uint64_t* stepdone = empty + NST;
     int* ssub = reinterpret_cast<int*>(stepdone + 1);
-    int* s_nb = ssub + S;  // [ns][6] face neighbours of the team's subdomains
+    int* s_id = ssub + S;        // [ns] the team's subdomains
+    int* s_nb = s_id + p.nsmax;  // [ns][6] their face neighbours
 
     for (int i = tid; i < S; i += (MT_NCW + 1) * 32) ssub[i] = p.shot_sub[i];
     if (tid == 0) {
@@ -499,11 +503,12 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
     }
     const int s0 = p.cta_sub_ptr[team], s1 = p.cta_sub_ptr[team + 1];
     const int ns = s1 - s0;
-    for (int i = tid; i < ns * 6; i += (MT_NCW + 1) * 32) s_nb[i] = p.nbr[s0 * 6 + i];
+    for (int i = tid; i < ns; i += (MT_NCW + 1) * 32) s_id[i] = p.team_subs[s0 + i];
+    for (int i = tid; i < ns * 6; i += (MT_NCW + 1) * 32) s_nb[i] = p.nbr[p.team_subs[s0 + i / 6] * 6 + i % 6];
     asm volatile("bar.sync %0, %1;" ::"r"(3 + tw), "r"((MT_NCW + 1) * 32) : "memory");
 
     if (warp < MT_NCW) {
-        mt_compute<M>(p, ring, full, empty, stepdone, ssub, s_nb, s0, ns, team, warp, lane);
+        mt_compute<M>(p, ring, full, empty, stepdone, ssub, s_id, s_nb, ns, team, warp, lane);
         return;
     }
     // ======== producer: one lane streams every item in consumption order ========
@@ -530,9 +535,9 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
         for (int sl = 0; sl < ns; ++sl) {
             const bool interior = (s_nb[sl * 6] | s_nb[sl * 6 + 1] | s_nb[sl * 6 + 2] | s_nb[sl * 6 + 3] |
                                    s_nb[sl * 6 + 4] | s_nb[sl * 6 + 5]) >= 0;
-            const double* uc = cur + (long long)(s0 + sl) * KS;
-            const double* up = prv + (long long)(s0 + sl) * KS;
-            const double* cf = p.tcoef + (long long)(s0 + sl) * 2 * L * TB;
+            const double* uc = cur + (long long)s_id[sl] * KS;
+            const double* up = prv + (long long)s_id[sl] * KS;
+            const double* cf = p.tcoef + (long long)s_id[sl] * 2 * L * TB;
             issue(uc, sbytes);
             issue(uc + SB, sbytes);
             issue(cf, cbytes);
@@ -545,9 +550,9 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
             }
         }
         for (int sl = 0; sl < ns; ++sl) {
-            issue(p.mtiles + (size_t)(s0 + sl) * NMT * 64, mbytes);
-            issue(cur + (long long)(s0 + sl) * KS, sbytes);
-            issue(prv + (long long)(s0 + sl) * KS, sbytes);
+            issue(p.mtiles + (size_t)s_id[sl] * NMT * 64, mbytes);
+            issue(cur + (long long)s_id[sl] * KS, sbytes);
+            issue(prv + (long long)s_id[sl] * KS, sbytes);
         }
     }
 }
@@ -583,7 +588,7 @@ static MtShape mt_shape(int m) {
 }
 
 static size_t mt_smem_bytes(const MtShape& d, int nst, int nsmax) {
-    const size_t b = (size_t)nst * d.STG * 8 + (2 * (size_t)nst + 1) * 8 + 4 * (32 + 6 * (size_t)nsmax);
+    const size_t b = (size_t)nst * d.STG * 8 + (2 * (size_t)nst + 1) * 8 + 4 * (32 + 7 * (size_t)nsmax);
     return (b + 127) & ~(size_t)127;  // one team
 }
 
@@ -693,11 +698,38 @@ extern "C" int sfw_shots_setup(sfw_stepper* h, int n_shots, const int* shot_sub,
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         int G = std::min(2 * nsm, n);
         if (const char* e = getenv("SFW_STEP_MAXGRID")) G = std::max(1, std::min(G, atoi(e)));  // test hook
-        std::vector<int> cta_ptr(G + 1);
-        for (int b = 0; b <= G; ++b) cta_ptr[b] = (int)((long long)b * n / G);
+        // A step ends at a grid-wide barrier, so the most loaded team sets its length.  Cost of a
+        // subdomain: 2L-1 block products, one more (Gamma-hat_0) on the domain boundary, plus the
+        // face pass.  Longest-processing-time assignment (costliest first, to the least loaded team;
+        // ties to the lower team so that runs of neighbours stay together), ascending within a team.
+        std::vector<int> order(n), cost(n);
+        for (int sdx = 0; sdx < n; ++sdx) {
+            bool interior = true;
+            for (int f = 0; f < 6; ++f) interior = interior && h->nbr_h[6 * sdx + f] >= 0;
+            cost[sdx] = 10 * (2 * L - 1) + 6 + (interior ? 0 : 10);
+            order[sdx] = sdx;
+        }
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+        std::vector<long long> load(G, 0);
+        std::vector<std::vector<int>> mine(G);
+        for (int sdx : order) {
+            int best = 0;
+            for (int b = 1; b < G; ++b)
+                if (load[b] < load[best]) best = b;
+            load[best] += cost[sdx];
+            mine[best].push_back(sdx);
+        }
+        std::vector<int> cta_ptr(G + 1, 0), subs;
         int nsmax = 0;
-        for (int b = 0; b < G; ++b) nsmax = std::max(nsmax, cta_ptr[b + 1] - cta_ptr[b]);
+        for (int b = 0; b < G; ++b) {
+            std::sort(mine[b].begin(), mine[b].end());
+            subs.insert(subs.end(), mine[b].begin(), mine[b].end());
+            cta_ptr[b + 1] = (int)subs.size();
+            nsmax = std::max(nsmax, (int)mine[b].size());
+        }
         if ((rc = upload(&h->mt_cta_ptr, cta_ptr, errbuf, errlen))) return rc;
+        if ((rc = upload(&h->mt_ncta, subs, errbuf, errlen))) return rc;  // the teams' subdomain lists
+        h->mt_nsmax = nsmax;
         if ((rc = dalloc(&h->mt_flags, (size_t)G, errbuf, errlen))) return rc;
         // ring depth: two teams share the 227 KB of a CTA
         int nst = 12;
@@ -774,6 +806,8 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
     p.acc1 = h->macc1;
     p.nbr = h->nbr;
     p.cta_sub_ptr = h->mt_cta_ptr;
+    p.team_subs = h->mt_ncta;
+    p.nsmax = h->mt_nsmax;
     p.shot_sub = h->shot_sub;
     p.shot_vec = h->shot_vec;
     p.shot_voff = h->shot_voff;

@@ -115,6 +115,7 @@ struct sfw_stepper {
     std::vector<int> nbr_h;           // host copy of the face-neighbour table [n_sub][6]
     int mt_grid = 0, mt_nst = 0, mt_team_smem = 0;  // k_step_mt: teams (two per CTA), ring stages, bytes per team
     int *mt_cta_ptr = nullptr, *mt_ncta_ptr = nullptr, *mt_ncta = nullptr;
+    int mt_nsmax = 0;
     unsigned int* mt_flags = nullptr;
     double* mmass = nullptr;  // multi-shot: per-subdomain interface mass tiles
     double* tcoef = nullptr;          // [n_blocks][TB] swizzled 8x8 lower tiles
