@@ -390,10 +390,11 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
         }
         asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
         // ---------------- faces: layer-0 coupling + leapfrog -----------------------------
-        for (int sl = 0; sl < ns; ++sl) {
+        // The face values of a subdomain (own + neighbour flux on shared faces, acc_0 on outer faces;
+        // a row takes exactly one of the two) are scattered L2 reads: those of subdomain sl + 1 are
+        // issued before the mass product of subdomain sl, so their latency hides behind it.
+        auto gather = [&](int sl, double (&y)[RT][2]) {
             const int s = s_id[sl];
-            const bool mine = my_src == s;
-            double x[RT][2], acc[RT][2], a1[RT][2];
             const double* fo = fx + (size_t)s * SB + lo;
             const double* ao = p.acc1 + (size_t)s * SB + lo;
 #pragma unroll
@@ -401,17 +402,33 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int row = 8 * t + 2 * c + e;
-                    x[t][e] = 0.0;
-                    a1[t][e] = 0.0;
+                    y[t][e] = 0.0;
                     if (row < W) {
                         const int f = row / M, nb = s_nb[sl * 6 + f];
                         if (nb >= 0)
-                            x[t][e] = __dadd_rn(__ldcg(fo + 8 * t + e),
+                            y[t][e] = __dadd_rn(__ldcg(fo + 8 * t + e),
                                                 __ldcg(fx + (size_t)nb * SB + q * WP + (f ^ 1) * M + row % M));
                         else
-                            a1[t][e] = __ldcg(ao + 8 * t + e);
+                            y[t][e] = __ldcg(ao + 8 * t + e);
                     }
                 }
+        };
+        double yn[RT][2];
+        if (ns > 0) gather(0, yn);
+        for (int sl = 0; sl < ns; ++sl) {
+            const int s = s_id[sl];
+            const bool mine = my_src == s;
+            double x[RT][2], acc[RT][2], a1[RT][2];
+#pragma unroll
+            for (int t = 0; t < RT; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = 8 * t + 2 * c + e;
+                    const bool outer = row < W && s_nb[sl * 6 + row / M] < 0;
+                    x[t][e] = outer ? 0.0 : yn[t][e];
+                    a1[t][e] = outer ? yn[t][e] : 0.0;
+                }
+            if (sl + 1 < ns) gather(sl + 1, yn);
             mt_gemm<M, true>(acquire(0), x, acc, dir, trn);
             const double* u0 = acquire(1);
             const double* uo = acquire(2);
