@@ -200,34 +200,56 @@ __device__ __forceinline__ void static_for(F&& f) {
     static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
+// B fragments of k-step KC (all row tiles): element for element what mt_gemm's MMAs of that k-step read
+template <int M, bool MASS, int KC>
+__device__ __forceinline__ void mt_ldb(const double* __restrict__ tiles, double (&b)[MtDims<M>::RT], const int (&dir)[2],
+                                       const int (&trn)[2]) {
+    constexpr int RT = MtDims<M>::RT, T = KC / 2, e = KC % 2;
+    static_for<RT>([&](auto tc) {
+        constexpr int t = decltype(tc)::value;
+        if constexpr (!MASS || mt_face_tile(M, T, t)) {
+            constexpr int hi = T >= t ? T : t, lo = T >= t ? t : T;
+            constexpr int tl = MASS ? mt_mass_idx(M, hi, lo) : hi * (hi + 1) / 2 + lo;
+            b[t] = tiles[tl * 64 + (T >= t ? dir[e] : trn[e])];
+        }
+    });
+}
+
+template <int M, bool MASS, int KC>
+__device__ __forceinline__ void mt_kstep(const double* __restrict__ tiles, const double (&x)[MtDims<M>::RT][2],
+                                         double (&acc)[MtDims<M>::RT][2], double (&bb)[3][MtDims<M>::RT],
+                                         const int (&dir)[2], const int (&trn)[2]) {
+    constexpr int RT = MtDims<M>::RT, T = KC / 2, e = KC % 2;
+    if constexpr (KC + 2 < 2 * RT) mt_ldb<M, MASS, KC + 2>(tiles, bb[(KC + 2) % 3], dir, trn);
+    const double a = x[T][e];
+    static_for<RT>([&](auto tc) {
+        constexpr int t = decltype(tc)::value;
+        if constexpr (!MASS || mt_face_tile(M, T, t)) dmma8x8x4(acc[t], a, bb[KC % 3][t]);
+    });
+    if constexpr (KC + 1 < 2 * RT) mt_kstep<M, MASS, KC + 1>(tiles, x, acc, bb, dir, trn);
+}
+
 // acc^T = x^T B over all row tiles; x, acc in accumulator-fragment layout (see the header comment).
 // MASS: B = block-diagonal interface mass, only the tiles that meet a face block.  RT independent
-// accumulator chains; every tile offset is an immediate.
+// accumulator chains; every tile offset is an immediate.  The B fragments of k-step kc + 1 are
+// loaded before the MMAs of k-step kc are issued (two register sets), so that a warp alone on its
+// scheduler still finds its operands loaded.
 template <int M, bool MASS>
 __device__ __forceinline__ void mt_gemm(const double* __restrict__ tiles, const double (&x)[MtDims<M>::RT][2],
                                         double (&acc)[MtDims<M>::RT][2], const int (&dir)[2], const int (&trn)[2]) {
     constexpr int RT = MtDims<M>::RT;
 #pragma unroll
     for (int t = 0; t < RT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    static_for<2 * RT>([&](auto kc) {
-        constexpr int T = decltype(kc)::value / 2, e = decltype(kc)::value % 2;
-        const double a = x[T][e];
-        static_for<RT>([&](auto tc) {
-            constexpr int t = decltype(tc)::value;
-            if constexpr (!MASS || mt_face_tile(M, T, t)) {
-                constexpr int hi = T >= t ? T : t, lo = T >= t ? t : T;
-                constexpr int tl = MASS ? mt_mass_idx(M, hi, lo) : hi * (hi + 1) / 2 + lo;
-                const double b = tiles[tl * 64 + (T >= t ? dir[e] : trn[e])];
-                dmma8x8x4(acc[t], a, b);
-            }
-        });
-    });
+    double bb[3][RT];
+    mt_ldb<M, MASS, 0>(tiles, bb[0], dir, trn);
+    mt_ldb<M, MASS, 1>(tiles, bb[1], dir, trn);
+    mt_kstep<M, MASS, 0>(tiles, x, acc, bb, dir, trn);
 }
 
 template <int M>
 __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring, uint64_t* full, uint64_t* empty,
                                            uint64_t* stepdone, const int* ssub, const int* s_id, const int* s_nb, int ns,
-                                           int team, int w, int lane) {
+                                           int team, int w, int lane, double* stash) {
     using D = MtDims<M>;
     constexpr int S = D::S, W = D::W, RT = D::RT, WP = D::WP, SB = D::SB, STG = D::STG;
     const int L = p.L, NST = p.nst;
@@ -280,6 +302,13 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
         for (int t = 0; t < RT; ++t)
             *reinterpret_cast<double2*>(blk + lo + 8 * t) = make_double2(v[t][0], v[t][1]);
     };
+    // warp-private scratch for the two state slices a layer needs again after its products
+    // (U_j for the leapfrog, U_{j+1} as the next layer's U_j): kept out of registers during the GEMMs
+    double2* stw = reinterpret_cast<double2*>(stash) + (size_t)w * (2 * RT * 32) + lane;
+    auto stash_put = [&](int slot, const double (&v)[RT][2]) {
+#pragma unroll
+        for (int t = 0; t < RT; ++t) stw[(slot * RT + t) * 32] = make_double2(v[t][0], v[t][1]);
+    };
     const double dt2 = p.dt2;
     const int barT = 1 + (int)(threadIdx.x >= (MT_NCW + 1) * 32);  // named barrier of the team's compute warps
     const int my_src = ssub[q];           // source subdomain of this lane's shot
@@ -298,8 +327,10 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
         for (int sl = 0; sl < ns; ++sl) {
             const int s = s_id[sl];
             const bool mine = my_src == s;
-            double ua[RT][2], ub[RT][2], fp[RT][2], x[RT][2], acc[RT][2];
+            double fp[RT][2], x[RT][2], acc[RT][2];
+            int cur = 0;  // stash slot of U_j
             {
+                double ua[RT][2];
                 const double* b0 = acquire(0);
                 const double* b1 = acquire(1);
                 load_slice(b0, x);   // U_0
@@ -311,6 +342,7 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                     x[t][0] = ua[t][0] - x[t][0];
                     x[t][1] = ua[t][1] - x[t][1];
                 }
+                stash_put(cur, ua);
             }
             mt_gemm<M, false>(acquire(0), x, fp, dir, trn);  // F_0
             settle(fp);
@@ -325,17 +357,22 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                 store_slice(p.acc1 + (size_t)s * SB, acc);
             }
             for (int j = 1; j < L; ++j) {
-                if (j + 1 < L) {
-                    load_slice(acquire(0), ub);  // U_{j+1}
-                    release();
-                } else {
+                {
+                    double ub[RT][2];
+                    if (j + 1 < L) {
+                        load_slice(acquire(0), ub);  // U_{j+1}
+                        release();
+                    } else {
 #pragma unroll
-                    for (int t = 0; t < RT; ++t) ub[t][0] = ub[t][1] = 0.0;
-                }
+                        for (int t = 0; t < RT; ++t) ub[t][0] = ub[t][1] = 0.0;
+                    }
 #pragma unroll
-                for (int t = 0; t < RT; ++t) {
-                    x[t][0] = ub[t][0] - ua[t][0];
-                    x[t][1] = ub[t][1] - ua[t][1];
+                    for (int t = 0; t < RT; ++t) {
+                        const double2 a = stw[(cur * RT + t) * 32];  // U_j
+                        x[t][0] = ub[t][0] - a.x;
+                        x[t][1] = ub[t][1] - a.y;
+                    }
+                    stash_put(cur ^ 1, ub);
                 }
                 mt_gemm<M, false>(acquire(0), x, acc, dir, trn);  // F_j
                 settle(acc);
@@ -355,23 +392,20 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
 #pragma unroll
                 for (int t = 0; t < RT; ++t) {
                     const double2 o = *reinterpret_cast<const double2*>(uo + lo + 8 * t);
+                    const double2 a = stw[(cur * RT + t) * 32];  // U_j
                     double v[2];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         double tot = acc[t][e];
                         const int row = 8 * t + 2 * c + e;
                         if (mine && row < W) tot = __dadd_rn(tot, __dmul_rn(svec[(long long)j * W + row], fq));
-                        v[e] = fma(dt2, tot, fma(2.0, ua[t][e], e ? -o.y : -o.x));
+                        v[e] = fma(dt2, tot, fma(2.0, e ? a.y : a.x, e ? -o.y : -o.x));
                         sq = fma(v[e], v[e], sq);
                     }
                     *reinterpret_cast<double2*>(un + lo + 8 * t) = make_double2(v[0], v[1]);
                 }
                 release();
-#pragma unroll
-                for (int t = 0; t < RT; ++t) {
-                    ua[t][0] = ub[t][0];
-                    ua[t][1] = ub[t][1];
-                }
+                cur ^= 1;
             }
         }
         // ---------------- grid-wide step barrier ------------------------------------------
@@ -502,7 +536,8 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
     const int L = p.L, NST = p.nst;
     const long long KS = (long long)L * SB;
     double* ring = reinterpret_cast<double*>(smem_raw + (size_t)tw * p.team_smem);  // [NST][STG]
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NST * STG);
+    double* stash = ring + (size_t)NST * STG;  // [MT_NCW][2][RT][32] double2, warp-private
+    uint64_t* full = reinterpret_cast<uint64_t*>(stash + (size_t)MT_NCW * 2 * D::RT * 32 * 2);
     uint64_t* empty = full + NST;
     uint64_t* stepdone = empty + NST;
     int* ssub = reinterpret_cast<int*>(stepdone + 1);
@@ -525,7 +560,7 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
     asm volatile("bar.sync %0, %1;" ::"r"(3 + tw), "r"((MT_NCW + 1) * 32) : "memory");
 
     if (warp < MT_NCW) {
-        mt_compute<M>(p, ring, full, empty, stepdone, ssub, s_id, s_nb, ns, team, warp, lane);
+        mt_compute<M>(p, ring, full, empty, stepdone, ssub, s_id, s_nb, ns, team, warp, lane, stash);
         return;
     }
     // ======== producer: one lane streams every item in consumption order ========
@@ -605,7 +640,8 @@ static MtShape mt_shape(int m) {
 }
 
 static size_t mt_smem_bytes(const MtShape& d, int nst, int nsmax) {
-    const size_t b = (size_t)nst * d.STG * 8 + (2 * (size_t)nst + 1) * 8 + 4 * (32 + 7 * (size_t)nsmax);
+    const size_t b = (size_t)nst * d.STG * 8 + (size_t)MT_NCW * 2 * d.RT * 32 * 16 + (2 * (size_t)nst + 1) * 8 +
+                     4 * (32 + 7 * (size_t)nsmax);
     return (b + 127) & ~(size_t)127;  // one team
 }
 
