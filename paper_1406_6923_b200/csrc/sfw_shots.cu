@@ -217,14 +217,14 @@ __device__ __forceinline__ void mt_ldb(const double* __restrict__ tiles, double 
 
 template <int M, bool MASS, int KC>
 __device__ __forceinline__ void mt_kstep(const double* __restrict__ tiles, const double (&x)[MtDims<M>::RT][2],
-                                         double (&acc)[MtDims<M>::RT][2], double (&bb)[3][MtDims<M>::RT],
+                                         double (&acc)[MtDims<M>::RT][2], double (&bb)[4][MtDims<M>::RT],
                                          const int (&dir)[2], const int (&trn)[2]) {
     constexpr int RT = MtDims<M>::RT, T = KC / 2, e = KC % 2;
-    if constexpr (KC + 2 < 2 * RT) mt_ldb<M, MASS, KC + 2>(tiles, bb[(KC + 2) % 3], dir, trn);
+    if constexpr (KC + 3 < 2 * RT) mt_ldb<M, MASS, KC + 3>(tiles, bb[(KC + 3) % 4], dir, trn);
     const double a = x[T][e];
     static_for<RT>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
-        if constexpr (!MASS || mt_face_tile(M, T, t)) dmma8x8x4(acc[t], a, bb[KC % 3][t]);
+        if constexpr (!MASS || mt_face_tile(M, T, t)) dmma8x8x4(acc[t], a, bb[KC % 4][t]);
     });
     if constexpr (KC + 1 < 2 * RT) mt_kstep<M, MASS, KC + 1>(tiles, x, acc, bb, dir, trn);
 }
@@ -240,9 +240,10 @@ __device__ __forceinline__ void mt_gemm(const double* __restrict__ tiles, const 
     constexpr int RT = MtDims<M>::RT;
 #pragma unroll
     for (int t = 0; t < RT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    double bb[3][RT];
+    double bb[4][RT];
     mt_ldb<M, MASS, 0>(tiles, bb[0], dir, trn);
     mt_ldb<M, MASS, 1>(tiles, bb[1], dir, trn);
+    mt_ldb<M, MASS, 2>(tiles, bb[2], dir, trn);
     mt_kstep<M, MASS, 0>(tiles, x, acc, bb, dir, trn);
 }
 
