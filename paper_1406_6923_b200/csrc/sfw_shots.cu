@@ -215,36 +215,82 @@ __device__ __forceinline__ void mt_ldb(const double* __restrict__ tiles, double 
     });
 }
 
+// Operand registers of an MMA must not be overwritten before the MMA has read them.  ptxas orders a
+// later write (here: the shared load of another B fragment into the same register) behind an
+// mma.sync.m8n8k4.f64 by a fixed issue distance only, and an MMA that queues behind the MMAs of the
+// other warps of its SMSP reads its operands later than that.  Measured (config 4): with
+// two compute warps per SMSP a few runs in a hundred had one warp's product computed with the next
+// tile's B fragment, with three warps 15 in a hundred, with one warp none.  mt_hold() is a cheap
+// (ALU-pipe) use of a register that keeps it live up to a point of the instruction stream: every B
+// fragment is held until the next MMA of its accumulator chain has been issued (that MMA waits for
+// the previous one's result, so the previous one has read its operands), the last fragments and
+// all A operands until the products are in registers.
+__device__ __forceinline__ void mt_hold(unsigned int& keep, double v) {
+    unsigned int w32;
+    asm volatile("{ .reg .b32 lo; mov.b64 {lo, %0}, %1; }" : "=r"(w32) : "d"(v));
+    keep ^= w32;
+}
+__device__ unsigned int g_mt_sink;
+
 template <int M, bool MASS, int KC>
 __device__ __forceinline__ void mt_kstep(const double* __restrict__ tiles, const double (&x)[MtDims<M>::RT][2],
-                                         double (&acc)[MtDims<M>::RT][2], double (&bb)[4][MtDims<M>::RT],
-                                         const int (&dir)[2], const int (&trn)[2]) {
+                                         double (&acc)[MtDims<M>::RT][2], double (&bb)[3][MtDims<M>::RT],
+                                         double (&pend)[MtDims<M>::RT], unsigned int& pmask, const int (&dir)[2],
+                                         const int (&trn)[2], unsigned int& keep) {
     constexpr int RT = MtDims<M>::RT, T = KC / 2, e = KC % 2;
-    if constexpr (KC + 3 < 2 * RT) mt_ldb<M, MASS, KC + 3>(tiles, bb[(KC + 3) % 4], dir, trn);
+    if constexpr (KC + 1 < 2 * RT) mt_ldb<M, MASS, KC + 1>(tiles, bb[(KC + 1) % 3], dir, trn);
     const double a = x[T][e];
     static_for<RT>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
-        if constexpr (!MASS || mt_face_tile(M, T, t)) dmma8x8x4(acc[t], a, bb[KC % 4][t]);
+        if constexpr (!MASS) {
+            // full product: chain t has an MMA in every k-step; the previous k-step's fragment of
+            // the chain is released once this k-step's MMA of the chain has been issued
+            dmma8x8x4(acc[t], a, bb[KC % 3][t]);
+            if constexpr (KC >= 1) mt_hold(keep, bb[(KC - 1) % 3][t]);
+        } else if constexpr (mt_face_tile(M, T, t)) {
+            // sparse product: the chain's last fragment is carried in pend[] until its next MMA
+            dmma8x8x4(acc[t], a, bb[KC % 3][t]);
+            if (pmask & (1u << t)) mt_hold(keep, pend[t]);  // (a compile-time constant after unrolling)
+            pend[t] = bb[KC % 3][t];
+            pmask |= 1u << t;
+        }
     });
-    if constexpr (KC + 1 < 2 * RT) mt_kstep<M, MASS, KC + 1>(tiles, x, acc, bb, dir, trn);
+    // every chain has now issued an MMA that waits for its MMA of the previous k-step: that
+    // k-step's A operand has been read (full product only; the sparse one holds all of x to the end)
+    if constexpr (!MASS && KC >= 1) mt_hold(keep, x[(KC - 1) / 2][(KC - 1) % 2]);
+    if constexpr (KC + 1 < 2 * RT) mt_kstep<M, MASS, KC + 1>(tiles, x, acc, bb, pend, pmask, dir, trn, keep);
 }
 
 // acc^T = x^T B over all row tiles; x, acc in accumulator-fragment layout (see the header comment).
 // MASS: B = block-diagonal interface mass, only the tiles that meet a face block.  RT independent
-// accumulator chains; every tile offset is an immediate.  The B fragments of k-step kc + 1 are
-// loaded before the MMAs of k-step kc are issued (two register sets), so that a warp alone on its
-// scheduler still finds its operands loaded.
+// accumulator chains; every tile offset is an immediate.  The B fragments of k-step kc + 1 are loaded
+// before the MMAs of k-step kc are issued.
 template <int M, bool MASS>
 __device__ __forceinline__ void mt_gemm(const double* __restrict__ tiles, const double (&x)[MtDims<M>::RT][2],
                                         double (&acc)[MtDims<M>::RT][2], const int (&dir)[2], const int (&trn)[2]) {
-    constexpr int RT = MtDims<M>::RT;
+    constexpr int RT = MtDims<M>::RT, LAST = 2 * RT - 1;
 #pragma unroll
     for (int t = 0; t < RT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    double bb[4][RT];
+    double bb[3][RT], pend[RT];
+    unsigned int keep = 0, pmask = 0;
     mt_ldb<M, MASS, 0>(tiles, bb[0], dir, trn);
-    mt_ldb<M, MASS, 1>(tiles, bb[1], dir, trn);
-    mt_ldb<M, MASS, 2>(tiles, bb[2], dir, trn);
-    mt_kstep<M, MASS, 0>(tiles, x, acc, bb, dir, trn);
+    mt_kstep<M, MASS, 0>(tiles, x, acc, bb, pend, pmask, dir, trn, keep);
+    // products in registers: every MMA has read its operands
+#pragma unroll
+    for (int t = 0; t < RT; ++t) asm volatile("" : "+d"(acc[t][0]), "+d"(acc[t][1])::"memory");
+    if constexpr (!MASS) {
+#pragma unroll
+        for (int t = 0; t < RT; ++t) mt_hold(keep, bb[LAST % 3][t]);
+        mt_hold(keep, x[LAST / 2][LAST % 2]);
+    } else {
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            if (pmask & (1u << t)) mt_hold(keep, pend[t]);
+            mt_hold(keep, x[t][0]);
+            mt_hold(keep, x[t][1]);
+        }
+    }
+    if (keep == 0x9e3779b9u) g_mt_sink = keep;  // practically never; keeps the holds alive
 }
 
 template <int M>
@@ -305,7 +351,7 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
     };
     // warp-private scratch for the two state slices a layer needs again after its products
     // (U_j for the leapfrog, U_{j+1} as the next layer's U_j): kept out of registers during the GEMMs
-    double2* stw = reinterpret_cast<double2*>(stash) + (size_t)w * (2 * RT * 32) + lane;
+    double2* stw = reinterpret_cast<double2*>(stash) + (size_t)w * (3 * RT * 32) + lane;
     auto stash_put = [&](int slot, const double (&v)[RT][2]) {
 #pragma unroll
         for (int t = 0; t < RT; ++t) stw[(slot * RT + t) * 32] = make_double2(v[t][0], v[t][1]);
@@ -328,8 +374,8 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
         for (int sl = 0; sl < ns; ++sl) {
             const int s = s_id[sl];
             const bool mine = my_src == s;
-            double fp[RT][2], x[RT][2], acc[RT][2];
-            int cur = 0;  // stash slot of U_j
+            double x[RT][2], acc[RT][2];
+            int cur = 0;  // stash slot of U_j (slot 2: the previous layer's flux F_{j-1})
             {
                 double ua[RT][2];
                 const double* b0 = acquire(0);
@@ -345,17 +391,19 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                 }
                 stash_put(cur, ua);
             }
-            mt_gemm<M, false>(acquire(0), x, fp, dir, trn);  // F_0
-            settle(fp);
+            {
+                double fp[RT][2];
+                mt_gemm<M, false>(acquire(0), x, fp, dir, trn);  // F_0
                 release();
-            store_slice(fx + (size_t)s * SB, fp);
-            const bool interior = (s_nb[sl * 6] | s_nb[sl * 6 + 1] | s_nb[sl * 6 + 2] | s_nb[sl * 6 + 3] |
-                                   s_nb[sl * 6 + 4] | s_nb[sl * 6 + 5]) >= 0;
-            if (!interior) {  // acc_0 = H_0 F_0: only outer-face rows are read back
-                mt_gemm<M, false>(acquire(0), fp, acc, dir, trn);
-                settle(acc);
-                release();
-                store_slice(p.acc1 + (size_t)s * SB, acc);
+                store_slice(fx + (size_t)s * SB, fp);
+                stash_put(2, fp);
+                const bool interior = (s_nb[sl * 6] | s_nb[sl * 6 + 1] | s_nb[sl * 6 + 2] | s_nb[sl * 6 + 3] |
+                                       s_nb[sl * 6 + 4] | s_nb[sl * 6 + 5]) >= 0;
+                if (!interior) {  // acc_0 = H_0 F_0: only outer-face rows are read back
+                    mt_gemm<M, false>(acquire(0), fp, acc, dir, trn);
+                    release();
+                    store_slice(p.acc1 + (size_t)s * SB, acc);
+                }
             }
             for (int j = 1; j < L; ++j) {
                 {
@@ -376,17 +424,15 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                     stash_put(cur ^ 1, ub);
                 }
                 mt_gemm<M, false>(acquire(0), x, acc, dir, trn);  // F_j
-                settle(acc);
                 release();
 #pragma unroll
                 for (int t = 0; t < RT; ++t) {
-                    x[t][0] = acc[t][0] - fp[t][0];
-                    x[t][1] = acc[t][1] - fp[t][1];
-                    fp[t][0] = acc[t][0];
-                    fp[t][1] = acc[t][1];
+                    const double2 f = stw[(2 * RT + t) * 32];  // F_{j-1}
+                    x[t][0] = acc[t][0] - f.x;
+                    x[t][1] = acc[t][1] - f.y;
                 }
+                stash_put(2, acc);
                 mt_gemm<M, false>(acquire(0), x, acc, dir, trn);  // A_j
-                settle(acc);
                 release();
                 const double* uo = acquire(0);  // Uprev_j
                 double* un = Un + (size_t)s * KS + (size_t)j * SB;
@@ -427,7 +473,7 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
         // ---------------- faces: layer-0 coupling + leapfrog -----------------------------
         // The face values of a subdomain (own + neighbour flux on shared faces, acc_0 on outer faces;
         // a row takes exactly one of the two) are scattered L2 reads: those of subdomain sl + 1 are
-        // issued before the mass product of subdomain sl, so their latency hides behind it.
+        // issued after the mass product of subdomain sl, so their latency hides behind its leapfrog.
         auto gather = [&](int sl, double (&y)[RT][2]) {
             const int s = s_id[sl];
             const double* fo = fx + (size_t)s * SB + lo;
@@ -463,8 +509,8 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
                     x[t][e] = outer ? 0.0 : yn[t][e];
                     a1[t][e] = outer ? yn[t][e] : 0.0;
                 }
-            if (sl + 1 < ns) gather(sl + 1, yn);
             mt_gemm<M, true>(acquire(0), x, acc, dir, trn);
+            if (sl + 1 < ns) gather(sl + 1, yn);  // lands while this subdomain's layer 0 is updated
             const double* u0 = acquire(1);
             const double* uo = acquire(2);
             double* un = Un + (size_t)s * KS;
@@ -537,8 +583,8 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
     const int L = p.L, NST = p.nst;
     const long long KS = (long long)L * SB;
     double* ring = reinterpret_cast<double*>(smem_raw + (size_t)tw * p.team_smem);  // [NST][STG]
-    double* stash = ring + (size_t)NST * STG;  // [MT_NCW][2][RT][32] double2, warp-private
-    uint64_t* full = reinterpret_cast<uint64_t*>(stash + (size_t)MT_NCW * 2 * D::RT * 32 * 2);
+    double* stash = ring + (size_t)NST * STG;  // [MT_NCW][3][RT][32] double2, warp-private
+    uint64_t* full = reinterpret_cast<uint64_t*>(stash + (size_t)MT_NCW * 3 * D::RT * 32 * 2);
     uint64_t* empty = full + NST;
     uint64_t* stepdone = empty + NST;
     int* ssub = reinterpret_cast<int*>(stepdone + 1);
@@ -641,7 +687,7 @@ static MtShape mt_shape(int m) {
 }
 
 static size_t mt_smem_bytes(const MtShape& d, int nst, int nsmax) {
-    const size_t b = (size_t)nst * d.STG * 8 + (size_t)MT_NCW * 2 * d.RT * 32 * 16 + (2 * (size_t)nst + 1) * 8 +
+    const size_t b = (size_t)nst * d.STG * 8 + (size_t)MT_NCW * 3 * d.RT * 32 * 16 + (2 * (size_t)nst + 1) * 8 +
                      4 * (32 + 7 * (size_t)nsmax);
     return (b + 127) & ~(size_t)127;  // one team
 }

@@ -127,8 +127,8 @@ def test_config4_full_size_shots(cfg3):
     n = 30
     with CoupledStepper(models, dt) as st:
         times, rows = st.run_shots(n, shots, probes=probes)
-        _, rows2 = st.run_shots(n, shots, probes=probes)
-    assert np.array_equal(rows, rows2)
+        for _ in range(8):  # run-to-run repeatability (config 4: MMA operand registers)
+            assert np.array_equal(rows, st.run_shots(n, shots, probes=probes)[1])
     for q in (0, 13, 31):
         with CoupledStepper(models, dt, sources=(shots[q],)) as st1:
             t1, r1 = st1.run(n, probes=probes)
