@@ -11,17 +11,19 @@
 // the k-steps kappa = 2T + e and letting position c of k-step kappa stand for row
 // 8T + 2c + e makes the accumulator of one GEMM, element for element in the same lane, the
 // A operand of the next: differences, leapfrog and the whole layer sweep of a subdomain
-// stay in registers.  One warp owns 8 shots of a subdomain and sweeps its layers alone; no
-// X tile goes through shared memory and no warp waits for another inside a sweep.  The row
-// permutation of the k-steps is folded into the stored chain blocks (the B operand).
+// stay with the warp.  One warp owns 8 shots of a subdomain and sweeps its layers alone; no
+// X tile is exchanged through shared memory and no warp waits for another inside a sweep
+// (the slices needed again after a product -- U_j, U_{j+1}, F_{j-1} -- rest in a warp-private
+// shared-memory scratch while the GEMMs run).  The row permutation of the k-steps is folded
+// into the stored chain blocks (the B operand).
 //
 // Chain block storage: the lower 8 x 8 tiles (T >= t) of the padded symmetric block, each
 // tile's 64 doubles at the swizzled positions mt_pos(r, c), so that the B fragment of tile
 // (T, t) -- element (2(l%4) + e, l/4) -- and that of its transpose -- element (l/4, 2(l%4) + e)
 // of tile (t, T) -- are both conflict-free 8-byte shared loads.  A block is streamed once.
 //
-// CTA = 4 compute warps (shots 8w .. 8w+7) + 1 producer warp; two CTAs per SM.  One lane of
-// the producer warp streams chain blocks and 32-shot state blocks, in the order the sweep
+// Team = 4 compute warps (shots 8w .. 8w+7) + 1 producer warp; two teams per CTA, one CTA per
+// SM.  One lane of the producer warp streams chain blocks and 32-shot state blocks, in the order the sweep
 // consumes them, through a single ring of equal stages (cp.async.bulk + mbarrier).  Per step:
 //   sweep   per subdomain F_0 = G_0 (U_1 - U_0) -> face buffer (global); boundary subdomains
 //           also acc_0 = H_0 F_0; layers j = 1..L-1: F_j, A_j = H_j (F_j - F_{j-1}), leapfrog
@@ -331,11 +333,6 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
             ph ^= 1;
         }
     };
-    // the stage of a GEMM is released only once the products that read it are in registers
-    auto settle = [&](double (&v)[RT][2]) {
-#pragma unroll
-        for (int t = 0; t < RT; ++t) asm volatile("" : "+d"(v[t][0]), "+d"(v[t][1])::"memory");
-    };
     auto load_slice = [&](const double* blk, double (&v)[RT][2]) {
 #pragma unroll
         for (int t = 0; t < RT; ++t) {
@@ -457,10 +454,8 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
         }
         // ---------------- grid-wide step barrier ------------------------------------------
         // (bar.sync orders the team's face-buffer writes before lane 0's release store: cumulativity.)
-        // The face phase reads only face neighbours' buffers, but the wait is for EVERY team: with
-        // neighbour-only step flags the traces were not reproducible run to run (rare differences at
-        // the leading edge of a wavefield, DESIGN.md config 4); with all teams in step they are, in
-        // every stress run, and the step is no slower.
+        // The face phase reads only face neighbours' buffers; the wait is for every team (the
+        // grid-wide barrier per step), which measured the same step time as neighbour-only flags.
         asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
         if (w == 0 && lane == 0) st_release(p.flags + team, (unsigned int)k);
         if (w == 0) {
