@@ -16,6 +16,9 @@ from paper_1406_6923_b200 import CoupledStepper, SourceTerm, project_source
 from paper_1406_6923_b200.configs import locate, make_workload
 from paper_1406_6923_b200.pulses import ricker
 from test_fullsize_gpu import _build
+import paper_1406_6923_b200.stepper as _ps
+if os.environ.get('MT_NOLIMIT'):
+    _ps.GROWTH_LIMIT = float('inf')
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 rep = int(sys.argv[2]) if len(sys.argv) > 2 else 300
@@ -27,10 +30,12 @@ for ijk in wl.sources:
     shots.append(SourceTerm(a, project_source(models[a], r), ricker(wl.f0, wl.delay)))
 with CoupledStepper(models, dt) as st:
     hs = collections.Counter()
+    nans = 0
     ms = []
     for i in range(rep):
         _, rows, norms = st.run_shots(n, shots, probes=probes, return_norms=True)
         ms.append(st.last_kernel_ms / n)
+        nans += int(np.isnan(rows).sum() + np.isnan(norms).sum())
         hs[hashlib.md5(rows.tobytes() + norms.tobytes()).hexdigest()[:8]] += 1
     print(f"{rep} runs of {n} steps: distinct results {len(hs)}, counts {sorted(hs.values(), reverse=True)[:8]}, "
-          f"ms/step {np.median(ms):.4f}")
+          f"ms/step {np.median(ms):.4f}, NaNs {nans}")
