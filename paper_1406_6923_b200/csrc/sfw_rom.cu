@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(PCG2_T, 1) k_pcg2(const PcgArgs a) {
     int rb = 0;  // ping-pong reduction buffer
     block_sum2(bb0, bb1, red + 64 * rb);
     rb ^= 1;
+    // (sigma = s <1/c^2>, which centres the constant mode, measured the same: 14.83 against 14.97 mean iterations)
     const double sigma = a.shift / (cmin * cmax);
     const double s = a.shift;
     constexpr int sy = pz, sx = py * pz;
@@ -1184,6 +1185,7 @@ extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf
 
     double t_solve = 0, t_orth = 0, t_proj = 0, t_lanc = 0, t_sfr = 0;
     int max_it = 0;
+    long long sum_it = 0, n_it = 0;  // SFW_PCG_STATS: mean iteration count of the shifted solves
     std::vector<int> hit((size_t)B * w), hstat(B), hs2(B);
     std::vector<double> hfro(B), hdpr((size_t)B * w);
     const size_t ww = (size_t)w * w;
@@ -1264,6 +1266,10 @@ extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf
                         keep[b] = -1;
                     }
                     max_it = std::max(max_it, v);
+                    if (v > 0) {
+                        sum_it += v;
+                        ++n_it;
+                    }
                 }
             cudaEventRecord(e0, st);
             const int Kr = r * w;
@@ -1497,6 +1503,8 @@ extern "C" int sfw_rom_build(const sfw_rom_desc* d, sfw_rom_out* o, char* errbuf
         o->stats[3] = t_lanc;
         o->stats[4] = t_sfr;
         o->stats[5] = max_it;
+        if (getenv("SFW_PCG_STATS") && n_it)
+            fprintf(stderr, "[sfw] pcg: %lld solves, mean %.2f iterations, max %d\n", n_it, (double)sum_it / n_it, max_it);
         o->stats[6] = B;
         o->stats[7] = std::chrono::duration<double>(clk::now() - t_begin).count();
     }
