@@ -24,12 +24,19 @@
 //
 // Team = 4 compute warps (shots 8w .. 8w+7) + 1 producer warp; two teams per CTA, one CTA per
 // SM.  One lane of the producer warp streams chain blocks and 32-shot state blocks, in the order the sweep
-// consumes them, through a single ring of equal stages (cp.async.bulk + mbarrier).  Per step:
-//   sweep   per subdomain F_0 = G_0 (U_1 - U_0) -> face buffer (global); boundary subdomains
-//           also acc_0 = H_0 F_0; layers j = 1..L-1: F_j, A_j = H_j (F_j - F_{j-1}), leapfrog
-//   barrier team barrier, step flag (release), wait for the step flags of ALL teams (acquire)
-//   faces   layer 0: T = F_0 + neighbour's F_0 on shared faces, acc_0 = mass T as a GEMM
-//           over the tiles that meet a face block (block-diagonal mass), leapfrog
+// consumes them, through a single ring of equal stages (cp.async.bulk + mbarrier).  Per step k:
+//   sweep   per subdomain: first the DEFERRED layer 0 of step k-1 (k >= 2): T = F_0 + neighbour's F_0 of
+//           step k-1 on shared faces, acc_0 = mass T as a GEMM over the tiles that meet a face block
+//           (block-diagonal mass), leapfrog into the layer-0 slot of U^{k-1}; the new U_0 stays in
+//           registers.  Then F_0 = G_0 (U_1 - U_0) -> face buffer (global); boundary subdomains also
+//           acc_0 = H_0 F_0; layers j = 1..L-1: F_j, A_j = H_j (F_j - F_{j-1}), leapfrog
+//   barrier team barrier, step flag (release), norms and the probes of step k-1, wait for the step flags
+//           of ALL teams (acquire)
+//   after the last step: one layer-0 pass for that step (epilogue).
+// Folding the layer-0 pass into the next sweep (as k_ustep does) overlaps its 209 MB of traffic per
+// step with the other warps' GEMMs and saves one U_0 read per subdomain-step; the face buffer is
+// double-buffered by step parity and a team starts step k+1 only after every team finished sweep k, so a
+// flux of step k-1 is never overwritten (by a sweep of step k+1) while a sweep of step k still reads it.
 // State layout in HBM: [subdomain][layer][shot][WP rows] (rows padded to 8 RT, pad = 0), so a
 // lane's two adjacent rows are one 16-byte access and a warp's 8 shots of a row tile are
 // eight 64-byte segments.
@@ -174,7 +181,7 @@ struct MtParams {
     const double* prb_w;
     const long long* prb_woff;
     double* rows;          // [n_rec][S][n_probe]
-    double* norm_part;     // [n_steps][grid][S]
+    double* norm_part;     // [n_steps][2][n_team][S]  (slot 0: layers >= 1, slot 1: layer 0)
     unsigned int* flags;   // [n_team] step of the last finished sweep
 };
 
@@ -278,6 +285,23 @@ __device__ __forceinline__ void mt_gemm(const double* __restrict__ tiles, const 
     // products in registers: every MMA has read its operands
 #pragma unroll
     for (int t = 0; t < RT; ++t) asm volatile("" : "+d"(acc[t][0]), "+d"(acc[t][1])::"memory");
+    if constexpr (MASS) {
+        // Drain after the sparse product: a real read of every accumulator right behind its MMAs.  A warp
+        // issues in order, so nothing that follows is issued before the last MMA of every chain has
+        // written its result (and therefore read its operands).  With the layer-0 pass inside the sweep
+        // the kernel was not repeatable without this (7-9 of 12 full-size runs equal, some diverging;
+        // with it 1500 of 1500, also with the warps of a team forced into lockstep); the same kind of
+        // measure as mt_hold() above, see DESIGN.md (config 4).
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            unsigned int d0, d1;
+            asm volatile("{ .reg .b32 lo; mov.b64 {lo, %0}, %2; mov.b64 {lo, %1}, %3; }"
+                         : "=r"(d0), "=r"(d1)
+                         : "d"(acc[t][0]), "d"(acc[t][1])
+                         : "memory");
+            keep ^= d0 ^ d1;
+        }
+    }
     if constexpr (!MASS) {
 #pragma unroll
         for (int t = 0; t < RT; ++t) mt_hold(keep, bb[LAST % 3][t]);
@@ -356,28 +380,118 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
     const int my_src = ssub[q];           // source subdomain of this lane's shot
     const double* svec = my_src >= 0 ? p.shot_vec + p.shot_voff[q] : nullptr;
 
+    // ---- layer 0 of one subdomain for the step whose fluxes are in fxb: T = F_0 + neighbour's F_0 on
+    // shared faces, acc_0 = mass T (sparse tile GEMM) or the stored H_0 F_0 rows on outer faces, source,
+    // leapfrog into ub (the buffer whose layer-0 slot still holds the older level); the new U_0 stays
+    // in v.  Ring items: mass tiles, U_0 (newer level), U_0 (older level).
+    auto layer0 = [&](int sl, const double* fxb, double fqv, double* ub, double& sqv, double (&v)[RT][2]) {
+        const int s = s_id[sl];
+        const bool mine = my_src == s;
+        double x[RT][2], a1[RT][2], acc[RT][2];
+        {
+            // face values (own + neighbour flux on shared faces, acc_0 on outer faces; a row takes
+            // exactly one of the two): scattered L2 reads
+            const double* fo = fxb + (size_t)s * SB + lo;
+            const double* ao = p.acc1 + (size_t)s * SB + lo;
+#pragma unroll
+            for (int t = 0; t < RT; ++t)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = 8 * t + 2 * c + e;
+                    x[t][e] = 0.0;
+                    a1[t][e] = 0.0;
+                    if (row < W) {
+                        const int f = row / M, nb = s_nb[sl * 6 + f];
+                        if (nb >= 0)
+                            x[t][e] = __dadd_rn(__ldcg(fo + 8 * t + e),
+                                                __ldcg(fxb + (size_t)nb * SB + q * WP + (f ^ 1) * M + row % M));
+                        else
+                            a1[t][e] = __ldcg(ao + 8 * t + e);
+                    }
+                }
+        }
+        mt_gemm<M, true>(acquire(0), x, acc, dir, trn);
+        const double* u0 = acquire(1);
+        const double* uo = acquire(2);
+        double* un = ub + (size_t)s * KS;
+#pragma unroll
+        for (int t = 0; t < RT; ++t) {
+            const double2 u = *reinterpret_cast<const double2*>(u0 + lo + 8 * t);
+            const double2 o = *reinterpret_cast<const double2*>(uo + lo + 8 * t);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = 8 * t + 2 * c + e;
+                double tot = __dadd_rn(acc[t][e], a1[t][e]);  // one of the two is zero
+                if (mine && row < W) tot = __dadd_rn(tot, __dmul_rn(svec[row], fqv));
+                v[t][e] = fma(dt2, tot, fma(2.0, e ? u.y : u.x, e ? -o.y : -o.x));
+                sqv = fma(v[t][e], v[t][e], sqv);
+            }
+            *reinterpret_cast<double2*>(un + lo + 8 * t) = make_double2(v[t][0], v[t][1]);
+        }
+        release();  // mass tiles
+        release();  // U_0, newer level
+        release();  // U_0, older level
+    };
+    // per-shot |U|^2 partial of this team (the 4 lanes of a shot hold its rows); slot 0: layers >= 1
+    // of step kz + 1, slot 1: its layer 0 (computed one sweep later)
+    auto put_norm = [&](int kz, int slot, double sqv) {
+        sqv += __shfl_xor_sync(0xffffffffu, sqv, 1);
+        sqv += __shfl_xor_sync(0xffffffffu, sqv, 2);
+        if (c == 0) p.norm_part[(((size_t)kz * 2 + slot) * p.n_team + team) * S + q] = sqv;
+    };
+    // probes: rows of the completed state after step kdone (thread = shot x every 4th probe); the
+    // caller has passed a team barrier after the last write of that state
+    auto record = [&](int kdone, const double* Ub) {
+        if (kdone % p.record_every != 0 || !p.rows) return;
+        const long long rec = kdone / p.record_every - 1;
+        const int pq0 = w, qs = lane;  // thread (w, lane): shot lane, probes w, w+4, ...
+        for (int sl = 0; sl < ns; ++sl) {
+            const int s = s_id[sl];
+            const double* us = Ub + (size_t)s * KS + (size_t)qs * WP;
+            for (int pq = p.prb_ptr[s] + pq0; pq < p.prb_ptr[s + 1]; pq += MT_NCW) {
+                const int pid = p.prb_ids[pq];
+                const int tap = p.prb_tap[pid];
+                double val;
+                if (tap >= 0) {
+                    val = us[(size_t)(tap / W) * SB + tap % W];
+                } else {
+                    const double* wv = p.prb_w + p.prb_woff[pid];
+                    val = 0.0;
+                    for (int j = 0; j < L; ++j)
+                        for (int r = 0; r < W; ++r) val = fma(wv[j * W + r], us[(size_t)j * SB + r], val);
+                }
+                p.rows[(rec * S + qs) * p.n_probe + pid] = val;  // [rec][shot][probe]
+            }
+        }
+    };
+
     for (int k = 1; k <= p.n_steps; ++k) {
         const int par = k & 1;
         const int cb = (k - 1) & 1;
-        double* Un = cb ? p.U0 : p.U1;
+        double* Un = cb ? p.U0 : p.U1;  // U^{k-2} -> U^k (layers >= 1 in this sweep, layer 0 one sweep later)
+        double* Uc = cb ? p.U1 : p.U0;  // U^{k-1}; its layer 0 is completed in this sweep
         double* fx = p.flux + (size_t)par * p.n_sub * SB;
+        const double* fxp = p.flux + (size_t)(par ^ 1) * p.n_sub * SB;  // F_0 of step k-1
         const int kk = k - 1;
         const double fq = my_src >= 0 ? p.ftab[(size_t)q * p.ftab_stride + kk] : 0.0;
-        double sq = 0.0;
+        const double fqp = (my_src >= 0 && k >= 2) ? p.ftab[(size_t)q * p.ftab_stride + kk - 1] : 0.0;
+        double sq = 0.0, sq0 = 0.0;
 
-        // ---------------- sweep: layers of every subdomain, all in registers ---------------
+        // ---- sweep: per subdomain the deferred layer 0 of step k-1, then the layers of step k, in registers
         for (int sl = 0; sl < ns; ++sl) {
             const int s = s_id[sl];
             const bool mine = my_src == s;
             double x[RT][2], acc[RT][2];
             int cur = 0;  // stash slot of U_j (slot 2: the previous layer's flux F_{j-1})
+            if (k == 1) {
+                load_slice(acquire(0), x);  // U_0 of the start state
+                release();
+            } else {
+                layer0(sl, fxp, fqp, Uc, sq0, x);  // U_0^{k-1}: all neighbours published F_0^{k-1} before the barrier
+            }
             {
                 double ua[RT][2];
-                const double* b0 = acquire(0);
-                const double* b1 = acquire(1);
-                load_slice(b0, x);   // U_0
-                load_slice(b1, ua);  // U_1
-                release();
+                load_slice(acquire(0), ua);  // U_1
                 release();
 #pragma unroll
                 for (int t = 0; t < RT; ++t) {
@@ -452,10 +566,17 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
         }
         // ---------------- grid-wide step barrier ------------------------------------------
         // (bar.sync orders the team's face-buffer writes before lane 0's release store: cumulativity.)
-        // The face phase reads only face neighbours' buffers; the wait is for every team (the
+        // Layer 0 of step k reads only face neighbours' buffers; the wait is for every team (the
         // grid-wide barrier per step), which measured the same step time as neighbour-only flags.
         asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
         if (w == 0 && lane == 0) st_release(p.flags + team, (unsigned int)k);
+        // while the other teams finish: norms, and the probes of step k-1 (its layer 0 was written by this
+        // team's warps before the barrier above)
+        put_norm(kk, 0, sq);
+        if (k >= 2) {
+            put_norm(kk - 1, 1, sq0);
+            record(k - 1, Uc);
+        }
         if (w == 0) {
             for (int i = lane; i < p.n_team; i += 32)
                 while (ld_acquire(p.flags + i) < (unsigned int)k) {
@@ -463,101 +584,25 @@ __device__ __forceinline__ void mt_compute(const MtParams& p, const double* ring
             __syncwarp();
         }
         asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");
-        // ---------------- faces: layer-0 coupling + leapfrog -----------------------------
-        // The face values of a subdomain (own + neighbour flux on shared faces, acc_0 on outer faces;
-        // a row takes exactly one of the two) are scattered L2 reads: those of subdomain sl + 1 are
-        // issued after the mass product of subdomain sl, so their latency hides behind its leapfrog.
-        auto gather = [&](int sl, double (&y)[RT][2]) {
-            const int s = s_id[sl];
-            const double* fo = fx + (size_t)s * SB + lo;
-            const double* ao = p.acc1 + (size_t)s * SB + lo;
-#pragma unroll
-            for (int t = 0; t < RT; ++t)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int row = 8 * t + 2 * c + e;
-                    y[t][e] = 0.0;
-                    if (row < W) {
-                        const int f = row / M, nb = s_nb[sl * 6 + f];
-                        if (nb >= 0)
-                            y[t][e] = __dadd_rn(__ldcg(fo + 8 * t + e),
-                                                __ldcg(fx + (size_t)nb * SB + q * WP + (f ^ 1) * M + row % M));
-                        else
-                            y[t][e] = __ldcg(ao + 8 * t + e);
-                    }
-                }
-        };
-        double yn[RT][2];
-        if (ns > 0) gather(0, yn);
-        for (int sl = 0; sl < ns; ++sl) {
-            const int s = s_id[sl];
-            const bool mine = my_src == s;
-            double x[RT][2], acc[RT][2], a1[RT][2];
-#pragma unroll
-            for (int t = 0; t < RT; ++t)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int row = 8 * t + 2 * c + e;
-                    const bool outer = row < W && s_nb[sl * 6 + row / M] < 0;
-                    x[t][e] = outer ? 0.0 : yn[t][e];
-                    a1[t][e] = outer ? yn[t][e] : 0.0;
-                }
-            mt_gemm<M, true>(acquire(0), x, acc, dir, trn);
-            if (sl + 1 < ns) gather(sl + 1, yn);  // lands while this subdomain's layer 0 is updated
-            const double* u0 = acquire(1);
-            const double* uo = acquire(2);
-            double* un = Un + (size_t)s * KS;
-#pragma unroll
-            for (int t = 0; t < RT; ++t) {
-                const double2 u = *reinterpret_cast<const double2*>(u0 + lo + 8 * t);
-                const double2 o = *reinterpret_cast<const double2*>(uo + lo + 8 * t);
-                double v[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int row = 8 * t + 2 * c + e;
-                    double tot = __dadd_rn(acc[t][e], a1[t][e]);  // one of the two is zero
-                    if (mine && row < W) tot = __dadd_rn(tot, __dmul_rn(svec[row], fq));
-                    v[e] = fma(dt2, tot, fma(2.0, e ? u.y : u.x, e ? -o.y : -o.x));
-                    sq = fma(v[e], v[e], sq);
-                }
-                *reinterpret_cast<double2*>(un + lo + 8 * t) = make_double2(v[0], v[1]);
-            }
-            release();  // mass tiles
-            release();  // U_0
-            release();  // Uprev_0
-        }
-        // per-shot |U|^2 of this CTA: the 4 lanes of a shot hold its rows
-        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
-        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
-        if (c == 0) p.norm_part[((size_t)kk * p.n_team + team) * S + q] = sq;
-        // probes: rows of U after the step (thread = shot x every 4th probe)
-        if (k % p.record_every == 0 && p.rows) {
-            asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");  // the team's U rows are written
-            const long long rec = k / p.record_every - 1;
-            const int pq0 = w, qs = lane;  // thread (w, lane): shot lane, probes w, w+4, ...
-            for (int sl = 0; sl < ns; ++sl) {
-                const int s = s_id[sl];
-                const double* us = Un + (size_t)s * KS + (size_t)qs * WP;
-                for (int pq = p.prb_ptr[s] + pq0; pq < p.prb_ptr[s + 1]; pq += MT_NCW) {
-                    const int pid = p.prb_ids[pq];
-                    const int tap = p.prb_tap[pid];
-                    double val;
-                    if (tap >= 0) {
-                        val = us[(size_t)(tap / W) * SB + tap % W];
-                    } else {
-                        const double* wv = p.prb_w + p.prb_woff[pid];
-                        val = 0.0;
-                        for (int j = 0; j < L; ++j)
-                            for (int r = 0; r < W; ++r) val = fma(wv[j * W + r], us[(size_t)j * SB + r], val);
-                    }
-                    p.rows[(rec * S + qs) * p.n_probe + pid] = val;  // [rec][shot][probe]
-                }
-            }
-        }
         // this step's state writes feed the next step's bulk-copy reads (async proxy)
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(stepdone);
+    }
+    // ---------------- epilogue: layer 0 of the last step ------------------------------------
+    {
+        const int k = p.n_steps;
+        double* Un = ((k - 1) & 1) ? p.U0 : p.U1;
+        const double* fx = p.flux + (size_t)(k & 1) * p.n_sub * SB;
+        const double fq = my_src >= 0 ? p.ftab[(size_t)q * p.ftab_stride + k - 1] : 0.0;
+        double sq0 = 0.0;
+        for (int sl = 0; sl < ns; ++sl) {
+            double v[RT][2];
+            layer0(sl, fx, fq, Un, sq0, v);
+        }
+        put_norm(k - 1, 1, sq0);
+        asm volatile("bar.sync %0, %1;" ::"r"(barT), "r"(MT_NCW * 32) : "memory");  // the team's U rows are written
+        record(k, Un);
     }
 }
 
@@ -630,7 +675,13 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
             const double* uc = cur + (long long)s_id[sl] * KS;
             const double* up = prv + (long long)s_id[sl] * KS;
             const double* cf = p.tcoef + (long long)s_id[sl] * 2 * L * TB;
-            issue(uc, sbytes);
+            if (k == 0) {
+                issue(uc, sbytes);
+            } else {  // deferred layer 0 of the previous step: its U_0 levels are prv (newer) and cur's stale slot
+                issue(p.mtiles + (size_t)s_id[sl] * NMT * 64, mbytes);
+                issue(up, sbytes);
+                issue(uc, sbytes);
+            }
             issue(uc + SB, sbytes);
             issue(cf, cbytes);
             if (!interior) issue(cf + TB, cbytes);
@@ -641,6 +692,13 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
                 issue(up + (long long)j * SB, sbytes);
             }
         }
+    }
+    // epilogue: layer 0 of the last step (its newer U_0 level was written during that step's sweep)
+    {
+        const int k = p.n_steps - 1;
+        mbar_wait(stepdone, (uint32_t)(k & 1));
+        const double* cur = (k & 1) ? p.U1 : p.U0;
+        const double* prv = (k & 1) ? p.U0 : p.U1;
         for (int sl = 0; sl < ns; ++sl) {
             issue(p.mtiles + (size_t)s_id[sl] * NMT * 64, mbytes);
             issue(cur + (long long)s_id[sl] * KS, sbytes);
@@ -871,7 +929,7 @@ extern "C" int sfw_shots_run(sfw_stepper* h, int n_steps, int record_every, cons
                                  h->stream));
     const long long nrec = n_steps / record_every;
     if ((rc = ms_ensure(&h->mrows, &h->mrows_cap, std::max(1LL, nrec * h->n_probe * S), errbuf, errlen))) return rc;
-    const int nparts = h->mt_grid;  // |U|^2 partials per step: one per CTA
+    const int nparts = 2 * h->mt_grid;  // |U|^2 partials per step: two per team (layers >= 1, layer 0)
     if ((rc = ms_ensure(&h->mnorm, &h->mnorm_cap, (long long)n_steps * nparts * S + (long long)n_steps * S, errbuf,
                         errlen)))
         return rc;
@@ -968,7 +1026,7 @@ extern "C" int sfw_shots_traffic(sfw_stepper* h, double* alg_bytes, double* alg_
         const double L = h->layers[i];
         b += 8.0 * ((2 * L - 1) * w * (w + 1) / 2 + 3 * L * w * S);
         f += S * (2.0 * (2 * L - 1) * w * w + 5 * L * w);
-        s += 8.0 * ((2 * L - 1) * d.TB + d.NMT * 64 + (3 * L + 2) * (double)d.SB);
+        s += 8.0 * ((2 * L - 1) * d.TB + d.NMT * 64 + (3 * L + 1) * (double)d.SB);
     }
     if (alg_bytes) *alg_bytes = b;
     if (alg_flops) *alg_flops = f;
