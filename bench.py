@@ -713,7 +713,7 @@ def _run_fdtd(args):
             "roofline": {"bound": "hbm", "achieved": alg * K / sec / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg * K / sec / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
                          "formula": "32 B per node-step (u, c, u_prev read once, u_next written once)"},
-            "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": 2 * K}
+            "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": K + 1}  # K x k_fdtd<0> + k_fd_norms
     print(json.dumps(line), flush=True)
 
 

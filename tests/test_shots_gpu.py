@@ -107,3 +107,37 @@ def test_shots_m9k8_physical_sources():
         e_single, e_oracle = rel(rows[:, q, :], r1), rel(rows[:, q, :], ro)
         print(f"shot {q}: vs single-source GPU {e_single:.2e}, vs oracle {e_oracle:.2e}, tol {tol:.2e}")
         assert e_single < tol and e_oracle < tol
+
+
+@pytest.mark.parametrize("maxgrid", [None, "3", "1"])
+def test_shots_short_runs_and_strided_records(maxgrid, monkeypatch):
+    """The layer-0 pass of step k runs inside the sweep of step k+1 and once more after the last step
+    (sfw_shots.cu): 1-, 2- and 3-step runs, strided records and several subdomains per team
+    (SFW_STEP_MAXGRID caps the number of teams) against the single-source stepper."""
+    if maxgrid:
+        monkeypatch.setenv("SFW_STEP_MAXGRID", maxgrid)
+    g = load_golden("golden_c1.npz")
+    wl = make_workload(1)
+    part = partition_for(wl.counts, wl.p, tuple((s - 1) * h for s, h in zip(wl.global_shape, wl.spacing)))
+    models = models_from_arrays(part, wl.c_field, 4, g["gammas"], g["hats"], g["scales"], shift=wl.shift)
+    probes = [Probe(a, w) for a, w in face_probes(models, wl)]
+    rng = np.random.default_rng(11)
+    order = sorted(models)
+    probes.append(Probe(order[3], rng.standard_normal(models[order[3]].state_size)))  # dense node-type weights
+    shots = _shots(models, 32, 5)
+    dt = float(g["dt"])
+    for n, every in ((1, 1), (2, 1), (3, 1), (7, 3), (40, 4)):
+        with CoupledStepper(models, dt) as st:
+            times, rows = st.run_shots(n, shots, probes=probes, record_every=every)
+            states = {q: st.shot_state(q) for q in (2, 30)}
+        assert rows.shape == (n // every + 1, 32, len(probes))
+        for q in (2, 30):
+            with CoupledStepper(models, dt, sources=(shots[q],)) as st1:
+                t1, r1 = st1.run(n, probes=probes, record_every=every)
+                u1, p1 = st1.u_curr, st1.u_prev
+            assert np.array_equal(times, t1)
+            assert rel(rows[:, q, :], r1) < 1e-10 or np.abs(r1).max() < 1e-300, (n, every, q)
+            big = max(np.abs(v).max() for v in u1.values())
+            for a in u1:  # both time levels, layer 0 included (completed by the pass after the last step)
+                assert np.abs(states[q][0][a] - u1[a]).max() <= 1e-10 * big, (n, every, q, a)
+                assert np.abs(states[q][1][a] - p1[a]).max() <= 1e-10 * big, (n, every, q, a)
