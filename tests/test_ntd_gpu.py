@@ -117,3 +117,18 @@ def test_face_inputs_and_verification_sweep_vs_reference():
     assert [n for n, _ in res["rows"]] == [1, 2, 3]
     assert np.allclose(rows, g["verify_rows"], rtol=1e-6, atol=0)
     assert res["agreement"] < 1e-9 and not res["truncated"]
+
+
+@pytest.mark.parametrize("gang", ["1", "3", "7", "40"])
+def test_ntd_full_gang_sizes_bitwise(gang, monkeypatch):
+    """The band LU of one frequency is shared by a gang of CTAs (sfw_ntdfull.cu: column c belongs to CTA
+    c mod G, one gang barrier per column, right-hand sides split over the gang).  Every gang size gives
+    the same bits: sparse 4913-node operator and the dense projected pair."""
+    from paper_1406_6923_b200.ntd import ntd_full_band, ntd_reduced
+    op, g = _c1_operator()
+    om = g["omegas"][:3]
+    ref = ntd_full_band(op.matrix, g["f"], om)          # default gang size
+    red = ntd_reduced(g["a_tilde"], g["f_tilde"], float(om[1]))
+    monkeypatch.setenv("SFW_NTD_GANG", gang)
+    assert np.array_equal(ntd_full_band(op.matrix, g["f"], om), ref)
+    assert np.array_equal(ntd_reduced(g["a_tilde"], g["f_tilde"], float(om[1])), red)
