@@ -231,7 +231,9 @@ __device__ __forceinline__ void mt_ldb(const double* __restrict__ tiles, double 
 // the MMA read it; every B fragment is therefore used again after the next MMA of its accumulator
 // chain has been issued, A operands one k-step later, the last ones after the products are in
 // registers.  Measured effect: three teams per CTA 15 deviating runs in 100 without, 0 in 200 with;
-// the committed two-team kernel 0 in 1500.
+// the committed two-team kernel 0 in 1500.  (tools/dmma_hazard_bench.cu, a bare DMMA/LDS stream with the same
+// operand pattern, shows no such hazard with up to 8 warps per SMSP: the mechanism is not confirmed, the measure is
+// empirical.)
 __device__ __forceinline__ void mt_hold(unsigned int& keep, double v) {
     unsigned int w32;
     asm volatile("{ .reg .b32 lo; mov.b64 {lo, %0}, %1; }" : "=r"(w32) : "d"(v));
