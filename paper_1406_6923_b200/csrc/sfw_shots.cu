@@ -224,50 +224,18 @@ __device__ __forceinline__ void mt_ldb(const double* __restrict__ tiles, double 
     });
 }
 
-// mt_hold(): a cheap (ALU-pipe) use of a register that lengthens its life in the instruction stream.
-// Config 4 was not repeatable run to run whenever two or more compute warps shared an SMSP's DMMA
-// pipe (one warp's product computed as if with slightly wrong operands, config 4, has
-// the investigation).  The leading hypothesis is a write to an MMA operand register landing before
-// the MMA read it; every B fragment is therefore used again after the next MMA of its accumulator
-// chain has been issued, A operands one k-step later, the last ones after the products are in
-// registers.  Measured effect: three teams per CTA 15 deviating runs in 100 without, 0 in 200 with;
-// the committed two-team kernel 0 in 1500.  (tools/dmma_hazard_bench.cu, a bare DMMA/LDS stream with the same
-// operand pattern, shows no such hazard with up to 8 warps per SMSP: the mechanism is not confirmed, the measure is
-// empirical.)
-__device__ __forceinline__ void mt_hold(unsigned int& keep, double v) {
-    unsigned int w32;
-    asm volatile("{ .reg .b32 lo; mov.b64 {lo, %0}, %1; }" : "=r"(w32) : "d"(v));
-    keep ^= w32;
-}
-__device__ unsigned int g_mt_sink;
-
 template <int M, bool MASS, int KC>
 __device__ __forceinline__ void mt_kstep(const double* __restrict__ tiles, const double (&x)[MtDims<M>::RT][2],
-                                         double (&acc)[MtDims<M>::RT][2], double (&bb)[3][MtDims<M>::RT],
-                                         double (&pend)[MtDims<M>::RT], unsigned int& pmask, const int (&dir)[2],
-                                         const int (&trn)[2], unsigned int& keep) {
+                                         double (&acc)[MtDims<M>::RT][2], double (&bb)[2][MtDims<M>::RT],
+                                         const int (&dir)[2], const int (&trn)[2]) {
     constexpr int RT = MtDims<M>::RT, T = KC / 2, e = KC % 2;
-    if constexpr (KC + 1 < 2 * RT) mt_ldb<M, MASS, KC + 1>(tiles, bb[(KC + 1) % 3], dir, trn);
+    if constexpr (KC + 1 < 2 * RT) mt_ldb<M, MASS, KC + 1>(tiles, bb[(KC + 1) % 2], dir, trn);
     const double a = x[T][e];
     static_for<RT>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
-        if constexpr (!MASS) {
-            // full product: chain t has an MMA in every k-step; the previous k-step's fragment of
-            // the chain is released once this k-step's MMA of the chain has been issued
-            dmma8x8x4(acc[t], a, bb[KC % 3][t]);
-            if constexpr (KC >= 1) mt_hold(keep, bb[(KC - 1) % 3][t]);
-        } else if constexpr (mt_face_tile(M, T, t)) {
-            // sparse product: the chain's last fragment is carried in pend[] until its next MMA
-            dmma8x8x4(acc[t], a, bb[KC % 3][t]);
-            if (pmask & (1u << t)) mt_hold(keep, pend[t]);  // (a compile-time constant after unrolling)
-            pend[t] = bb[KC % 3][t];
-            pmask |= 1u << t;
-        }
+        if constexpr (!MASS || mt_face_tile(M, T, t)) dmma8x8x4(acc[t], a, bb[KC % 2][t]);
     });
-    // every chain has now issued an MMA that waits for its MMA of the previous k-step: that
-    // k-step's A operand has been read (full product only; the sparse one holds all of x to the end)
-    if constexpr (!MASS && KC >= 1) mt_hold(keep, x[(KC - 1) / 2][(KC - 1) % 2]);
-    if constexpr (KC + 1 < 2 * RT) mt_kstep<M, MASS, KC + 1>(tiles, x, acc, bb, pend, pmask, dir, trn, keep);
+    if constexpr (KC + 1 < 2 * RT) mt_kstep<M, MASS, KC + 1>(tiles, x, acc, bb, dir, trn);
 }
 
 // acc^T = x^T B over all row tiles; x, acc in accumulator-fragment layout (see the header comment).
@@ -277,46 +245,12 @@ __device__ __forceinline__ void mt_kstep(const double* __restrict__ tiles, const
 template <int M, bool MASS>
 __device__ __forceinline__ void mt_gemm(const double* __restrict__ tiles, const double (&x)[MtDims<M>::RT][2],
                                         double (&acc)[MtDims<M>::RT][2], const int (&dir)[2], const int (&trn)[2]) {
-    constexpr int RT = MtDims<M>::RT, LAST = 2 * RT - 1;
+    constexpr int RT = MtDims<M>::RT;
 #pragma unroll
     for (int t = 0; t < RT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    double bb[3][RT], pend[RT];
-    unsigned int keep = 0, pmask = 0;
+    double bb[2][RT];
     mt_ldb<M, MASS, 0>(tiles, bb[0], dir, trn);
-    mt_kstep<M, MASS, 0>(tiles, x, acc, bb, pend, pmask, dir, trn, keep);
-    // products in registers: every MMA has read its operands
-#pragma unroll
-    for (int t = 0; t < RT; ++t) asm volatile("" : "+d"(acc[t][0]), "+d"(acc[t][1])::"memory");
-    if constexpr (MASS) {
-        // Drain after the sparse product: a real read of every accumulator right behind its MMAs.  A warp
-        // issues in order, so nothing that follows is issued before the last MMA of every chain has
-        // written its result (and therefore read its operands).  With the layer-0 pass inside the sweep
-        // the kernel was not repeatable without this (7-9 of 12 full-size runs equal, some diverging;
-        // with it 1500 of 1500, also with the warps of a team forced into lockstep); the same kind of
-        // measure as mt_hold() above, see DESIGN.md (config 4).
-#pragma unroll
-        for (int t = 0; t < RT; ++t) {
-            unsigned int d0, d1;
-            asm volatile("{ .reg .b32 lo; mov.b64 {lo, %0}, %2; mov.b64 {lo, %1}, %3; }"
-                         : "=r"(d0), "=r"(d1)
-                         : "d"(acc[t][0]), "d"(acc[t][1])
-                         : "memory");
-            keep ^= d0 ^ d1;
-        }
-    }
-    if constexpr (!MASS) {
-#pragma unroll
-        for (int t = 0; t < RT; ++t) mt_hold(keep, bb[LAST % 3][t]);
-        mt_hold(keep, x[LAST / 2][LAST % 2]);
-    } else {
-#pragma unroll
-        for (int t = 0; t < RT; ++t) {
-            if (pmask & (1u << t)) mt_hold(keep, pend[t]);
-            mt_hold(keep, x[t][0]);
-            mt_hold(keep, x[t][1]);
-        }
-    }
-    if (keep == 0x9e3779b9u) g_mt_sink = keep;  // practically never; keeps the holds alive
+    mt_kstep<M, MASS, 0>(tiles, x, acc, bb, dir, trn);
 }
 
 template <int M>
@@ -660,6 +594,11 @@ __global__ void __launch_bounds__(2 * (MT_NCW + 1) * 32, 1) k_step_mt(const MtPa
     uint32_t ph = 0;
     auto issue = [&](const double* src, uint32_t bytes) {
         mbar_wait(&empty[st], ph ^ 1);
+        // The compute warps read this stage through the generic proxy; the bulk copy writes it through
+        // the async proxy.  The proxy fence between the acquire above and the copy is REQUIRED: without it
+        // the kernel was not repeatable run to run at full size (a refill could overtake reads of the
+        // stage still in flight, config 4, has the history of that bug).
+        fence_proxy_async();
         mbar_arrive_expect_tx(&full[st], bytes);
         bulk_g2s(ring + (size_t)st * STG, src, bytes, &full[st], pol);
         if (++st == NST) {
