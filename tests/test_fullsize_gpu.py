@@ -127,8 +127,8 @@ def test_config4_full_size_shots(cfg3):
     n = 30
     with CoupledStepper(models, dt) as st:
         times, rows = st.run_shots(n, shots, probes=probes)
-        for _ in range(40):  # run-to-run repeatability (config 4: MMA operand registers; the protection
-            # is tied to the compiled instruction stream, equivalent source variants lost it in 1-19 of 40 runs)
+        for _ in range(40):  # run-to-run repeatability (config 4: a ring refill without a proxy fence
+            # once overtook generic-proxy reads of the stage; 7-9 of 12 such runs were equal)
             assert np.array_equal(rows, st.run_shots(n, shots, probes=probes)[1])
     for q in (0, 13, 31):
         with CoupledStepper(models, dt, sources=(shots[q],)) as st1:

@@ -1,4 +1,5 @@
-// Reproducer attempt for the config-4 repeatability problem (config 4): does a queued
+// Negative control of the config-4 repeatability investigation (config 4; the cause was a missing
+// proxy fence before the ring refills, not this): does a queued
 // mma.sync.m8n8k4.f64 read its operand registers after later instructions of the same warp have
 // overwritten them?  Every warp of every CTA computes the SAME sequence of GEMM-like products from the
 // same shared-memory operands (7 independent accumulator chains, B fragments loaded one k-step ahead into

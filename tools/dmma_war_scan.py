@@ -1,4 +1,6 @@
-"""Static scan of the library's SASS: for every DMMA, how many instructions later is one of its
+"""(History: diagnostic of the config-4 repeatability investigation; the cause turned out to be a missing proxy
+fence before the ring refills, not an MMA operand hazard -- DESIGN.md, config 4.)
+Static scan of the library's SASS: for every DMMA, how many instructions later is one of its
 source operand registers (A, B pairs) overwritten by an instruction that does not depend on the
 DMMA's result?  (Diagnostic for the config-4 repeatability investigation: ptxas protects some of these
 writes with a read scoreboard on the DMMA and relies on issue distance for others.)  Straight-line distance within a basic block; prints the closest cases per kernel.
